@@ -1,0 +1,32 @@
+"""Shared test configuration.
+
+Markers: ``gpu`` tests need a B200 (run by the driver with ``-m gpu``);
+everything else runs on CPU.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TESTS = os.path.join(ROOT, "tests")
+for _p in (TESTS, ROOT):
+    if _p not in sys.path:
+        sys.path.insert(0, _p)
+
+GOLDEN_PATH = os.path.join(ROOT, "tests", "golden", "golden.npz")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 device")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+@pytest.fixture(scope="session")
+def golden():
+    data = np.load(GOLDEN_PATH, allow_pickle=False)
+    return {k: data[k] for k in data.files}
