@@ -1,0 +1,158 @@
+/*
+ * moe_b200.h — C-ABI of the B200-native fused MoE-layer forward.
+ *
+ * Drop-in boundary for the reference `moeperf` hot path
+ * (/root/reference/pkg/src/moeperf/pipeline.py:572 `moe_forward`).  The
+ * reference has no FFI of its own (it is pure Python/numpy), so the entry
+ * points below are exactly the stage functions its Python API exports
+ * (moeperf/__init__.py:56-78); each one cites the reference function it
+ * replaces.  The Python host mirror (paper_2605_23911_b200/) binds them with
+ * ctypes; INTEGRATION.md shows the binding a maintainer would add.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  All tensor pointers are DEVICE pointers
+ *    (cudaMalloc'd or torch-owned), row-major and contiguous.
+ *  - The caller owns every buffer, including the workspace; the library
+ *    never allocates in the forward path.
+ *  - All calls are asynchronous on `stream` (a cudaStream_t passed as void*),
+ *    never synchronise the host, and are CUDA-graph capturable.
+ *  - Return value: MOE_B200_OK (0) or one status code per reference
+ *    exception class (moeperf/errors.py:9-50) plus CUDA / unsupported codes.
+ *  - Expert weights use the reference's stacked layout (moeperf/model.py:119-165):
+ *        gate, up : (E*d, f)  bf16, expert e owns rows [e*d, (e+1)*d)
+ *        down     : (E*f, d)  bf16, expert e owns rows [e*f, (e+1)*f)
+ *    The router weight is (d, E) fp32 (model/router.py:116-133).
+ *  - Routing indices are int32 on device (the reference's int64 values fit).
+ *  - d and f must be multiples of 8 (16-byte TMA row pitch).
+ */
+#ifndef MOE_B200_H
+#define MOE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  Names follow moeperf/errors.py. */
+typedef enum moe_b200_status {
+  MOE_B200_OK = 0,
+  MOE_B200_ERR_NON_FINITE_INPUT = 1,   /* NonFiniteInput      errors.py:13 */
+  MOE_B200_ERR_SHAPE_MISMATCH = 2,     /* ShapeMismatch       errors.py:17 */
+  MOE_B200_ERR_INVALID_K = 3,          /* InvalidK            errors.py:21 */
+  MOE_B200_ERR_INDEX_OUT_OF_RANGE = 4, /* IndexOutOfRange     errors.py:25 */
+  MOE_B200_ERR_INVALID_BLOCK_M = 5,    /* InvalidBlockM       errors.py:29 */
+  MOE_B200_ERR_SCHEDULE_MISMATCH = 6,  /* ScheduleMismatch    errors.py:33 */
+  MOE_B200_ERR_INVALID_VALUE = 7,      /* ValueError (ModelConfig/PipelineParams) */
+  MOE_B200_ERR_WORKSPACE = 8,          /* workspace too small / misaligned */
+  MOE_B200_ERR_UNSUPPORTED = 9,        /* shape the sm_100a path does not take */
+  MOE_B200_ERR_CUDA = 10,              /* CUDA runtime/driver failure */
+  MOE_B200_ERR_NCCL = 11               /* expert-parallel collective failure */
+} moe_b200_status;
+
+/* Gating mode (moeperf/model.py:14-18). */
+#define MOE_B200_GATING_SOFTMAX 0
+#define MOE_B200_GATING_SIGMOID_NORMALIZED 1
+
+/* Element dtypes for activations. */
+#define MOE_B200_DTYPE_F32 0
+#define MOE_B200_DTYPE_BF16 1
+
+/* Static layer shape (moeperf/model.py:21-48 ModelConfig). */
+typedef struct moe_b200_config {
+  int32_t num_experts; /* E */
+  int32_t top_k;       /* k, 1 <= k <= E */
+  int32_t hidden_dim;  /* d */
+  int32_t ffn_dim;     /* f */
+  int32_t gating;      /* MOE_B200_GATING_* */
+} moe_b200_config;
+
+/* Device-side status bits, readable with moe_b200_read_flags. */
+#define MOE_B200_FLAG_NONFINITE_TOKENS 1u
+#define MOE_B200_FLAG_NONFINITE_ROUTER 2u
+
+/* Bytes of workspace needed for up to `max_tokens` tokens.  The workspace
+ * holds the router logits, schedule tables, the permuted bf16 tokens, the
+ * bf16 SwiGLU intermediate and the per-slot fp32 expert outputs. */
+int moe_b200_workspace_size(const moe_b200_config* cfg, int64_t max_tokens, size_t* bytes);
+
+/* Zero the workspace's self-resetting counters and flags.  Call once after
+ * allocating a workspace (the kernels leave them zeroed afterwards). */
+int moe_b200_workspace_init(const moe_b200_config* cfg, int64_t max_tokens, void* ws,
+                            size_t ws_bytes, void* stream);
+
+/* Router + scheduler, one launch.
+ * Replaces router.py:116 `route` (logits, gate_scores, topk_select) and
+ * scheduler.py:78-117 (`expert_histogram`, `expert_offsets`,
+ * `build_permutation`, `build_block_schedule` as a device tile table).
+ * Bit-exact with the reference: fp64 ascending-k logits, numpy pairwise
+ * softmax sum / numpy-SIMD sigmoid, lowest-index tie-break, stable sort.
+ *   x        (B, d)   fp32 or bf16 (x_dtype)
+ *   w_router (d, E)   fp32
+ *   topk_idx (B, k)   int32   out: expert ids, descending score
+ *   topk_w   (B, k)   fp32    out: combine weights
+ *   counts   (E)      int32   out: expert histogram
+ *   offsets  (E+1)    int32   out: exclusive prefix sum
+ *   perm_fwd (B*k)    int32   out: permuted row -> expanded id t*k+j
+ *   perm_inv (B*k)    int32   out: expanded id -> permuted row
+ *   logits   (B, E)   fp32    out, optional (NULL): router logits        */
+int moe_b200_route(const moe_b200_config* cfg, int64_t num_tokens, const void* x, int x_dtype,
+                   const float* w_router, int32_t* topk_idx, float* topk_w, int32_t* counts,
+                   int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv, float* logits,
+                   void* ws, size_t ws_bytes, void* stream);
+
+/* Gather expert-major rows (pipeline.py:165-183 `permute_tokens`), cast to
+ * bf16.  xp (B*k, d) bf16 out. */
+int moe_b200_permute(const moe_b200_config* cfg, int64_t num_tokens, const void* x, int x_dtype,
+                     const int32_t* perm_fwd, void* xp, void* stream);
+
+/* Fused gate+up grouped GEMM with SiLU*up epilogue (pipeline.py:250-313
+ * `fused_gate_up`): h (B*k, f) bf16 out.  Uses the tile table written by
+ * moe_b200_route into `ws`. */
+int moe_b200_gate_up(const moe_b200_config* cfg, int64_t num_tokens, const void* xp,
+                     const void* w_gate, const void* w_up, void* h, void* ws, size_t ws_bytes,
+                     void* stream);
+
+/* Down-projection grouped GEMM (pipeline.py:186-247 `grouped_gemm`) whose
+ * epilogue multiplies by the routing weight and scatters each row to its
+ * expanded slot (the first half of pipeline.py:373-399):
+ *   ys (B*k, d) fp32 out, row t*k+j = w[t,j] * (h_row @ W_down_e). */
+int moe_b200_down_scatter(const moe_b200_config* cfg, int64_t num_tokens, const void* h,
+                          const void* w_down, const float* topk_w, const int32_t* perm_fwd,
+                          float* ys, void* ws, size_t ws_bytes, void* stream);
+
+/* Deterministic combine (second half of pipeline.py:373-399):
+ *   y[t] = sum_{j=0..k-1} ys[t*k+j], ascending j, fp32.  y (B, d). */
+int moe_b200_combine(const moe_b200_config* cfg, int64_t num_tokens, const float* ys, void* y,
+                     int y_dtype, void* stream);
+
+/* Whole layer (pipeline.py:572-615 `moe_forward`): route, permute, gate+up,
+ * down+scatter, combine — five launches, no host synchronisation.
+ * Intermediates live in `ws`; routing outputs are written to the caller's
+ * buffers so the host can build the trace lazily from `counts`. */
+int moe_b200_forward(const moe_b200_config* cfg, int64_t num_tokens, const void* x, int x_dtype,
+                     const float* w_router, const void* w_gate, const void* w_up,
+                     const void* w_down, void* y, int y_dtype, int32_t* topk_idx, float* topk_w,
+                     int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* Copy the device status flags (MOE_B200_FLAG_*) to the host and clear them.
+ * Synchronises `stream`. */
+int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws,
+                        size_t ws_bytes, uint32_t* flags, void* stream);
+
+/* Human-readable status. */
+const char* moe_b200_strerror(int status);
+
+/* Last CUDA error string recorded by the library (thread-local). */
+const char* moe_b200_last_error_detail(void);
+
+/* Library version string. */
+const char* moe_b200_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOE_B200_H */

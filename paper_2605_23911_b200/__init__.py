@@ -1,0 +1,54 @@
+"""B200-native fused MoE-layer forward (sm_100a), drop-in for the reference
+``moeperf`` hot path (``moeperf/pipeline.py:572`` ``moe_forward``).
+
+Public API mirrors the reference's names (``moeperf/__init__.py:56-78``):
+``moe_forward``, ``route``, ``ModelConfig``, ``Gating``, ``ExpertWeights``,
+``PipelineParams``, ``RoutingResult``, the error classes, and the trace
+types.  ``MoELayer`` is the resident-weights device layer used by the bench.
+"""
+
+from .errors import (
+    DeviceError,
+    IndexOutOfRange,
+    InvalidBlockM,
+    InvalidK,
+    MoeperfError,
+    NativeLibraryMissing,
+    NonFiniteInput,
+    ScheduleMismatch,
+    ShapeMismatch,
+)
+from .trace import (
+    DEVICE_STAGES,
+    PipelineTrace,
+    StageRecord,
+    build_block_schedule,
+    expert_offsets,
+    stage_bytes,
+    stage_flops,
+    trace_from_counts,
+)
+from .types import (
+    MODEL_PRESETS,
+    BlockSchedule,
+    ExpertOffsets,
+    ExpertWeights,
+    Gating,
+    ModelConfig,
+    Permutation,
+    PipelineParams,
+    RoutingResult,
+    preset,
+)
+
+__version__ = "0.1.0"
+
+
+def __getattr__(name):
+    # Device-facing symbols import torch lazily so host-only users (trace,
+    # types) do not pay for it.
+    if name in ("MoELayer", "DeviceExpertWeights", "upload_weights", "moe_forward", "route"):
+        from . import layer
+
+        return getattr(layer, name)
+    raise AttributeError(name)

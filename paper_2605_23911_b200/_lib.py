@@ -1,0 +1,110 @@
+"""ctypes binding of libmoe_b200.so (the C-ABI in include/moe_b200.h).
+
+There is deliberately no fallback: if the library is missing or fails to
+load, every entry point raises ``NativeLibraryMissing``.  Status codes map
+onto the reference's exception classes (``moeperf/errors.py:9-50``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from . import errors
+
+LIB_NAME = "libmoe_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+OK = 0
+STATUS_TO_EXC = {
+    1: errors.NonFiniteInput,
+    2: errors.ShapeMismatch,
+    3: errors.InvalidK,
+    4: errors.IndexOutOfRange,
+    5: errors.InvalidBlockM,
+    6: errors.ScheduleMismatch,
+    7: ValueError,
+    8: errors.DeviceError,
+    9: errors.DeviceError,
+    10: errors.DeviceError,
+    11: errors.DeviceError,
+}
+
+DTYPE_F32 = 0
+DTYPE_BF16 = 1
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("num_experts", ctypes.c_int32),
+        ("top_k", ctypes.c_int32),
+        ("hidden_dim", ctypes.c_int32),
+        ("ffn_dim", ctypes.c_int32),
+        ("gating", ctypes.c_int32),
+    ]
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_INT = ctypes.c_int
+_CFG = ctypes.POINTER(Config)
+_SZ = ctypes.c_size_t
+
+#: symbol -> (restype, argtypes); every symbol declared in include/moe_b200.h
+SIGNATURES = {
+    "moe_b200_workspace_size": (_INT, [_CFG, _I64, ctypes.POINTER(_SZ)]),
+    "moe_b200_workspace_init": (_INT, [_CFG, _I64, _P, _SZ, _P]),
+    "moe_b200_route": (_INT, [_CFG, _I64, _P, _INT, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_permute": (_INT, [_CFG, _I64, _P, _INT, _P, _P, _P]),
+    "moe_b200_gate_up": (_INT, [_CFG, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_down_scatter": (_INT, [_CFG, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_combine": (_INT, [_CFG, _I64, _P, _P, _INT, _P]),
+    "moe_b200_forward": (_INT, [_CFG, _I64, _P, _INT, _P, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_read_flags": (_INT, [_CFG, _I64, _P, _SZ, ctypes.POINTER(ctypes.c_uint32), _P]),
+    "moe_b200_strerror": (ctypes.c_char_p, [_INT]),
+    "moe_b200_last_error_detail": (ctypes.c_char_p, []),
+    "moe_b200_version": (ctypes.c_char_p, []),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str | None = None):
+    """Load (once) and return the ctypes library handle."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise errors.NativeLibraryMissing(
+                f"{p} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)"
+            )
+        try:
+            lib = ctypes.CDLL(p)
+        except OSError as exc:  # pragma: no cover - environment specific
+            raise errors.NativeLibraryMissing(f"cannot load {p}: {exc}") from exc
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(status: int, what: str) -> None:
+    """Raise the reference exception class for a non-zero status."""
+    if status == OK:
+        return
+    lib = load()
+    msg = lib.moe_b200_strerror(status).decode()
+    detail = lib.moe_b200_last_error_detail().decode()
+    exc = STATUS_TO_EXC.get(status, errors.DeviceError)
+    raise exc(f"{what}: {msg}" + (f" ({detail})" if detail else ""))
+
+
+def config_struct(num_experts, top_k, hidden_dim, ffn_dim, gating_code) -> Config:
+    return Config(num_experts, top_k, hidden_dim, ffn_dim, gating_code)

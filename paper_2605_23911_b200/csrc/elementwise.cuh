@@ -1,0 +1,76 @@
+// elementwise.cuh — HBM-bound row kernels: the expert-major gather
+// (pipeline.py:165-183 permute_tokens, fused fp32->bf16 cast) and the
+// deterministic k-slot combine (pipeline.py:396-399, ascending j, fp32).
+#pragma once
+
+#include "common.cuh"
+
+namespace moe {
+
+constexpr int kRowThreads = 256;
+
+// xp[r, :] = bf16(x[fwd[r] / k, :]); 16-byte vectors.  One CTA per row block.
+template <bool kBf16In>
+__global__ void __launch_bounds__(kRowThreads)
+permute_kernel(const void* __restrict__ x, const int32_t* __restrict__ fwd,
+               __nv_bfloat16* __restrict__ xp, int T, int k, int d) {
+  const int vec_per_row = d / 8;  // 8 bf16 = 16 B out
+  const long total = (long)T * vec_per_row;
+  for (long i = (long)blockIdx.x * kRowThreads + threadIdx.x; i < total;
+       i += (long)gridDim.x * kRowThreads) {
+    const int r = static_cast<int>(i / vec_per_row);
+    const int v = static_cast<int>(i % vec_per_row);
+    const int t = __ldg(fwd + r) / k;
+    int4 out;
+    if (kBf16In) {
+      out = __ldg(reinterpret_cast<const int4*>(static_cast<const __nv_bfloat16*>(x) + (size_t)t * d) + v);
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(x) + (size_t)t * d) + 2 * v;
+      float4 a = __ldg(src), b = __ldg(src + 1);
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(a.x, a.y);
+      __nv_bfloat162 p1 = __floats2bfloat162_rn(a.z, a.w);
+      __nv_bfloat162 p2 = __floats2bfloat162_rn(b.x, b.y);
+      __nv_bfloat162 p3 = __floats2bfloat162_rn(b.z, b.w);
+      out.x = *reinterpret_cast<int*>(&p0);
+      out.y = *reinterpret_cast<int*>(&p1);
+      out.z = *reinterpret_cast<int*>(&p2);
+      out.w = *reinterpret_cast<int*>(&p3);
+    }
+    reinterpret_cast<int4*>(xp + (size_t)r * d)[v] = out;
+  }
+}
+
+// y[t, :] = sum_{j<k} ys[t*k + j, :], ascending j in fp32, starting from
+// +0 like the reference's zero-initialised accumulator.  float4 vectors.
+template <bool kBf16Out>
+__global__ void __launch_bounds__(kRowThreads)
+combine_kernel(const float* __restrict__ ys, void* __restrict__ y, int B, int k, int d) {
+  const int vec_per_row = d / 4;
+  const long total = (long)B * vec_per_row;
+  for (long i = (long)blockIdx.x * kRowThreads + threadIdx.x; i < total;
+       i += (long)gridDim.x * kRowThreads) {
+    const int t = static_cast<int>(i / vec_per_row);
+    const int v = static_cast<int>(i % vec_per_row);
+    const float4* src = reinterpret_cast<const float4*>(ys + (size_t)t * k * d) + v;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < k; ++j) {
+      float4 a = __ldg(src + (size_t)j * (d / 4));
+      acc.x = __fadd_rn(acc.x, a.x);
+      acc.y = __fadd_rn(acc.y, a.y);
+      acc.z = __fadd_rn(acc.z, a.z);
+      acc.w = __fadd_rn(acc.w, a.w);
+    }
+    if (kBf16Out) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y);
+      __nv_bfloat162 p1 = __floats2bfloat162_rn(acc.z, acc.w);
+      uint2 o;
+      o.x = *reinterpret_cast<uint32_t*>(&p0);
+      o.y = *reinterpret_cast<uint32_t*>(&p1);
+      reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(y) + (size_t)t * d)[v] = o;
+    } else {
+      reinterpret_cast<float4*>(static_cast<float*>(y) + (size_t)t * d)[v] = acc;
+    }
+  }
+}
+
+}  // namespace moe

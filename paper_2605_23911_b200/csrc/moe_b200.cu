@@ -1,0 +1,422 @@
+// moe_b200.cu — C-ABI entry points (include/moe_b200.h): argument checks,
+// workspace layout, TMA descriptor encoding and kernel launches.
+#include "../../include/moe_b200.h"
+
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+#include "elementwise.cuh"
+#include "grouped_gemm.cuh"
+#include "router.cuh"
+
+using namespace moe;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int cuda_fail(cudaError_t e, const char* what) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
+  g_last_error = buf;
+  return MOE_B200_ERR_CUDA;
+}
+
+#define MOE_CUDA(call)                                \
+  do {                                                \
+    cudaError_t _e = (call);                          \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+#define MOE_LAUNCH_CHECK(what)                          \
+  do {                                                  \
+    cudaError_t _e = cudaGetLastError();                \
+    if (_e != cudaSuccess) return cuda_fail(_e, what);  \
+  } while (0)
+
+constexpr size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+constexpr int kTbCap = 4096;  // max router token blocks per launch
+
+// Fixed header at the start of the workspace (zeroed by workspace_init):
+//   [0] flags  [1] done_counter  [2] n_chunks  [16, 16 + kTbCap) token-block counters
+constexpr size_t kHeaderBytes = align256((16 + kTbCap) * sizeof(int32_t));
+
+struct Layout {
+  size_t logits, chunk_tab, xp, h, ys, total;
+  int max_chunks;
+};
+
+int chunk_rows_for(const moe_b200_config& c, int64_t B) {
+  // Tokens per expert on average; big chunks keep one weight pass per expert
+  // (Mixtral), small chunks allow shallower TMEM use (DeepSeek / Qwen).
+  const int64_t T = B * c.top_k;
+  return (T > 96LL * c.num_experts) ? 256 : 128;
+}
+
+Layout layout_for(const moe_b200_config& c, int64_t B) {
+  Layout L{};
+  const int64_t T = B * c.top_k;
+  const int bn = chunk_rows_for(c, B);
+  L.max_chunks = static_cast<int>(std::min<int64_t>(c.num_experts, T) + T / bn + 1);
+  size_t off = kHeaderBytes;
+  L.logits = off;    off = align256(off + (size_t)B * c.num_experts * sizeof(float));
+  L.chunk_tab = off; off = align256(off + (size_t)L.max_chunks * sizeof(int4));
+  L.xp = off;        off = align256(off + (size_t)T * c.hidden_dim * 2);
+  L.h = off;         off = align256(off + (size_t)T * c.ffn_dim * 2);
+  L.ys = off;        off = align256(off + (size_t)T * c.hidden_dim * sizeof(float));
+  L.total = off;
+  return L;
+}
+
+int check_config(const moe_b200_config* c) {
+  if (!c) return MOE_B200_ERR_INVALID_VALUE;
+  if (c->num_experts < 1 || c->hidden_dim < 1 || c->ffn_dim < 1) return MOE_B200_ERR_INVALID_VALUE;
+  if (c->top_k < 1 || c->top_k > c->num_experts) return MOE_B200_ERR_INVALID_K;
+  if (c->gating != MOE_B200_GATING_SOFTMAX && c->gating != MOE_B200_GATING_SIGMOID_NORMALIZED)
+    return MOE_B200_ERR_INVALID_VALUE;
+  if (c->num_experts > kMaxExperts) return MOE_B200_ERR_UNSUPPORTED;
+  if (c->hidden_dim % 8 || c->ffn_dim % 8) return MOE_B200_ERR_UNSUPPORTED;
+  return MOE_B200_OK;
+}
+
+int check_ws(const moe_b200_config* c, int64_t B, void* ws, size_t ws_bytes, Layout* L) {
+  *L = layout_for(*c, B);
+  if (!ws || ws_bytes < L->total) {
+    g_last_error = "workspace too small";
+    return MOE_B200_ERR_WORKSPACE;
+  }
+  if (reinterpret_cast<uintptr_t>(ws) % 256) {
+    g_last_error = "workspace must be 256-byte aligned";
+    return MOE_B200_ERR_WORKSPACE;
+  }
+  return MOE_B200_OK;
+}
+
+// --------------------------- TMA descriptor encoding --------------------------
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+int get_encoder() {
+  std::call_once(g_encode_once, []() {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) {
+    g_last_error = "cuTensorMapEncodeTiled unavailable";
+    return MOE_B200_ERR_CUDA;
+  }
+  return MOE_B200_OK;
+}
+
+// Row-major bf16 matrix (rows x cols), box (box_cols x box_rows), 128B swizzle.
+int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
+                  uint32_t box_cols, uint32_t box_rows) {
+  int rc = get_encoder();
+  if (rc) return rc;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[128];
+    snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    g_last_error = buf;
+    return MOE_B200_ERR_CUDA;
+  }
+  return MOE_B200_OK;
+}
+
+// ------------------------------- launches --------------------------------------
+struct RouterPlan {
+  int expc, tg, tokc, n_eblocks, n_tblocks;
+  size_t smem;
+};
+
+RouterPlan plan_router(const moe_b200_config& c, int64_t B, int x_bf16) {
+  RouterPlan r{};
+  r.expc = std::min(c.num_experts, 32);
+  const int n_groups = kRouterThreads / r.expc;
+  r.n_eblocks = (c.num_experts + r.expc - 1) / r.expc;
+  const int tgs[4] = {8, 4, 2, 1};
+  r.tg = 1;
+  for (int i = 0; i < 4; ++i) {
+    int tokc = tgs[i] * n_groups;
+    int64_t grid = ((B + tokc - 1) / tokc) * r.n_eblocks;
+    if (grid >= (kNumSMs * 4) / 5) { r.tg = tgs[i]; break; }
+  }
+  r.tokc = r.tg * n_groups;
+  r.n_tblocks = static_cast<int>((B + r.tokc - 1) / r.tokc);
+  r.smem = RouterSmem::total_bytes(r.tokc, r.expc, x_bf16 ? 2 : 4, c.num_experts);
+  return r;
+}
+
+template <bool kBf16, int kTG>
+int launch_router_t(const RouterParams& p, const RouterPlan& plan, cudaStream_t s) {
+  auto kern = router_kernel<kBf16, kTG>;
+  MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
+  kern<<<plan.n_tblocks * plan.n_eblocks, kRouterThreads, plan.smem, s>>>(p);
+  MOE_LAUNCH_CHECK("router_kernel");
+  return MOE_B200_OK;
+}
+
+template <bool kBf16>
+int launch_router_x(const RouterParams& p, const RouterPlan& plan, cudaStream_t s) {
+  switch (plan.tg) {
+    case 1: return launch_router_t<kBf16, 1>(p, plan, s);
+    case 2: return launch_router_t<kBf16, 2>(p, plan, s);
+    case 4: return launch_router_t<kBf16, 4>(p, plan, s);
+    default: return launch_router_t<kBf16, 8>(p, plan, s);
+  }
+}
+
+template <int kBN, bool kGateUp>
+int launch_gemm_t(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
+                  const GemmParams& gp, int grid, cudaStream_t s) {
+  using C = GemmCfg<kBN, kGateUp>;
+  auto kern = grouped_gemm_kernel<kBN, kGateUp>;
+  MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+  kern<<<grid, kGemmThreads, C::kSmemBytes, s>>>(a0, a1, b, gp);
+  MOE_LAUNCH_CHECK(kGateUp ? "grouped_gemm_kernel<gate_up>" : "grouped_gemm_kernel<down>");
+  return MOE_B200_OK;
+}
+
+int grid_for_rows(long total_vec) {
+  long blocks = (total_vec + kRowThreads - 1) / kRowThreads;
+  long cap = (long)kNumSMs * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return static_cast<int>(blocks);
+}
+
+uint8_t* ws8(void* ws) { return static_cast<uint8_t*>(ws); }
+
+}  // namespace
+
+// ================================ C ABI =======================================
+extern "C" {
+
+const char* moe_b200_version(void) { return "moe_b200 0.1.0 (sm_100a)"; }
+
+const char* moe_b200_last_error_detail(void) { return g_last_error.c_str(); }
+
+const char* moe_b200_strerror(int status) {
+  switch (status) {
+    case MOE_B200_OK: return "ok";
+    case MOE_B200_ERR_NON_FINITE_INPUT: return "NonFiniteInput: input contains NaN or infinity";
+    case MOE_B200_ERR_SHAPE_MISMATCH: return "ShapeMismatch: operand shapes are inconsistent";
+    case MOE_B200_ERR_INVALID_K: return "InvalidK: top_k outside [1, num_experts]";
+    case MOE_B200_ERR_INDEX_OUT_OF_RANGE: return "IndexOutOfRange: index outside its valid range";
+    case MOE_B200_ERR_INVALID_BLOCK_M: return "InvalidBlockM: block_m must be a positive integer";
+    case MOE_B200_ERR_SCHEDULE_MISMATCH: return "ScheduleMismatch: schedule does not tile offsets";
+    case MOE_B200_ERR_INVALID_VALUE: return "ValueError: invalid configuration value";
+    case MOE_B200_ERR_WORKSPACE: return "workspace too small or misaligned";
+    case MOE_B200_ERR_UNSUPPORTED: return "unsupported shape for the sm_100a path";
+    case MOE_B200_ERR_CUDA: return "CUDA error";
+    case MOE_B200_ERR_NCCL: return "NCCL error";
+    default: return "unknown status";
+  }
+}
+
+int moe_b200_workspace_size(const moe_b200_config* cfg, int64_t max_tokens, size_t* bytes) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (max_tokens < 0 || !bytes) return MOE_B200_ERR_INVALID_VALUE;
+  *bytes = layout_for(*cfg, max_tokens).total;
+  return MOE_B200_OK;
+}
+
+int moe_b200_workspace_init(const moe_b200_config* cfg, int64_t max_tokens, void* ws,
+                            size_t ws_bytes, void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (!ws || ws_bytes < kHeaderBytes) return MOE_B200_ERR_WORKSPACE;
+  (void)max_tokens;
+  MOE_CUDA(cudaMemsetAsync(ws, 0, kHeaderBytes, static_cast<cudaStream_t>(stream)));
+  return MOE_B200_OK;
+}
+
+int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws, size_t ws_bytes,
+                        uint32_t* flags, void* stream) {
+  (void)cfg; (void)max_tokens;
+  if (!ws || ws_bytes < kHeaderBytes || !flags) return MOE_B200_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  MOE_CUDA(cudaMemcpyAsync(flags, ws, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  MOE_CUDA(cudaMemsetAsync(ws, 0, sizeof(uint32_t), s));
+  MOE_CUDA(cudaStreamSynchronize(s));
+  return MOE_B200_OK;
+}
+
+int moe_b200_route(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
+                   const float* w_router, int32_t* topk_idx, float* topk_w, int32_t* counts,
+                   int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv, float* logits,
+                   void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (B < 0) return MOE_B200_ERR_SHAPE_MISMATCH;
+  if (x_dtype != MOE_B200_DTYPE_F32 && x_dtype != MOE_B200_DTYPE_BF16) return MOE_B200_ERR_INVALID_VALUE;
+  Layout L;
+  if ((rc = check_ws(cfg, B, ws, ws_bytes, &L))) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* hdr = reinterpret_cast<int32_t*>(ws);
+  if (B == 0) {
+    MOE_CUDA(cudaMemsetAsync(counts, 0, cfg->num_experts * sizeof(int32_t), s));
+    MOE_CUDA(cudaMemsetAsync(offsets, 0, (cfg->num_experts + 1) * sizeof(int32_t), s));
+    MOE_CUDA(cudaMemsetAsync(hdr + 2, 0, sizeof(int32_t), s));
+    return MOE_B200_OK;
+  }
+  if (!x || !w_router || !topk_idx || !topk_w || !counts || !offsets || !perm_fwd || !perm_inv)
+    return MOE_B200_ERR_INVALID_VALUE;
+  const int xb = x_dtype == MOE_B200_DTYPE_BF16;
+  RouterPlan plan = plan_router(*cfg, B, xb);
+  if (plan.n_tblocks > kTbCap) return MOE_B200_ERR_UNSUPPORTED;
+  RouterParams p{};
+  p.x = x; p.wr = w_router; p.x_bf16 = xb;
+  p.B = static_cast<int>(B); p.d = cfg->hidden_dim; p.E = cfg->num_experts; p.k = cfg->top_k;
+  p.gating = cfg->gating;
+  p.tokc = plan.tokc; p.expc = plan.expc; p.tg = plan.tg;
+  p.n_eblocks = plan.n_eblocks; p.n_tblocks = plan.n_tblocks;
+  p.chunk_rows = chunk_rows_for(*cfg, B);
+  p.logits = logits ? logits : reinterpret_cast<float*>(ws8(ws) + L.logits);
+  p.topk_idx = topk_idx; p.topk_w = topk_w; p.counts = counts; p.offsets = offsets;
+  p.fwd = perm_fwd; p.inv = perm_inv;
+  p.chunk_tab = reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab);
+  p.n_chunks = hdr + 2;
+  p.tb_counter = hdr + 16;
+  p.done_counter = hdr + 1;
+  p.flags = reinterpret_cast<uint32_t*>(hdr);
+  return xb ? launch_router_x<true>(p, plan, s) : launch_router_x<false>(p, plan, s);
+}
+
+int moe_b200_permute(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
+                     const int32_t* perm_fwd, void* xp, void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (B == 0) return MOE_B200_OK;
+  if (!x || !perm_fwd || !xp) return MOE_B200_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int T = static_cast<int>(B * cfg->top_k);
+  const int d = cfg->hidden_dim;
+  const int grid = grid_for_rows((long)T * (d / 8));
+  if (x_dtype == MOE_B200_DTYPE_BF16)
+    permute_kernel<true><<<grid, kRowThreads, 0, s>>>(x, perm_fwd, static_cast<__nv_bfloat16*>(xp), T, cfg->top_k, d);
+  else if (x_dtype == MOE_B200_DTYPE_F32)
+    permute_kernel<false><<<grid, kRowThreads, 0, s>>>(x, perm_fwd, static_cast<__nv_bfloat16*>(xp), T, cfg->top_k, d);
+  else
+    return MOE_B200_ERR_INVALID_VALUE;
+  MOE_LAUNCH_CHECK("permute_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_gate_up(const moe_b200_config* cfg, int64_t B, const void* xp, const void* w_gate,
+                     const void* w_up, void* h, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (B == 0) return MOE_B200_OK;
+  if (!xp || !w_gate || !w_up || !h) return MOE_B200_ERR_INVALID_VALUE;
+  Layout L;
+  if ((rc = check_ws(cfg, B, ws, ws_bytes, &L))) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int E = cfg->num_experts, d = cfg->hidden_dim, f = cfg->ffn_dim;
+  const int64_t T = B * cfg->top_k;
+  CUtensorMap ma0, ma1, mb;
+  if ((rc = make_map_bf16(&ma0, w_gate, (uint64_t)E * d, f, 64, 64))) return rc;
+  if ((rc = make_map_bf16(&ma1, w_up, (uint64_t)E * d, f, 64, 64))) return rc;
+  if ((rc = make_map_bf16(&mb, xp, T, d, 64, kBoxRows))) return rc;
+  GemmParams gp{};
+  gp.chunk_tab = reinterpret_cast<const int4*>(ws8(ws) + L.chunk_tab);
+  gp.n_chunks = reinterpret_cast<const int32_t*>(ws) + 2;
+  gp.n_mtiles = (f + kBM - 1) / kBM;
+  gp.K = d;
+  gp.out_features = f;
+  gp.h = static_cast<__nv_bfloat16*>(h);
+  const long max_tiles = (long)L.max_chunks * gp.n_mtiles;
+  const int grid = static_cast<int>(std::min<long>(kNumSMs, max_tiles));
+  if (chunk_rows_for(*cfg, B) == 256) return launch_gemm_t<256, true>(ma0, ma1, mb, gp, grid, s);
+  return launch_gemm_t<128, true>(ma0, ma1, mb, gp, grid, s);
+}
+
+int moe_b200_down_scatter(const moe_b200_config* cfg, int64_t B, const void* h, const void* w_down,
+                          const float* topk_w, const int32_t* perm_fwd, float* ys, void* ws,
+                          size_t ws_bytes, void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (B == 0) return MOE_B200_OK;
+  if (!h || !w_down || !topk_w || !perm_fwd || !ys) return MOE_B200_ERR_INVALID_VALUE;
+  Layout L;
+  if ((rc = check_ws(cfg, B, ws, ws_bytes, &L))) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int E = cfg->num_experts, d = cfg->hidden_dim, f = cfg->ffn_dim;
+  const int64_t T = B * cfg->top_k;
+  CUtensorMap ma0, mb;
+  if ((rc = make_map_bf16(&ma0, w_down, (uint64_t)E * f, d, 64, 64))) return rc;
+  if ((rc = make_map_bf16(&mb, h, T, f, 64, kBoxRows))) return rc;
+  GemmParams gp{};
+  gp.chunk_tab = reinterpret_cast<const int4*>(ws8(ws) + L.chunk_tab);
+  gp.n_chunks = reinterpret_cast<const int32_t*>(ws) + 2;
+  gp.n_mtiles = (d + kBM - 1) / kBM;
+  gp.K = f;
+  gp.out_features = d;
+  gp.ys = ys;
+  gp.topk_w = topk_w;
+  gp.fwd = perm_fwd;
+  const long max_tiles = (long)L.max_chunks * gp.n_mtiles;
+  const int grid = static_cast<int>(std::min<long>(kNumSMs, max_tiles));
+  if (chunk_rows_for(*cfg, B) == 256) return launch_gemm_t<256, false>(ma0, ma0, mb, gp, grid, s);
+  return launch_gemm_t<128, false>(ma0, ma0, mb, gp, grid, s);
+}
+
+int moe_b200_combine(const moe_b200_config* cfg, int64_t B, const float* ys, void* y, int y_dtype,
+                     void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (B == 0) return MOE_B200_OK;
+  if (!ys || !y) return MOE_B200_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int d = cfg->hidden_dim;
+  const int grid = grid_for_rows((long)B * (d / 4));
+  if (y_dtype == MOE_B200_DTYPE_F32)
+    combine_kernel<false><<<grid, kRowThreads, 0, s>>>(ys, y, (int)B, cfg->top_k, d);
+  else if (y_dtype == MOE_B200_DTYPE_BF16)
+    combine_kernel<true><<<grid, kRowThreads, 0, s>>>(ys, y, (int)B, cfg->top_k, d);
+  else
+    return MOE_B200_ERR_INVALID_VALUE;
+  MOE_LAUNCH_CHECK("combine_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_forward(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
+                     const float* w_router, const void* w_gate, const void* w_up,
+                     const void* w_down, void* y, int y_dtype, int32_t* topk_idx, float* topk_w,
+                     int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
+                     void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  Layout L;
+  if ((rc = check_ws(cfg, B, ws, ws_bytes, &L))) return rc;
+  if ((rc = moe_b200_route(cfg, B, x, x_dtype, w_router, topk_idx, topk_w, counts, offsets, perm_fwd,
+                           perm_inv, nullptr, ws, ws_bytes, stream)))
+    return rc;
+  if (B == 0) return MOE_B200_OK;
+  void* xp = ws8(ws) + L.xp;
+  void* h = ws8(ws) + L.h;
+  float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);
+  if ((rc = moe_b200_permute(cfg, B, x, x_dtype, perm_fwd, xp, stream))) return rc;
+  if ((rc = moe_b200_gate_up(cfg, B, xp, w_gate, w_up, h, ws, ws_bytes, stream))) return rc;
+  if ((rc = moe_b200_down_scatter(cfg, B, h, w_down, topk_w, perm_fwd, ys, ws, ws_bytes, stream)))
+    return rc;
+  return moe_b200_combine(cfg, B, ys, y, y_dtype, stream);
+}
+
+}  // extern "C"

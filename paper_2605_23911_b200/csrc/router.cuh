@@ -1,0 +1,543 @@
+// router.cuh — bit-exact router + scheduler, one launch.
+//
+// Reference semantics (cited per step):
+//   logits  = tokens @ W_r, fp64 exact products, ascending-k fold, one fp32
+//             rounding                          (linalg.py:45-57, router.py:131)
+//   softmax = fp32 max-subtract, fp64 exp, numpy pairwise fp64 row sum,
+//             fp64 divide, fp32 round           (router.py:78-83)
+//   sigmoid = float32 split-form logistic with numpy's SIMD expf
+//                                                 (linalg.py:71-80)
+//   top-k   = k rounds of argmax, lowest index on ties, -1.0 masking
+//             == k largest keys (score desc, index asc) (router.py:99-107)
+//   sigmoid renormalisation by the fp32 pairwise sum, 1/k on zero sum
+//                                                 (router.py:108-112)
+//   histogram / offsets / stable permutation    (scheduler.py:78-103)
+//   block schedule (device tile table)          (scheduler.py:106-117)
+//
+// Launch structure: grid = (token blocks) x (expert blocks).  Phase 1: every
+// CTA runs TOKC x EXPC sequential fp64 FMA chains (TG chains per thread for
+// ILP), staging x / W_r chunks through a cp.async ring and an fp64 smem
+// buffer.  Phase 2: the last CTA to finish a token block (atomic counter)
+// computes scores and top-k for it, one warp per token.  Phase 3: the last
+// token block to finish builds counts, offsets, the stable permutation and
+// the GEMM tile table in one CTA.  All counters self-reset.
+#pragma once
+
+#include "common.cuh"
+
+namespace moe {
+
+constexpr int kRouterThreads = 256;
+constexpr int kRouterKC = 64;      // k-chunk staged per pipeline step
+constexpr int kRouterStages = 4;   // cp.async ring depth
+constexpr int kMaxExperts = 1024;
+
+struct RouterParams {
+  const void* x;        // (B, d) fp32 or bf16
+  const float* wr;      // (d, E) fp32
+  int x_bf16;
+  int B, d, E, k, gating;
+  int tokc, expc, tg;   // CTA tile: tokc tokens x expc experts, tg chains per thread
+  int n_eblocks, n_tblocks;
+  int chunk_rows;       // GEMM row-chunk cap (BN)
+  float* logits;        // (B, E) fp32
+  int32_t* topk_idx;    // (B, k)
+  float* topk_w;        // (B, k)
+  int32_t* counts;      // (E)
+  int32_t* offsets;     // (E+1)
+  int32_t* fwd;         // (T)
+  int32_t* inv;         // (T)
+  int4* chunk_tab;      // (max_chunks) {expert, row0, nrows, 0}
+  int32_t* n_chunks;    // [1]
+  int32_t* tb_counter;  // (n_tblocks) self-resetting
+  int32_t* done_counter;// [1] self-resetting
+  uint32_t* flags;      // [1]
+};
+
+// ---------------------------------------------------------------------------
+// numpy-compatible pairwise sum (numpy loops_utils pairwise_sum; verified
+// against ndarray.sum in tests/test_host.py for every n used here).
+// ---------------------------------------------------------------------------
+template <typename T>
+MOE_DEVICE T pairwise_sum_block(const T* a, int n) {
+  // n <= 128
+  if (n < 8) {
+    T res = T(0);
+    for (int i = 0; i < n; ++i) res = res + a[i];
+    return res;
+  }
+  T r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+    r0 = r0 + a[i + 0]; r1 = r1 + a[i + 1]; r2 = r2 + a[i + 2]; r3 = r3 + a[i + 3];
+    r4 = r4 + a[i + 4]; r5 = r5 + a[i + 5]; r6 = r6 + a[i + 6]; r7 = r7 + a[i + 7];
+  }
+  T res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+  for (; i < n; ++i) res = res + a[i];
+  return res;
+}
+
+template <typename T>
+MOE_DEVICE T pairwise_sum(const T* a, int n) {
+  // Iterative form of numpy's recursion: n > 128 splits at n2 = n/2 - (n/2)%8.
+  // Depth is at most 3 for n <= 1024; an explicit stack keeps it non-recursive.
+  if (n <= 128) return pairwise_sum_block(a, n);
+  struct Frame { int lo, n, state; T left; };
+  Frame st[8];
+  int sp = 0;
+  st[0] = {0, n, 0, T(0)};
+  T ret = T(0);
+  while (sp >= 0) {
+    Frame& f = st[sp];
+    if (f.n <= 128) {
+      ret = pairwise_sum_block(a + f.lo, f.n);
+      --sp;
+      continue;
+    }
+    int n2 = f.n / 2;
+    n2 -= n2 % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      st[sp + 1] = {f.lo, n2, 0, T(0)};
+      ++sp;
+    } else if (f.state == 1) {
+      f.left = ret;
+      f.state = 2;
+      st[sp + 1] = {f.lo + n2, f.n - n2, 0, T(0)};
+      ++sp;
+    } else {
+      ret = f.left + ret;
+      --sp;
+    }
+  }
+  return ret;
+}
+
+// ---------------------------------------------------------------------------
+// numpy float32 exp (AVX512F/AVX2 SIMD kernel), reconstructed per SURVEY
+// Appendix A step 3 and checked against np.exp (tests).  Every operation is
+// an explicit round-to-nearest intrinsic so nvcc cannot contract it.
+// ---------------------------------------------------------------------------
+MOE_DEVICE float np_expf(float x) {
+  if (x <= -103.97208404541015625f) return 0.0f;
+  if (x >= 88.72283935546875f) return __int_as_float(0x7f800000);
+  float q = __fmul_rn(x, 1.442695040888963407359924681001892137f);
+  q = __fsub_rn(__fadd_rn(q, 0x1.8p+23f), 0x1.8p+23f);
+  float r = __fmaf_rn(q, -6.93145752e-1f, x);
+  r = __fmaf_rn(q, -1.42860677e-6f, r);
+  r = __fmaf_rn(q, 0.0f, r);
+  float num = __fmaf_rn(5.082762527590693718096e-04f, r, 6.757896990527504603057e-03f);
+  num = __fmaf_rn(num, r, 5.114512081637298353406e-02f);
+  num = __fmaf_rn(num, r, 2.473615434895520810817e-01f);
+  num = __fmaf_rn(num, r, 7.257664613233124478488e-01f);
+  num = __fmaf_rn(num, r, 9.999999999980870924916e-01f);
+  float den = __fmaf_rn(2.159509375685829852307e-02f, r, -2.742335390411667452936e-01f);
+  den = __fmaf_rn(den, r, 1.0f);
+  float p = __fdiv_rn(num, den);
+  // p * 2^q with a single rounding (scalef): exact in fp64, then one fp32 rounding.
+  return __double2float_rn(static_cast<double>(p) * ldexp(1.0, static_cast<int>(q)));
+}
+
+MOE_DEVICE float np_sigmoid(float x) {
+  float t = np_expf(-fabsf(x));
+  float den = __fadd_rn(1.0f, t);
+  return x >= 0.0f ? __fdiv_rn(1.0f, den) : __fdiv_rn(t, den);
+}
+
+// ---------------------------------------------------------------------------
+// Warp helpers
+// ---------------------------------------------------------------------------
+MOE_DEVICE uint64_t shfl_xor_u64(uint64_t v, int m) {
+  uint32_t lo = __shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(v), m);
+  uint32_t hi = __shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(v >> 32), m);
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+MOE_DEVICE void cp_async_16(void* smem, const void* gmem, bool valid) {
+  uint32_t s = smem_u32(smem);
+  int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(sz)
+               : "memory");
+}
+MOE_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+MOE_DEVICE void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Shared-memory carve-up for phase 1
+// ---------------------------------------------------------------------------
+struct RouterSmem {
+  // raw ring: stages x {x chunk (tokc x KC elems of x dtype), wr chunk (KC x expc fp32)}
+  // f64 double buffer: {x (tokc x (KC+1)), wr (KC x expc)}
+  static __host__ __device__ size_t raw_x_bytes(int tokc, int xb) { return (size_t)tokc * kRouterKC * xb; }
+  static __host__ __device__ size_t raw_w_bytes(int expc) {
+    // rounded so each stage stays 16-byte aligned
+    return ((size_t)kRouterKC * expc * 4 + 15) / 16 * 16;
+  }
+  static __host__ __device__ size_t raw_stage_bytes(int tokc, int expc, int xb) {
+    return raw_x_bytes(tokc, xb) + raw_w_bytes(expc);
+  }
+  static __host__ __device__ size_t f64_x_elems(int tokc) { return (size_t)tokc * (kRouterKC + 1); }
+  static __host__ __device__ size_t f64_w_elems(int expc) { return (size_t)kRouterKC * expc; }
+  static __host__ __device__ size_t total_bytes(int tokc, int expc, int xb, int E) {
+    size_t ph1 = kRouterStages * raw_stage_bytes(tokc, expc, xb) +
+                 2 * (f64_x_elems(tokc) + f64_w_elems(expc)) * sizeof(double);
+    // phase 2: one fp64 row of E per warp; phase 3: 8 x E ints + scan scratch
+    size_t ph2 = (size_t)(kRouterThreads / 32) * E * sizeof(double);
+    size_t ph3 = ((size_t)(kRouterThreads / 32) + 4) * E * sizeof(int32_t) + 256;
+    size_t m = ph1 > ph2 ? ph1 : ph2;
+    return m > ph3 ? m : ph3;
+  }
+};
+
+// Issue the cp.async copies of k-chunk `c` into ring slot `slot`.
+template <bool kXBf16>
+MOE_DEVICE void router_issue_chunk(const RouterParams& p, uint8_t* raw, int slot, int c, int t0,
+                                   int e0, int tid) {
+  const int xb = kXBf16 ? 2 : 4;
+  uint8_t* sx = raw + (size_t)slot * RouterSmem::raw_stage_bytes(p.tokc, p.expc, xb);
+  uint8_t* sw = sx + RouterSmem::raw_x_bytes(p.tokc, xb);
+  const int k0 = c * kRouterKC;
+  // x: tokc rows x (KC*xb) bytes, 16-byte pieces
+  const int x_pieces_per_row = kRouterKC * xb / 16;
+  const int x_pieces = p.tokc * x_pieces_per_row;
+  const uint8_t* xg = static_cast<const uint8_t*>(p.x);
+  for (int i = tid; i < x_pieces; i += kRouterThreads) {
+    int row = i / x_pieces_per_row, pc = i % x_pieces_per_row;
+    int t = t0 + row;
+    int kk = k0 + pc * (16 / xb);
+    bool valid = (t < p.B) && (kk < p.d);
+    const uint8_t* src = valid ? xg + ((size_t)t * p.d + kk) * xb : xg;
+    cp_async_16(sx + (size_t)i * 16, src, valid);
+  }
+  // wr: KC rows x expc fp32.  Rows are E-contiguous in global; the expert
+  // slice [e0, e0+expc) is 16-byte aligned only when E % 4 == 0, so fall back
+  // to 4-byte copies otherwise.
+  if ((p.E % 4) == 0 && (p.expc % 4) == 0) {
+    const int w_pieces_per_row = p.expc / 4;
+    const int w_pieces = kRouterKC * w_pieces_per_row;
+    for (int i = tid; i < w_pieces; i += kRouterThreads) {
+      int kr = i / w_pieces_per_row, pc = i % w_pieces_per_row;
+      int kk = k0 + kr;
+      int e = e0 + pc * 4;
+      bool valid = (kk < p.d) && (e < p.E);
+      const float* src = valid ? p.wr + (size_t)kk * p.E + e : p.wr;
+      cp_async_16(sw + (size_t)(kr * p.expc + pc * 4) * 4, src, valid);
+    }
+  } else {
+    float* swf = reinterpret_cast<float*>(sw);
+    for (int i = tid; i < kRouterKC * p.expc; i += kRouterThreads) {
+      int kr = i / p.expc, el = i % p.expc;
+      int kk = k0 + kr, e = e0 + el;
+      swf[i] = (kk < p.d && e < p.E) ? __ldg(p.wr + (size_t)kk * p.E + e) : 0.0f;
+    }
+  }
+}
+
+template <bool kXBf16, int kTG>
+__global__ void __launch_bounds__(kRouterThreads)
+router_kernel(const RouterParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x;
+  const int tb = blockIdx.x / p.n_eblocks;
+  const int eb = blockIdx.x % p.n_eblocks;
+  const int t0 = tb * p.tokc;
+  const int e0 = eb * p.expc;
+  const int xb = kXBf16 ? 2 : 4;
+
+  // ------------------------------- phase 1: logits ---------------------------
+  uint8_t* raw = smem;
+  const size_t raw_total = kRouterStages * RouterSmem::raw_stage_bytes(p.tokc, p.expc, xb);
+  double* f64 = reinterpret_cast<double*>(smem + raw_total);
+  const size_t fx = RouterSmem::f64_x_elems(p.tokc), fw = RouterSmem::f64_w_elems(p.expc);
+
+  const int el = tid % p.expc;        // expert lane
+  const int tgi = tid / p.expc;       // token group
+  const int n_groups = kRouterThreads / p.expc;
+  const bool active = (tgi < n_groups) && (e0 + el < p.E);
+  double acc[kTG];
+#pragma unroll
+  for (int i = 0; i < kTG; ++i) acc[i] = -0.0;  // fma(a,b,-0) == a*b exactly, sign included
+  bool nonfinite_x = false, nonfinite_w = false;
+
+  const int nch = (p.d + kRouterKC - 1) / kRouterKC;
+#pragma unroll 1
+  for (int s = 0; s < kRouterStages - 1; ++s) {
+    if (s < nch) router_issue_chunk<kXBf16>(p, raw, s, s, t0, e0, tid);
+    cp_async_commit();
+  }
+#pragma unroll 1
+  for (int c = 0; c < nch; ++c) {
+    cp_async_wait<kRouterStages - 2>();
+    __syncthreads();
+    // convert raw chunk c -> fp64 buffer (c & 1), checking finiteness
+    {
+      const uint8_t* sx = raw + (size_t)(c % kRouterStages) * RouterSmem::raw_stage_bytes(p.tokc, p.expc, xb);
+      const float* sw = reinterpret_cast<const float*>(sx + RouterSmem::raw_x_bytes(p.tokc, xb));
+      double* dx = f64 + (size_t)(c & 1) * (fx + fw);
+      double* dw = dx + fx;
+      const int kvalid = min(kRouterKC, p.d - c * kRouterKC);
+      for (int i = tid; i < p.tokc * kRouterKC; i += kRouterThreads) {
+        int row = i / kRouterKC, kk = i % kRouterKC;
+        float v;
+        if (kXBf16) {
+          v = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(sx)[i]);
+        } else {
+          v = reinterpret_cast<const float*>(sx)[i];
+        }
+        if (kk < kvalid && t0 + row < p.B && !isfinite(v)) nonfinite_x = true;
+        dx[row * (kRouterKC + 1) + kk] = static_cast<double>(v);
+      }
+      for (int i = tid; i < kRouterKC * p.expc; i += kRouterThreads) {
+        float v = sw[i];
+        int kk = i / p.expc, e = i % p.expc;
+        if (kk < kvalid && e0 + e < p.E && !isfinite(v)) nonfinite_w = true;
+        dw[i] = static_cast<double>(v);
+      }
+    }
+    // refill the ring slot freed by chunk c-1
+    {
+      int nc = c + kRouterStages - 1;
+      if (nc < nch) router_issue_chunk<kXBf16>(p, raw, nc % kRouterStages, nc, t0, e0, tid);
+      cp_async_commit();
+    }
+    __syncthreads();
+    if (active) {
+      const double* dx = f64 + (size_t)(c & 1) * (fx + fw);
+      const double* dw = dx + fx;
+      const int kvalid = min(kRouterKC, p.d - c * kRouterKC);
+      const double* xr = dx + (size_t)(tgi * kTG) * (kRouterKC + 1);
+      if (kvalid == kRouterKC) {
+#pragma unroll 8
+        for (int kk = 0; kk < kRouterKC; ++kk) {
+          double w = dw[kk * p.expc + el];
+#pragma unroll
+          for (int i = 0; i < kTG; ++i) acc[i] = __fma_rn(xr[i * (kRouterKC + 1) + kk], w, acc[i]);
+        }
+      } else {
+        for (int kk = 0; kk < kvalid; ++kk) {
+          double w = dw[kk * p.expc + el];
+#pragma unroll
+          for (int i = 0; i < kTG; ++i) acc[i] = __fma_rn(xr[i * (kRouterKC + 1) + kk], w, acc[i]);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (nonfinite_x) atomicOr(p.flags, 1u);
+  if (nonfinite_w) atomicOr(p.flags, 2u);
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < kTG; ++i) {
+      int t = t0 + tgi * kTG + i;
+      if (t < p.B) p.logits[(size_t)t * p.E + e0 + el] = __double2float_rn(acc[i]);
+    }
+  }
+
+  // --------------------- phase 2: scores + top-k (last CTA of block) --------
+  __shared__ int s_flag;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    int prev = atomicAdd(p.tb_counter + tb, 1);
+    s_flag = (prev == p.n_eblocks - 1);
+  }
+  __syncthreads();
+  if (!s_flag) return;
+  __threadfence();
+
+  {
+    const int warp = tid / 32, lane = tid % 32;
+    double* row = reinterpret_cast<double*>(smem) + (size_t)warp * p.E;
+    const int tend = min(t0 + p.tokc, p.B);
+    for (int t = t0 + warp; t < tend; t += kRouterThreads / 32) {
+      const float* lg = p.logits + (size_t)t * p.E;
+      // scores -> row (as double for softmax, float bits stored in double for sigmoid)
+      if (p.gating == 0) {
+        float m = -__int_as_float(0x7f800000);
+        for (int e = lane; e < p.E; e += 32) m = fmaxf(m, __ldcg(lg + e));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        for (int e = lane; e < p.E; e += 32) {
+          float s = __fsub_rn(__ldcg(lg + e), m);
+          row[e] = exp(static_cast<double>(s));
+        }
+        __syncwarp();
+        double S = 0.0;
+        if (lane == 0) S = pairwise_sum<double>(row, p.E);
+        S = __shfl_sync(0xffffffffu, S, 0);
+        __syncwarp();
+        for (int e = lane; e < p.E; e += 32) {
+          float sc = __double2float_rn(__ddiv_rn(row[e], S));
+          row[e] = static_cast<double>(sc);
+        }
+      } else {
+        for (int e = lane; e < p.E; e += 32) row[e] = static_cast<double>(np_sigmoid(__ldcg(lg + e)));
+      }
+      __syncwarp();
+      // top-k over keys (score bits desc, index asc); scores are >= +0.
+      float wsel = 0.0f;
+      int isel = 0;
+      for (int j = 0; j < p.k; ++j) {
+        uint64_t best = 0;
+        for (int e = lane; e < p.E; e += 32) {
+          float sc = static_cast<float>(row[e]);
+          if (sc < 0.0f) continue;  // already selected (marked -1)
+          uint32_t bits = (sc == 0.0f) ? 0u : __float_as_uint(sc);
+          uint64_t key = (static_cast<uint64_t>(bits) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(e));
+          best = key > best ? key : best;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          uint64_t other = shfl_xor_u64(best, o);
+          best = other > best ? other : best;
+        }
+        int e_best = static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFu));
+        float s_best = __uint_as_float(static_cast<uint32_t>(best >> 32));
+        __syncwarp();
+        if (lane == (e_best & 31)) row[e_best] = -1.0;
+        __syncwarp();
+        if (lane == j) { wsel = s_best; isel = e_best; }
+        if (j >= 32) {  // k > 32: write directly (rare)
+          if (lane == 0) {
+            p.topk_idx[(size_t)t * p.k + j] = e_best;
+            p.topk_w[(size_t)t * p.k + j] = s_best;
+          }
+        }
+      }
+      __syncwarp();
+      if (p.gating == 1) {
+        // renormalise over the selected k with numpy's fp32 pairwise sum
+        float* wrow = reinterpret_cast<float*>(row);
+        if (lane < p.k && lane < 32) wrow[lane] = wsel;
+        __syncwarp();
+        if (p.k > 32 && lane == 0) {
+          for (int j = 32; j < p.k; ++j) wrow[j] = p.topk_w[(size_t)t * p.k + j];
+        }
+        __syncwarp();
+        float S = 0.0f;
+        if (lane == 0) S = pairwise_sum<float>(wrow, p.k);
+        S = __shfl_sync(0xffffffffu, S, 0);
+        const float uni = __double2float_rn(1.0 / static_cast<double>(p.k));
+        if (lane < p.k) wsel = (S == 0.0f) ? uni : __fdiv_rn(wsel, S);
+        if (p.k > 32 && lane == 0) {
+          for (int j = 32; j < p.k; ++j) {
+            float v = wrow[j];
+            p.topk_w[(size_t)t * p.k + j] = (S == 0.0f) ? uni : __fdiv_rn(v, S);
+          }
+        }
+        __syncwarp();
+      }
+      if (lane < p.k) {
+        p.topk_idx[(size_t)t * p.k + lane] = isel;
+        p.topk_w[(size_t)t * p.k + lane] = wsel;
+      }
+      __syncwarp();
+    }
+  }
+
+  // -------------------- phase 3: scheduler (last token block) ---------------
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    p.tb_counter[tb] = 0;  // every CTA of this block has arrived: reset for the next launch
+    int prev = atomicAdd(p.done_counter, 1);
+    s_flag = (prev == p.n_tblocks - 1);
+  }
+  __syncthreads();
+  if (!s_flag) return;
+  __threadfence();
+
+  {
+    const int nw = kRouterThreads / 32;
+    const int warp = tid / 32, lane = tid % 32;
+    const int T = p.B * p.k;
+    const int E = p.E;
+    int32_t* hist = reinterpret_cast<int32_t*>(smem);       // [nw][E] -> per-warp base
+    int32_t* s_cnt = hist + (size_t)nw * E;                  // [E]
+    int32_t* s_off = s_cnt + E;                              // [E+1]
+    int32_t* s_cpre = s_off + E + 1;                         // [E+1] chunk prefix
+    for (int i = tid; i < nw * E; i += kRouterThreads) hist[i] = 0;
+    __syncthreads();
+    const int seg = (T + nw - 1) / nw;
+    const int s0 = warp * seg, s1 = min(T, s0 + seg);
+    for (int i = s0 + lane; i < s1; i += 32) atomicAdd(&hist[warp * E + __ldcg(p.topk_idx + i)], 1);
+    __syncthreads();
+    // per-expert totals and per-warp exclusive bases
+    for (int e = tid; e < E; e += kRouterThreads) {
+      int run = 0;
+      for (int w = 0; w < nw; ++w) {
+        int h = hist[w * E + e];
+        hist[w * E + e] = run;
+        run += h;
+      }
+      s_cnt[e] = run;
+    }
+    __syncthreads();
+    // warp 0: exclusive scans of counts and of chunk counts
+    if (warp == 0) {
+      const int per = (E + 31) / 32;
+      const int lo = lane * per, hi = min(E, lo + per);
+      int sum_c = 0, sum_ch = 0;
+      for (int e = lo; e < hi; ++e) {
+        sum_c += s_cnt[e];
+        sum_ch += (s_cnt[e] + p.chunk_rows - 1) / p.chunk_rows;
+      }
+      int inc_c = sum_c, inc_ch = sum_ch;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int a = __shfl_up_sync(0xffffffffu, inc_c, o);
+        int b = __shfl_up_sync(0xffffffffu, inc_ch, o);
+        if (lane >= o) { inc_c += a; inc_ch += b; }
+      }
+      int run_c = inc_c - sum_c, run_ch = inc_ch - sum_ch;
+      for (int e = lo; e < hi; ++e) {
+        s_off[e] = run_c;
+        s_cpre[e] = run_ch;
+        run_c += s_cnt[e];
+        run_ch += (s_cnt[e] + p.chunk_rows - 1) / p.chunk_rows;
+      }
+      if (lane == 31) {
+        s_off[E] = inc_c;
+        s_cpre[E] = inc_ch;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < E; e += kRouterThreads) {
+      p.counts[e] = s_cnt[e];
+      p.offsets[e] = s_off[e];
+      const int n_e = s_cnt[e];
+      const int nchunk = (n_e + p.chunk_rows - 1) / p.chunk_rows;
+      for (int c = 0; c < nchunk; ++c) {
+        int r0 = c * p.chunk_rows;
+        p.chunk_tab[s_cpre[e] + c] = make_int4(e, s_off[e] + r0, min(p.chunk_rows, n_e - r0), 0);
+      }
+    }
+    if (tid == 0) {
+      p.offsets[E] = s_off[E];
+      p.n_chunks[0] = s_cpre[E];
+    }
+    // stable counting sort: warp w walks its segment in id order
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int base = s0; base < s1; base += 32) {
+      int i = base + lane;
+      bool valid = i < s1;
+      int e = valid ? __ldcg(p.topk_idx + i) : -1 - lane;  // unique sentinel per invalid lane
+      uint32_t peers = __match_any_sync(0xffffffffu, e);
+      if (valid) {
+        int rank = __popc(peers & lt_mask);
+        int pos = s_off[e] + hist[warp * E + e] + rank;
+        p.fwd[pos] = i;
+        p.inv[i] = pos;
+      }
+      __syncwarp();
+      if (valid && (__ffs(peers) - 1) == static_cast<int>(lane)) hist[warp * E + e] += __popc(peers);
+      __syncwarp();
+    }
+    if (tid == 0) *p.done_counter = 0;
+  }
+}
+
+}  // namespace moe

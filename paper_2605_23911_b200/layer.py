@@ -1,0 +1,338 @@
+"""Device-side MoE layer over the C-ABI, and the reference-compatible drop-in.
+
+``MoELayer`` owns the uploaded bf16 expert weights, the fp32 router weight,
+the routing buffers and the workspace, and runs the whole layer as ONE C-ABI
+call (five sm_100a launches, no host synchronisation, CUDA-graph
+capturable).  ``moe_forward`` / ``route`` mirror the reference functions
+(``moeperf/pipeline.py:572-615``, ``moeperf/router.py:116-133``) — same
+signature, same exception classes — and return numpy when given numpy.
+
+PyTorch is used only for device memory and the current CUDA stream; all
+arithmetic runs in libmoe_b200.so.  A missing library raises; there is no
+CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import NonFiniteInput, ShapeMismatch
+from .trace import PipelineTrace, trace_from_counts
+from .types import GATING_CODE, ExpertWeights, ModelConfig, PipelineParams, RoutingResult
+
+
+def _round8(n: int) -> int:
+    return (n + 7) // 8 * 8
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def _as_tensor(a, device, dtype=None) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        t = a
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(a)))
+    if dtype is not None and t.dtype != dtype:
+        t = t.to(dtype)
+    return t.to(device, non_blocking=True).contiguous()
+
+
+@dataclass
+class DeviceExpertWeights:
+    """Expert weights resident in HBM as bf16, reference stacked layout.
+
+    ``gate``/``up`` (E*d_pad, f_pad), ``down`` (E*f_pad, d_pad); d and f are
+    zero-padded to multiples of 8 (16-byte TMA pitch) when needed, which
+    leaves every product unchanged.
+    """
+
+    config: ModelConfig
+    hidden_pad: int
+    ffn_pad: int
+    gate: torch.Tensor
+    up: torch.Tensor
+    down: torch.Tensor
+
+    @property
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.gate, self.up, self.down))
+
+
+def _pad_stack(w: torch.Tensor, E: int, rows: int, cols: int, rows_pad: int, cols_pad: int) -> torch.Tensor:
+    if rows == rows_pad and cols == cols_pad:
+        return w.contiguous()
+    out = torch.zeros((E, rows_pad, cols_pad), dtype=w.dtype, device=w.device)
+    out[:, :rows, :cols] = w.reshape(E, rows, cols)
+    return out.reshape(E * rows_pad, cols_pad)
+
+
+def upload_weights(weights, config: ModelConfig, device=None, check_finite: bool = True) -> DeviceExpertWeights:
+    """Validate and upload ExpertWeights to the GPU as bf16 (one-time cost).
+
+    Mirrors the reference's per-call checks (``pipeline.py:585-589``:
+    ``weights.validate`` + ``require_finite`` on every stack), done once here.
+    """
+    if isinstance(weights, DeviceExpertWeights):
+        return weights
+    device = torch.device(device or "cuda")
+    weights.validate(config)
+    E, d, f = config.num_experts, config.hidden_dim, config.ffn_dim
+    dp, fp = _round8(d), _round8(f)
+    out = {}
+    for name, rows, cols, rp, cp in (("gate", d, f, dp, fp), ("up", d, f, dp, fp), ("down", f, d, fp, dp)):
+        t = _as_tensor(getattr(weights, name), device)
+        if check_finite and t.numel() and not bool(torch.isfinite(t).all()):
+            raise NonFiniteInput(f"{name} weights contains non-finite values")
+        t = t.to(torch.bfloat16)
+        out[name] = _pad_stack(t, E, rows, cols, rp, cp)
+    return DeviceExpertWeights(config=config, hidden_pad=dp, ffn_pad=fp, **out)
+
+
+class MoELayer:
+    """One MoE layer on one B200: route → permute → gate+up → down → combine."""
+
+    def __init__(self, config: ModelConfig, weights, router_weight, max_tokens: int,
+                 device=None, out_dtype=torch.float32):
+        self.lib = _lib.load()
+        self.device = torch.device(device or "cuda")
+        self.config = config
+        self.weights = upload_weights(weights, config, self.device)
+        self.d, self.f = config.hidden_dim, config.ffn_dim
+        self.dp, self.fp = self.weights.hidden_pad, self.weights.ffn_pad
+        self.E, self.k = config.num_experts, config.top_k
+        self.cfg = _lib.config_struct(self.E, self.k, self.dp, self.fp, GATING_CODE[Gating(config.gating)])
+        self.out_dtype = out_dtype
+        self.max_tokens = int(max_tokens)
+        self.set_router_weight(router_weight)
+        n = ctypes.c_size_t(0)
+        _lib.check(self.lib.moe_b200_workspace_size(ctypes.byref(self.cfg), max(self.max_tokens, 1), ctypes.byref(n)),
+                   "workspace_size")
+        self.ws_bytes = int(n.value)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        _lib.check(self.lib.moe_b200_workspace_init(ctypes.byref(self.cfg), self.max_tokens, _ptr(self.ws),
+                                                    self.ws_bytes, _stream_ptr(self.device)), "workspace_init")
+        B, T = self.max_tokens, self.max_tokens * self.k
+        dev = self.device
+        self.topk_idx = torch.empty((B, self.k), dtype=torch.int32, device=dev)
+        self.topk_w = torch.empty((B, self.k), dtype=torch.float32, device=dev)
+        self.counts = torch.empty(self.E, dtype=torch.int32, device=dev)
+        self.offsets = torch.empty(self.E + 1, dtype=torch.int32, device=dev)
+        self.fwd = torch.empty(T, dtype=torch.int32, device=dev)
+        self.inv = torch.empty(T, dtype=torch.int32, device=dev)
+
+    # -- inputs ---------------------------------------------------------------
+    def set_router_weight(self, router_weight) -> None:
+        wr = _as_tensor(router_weight, self.device, torch.float32)
+        if tuple(wr.shape) != (self.d, self.E):
+            raise ShapeMismatch(f"router weight is {tuple(wr.shape)}, expected ({self.d}, {self.E})")
+        if self.dp != self.d:
+            wr = torch.nn.functional.pad(wr, (0, 0, 0, self.dp - self.d))
+        self.router_weight = wr.contiguous()
+
+    def _prep_x(self, x: torch.Tensor):
+        if x.dim() != 2 or x.shape[1] != self.d:
+            raise ShapeMismatch(f"tokens are {tuple(x.shape)}, expected (B, {self.d})")
+        if x.shape[0] > self.max_tokens:
+            raise ShapeMismatch(f"{x.shape[0]} tokens exceed the layer's max_tokens={self.max_tokens}")
+        if x.dtype not in (torch.float32, torch.bfloat16):
+            x = x.float()
+        if self.dp != self.d:
+            x = torch.nn.functional.pad(x, (0, self.dp - self.d))
+        x = x.contiguous()
+        return x, (_lib.DTYPE_BF16 if x.dtype == torch.bfloat16 else _lib.DTYPE_F32)
+
+    # -- whole layer ------------------------------------------------------------
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """y = MoE(x) on the current stream; asynchronous, graph-capturable."""
+        x, xdt = self._prep_x(x)
+        B = x.shape[0]
+        if out is None:
+            out = torch.empty((B, self.dp), dtype=self.out_dtype, device=self.device)
+        ydt = _lib.DTYPE_BF16 if out.dtype == torch.bfloat16 else _lib.DTYPE_F32
+        rc = self.lib.moe_b200_forward(
+            ctypes.byref(self.cfg), B, _ptr(x), xdt, _ptr(self.router_weight),
+            _ptr(self.weights.gate), _ptr(self.weights.up), _ptr(self.weights.down),
+            _ptr(out), ydt, _ptr(self.topk_idx), _ptr(self.topk_w), _ptr(self.counts), _ptr(self.offsets),
+            _ptr(self.fwd), _ptr(self.inv), _ptr(self.ws), self.ws_bytes, _stream_ptr(self.device))
+        _lib.check(rc, "moe_b200_forward")
+        return out if self.dp == self.d else out[:, : self.d]
+
+    __call__ = forward
+
+    def read_flags(self) -> int:
+        """Device non-finite flags (synchronises); clears them."""
+        v = ctypes.c_uint32(0)
+        _lib.check(self.lib.moe_b200_read_flags(ctypes.byref(self.cfg), self.max_tokens, _ptr(self.ws),
+                                                self.ws_bytes, ctypes.byref(v), _stream_ptr(self.device)),
+                   "read_flags")
+        return int(v.value)
+
+    def raise_if_nonfinite(self) -> None:
+        flags = self.read_flags()
+        if flags & 1:
+            raise NonFiniteInput("tokens contains non-finite values")
+        if flags & 2:
+            raise NonFiniteInput("router_weight contains non-finite values")
+
+    # -- stage-level entry points (parity tests, reference stage API) ----------
+    def route(self, x: torch.Tensor, logits: bool = False) -> dict:
+        x, xdt = self._prep_x(x)
+        B = x.shape[0]
+        lg = torch.empty((B, self.E), dtype=torch.float32, device=self.device) if logits else None
+        rc = self.lib.moe_b200_route(
+            ctypes.byref(self.cfg), B, _ptr(x), xdt, _ptr(self.router_weight), _ptr(self.topk_idx),
+            _ptr(self.topk_w), _ptr(self.counts), _ptr(self.offsets), _ptr(self.fwd), _ptr(self.inv),
+            _ptr(lg), _ptr(self.ws), self.ws_bytes, _stream_ptr(self.device))
+        _lib.check(rc, "moe_b200_route")
+        T = B * self.k
+        res = dict(indices=self.topk_idx[:B], weights=self.topk_w[:B], counts=self.counts,
+                   offsets=self.offsets, forward=self.fwd[:T], inverse=self.inv[:T])
+        if logits:
+            res["logits"] = lg
+        return res
+
+    def run_stages(self, x: torch.Tensor) -> dict:
+        """Route, then each stage as its own C-ABI call, keeping every intermediate."""
+        r = self.route(x, logits=True)
+        x, xdt = self._prep_x(x)
+        B, T = x.shape[0], x.shape[0] * self.k
+        dev, s = self.device, _stream_ptr(self.device)
+        xp = torch.empty((T, self.dp), dtype=torch.bfloat16, device=dev)
+        h = torch.empty((T, self.fp), dtype=torch.bfloat16, device=dev)
+        ys = torch.empty((T, self.dp), dtype=torch.float32, device=dev)
+        y = torch.empty((B, self.dp), dtype=self.out_dtype, device=dev)
+        cfg = ctypes.byref(self.cfg)
+        _lib.check(self.lib.moe_b200_permute(cfg, B, _ptr(x), xdt, _ptr(self.fwd), _ptr(xp), s), "permute")
+        _lib.check(self.lib.moe_b200_gate_up(cfg, B, _ptr(xp), _ptr(self.weights.gate), _ptr(self.weights.up),
+                                             _ptr(h), _ptr(self.ws), self.ws_bytes, s), "gate_up")
+        _lib.check(self.lib.moe_b200_down_scatter(cfg, B, _ptr(h), _ptr(self.weights.down), _ptr(self.topk_w),
+                                                  _ptr(self.fwd), _ptr(ys), _ptr(self.ws), self.ws_bytes, s),
+                   "down_scatter")
+        ydt = _lib.DTYPE_BF16 if y.dtype == torch.bfloat16 else _lib.DTYPE_F32
+        _lib.check(self.lib.moe_b200_combine(cfg, B, _ptr(ys), _ptr(y), ydt, s), "combine")
+        r.update(permuted=xp[:, : self.d], h=h[:, : self.f], expert_out=ys[:, : self.d], y=y[:, : self.d])
+        return r
+
+
+from .types import Gating  # noqa: E402  (used in MoELayer.__init__)
+
+# ---------------------------------------------------------------------------
+# Reference-compatible drop-in functions
+# ---------------------------------------------------------------------------
+_LAYER_CACHE: dict = {}  # id(weights) -> (weakref to weights, MoELayer); small LRU
+_LAYER_CACHE_MAX = 4
+
+
+def _to_2d(a, name: str):
+    shape = tuple(a.shape) if hasattr(a, "shape") else np.asarray(a).shape
+    if len(shape) != 2:
+        raise ShapeMismatch(f"{name} must be 2-D, got shape {shape}")
+    return a
+
+
+def _layer_for(weights, config: ModelConfig, router_weight, batch: int) -> MoELayer:
+    key = id(weights)
+    entry = _LAYER_CACHE.get(key)
+    if entry is not None:
+        ref, layer = entry
+        if ref() is weights and layer.config == config and layer.max_tokens >= batch:
+            layer.set_router_weight(router_weight)
+            return layer
+    layer = MoELayer(config, weights, router_weight, max_tokens=max(batch, 1))
+    if len(_LAYER_CACHE) >= _LAYER_CACHE_MAX:
+        _LAYER_CACHE.pop(next(iter(_LAYER_CACHE)))
+    _LAYER_CACHE[key] = (weakref.ref(weights), layer)
+    return layer
+
+
+def _finish(t: torch.Tensor, like_numpy: bool):
+    return t.cpu().numpy() if like_numpy else t
+
+
+def moe_forward(tokens, router_weight, weights, config: ModelConfig,
+                params: PipelineParams = PipelineParams()):
+    """Drop-in for ``moeperf.pipeline.moe_forward`` (``pipeline.py:572-615``).
+
+    Returns ``(y, trace)``: y (B, d) fp32 (numpy if ``tokens`` is numpy, else a
+    CUDA tensor) and the six-record ``PipelineTrace`` replayed from the device
+    histogram.  Synchronises once (to read the histogram and the device
+    non-finite flags, as the reference raises ``NonFiniteInput``).
+    """
+    like_numpy = not isinstance(tokens, torch.Tensor)
+    _to_2d(tokens, "tokens")
+    if not isinstance(weights, DeviceExpertWeights):
+        weights.validate(config)
+    _to_2d(router_weight, "router_weight")
+    if tuple(router_weight.shape) != (config.hidden_dim, config.num_experts):
+        raise ShapeMismatch(
+            f"router weight is {tuple(router_weight.shape)}, expected ({config.hidden_dim}, {config.num_experts})")
+    if tokens.shape[1] != config.hidden_dim:
+        raise ShapeMismatch(f"tokens are {tuple(tokens.shape)}, expected hidden dim {config.hidden_dim}")
+    B = int(tokens.shape[0])
+    layer = _layer_for(weights, config, router_weight, B)
+    x = _as_tensor(tokens, layer.device)
+    if B == 0:
+        y = torch.zeros((0, config.hidden_dim), dtype=torch.float32, device=layer.device)
+        return _finish(y, like_numpy), trace_from_counts(config, 0, np.zeros(config.num_experts, np.int64), params)
+    y = layer.forward(x)
+    counts = layer.counts.cpu().numpy().astype(np.int64)
+    layer.raise_if_nonfinite()
+    trace = trace_from_counts(config, B, counts, params)
+    return _finish(y, like_numpy), trace
+
+
+def route(tokens, router_weight, config: ModelConfig) -> RoutingResult:
+    """Drop-in for ``moeperf.router.route`` (``router.py:116-133``), bit-exact.
+
+    Indices are returned as int64 like the reference.
+    """
+    like_numpy = not isinstance(tokens, torch.Tensor)
+    _to_2d(tokens, "tokens")
+    _to_2d(router_weight, "router_weight")
+    if tokens.shape[1] != config.hidden_dim:
+        raise ShapeMismatch(f"tokens are {tuple(tokens.shape)}, expected hidden dim {config.hidden_dim}")
+    if tuple(router_weight.shape) != (config.hidden_dim, config.num_experts):
+        raise ShapeMismatch(
+            f"router weight is {tuple(router_weight.shape)}, expected ({config.hidden_dim}, {config.num_experts})")
+    B = int(tokens.shape[0])
+    k = config.top_k
+    if B == 0:
+        idx = np.zeros((0, k), np.int64)
+        w = np.zeros((0, k), np.float32)
+        return RoutingResult(indices=idx, weights=w)
+    small = ModelConfig(config.num_experts, k, config.hidden_dim, 8, config.gating)
+    layer = _layer_for(_router_only_weights(small), small, router_weight, B)
+    r = layer.route(_as_tensor(tokens, layer.device))
+    layer.raise_if_nonfinite()
+    idx = r["indices"].to(torch.int64)
+    w = r["weights"].clone()
+    if like_numpy:
+        return RoutingResult(indices=idx.cpu().numpy(), weights=w.cpu().numpy())
+    return RoutingResult(indices=idx, weights=w)
+
+
+_ROUTER_ONLY: dict = {}
+
+
+def _router_only_weights(small: ModelConfig) -> ExpertWeights:
+    """Placeholder zero expert stacks (f = 8) so a router-only layer can be built."""
+    key = (small.num_experts, small.hidden_dim)
+    w = _ROUTER_ONLY.get(key)
+    if w is None:
+        E, d = small.num_experts, small.hidden_dim
+        w = ExpertWeights(gate=np.zeros((E * d, 8), np.float32), up=np.zeros((E * d, 8), np.float32),
+                          down=np.zeros((E * 8, d), np.float32))
+        _ROUTER_ONLY[key] = w
+    return w

@@ -1,0 +1,268 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle and
+the reference's golden outputs.
+
+Bar (BASELINE.json north_star): routing indices, weights, logits, counts and
+permutation BIT-EXACT; layer output within max-rel-err 2e-2 of the
+reference's fp32 result (metric of moeperf/cli.py:733-737).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from golden_util import bits_equal, golden_meta  # noqa: E402
+from oracle import moe_oracle as O  # noqa: E402
+
+TOL = 2e-2  # north_star bf16 tolerance on max|y - y_ref| / max|y_ref|
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2605_23911_b200 as P
+    from paper_2605_23911_b200 import _lib
+    _lib.load()  # raises if the native library is missing — no fallback
+    return P
+
+
+def _cfg(P, e, k, d, f, g):
+    return P.ModelConfig(e, k, d, f, P.Gating(g))
+
+
+def _layer(P, cfg, wr, gate, up, down, max_tokens, out_dtype=None):
+    w = P.ExpertWeights(gate=gate, up=up, down=down)
+    kw = {} if out_dtype is None else {"out_dtype": out_dtype}
+    return P.MoELayer(cfg, w, wr, max_tokens=max(max_tokens, 1), **kw)
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# routing: bit-exact against the reference goldens
+# ---------------------------------------------------------------------------
+
+def test_route_bitexact_golden_full_shapes(pkg, golden):
+    P = pkg
+    for _, name, seed, e, k, d, scaled, b, g, bf16 in [m for m in golden_meta(golden) if m[0] == "route"]:
+        tokens, wr = O.make_router_instance(seed, b, d, e, scaled=bool(scaled), bf16_tokens=bool(bf16))
+        cfg = _cfg(P, e, k, d, 8, g)
+        z = np.zeros((e * d, 8), np.float32)
+        layer = _layer(P, cfg, wr, z, z, np.zeros((e * 8, d), np.float32), b)
+        feeds = [torch.from_numpy(tokens).cuda()]
+        if bf16:
+            feeds.append(torch.from_numpy(tokens).cuda().to(torch.bfloat16))  # exact: values are bf16
+        for x in feeds:
+            r = layer.route(x, logits=True)
+            p = f"route/{name}/"
+            bits_equal(_np(r["logits"]), golden[p + "logits"])
+            bits_equal(_np(r["indices"]).astype(np.int64), golden[p + "indices"])
+            bits_equal(_np(r["weights"]), golden[p + "weights"])
+            bits_equal(_np(r["counts"]).astype(np.int64), golden[p + "counts"])
+            bits_equal(_np(r["forward"]).astype(np.int64), golden[p + "forward"])
+            bits_equal(_np(r["inverse"]).astype(np.int64), golden[p + "inverse"])
+            assert layer.read_flags() == 0
+
+
+def test_forward_golden_cases(pkg, golden):
+    """Every reference forward case: exact routing, y within tolerance."""
+    P = pkg
+    for _, name, seed, e, k, d, f, b, g in [m for m in golden_meta(golden) if m[0] == "fwd"]:
+        tokens, wr, gate, up, down = O.make_instance(seed, e, k, d, f, b)
+        cfg = _cfg(P, e, k, d, f, g)
+        p = f"fwd/{name}/"
+        if b == 0:
+            y, trace = P.moe_forward(tokens, wr, P.ExpertWeights(gate, up, down), cfg)
+            assert y.shape == (0, d)
+            continue
+        layer = _layer(P, cfg, wr, gate, up, down, b)
+        st = layer.run_stages(torch.from_numpy(tokens).cuda())
+        bits_equal(_np(st["indices"]).astype(np.int64), golden[p + "indices"])
+        bits_equal(_np(st["weights"]), golden[p + "weights"])
+        bits_equal(_np(st["counts"]).astype(np.int64), golden[p + "counts"])
+        bits_equal(_np(st["forward"]).astype(np.int64), golden[p + "forward"])
+        bits_equal(_np(st["inverse"]).astype(np.int64), golden[p + "inverse"])
+        err = O.max_rel_error(_np(st["y"]), golden[p + "y"])
+        assert err <= TOL, (name, err)
+        # the one-call forward gives the same bits as the staged path
+        y1 = layer.forward(torch.from_numpy(tokens).cuda())
+        bits_equal(_np(y1), _np(st["y"]))
+
+
+def test_dropin_moe_forward_numpy_roundtrip(pkg, golden):
+    P = pkg
+    _, name, seed, e, k, d, f, b, g = [m for m in golden_meta(golden) if m[0] == "fwd" and m[1] == "small_s0"][0]
+    tokens, wr, gate, up, down = O.make_instance(seed, e, k, d, f, b)
+    cfg = _cfg(P, e, k, d, f, g)
+    y, trace = P.moe_forward(tokens, wr, P.ExpertWeights(gate, up, down), cfg, P.PipelineParams())
+    assert isinstance(y, np.ndarray) and y.dtype == np.float32 and y.shape == (b, d)
+    assert O.max_rel_error(y, golden[f"fwd/{name}/y"]) <= TOL
+    np.testing.assert_array_equal([r.flops for r in trace.records], golden[f"fwd/{name}/trace_flops"])
+    np.testing.assert_array_equal([r.total_bytes for r in trace.records], golden[f"fwd/{name}/trace_bytes"])
+    np.testing.assert_array_equal([r.tiles for r in trace.records], golden[f"fwd/{name}/trace_tiles"])
+    r = P.route(tokens, wr, cfg)
+    bits_equal(r.indices, golden[f"fwd/{name}/indices"])
+    bits_equal(r.weights, golden[f"fwd/{name}/weights"])
+
+
+def test_stage_intermediates_vs_oracle(pkg):
+    """h and expert_out against the oracle fed the same bf16-rounded operands."""
+    P = pkg
+    e, k, d, f, b = 8, 2, 256, 512, 96
+    tokens, wr, gate, up, down = O.make_instance(21, e, k, d, f, b)
+    cfg = _cfg(P, e, k, d, f, "softmax")
+    layer = _layer(P, cfg, wr, gate, up, down, b)
+    st = layer.run_stages(torch.from_numpy(tokens).cuda())
+    ref = O.moe_forward(O.round_to_bf16(tokens), wr, O.round_to_bf16(gate), O.round_to_bf16(up),
+                        O.round_to_bf16(down), e, k, "softmax")
+    # permuted tokens are an exact gather of bf16(x)
+    bits_equal(_np(st["permuted"].float()), ref["permuted"])
+    h = _np(st["h"].float())
+    assert O.max_rel_error(h, ref["h"]) < 1e-2
+    ys = _np(st["expert_out"])
+    # expert_out rows are stored at the expanded slot t*k+j, scaled by w[t,j]
+    w = ref["weights"].reshape(-1)
+    ref_slot = ref["expert_out"][ref["inverse"]] * w[:, None]
+    assert O.max_rel_error(ys, ref_slot) < 1e-2
+
+
+def test_determinism_bitwise(pkg):
+    P = pkg
+    e, k, d, f, b = 16, 4, 512, 768, 200
+    tokens, wr, gate, up, down = O.make_instance(3, e, k, d, f, b)
+    layer = _layer(P, _cfg(P, e, k, d, f, "sigmoid_normalized"), wr, gate, up, down, b)
+    x = torch.from_numpy(tokens).cuda()
+    y0 = _np(layer.forward(x))
+    for _ in range(3):
+        bits_equal(_np(layer.forward(x)), y0)
+
+
+def test_nonfinite_tokens_raise(pkg):
+    P = pkg
+    e, k, d, f, b = 4, 2, 64, 64, 8
+    tokens, wr, gate, up, down = O.make_instance(1, e, k, d, f, b)
+    tokens[3, 5] = np.nan
+    with pytest.raises(P.NonFiniteInput):
+        P.moe_forward(tokens, wr, P.ExpertWeights(gate, up, down), _cfg(P, e, k, d, f, "softmax"))
+    gate2 = gate.copy()
+    gate2[0, 0] = np.inf
+    tokens[3, 5] = 0.0
+    with pytest.raises(P.NonFiniteInput):
+        P.moe_forward(tokens, wr, P.ExpertWeights(gate2, up, down), _cfg(P, e, k, d, f, "softmax"))
+
+
+def test_shape_errors(pkg):
+    P = pkg
+    cfg = _cfg(P, 4, 2, 8, 8, "softmax")
+    w = P.ExpertWeights(np.zeros((32, 8), np.float32), np.zeros((32, 8), np.float32), np.zeros((32, 8), np.float32))
+    with pytest.raises(P.ShapeMismatch):
+        P.moe_forward(np.zeros((2, 5), np.float32), np.zeros((8, 4), np.float32), w, cfg)
+    with pytest.raises(P.ShapeMismatch):
+        P.moe_forward(np.zeros((2, 8), np.float32), np.zeros((8, 3), np.float32), w, cfg)
+    with pytest.raises(P.ShapeMismatch):
+        P.moe_forward(np.zeros((2, 8), np.float32), np.zeros((8, 4), np.float32),
+                      P.ExpertWeights(np.zeros((31, 8), np.float32), w.up, w.down), cfg)
+
+
+# ---------------------------------------------------------------------------
+# full BASELINE shapes: exact routing vs the oracle; y vs a torch fp32
+# reference fed the same bf16 operands and the same (exact) routing.
+# ---------------------------------------------------------------------------
+
+def _torch_ref_y(x_bf16, idx, w, gate, up, down, d, f):
+    """fp32 torch reference of the expert FFN + combine on identical bf16 operands."""
+    B, k = idx.shape
+    xf = x_bf16.float()
+    y = torch.zeros((B, d), dtype=torch.float32, device=x_bf16.device)
+    idx_l = idx.long()
+    for e in torch.unique(idx_l).tolist():
+        tok, slot = torch.nonzero(idx_l == e, as_tuple=True)
+        a = xf[tok]
+        g = a @ gate[e * d:(e + 1) * d].float()
+        u = a @ up[e * d:(e + 1) * d].float()
+        h = (torch.nn.functional.silu(g) * u)
+        o = h @ down[e * f:(e + 1) * f].float()
+        y.index_add_(0, tok, o * w[tok, slot][:, None])
+    return y
+
+
+@pytest.mark.parametrize("shape", [
+    ("mixtral", 8, 2, 4096, 14336, 512, "softmax"),
+    ("qwen60", 60, 4, 2048, 1408, 512, "softmax"),
+    ("deepseek", 256, 8, 7168, 2048, 128, "sigmoid_normalized"),
+])
+def test_full_shape_parity(pkg, shape):
+    P = pkg
+    name, e, k, d, f, b, g = shape
+    gen = torch.Generator(device="cuda").manual_seed(1234)
+    x = torch.randn((b, d), generator=gen, device="cuda").to(torch.bfloat16)
+    wr = (torch.randn((d, e), generator=gen, device="cuda") / d ** 0.5).float()
+    gate = (torch.randn((e * d, f), generator=gen, device="cuda") / d ** 0.5).to(torch.bfloat16)
+    up = (torch.randn((e * d, f), generator=gen, device="cuda") / d ** 0.5).to(torch.bfloat16)
+    down = (torch.randn((e * f, d), generator=gen, device="cuda") / f ** 0.5).to(torch.bfloat16)
+    cfg = _cfg(P, e, k, d, f, g)
+    layer = P.MoELayer(cfg, P.ExpertWeights(gate, up, down), wr, max_tokens=b)
+    y = layer.forward(x)
+    torch.cuda.synchronize()
+    # routing: bit-exact against the oracle on the same fp32 values
+    idx_ref, w_ref = O.route(_np(x.float()), _np(wr), k, g)
+    bits_equal(_np(layer.topk_idx[:b]).astype(np.int64), idx_ref)
+    bits_equal(_np(layer.topk_w[:b]), w_ref)
+    bits_equal(_np(layer.counts).astype(np.int64), O.expert_histogram(idx_ref, e))
+    fwd_ref, inv_ref = O.build_permutation(idx_ref)
+    bits_equal(_np(layer.fwd[: b * k]).astype(np.int64), fwd_ref)
+    y_ref = _torch_ref_y(x, layer.topk_idx[:b], layer.topk_w[:b], gate, up, down, d, f)
+    err = O.max_rel_error(_np(y), _np(y_ref))
+    assert err <= TOL, (name, err)
+    assert err <= 1e-2, (name, err)  # expected ~2-3e-3 (bf16 h)
+
+
+def test_skewed_routing_single_hot_expert(pkg):
+    """All tokens to the same experts: chunks > BN rows, empty experts."""
+    P = pkg
+    e, k, d, f, b = 8, 2, 1024, 2048, 600
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randn((b, d), generator=gen, device="cuda")
+    wr = torch.zeros((d, e), device="cuda")
+    wr[:, 3] = 1.0 / d ** 0.5 * torch.sign(x.mean(0))  # expert 3 dominates
+    wr[:, 5] = 0.5 / d ** 0.5 * torch.sign(x.mean(0))
+    gate = (torch.randn((e * d, f), generator=gen, device="cuda") / d ** 0.5).to(torch.bfloat16)
+    up = (torch.randn((e * d, f), generator=gen, device="cuda") / d ** 0.5).to(torch.bfloat16)
+    down = (torch.randn((e * f, d), generator=gen, device="cuda") / f ** 0.5).to(torch.bfloat16)
+    layer = P.MoELayer(_cfg(P, e, k, d, f, "softmax"), P.ExpertWeights(gate, up, down), wr, max_tokens=b)
+    y = layer.forward(x)
+    idx_ref, w_ref = O.route(_np(x), _np(wr), k, "softmax")
+    bits_equal(_np(layer.topk_idx[:b]).astype(np.int64), idx_ref)
+    y_ref = _torch_ref_y(x.to(torch.bfloat16), layer.topk_idx[:b], layer.topk_w[:b], gate, up, down, d, f)
+    assert O.max_rel_error(_np(y), _np(y_ref)) <= 1e-2
+
+
+def test_sigmoid_port_matches_numpy_on_device(pkg):
+    """The router's numpy-expf port: sigmoid scores of 1e6 logits vs numpy."""
+    P = pkg
+    rng = np.random.default_rng(0)
+    # logits chosen so every (token, expert) score is visible through top-k = E
+    e, k, d, b = 8, 8, 8, 4096
+    x = np.zeros((b, d), np.float32)
+    x[:, 0] = 1.0
+    vals = np.concatenate([rng.uniform(-110, 20, b * e // 2), rng.standard_normal(b * e // 2) * 4]).astype(np.float32)
+    logits = vals.reshape(b, e)
+    # W_r row 0 = logits is per-token here, so route each token with its own W_r via d = e trick:
+    # tokens one-hot over d = e positions; W_r = diag scale -> logits[t, e] = x[t, e] * 1
+    x = logits.copy()
+    wr = np.eye(e, dtype=np.float32)
+    cfg = _cfg(P, e, k, e, 8, "sigmoid_normalized")
+    z = np.zeros((e * e, 8), np.float32)
+    layer = _layer(P, cfg, wr, z, z, np.zeros((e * 8, e), np.float32), b)
+    r = layer.route(torch.from_numpy(x).cuda(), logits=True)
+    bits_equal(_np(r["logits"]), logits)
+    idx_ref, w_ref = O.route(x, wr, k, "sigmoid_normalized")
+    bits_equal(_np(r["indices"]).astype(np.int64), idx_ref)
+    bits_equal(_np(r["weights"]), w_ref)
