@@ -1,0 +1,66 @@
+"""CPU baseline runner — TEST/BENCH INFRASTRUCTURE ONLY.
+
+Times the oracle port of the reference MoE forward (``oracle.moe_oracle``,
+a numpy restatement of ``moeperf.pipeline.moe_forward``,
+``pipeline.py:572-615``) on the host cores.  The reference is single-threaded
+numpy; rows are independent, so the token batch is sharded across one
+forked worker per core (bit-identical to the unsharded run — the reference's
+row-parallel guarantee).  Only ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs call this.
+"""
+
+from __future__ import annotations
+
+import multiprocessing as mp
+import os
+import time
+
+import numpy as np
+
+from . import moe_oracle as O
+
+_STATE: dict = {}
+
+
+def _worker(args):
+    lo, hi = args
+    s = _STATE
+    res = O.moe_forward(s["tokens"][lo:hi], s["wr"], s["gate"], s["up"], s["down"],
+                        s["E"], s["k"], s["gating"])
+    return lo, res["y"], res["indices"]
+
+
+def _noop(_):
+    return None
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def run_sharded(tokens, wr, gate, up, down, num_experts, k, gating, procs=None):
+    """Oracle forward over ``tokens`` sharded across ``procs`` forked workers.
+
+    Returns ``(y, indices, wall_seconds, procs)``.  Weight arrays are shared
+    with the workers through fork (copy-on-write, never written).
+    """
+    procs = procs or host_cores()
+    B = tokens.shape[0]
+    procs = max(1, min(procs, B))
+    _STATE.update(tokens=tokens, wr=wr, gate=gate, up=up, down=down, E=num_experts, k=k, gating=gating)
+    bounds = np.linspace(0, B, procs + 1).astype(int)
+    jobs = [(int(bounds[i]), int(bounds[i + 1])) for i in range(procs) if bounds[i + 1] > bounds[i]]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(len(jobs)) as pool:
+        pool.map(_noop, range(len(jobs)))  # workers forked and ready before timing
+        t0 = time.perf_counter()
+        parts = pool.map(_worker, jobs, chunksize=1)
+        wall = time.perf_counter() - t0
+    parts.sort(key=lambda p: p[0])
+    y = np.concatenate([p[1] for p in parts]) if parts else np.zeros((0, tokens.shape[1]), np.float32)
+    idx = np.concatenate([p[2] for p in parts]) if parts else np.zeros((0, k), np.int64)
+    _STATE.clear()
+    return y, idx, wall, len(jobs)

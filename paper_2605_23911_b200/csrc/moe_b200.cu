@@ -147,16 +147,17 @@ struct RouterPlan {
 RouterPlan plan_router(const moe_b200_config& c, int64_t B, int x_bf16) {
   RouterPlan r{};
   r.expc = std::min(c.num_experts, 32);
-  const int n_groups = kRouterThreads / r.expc;
+  // token groups per CTA; tokens per CTA capped at 64 to bound shared memory
+  auto groups_for = [&](int tg) { return std::min(kRouterThreads / r.expc, 64 / tg); };
   r.n_eblocks = (c.num_experts + r.expc - 1) / r.expc;
   const int tgs[4] = {8, 4, 2, 1};
   r.tg = 1;
   for (int i = 0; i < 4; ++i) {
-    int tokc = tgs[i] * n_groups;
+    int tokc = tgs[i] * groups_for(tgs[i]);
     int64_t grid = ((B + tokc - 1) / tokc) * r.n_eblocks;
     if (grid >= (kNumSMs * 4) / 5) { r.tg = tgs[i]; break; }
   }
-  r.tokc = r.tg * n_groups;
+  r.tokc = r.tg * groups_for(r.tg);
   r.n_tblocks = static_cast<int>((B + r.tokc - 1) / r.tokc);
   r.smem = RouterSmem::total_bytes(r.tokc, r.expc, x_bf16 ? 2 : 4, c.num_experts);
   return r;

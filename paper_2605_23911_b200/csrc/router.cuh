@@ -255,7 +255,7 @@ router_kernel(const RouterParams p) {
 
   const int el = tid % p.expc;        // expert lane
   const int tgi = tid / p.expc;       // token group
-  const int n_groups = kRouterThreads / p.expc;
+  const int n_groups = p.tokc / kTG;
   const bool active = (tgi < n_groups) && (e0 + el < p.E);
   double acc[kTG];
 #pragma unroll

@@ -226,6 +226,47 @@ class MoELayer:
         return r
 
 
+    def timed_stages(self, x: torch.Tensor, iters: int = 10, flush: torch.Tensor | None = None) -> dict:
+        """Per-stage device time (ms, mean over ``iters``) with CUDA events between
+        the five C-ABI stage calls on the current stream (optional L2 flush
+        between iterations, outside the timed events)."""
+        x, xdt = self._prep_x(x)
+        B, T = x.shape[0], x.shape[0] * self.k
+        dev, s = self.device, _stream_ptr(self.device)
+        L = _lib.load()
+        cfg = ctypes.byref(self.cfg)
+        xp = torch.empty((T, self.dp), dtype=torch.bfloat16, device=dev)
+        h = torch.empty((T, self.fp), dtype=torch.bfloat16, device=dev)
+        ys = torch.empty((T, self.dp), dtype=torch.float32, device=dev)
+        y = torch.empty((B, self.dp), dtype=self.out_dtype, device=dev)
+        ydt = _lib.DTYPE_BF16 if y.dtype == torch.bfloat16 else _lib.DTYPE_F32
+        names = ("route", "permute", "gate_up", "down_scatter", "combine")
+        tot = dict.fromkeys(names, 0.0)
+        for _ in range(iters):
+            if flush is not None:
+                flush.zero_()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+            ev[0].record()
+            _lib.check(L.moe_b200_route(cfg, B, _ptr(x), xdt, _ptr(self.router_weight), _ptr(self.topk_idx),
+                                        _ptr(self.topk_w), _ptr(self.counts), _ptr(self.offsets), _ptr(self.fwd),
+                                        _ptr(self.inv), 0, _ptr(self.ws), self.ws_bytes, s), "route")
+            ev[1].record()
+            _lib.check(L.moe_b200_permute(cfg, B, _ptr(x), xdt, _ptr(self.fwd), _ptr(xp), s), "permute")
+            ev[2].record()
+            _lib.check(L.moe_b200_gate_up(cfg, B, _ptr(xp), _ptr(self.weights.gate), _ptr(self.weights.up),
+                                          _ptr(h), _ptr(self.ws), self.ws_bytes, s), "gate_up")
+            ev[3].record()
+            _lib.check(L.moe_b200_down_scatter(cfg, B, _ptr(h), _ptr(self.weights.down), _ptr(self.topk_w),
+                                               _ptr(self.fwd), _ptr(ys), _ptr(self.ws), self.ws_bytes, s), "down")
+            ev[4].record()
+            _lib.check(L.moe_b200_combine(cfg, B, _ptr(ys), _ptr(y), ydt, s), "combine")
+            ev[5].record()
+            torch.cuda.synchronize(dev)
+            for i, n in enumerate(names):
+                tot[n] += ev[i].elapsed_time(ev[i + 1])
+        return {n: v / iters for n, v in tot.items()}
+
+
 from .types import Gating  # noqa: E402  (used in MoELayer.__init__)
 
 # ---------------------------------------------------------------------------
