@@ -140,26 +140,50 @@ int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 
 // ------------------------------- launches --------------------------------------
 struct RouterPlan {
-  int expc, tg, tokc, n_eblocks, n_tblocks;
+  int expc, tg, tokc, n_eblocks, n_tblocks, threads;
   size_t smem;
 };
 
+// Router CTA shape.  expc experts x (tokc / tg) token groups of compute
+// threads (<= 256) plus 4 producer warps.  Prefer more chains per thread
+// (tg) when the grid still fills the GPU; otherwise shrink tokens per CTA so
+// that enough SMs run chains in parallel (latency regime: Mixtral, Qwen).
 RouterPlan plan_router(const moe_b200_config& c, int64_t B, int x_bf16) {
   RouterPlan r{};
-  r.expc = std::min(c.num_experts, 32);
-  // token groups per CTA; tokens per CTA capped at 64 to bound shared memory
-  auto groups_for = [&](int tg) { return std::min(kRouterThreads / r.expc, 64 / tg); };
-  r.n_eblocks = (c.num_experts + r.expc - 1) / r.expc;
-  const int tgs[4] = {8, 4, 2, 1};
-  r.tg = 1;
-  for (int i = 0; i < 4; ++i) {
-    int tokc = tgs[i] * groups_for(tgs[i]);
-    int64_t grid = ((B + tokc - 1) / tokc) * r.n_eblocks;
-    if (grid >= (kNumSMs * 4) / 5) { r.tg = tgs[i]; break; }
+  const int E = c.num_experts;
+  const int xb = x_bf16 ? 2 : 4;
+  r.expc = std::min(E, 32);
+  r.n_eblocks = (E + r.expc - 1) / r.expc;
+  const int maxg = 256 / r.expc;
+  const int64_t target = (kNumSMs * 4) / 5;
+  auto smem_for = [&](int tokc, int groups) {
+    const int nthreads = ((r.expc * groups + 31) / 32) * 32 + kRouterProducers;
+    return RouterSmem::total_bytes(tokc, r.expc, xb, E, nthreads);
+  };
+  const size_t smem_cap = 200 * 1024;
+  r.tg = 0;
+  const int tgs[3] = {8, 4, 2};
+  for (int i = 0; i < 3 && !r.tg; ++i) {
+    int g = std::min(maxg, 64 / tgs[i]);
+    while (g > 1 && smem_for(tgs[i] * g, g) > smem_cap) g /= 2;
+    const int tokc = tgs[i] * g;
+    if (((B + tokc - 1) / tokc) * r.n_eblocks >= target && smem_for(tokc, g) <= smem_cap) {
+      r.tg = tgs[i];
+      r.tokc = tokc;
+    }
   }
-  r.tokc = r.tg * groups_for(r.tg);
+  if (!r.tg) {
+    r.tg = 1;
+    int g = 1;
+    while (g * 2 <= std::min(maxg, 64) && ((B + g * 2 - 1) / (g * 2)) * r.n_eblocks >= target &&
+           smem_for(g * 2, g * 2) <= smem_cap)
+      g *= 2;
+    r.tokc = g;
+  }
+  const int groups = r.tokc / r.tg;
+  r.threads = ((r.expc * groups + 31) / 32) * 32 + kRouterProducers;
   r.n_tblocks = static_cast<int>((B + r.tokc - 1) / r.tokc);
-  r.smem = RouterSmem::total_bytes(r.tokc, r.expc, x_bf16 ? 2 : 4, c.num_experts);
+  r.smem = smem_for(r.tokc, groups);
   return r;
 }
 
@@ -167,7 +191,7 @@ template <bool kBf16, int kTG>
 int launch_router_t(const RouterParams& p, const RouterPlan& plan, cudaStream_t s) {
   auto kern = router_kernel<kBf16, kTG>;
   MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
-  kern<<<plan.n_tblocks * plan.n_eblocks, kRouterThreads, plan.smem, s>>>(p);
+  kern<<<plan.n_tblocks * plan.n_eblocks, plan.threads, plan.smem, s>>>(p);
   MOE_LAUNCH_CHECK("router_kernel");
   return MOE_B200_OK;
 }

@@ -27,9 +27,8 @@
 
 namespace moe {
 
-constexpr int kRouterThreads = 256;
-constexpr int kRouterKC = 64;      // k-chunk staged per pipeline step
-constexpr int kRouterStages = 4;   // cp.async ring depth
+constexpr int kRouterKC = 128;     // k-chunk staged per pipeline step
+constexpr int kRouterStages = 3;   // cp.async ring depth
 constexpr int kMaxExperts = 1024;
 
 struct RouterParams {
@@ -166,14 +165,25 @@ MOE_DEVICE void cp_async_wait() {
 }
 
 // ---------------------------------------------------------------------------
+// Named barriers (ids 1..5; 0 is __syncthreads)
+// ---------------------------------------------------------------------------
+MOE_DEVICE void nbar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+MOE_DEVICE void nbar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+constexpr int kRouterProducers = 128;  // 4 warps: cp.async ring + fp64 conversion
+
+// ---------------------------------------------------------------------------
 // Shared-memory carve-up for phase 1
+//   raw ring : kRouterStages x {x chunk (tokc x KC, x dtype), w chunk (KC x expc fp32)}
+//   f64 bufs : 2 x {x (tokc x (KC+1)) fp64, w (KC x expc) fp64}
 // ---------------------------------------------------------------------------
 struct RouterSmem {
-  // raw ring: stages x {x chunk (tokc x KC elems of x dtype), wr chunk (KC x expc fp32)}
-  // f64 double buffer: {x (tokc x (KC+1)), wr (KC x expc)}
   static __host__ __device__ size_t raw_x_bytes(int tokc, int xb) { return (size_t)tokc * kRouterKC * xb; }
   static __host__ __device__ size_t raw_w_bytes(int expc) {
-    // rounded so each stage stays 16-byte aligned
     return ((size_t)kRouterKC * expc * 4 + 15) / 16 * 16;
   }
   static __host__ __device__ size_t raw_stage_bytes(int tokc, int expc, int xb) {
@@ -181,66 +191,67 @@ struct RouterSmem {
   }
   static __host__ __device__ size_t f64_x_elems(int tokc) { return (size_t)tokc * (kRouterKC + 1); }
   static __host__ __device__ size_t f64_w_elems(int expc) { return (size_t)kRouterKC * expc; }
-  static __host__ __device__ size_t total_bytes(int tokc, int expc, int xb, int E) {
+  static __host__ __device__ size_t total_bytes(int tokc, int expc, int xb, int E, int nthreads) {
     size_t ph1 = kRouterStages * raw_stage_bytes(tokc, expc, xb) +
                  2 * (f64_x_elems(tokc) + f64_w_elems(expc)) * sizeof(double);
-    // phase 2: one fp64 row of E per warp; phase 3: 8 x E ints + scan scratch
-    size_t ph2 = (size_t)(kRouterThreads / 32) * E * sizeof(double);
-    size_t ph3 = ((size_t)(kRouterThreads / 32) + 4) * E * sizeof(int32_t) + 256;
+    size_t ph2 = (size_t)(nthreads / 32) * E * sizeof(double);
+    size_t ph3 = ((size_t)(nthreads / 32) + 4) * E * sizeof(int32_t) + 256;
     size_t m = ph1 > ph2 ? ph1 : ph2;
     return m > ph3 ? m : ph3;
   }
 };
 
-// Issue the cp.async copies of k-chunk `c` into ring slot `slot`.
+// Producer-side: issue the cp.async copies of k-chunk `c` into ring slot `slot`.
 template <bool kXBf16>
 MOE_DEVICE void router_issue_chunk(const RouterParams& p, uint8_t* raw, int slot, int c, int t0,
-                                   int e0, int tid) {
+                                   int e0, int ptid) {
   const int xb = kXBf16 ? 2 : 4;
   uint8_t* sx = raw + (size_t)slot * RouterSmem::raw_stage_bytes(p.tokc, p.expc, xb);
   uint8_t* sw = sx + RouterSmem::raw_x_bytes(p.tokc, xb);
   const int k0 = c * kRouterKC;
-  // x: tokc rows x (KC*xb) bytes, 16-byte pieces
-  const int x_pieces_per_row = kRouterKC * xb / 16;
-  const int x_pieces = p.tokc * x_pieces_per_row;
+  constexpr int x_ppr = kRouterKC * (kXBf16 ? 2 : 4) / 16;  // 16-byte pieces per x row
+  const int x_pieces = p.tokc * x_ppr;
   const uint8_t* xg = static_cast<const uint8_t*>(p.x);
-  for (int i = tid; i < x_pieces; i += kRouterThreads) {
-    int row = i / x_pieces_per_row, pc = i % x_pieces_per_row;
-    int t = t0 + row;
-    int kk = k0 + pc * (16 / xb);
-    bool valid = (t < p.B) && (kk < p.d);
+  for (int i = ptid; i < x_pieces; i += kRouterProducers) {
+    const int row = i / x_ppr, pc = i % x_ppr;
+    const int t = t0 + row;
+    const int kk = k0 + pc * (16 / xb);
+    const bool valid = (t < p.B) && (kk < p.d);
     const uint8_t* src = valid ? xg + ((size_t)t * p.d + kk) * xb : xg;
     cp_async_16(sx + (size_t)i * 16, src, valid);
   }
-  // wr: KC rows x expc fp32.  Rows are E-contiguous in global; the expert
-  // slice [e0, e0+expc) is 16-byte aligned only when E % 4 == 0, so fall back
-  // to 4-byte copies otherwise.
   if ((p.E % 4) == 0 && (p.expc % 4) == 0) {
-    const int w_pieces_per_row = p.expc / 4;
-    const int w_pieces = kRouterKC * w_pieces_per_row;
-    for (int i = tid; i < w_pieces; i += kRouterThreads) {
-      int kr = i / w_pieces_per_row, pc = i % w_pieces_per_row;
-      int kk = k0 + kr;
-      int e = e0 + pc * 4;
-      bool valid = (kk < p.d) && (e < p.E);
+    const int w_ppr = p.expc / 4;
+    const int w_pieces = kRouterKC * w_ppr;
+    for (int i = ptid; i < w_pieces; i += kRouterProducers) {
+      const int kr = i / w_ppr, pc = i % w_ppr;
+      const int kk = k0 + kr;
+      const int e = e0 + pc * 4;
+      const bool valid = (kk < p.d) && (e < p.E);
       const float* src = valid ? p.wr + (size_t)kk * p.E + e : p.wr;
       cp_async_16(sw + (size_t)(kr * p.expc + pc * 4) * 4, src, valid);
     }
   } else {
     float* swf = reinterpret_cast<float*>(sw);
-    for (int i = tid; i < kRouterKC * p.expc; i += kRouterThreads) {
-      int kr = i / p.expc, el = i % p.expc;
-      int kk = k0 + kr, e = e0 + el;
+    for (int i = ptid; i < kRouterKC * p.expc; i += kRouterProducers) {
+      const int kr = i / p.expc, el = i % p.expc;
+      const int kk = k0 + kr, e = e0 + el;
       swf[i] = (kk < p.d && e < p.E) ? __ldg(p.wr + (size_t)kk * p.E + e) : 0.0f;
     }
   }
 }
 
+// Launch shape: blockDim = n_compute + kRouterProducers.  Compute threads
+// [0, n_compute) own (expert lane, token group) chains; producer warps stage
+// and convert the operands one chunk ahead, synchronised by named barriers
+// FULL[b] (ids 1,2) and EMPTY[b] (ids 3,4); id 5 syncs the producers.
 template <bool kXBf16, int kTG>
-__global__ void __launch_bounds__(kRouterThreads)
+__global__ void __launch_bounds__(384)
 router_kernel(const RouterParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x;
+  const int nthreads = blockDim.x;
+  const int n_compute = nthreads - kRouterProducers;
   const int tb = blockIdx.x / p.n_eblocks;
   const int eb = blockIdx.x % p.n_eblocks;
   const int t0 = tb * p.tokc;
@@ -252,87 +263,97 @@ router_kernel(const RouterParams p) {
   const size_t raw_total = kRouterStages * RouterSmem::raw_stage_bytes(p.tokc, p.expc, xb);
   double* f64 = reinterpret_cast<double*>(smem + raw_total);
   const size_t fx = RouterSmem::f64_x_elems(p.tokc), fw = RouterSmem::f64_w_elems(p.expc);
-
-  const int el = tid % p.expc;        // expert lane
-  const int tgi = tid / p.expc;       // token group
-  const int n_groups = p.tokc / kTG;
-  const bool active = (tgi < n_groups) && (e0 + el < p.E);
-  double acc[kTG];
-#pragma unroll
-  for (int i = 0; i < kTG; ++i) acc[i] = -0.0;  // fma(a,b,-0) == a*b exactly, sign included
-  bool nonfinite_x = false, nonfinite_w = false;
-
   const int nch = (p.d + kRouterKC - 1) / kRouterKC;
-#pragma unroll 1
-  for (int s = 0; s < kRouterStages - 1; ++s) {
-    if (s < nch) router_issue_chunk<kXBf16>(p, raw, s, s, t0, e0, tid);
-    cp_async_commit();
-  }
-#pragma unroll 1
-  for (int c = 0; c < nch; ++c) {
-    cp_async_wait<kRouterStages - 2>();
-    __syncthreads();
-    // convert raw chunk c -> fp64 buffer (c & 1), checking finiteness
-    {
+  const int nbar = nthreads;
+
+  if (tid >= n_compute) {
+    // ============================ producers ================================
+    const int ptid = tid - n_compute;
+    bool nonfinite_x = false, nonfinite_w = false;
+    for (int s = 0; s < kRouterStages - 1; ++s) {
+      if (s < nch) router_issue_chunk<kXBf16>(p, raw, s, s, t0, e0, ptid);
+      cp_async_commit();
+    }
+    for (int c = 0; c < nch; ++c) {
+      cp_async_wait<kRouterStages - 2>();
+      nbar_sync(5, kRouterProducers);  // chunk c landed for every producer thread
+      const int b = c & 1;
+      if (c >= 2) nbar_sync(3 + b, nbar);  // consumers released buffer b (chunk c-2)
       const uint8_t* sx = raw + (size_t)(c % kRouterStages) * RouterSmem::raw_stage_bytes(p.tokc, p.expc, xb);
       const float* sw = reinterpret_cast<const float*>(sx + RouterSmem::raw_x_bytes(p.tokc, xb));
-      double* dx = f64 + (size_t)(c & 1) * (fx + fw);
+      double* dx = f64 + (size_t)b * (fx + fw);
       double* dw = dx + fx;
       const int kvalid = min(kRouterKC, p.d - c * kRouterKC);
-      for (int i = tid; i < p.tokc * kRouterKC; i += kRouterThreads) {
-        int row = i / kRouterKC, kk = i % kRouterKC;
+      const int nx = p.tokc * kRouterKC;
+#pragma unroll 4
+      for (int i = ptid; i < nx; i += kRouterProducers) {
+        const int row = i / kRouterKC, kk = i % kRouterKC;
         float v;
-        if (kXBf16) {
-          v = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(sx)[i]);
-        } else {
-          v = reinterpret_cast<const float*>(sx)[i];
-        }
+        if (kXBf16) v = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(sx)[i]);
+        else v = reinterpret_cast<const float*>(sx)[i];
         if (kk < kvalid && t0 + row < p.B && !isfinite(v)) nonfinite_x = true;
         dx[row * (kRouterKC + 1) + kk] = static_cast<double>(v);
       }
-      for (int i = tid; i < kRouterKC * p.expc; i += kRouterThreads) {
-        float v = sw[i];
-        int kk = i / p.expc, e = i % p.expc;
+      const int nw = kRouterKC * p.expc;
+#pragma unroll 4
+      for (int i = ptid; i < nw; i += kRouterProducers) {
+        const float v = sw[i];
+        const int kk = i / p.expc, e = i % p.expc;
         if (kk < kvalid && e0 + e < p.E && !isfinite(v)) nonfinite_w = true;
         dw[i] = static_cast<double>(v);
       }
-    }
-    // refill the ring slot freed by chunk c-1
-    {
-      int nc = c + kRouterStages - 1;
-      if (nc < nch) router_issue_chunk<kXBf16>(p, raw, nc % kRouterStages, nc, t0, e0, tid);
+      nbar_arrive(1 + b, nbar);  // buffer b full
+      // refill the raw slot of chunk c-1 (every producer converted it before
+      // the barrier at the top of this iteration) with chunk c + S - 1
+      const int nc = c + kRouterStages - 1;
+      if (nc < nch) router_issue_chunk<kXBf16>(p, raw, nc % kRouterStages, nc, t0, e0, ptid);
       cp_async_commit();
     }
-    __syncthreads();
-    if (active) {
-      const double* dx = f64 + (size_t)(c & 1) * (fx + fw);
-      const double* dw = dx + fx;
-      const int kvalid = min(kRouterKC, p.d - c * kRouterKC);
-      const double* xr = dx + (size_t)(tgi * kTG) * (kRouterKC + 1);
-      if (kvalid == kRouterKC) {
-#pragma unroll 8
-        for (int kk = 0; kk < kRouterKC; ++kk) {
-          double w = dw[kk * p.expc + el];
+    cp_async_wait<0>();
+    // balance the consumers' final EMPTY arrivals
+    for (int c = max(nch - 2, 0); c < nch; ++c) nbar_sync(3 + (c & 1), nbar);
+    if (nonfinite_x) atomicOr(p.flags, 1u);
+    if (nonfinite_w) atomicOr(p.flags, 2u);
+  } else {
+    // ============================ compute chains ===========================
+    const int el = tid % p.expc;
+    const int tgi = tid / p.expc;
+    const int n_groups = p.tokc / kTG;
+    const bool active = (tgi < n_groups) && (e0 + el < p.E);
+    double acc[kTG];
 #pragma unroll
-          for (int i = 0; i < kTG; ++i) acc[i] = __fma_rn(xr[i * (kRouterKC + 1) + kk], w, acc[i]);
-        }
-      } else {
-        for (int kk = 0; kk < kvalid; ++kk) {
-          double w = dw[kk * p.expc + el];
+    for (int i = 0; i < kTG; ++i) acc[i] = -0.0;  // fma(a,b,-0) == a*b exactly, sign included
+    for (int c = 0; c < nch; ++c) {
+      const int b = c & 1;
+      nbar_sync(1 + b, nbar);
+      if (active) {
+        const double* dx = f64 + (size_t)b * (fx + fw);
+        const double* dw = dx + fx + el;
+        const double* xr = dx + (size_t)(tgi * kTG) * (kRouterKC + 1);
+        const int kvalid = min(kRouterKC, p.d - c * kRouterKC);
+        if (kvalid == kRouterKC) {
+#pragma unroll 16
+          for (int kk = 0; kk < kRouterKC; ++kk) {
+            const double w = dw[kk * p.expc];
 #pragma unroll
-          for (int i = 0; i < kTG; ++i) acc[i] = __fma_rn(xr[i * (kRouterKC + 1) + kk], w, acc[i]);
+            for (int i = 0; i < kTG; ++i) acc[i] = __fma_rn(xr[i * (kRouterKC + 1) + kk], w, acc[i]);
+          }
+        } else {
+          for (int kk = 0; kk < kvalid; ++kk) {
+            const double w = dw[kk * p.expc];
+#pragma unroll
+            for (int i = 0; i < kTG; ++i) acc[i] = __fma_rn(xr[i * (kRouterKC + 1) + kk], w, acc[i]);
+          }
         }
       }
+      nbar_arrive(3 + b, nbar);  // buffer b free
     }
-  }
-  cp_async_wait<0>();
-  if (nonfinite_x) atomicOr(p.flags, 1u);
-  if (nonfinite_w) atomicOr(p.flags, 2u);
-  if (active) {
+    if (active) {
 #pragma unroll
-    for (int i = 0; i < kTG; ++i) {
-      int t = t0 + tgi * kTG + i;
-      if (t < p.B) p.logits[(size_t)t * p.E + e0 + el] = __double2float_rn(acc[i]);
+      for (int i = 0; i < kTG; ++i) {
+        const int t = t0 + tgi * kTG + i;
+        if (t < p.B) p.logits[(size_t)t * p.E + e0 + el] = __double2float_rn(acc[i]);
+      }
     }
   }
 
@@ -352,7 +373,7 @@ router_kernel(const RouterParams p) {
     const int warp = tid / 32, lane = tid % 32;
     double* row = reinterpret_cast<double*>(smem) + (size_t)warp * p.E;
     const int tend = min(t0 + p.tokc, p.B);
-    for (int t = t0 + warp; t < tend; t += kRouterThreads / 32) {
+    for (int t = t0 + warp; t < tend; t += nthreads / 32) {
       const float* lg = p.logits + (size_t)t * p.E;
       // scores -> row (as double for softmax, float bits stored in double for sigmoid)
       if (p.gating == 0) {
@@ -451,7 +472,7 @@ router_kernel(const RouterParams p) {
   __threadfence();
 
   {
-    const int nw = kRouterThreads / 32;
+    const int nw = nthreads / 32;
     const int warp = tid / 32, lane = tid % 32;
     const int T = p.B * p.k;
     const int E = p.E;
@@ -459,14 +480,14 @@ router_kernel(const RouterParams p) {
     int32_t* s_cnt = hist + (size_t)nw * E;                  // [E]
     int32_t* s_off = s_cnt + E;                              // [E+1]
     int32_t* s_cpre = s_off + E + 1;                         // [E+1] chunk prefix
-    for (int i = tid; i < nw * E; i += kRouterThreads) hist[i] = 0;
+    for (int i = tid; i < nw * E; i += nthreads) hist[i] = 0;
     __syncthreads();
     const int seg = (T + nw - 1) / nw;
     const int s0 = warp * seg, s1 = min(T, s0 + seg);
     for (int i = s0 + lane; i < s1; i += 32) atomicAdd(&hist[warp * E + __ldcg(p.topk_idx + i)], 1);
     __syncthreads();
     // per-expert totals and per-warp exclusive bases
-    for (int e = tid; e < E; e += kRouterThreads) {
+    for (int e = tid; e < E; e += nthreads) {
       int run = 0;
       for (int w = 0; w < nw; ++w) {
         int h = hist[w * E + e];
@@ -505,7 +526,7 @@ router_kernel(const RouterParams p) {
       }
     }
     __syncthreads();
-    for (int e = tid; e < E; e += kRouterThreads) {
+    for (int e = tid; e < E; e += nthreads) {
       p.counts[e] = s_cnt[e];
       p.offsets[e] = s_off[e];
       const int n_e = s_cnt[e];
