@@ -140,56 +140,53 @@ int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 
 // ------------------------------- launches --------------------------------------
 struct RouterPlan {
-  int expc, tg, tokc, n_eblocks, n_tblocks, threads;
+  int expc, te, tt, tokc, n_eblocks, n_tblocks, threads;
   size_t smem;
 };
 
-// Router CTA shape.  expc experts x (tokc / tg) token groups of compute
-// threads (<= 256) plus 4 producer warps.  Prefer more chains per thread
-// (tg) when the grid still fills the GPU; otherwise shrink tokens per CTA so
-// that enough SMs run chains in parallel (latency regime: Mixtral, Qwen).
+// Router CTA shape: expc experts x tokc tokens; each compute thread owns a
+// te x tt register tile of sequential fp64 chains; 4 producer warps stage
+// operands.  Large B*E (DeepSeek) is fp64-throughput bound: 2x2 tiles keep
+// shared-memory traffic under the DFMA rate.  Small B*E (Mixtral, Qwen) is
+// chain-latency bound: 1x1 tiles and few tokens per CTA spread the chains
+// over >= ~120 SMs.
 RouterPlan plan_router(const moe_b200_config& c, int64_t B, int x_bf16) {
   RouterPlan r{};
   const int E = c.num_experts;
   const int xb = x_bf16 ? 2 : 4;
   r.expc = std::min(E, 32);
   r.n_eblocks = (E + r.expc - 1) / r.expc;
-  const int maxg = 256 / r.expc;
   const int64_t target = (kNumSMs * 4) / 5;
-  auto smem_for = [&](int tokc, int groups) {
-    const int nthreads = ((r.expc * groups + 31) / 32) * 32 + kRouterProducers;
-    return RouterSmem::total_bytes(tokc, r.expc, xb, E, nthreads);
+  auto threads_for = [&](int tokc, int te, int tt) {
+    return ((r.expc / te) * (tokc / tt) + 31) / 32 * 32 + kRouterProducers;
+  };
+  auto smem_for = [&](int tokc, int te, int tt) {
+    return RouterSmem::total_bytes(tokc, r.expc, xb, E, threads_for(tokc, te, tt));
   };
   const size_t smem_cap = 200 * 1024;
-  r.tg = 0;
-  const int tgs[3] = {8, 4, 2};
-  for (int i = 0; i < 3 && !r.tg; ++i) {
-    int g = std::min(maxg, 64 / tgs[i]);
-    while (g > 1 && smem_for(tgs[i] * g, g) > smem_cap) g /= 2;
-    const int tokc = tgs[i] * g;
-    if (((B + tokc - 1) / tokc) * r.n_eblocks >= target && smem_for(tokc, g) <= smem_cap) {
-      r.tg = tgs[i];
-      r.tokc = tokc;
-    }
-  }
-  if (!r.tg) {
-    r.tg = 1;
+  const int64_t chains = B * (int64_t)E;
+  if (chains >= 64LL * 1024 && r.expc % 2 == 0) {
+    r.te = 2; r.tt = 2;
+    int tokc = 32;
+    while (tokc > 2 && (smem_for(tokc, 2, 2) > smem_cap || threads_for(tokc, 2, 2) > 384)) tokc /= 2;
+    r.tokc = tokc;
+  } else {
+    r.te = 1; r.tt = 1;
     int g = 1;
-    while (g * 2 <= std::min(maxg, 64) && ((B + g * 2 - 1) / (g * 2)) * r.n_eblocks >= target &&
-           smem_for(g * 2, g * 2) <= smem_cap)
+    while (g * 2 <= 256 / r.expc && ((B + g * 2 - 1) / (g * 2)) * r.n_eblocks >= target &&
+           smem_for(g * 2, 1, 1) <= smem_cap)
       g *= 2;
     r.tokc = g;
   }
-  const int groups = r.tokc / r.tg;
-  r.threads = ((r.expc * groups + 31) / 32) * 32 + kRouterProducers;
+  r.threads = threads_for(r.tokc, r.te, r.tt);
   r.n_tblocks = static_cast<int>((B + r.tokc - 1) / r.tokc);
-  r.smem = smem_for(r.tokc, groups);
+  r.smem = smem_for(r.tokc, r.te, r.tt);
   return r;
 }
 
-template <bool kBf16, int kTG>
+template <bool kBf16, int kTE, int kTT>
 int launch_router_t(const RouterParams& p, const RouterPlan& plan, cudaStream_t s) {
-  auto kern = router_kernel<kBf16, kTG>;
+  auto kern = router_kernel<kBf16, kTE, kTT>;
   MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
   kern<<<plan.n_tblocks * plan.n_eblocks, plan.threads, plan.smem, s>>>(p);
   MOE_LAUNCH_CHECK("router_kernel");
@@ -198,12 +195,8 @@ int launch_router_t(const RouterParams& p, const RouterPlan& plan, cudaStream_t 
 
 template <bool kBf16>
 int launch_router_x(const RouterParams& p, const RouterPlan& plan, cudaStream_t s) {
-  switch (plan.tg) {
-    case 1: return launch_router_t<kBf16, 1>(p, plan, s);
-    case 2: return launch_router_t<kBf16, 2>(p, plan, s);
-    case 4: return launch_router_t<kBf16, 4>(p, plan, s);
-    default: return launch_router_t<kBf16, 8>(p, plan, s);
-  }
+  if (plan.te == 2) return launch_router_t<kBf16, 2, 2>(p, plan, s);
+  return launch_router_t<kBf16, 1, 1>(p, plan, s);
 }
 
 template <int kBN, bool kGateUp>
@@ -310,7 +303,7 @@ int moe_b200_route(const moe_b200_config* cfg, int64_t B, const void* x, int x_d
   p.x = x; p.wr = w_router; p.x_bf16 = xb;
   p.B = static_cast<int>(B); p.d = cfg->hidden_dim; p.E = cfg->num_experts; p.k = cfg->top_k;
   p.gating = cfg->gating;
-  p.tokc = plan.tokc; p.expc = plan.expc; p.tg = plan.tg;
+  p.tokc = plan.tokc; p.expc = plan.expc;
   p.n_eblocks = plan.n_eblocks; p.n_tblocks = plan.n_tblocks;
   p.chunk_rows = chunk_rows_for(*cfg, B);
   p.logits = logits ? logits : reinterpret_cast<float*>(ws8(ws) + L.logits);

@@ -36,7 +36,7 @@ struct RouterParams {
   const float* wr;      // (d, E) fp32
   int x_bf16;
   int B, d, E, k, gating;
-  int tokc, expc, tg;   // CTA tile: tokc tokens x expc experts, tg chains per thread
+  int tokc, expc;       // CTA tile: tokc tokens x expc experts
   int n_eblocks, n_tblocks;
   int chunk_rows;       // GEMM row-chunk cap (BN)
   float* logits;        // (B, E) fp32
@@ -245,7 +245,7 @@ MOE_DEVICE void router_issue_chunk(const RouterParams& p, uint8_t* raw, int slot
 // [0, n_compute) own (expert lane, token group) chains; producer warps stage
 // and convert the operands one chunk ahead, synchronised by named barriers
 // FULL[b] (ids 1,2) and EMPTY[b] (ids 3,4); id 5 syncs the producers.
-template <bool kXBf16, int kTG>
+template <bool kXBf16, int kTE, int kTT>
 __global__ void __launch_bounds__(384)
 router_kernel(const RouterParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -316,33 +316,60 @@ router_kernel(const RouterParams p) {
     if (nonfinite_w) atomicOr(p.flags, 2u);
   } else {
     // ============================ compute chains ===========================
-    const int el = tid % p.expc;
-    const int tgi = tid / p.expc;
-    const int n_groups = p.tokc / kTG;
-    const bool active = (tgi < n_groups) && (e0 + el < p.E);
-    double acc[kTG];
+    // Thread tile: kTE experts x kTT tokens of independent sequential chains.
+    // Experts e0 + eg + i*n_eg, tokens t0 + tg + j*n_tg: the warp's w loads are
+    // contiguous and its x loads near-broadcast, so shared-memory wavefronts
+    // stay below the fp64 FMA rate; operands are register double-buffered
+    // U steps ahead of the dependent FMA chain.
+    constexpr int U = 8;
+    const int n_eg = p.expc / kTE;
+    const int n_tg = p.tokc / kTT;
+    const int eg = tid % n_eg;
+    const int tg = tid / n_eg;
+    const bool active = tg < n_tg;
+    double acc[kTE][kTT];
 #pragma unroll
-    for (int i = 0; i < kTG; ++i) acc[i] = -0.0;  // fma(a,b,-0) == a*b exactly, sign included
+    for (int i = 0; i < kTE; ++i)
+#pragma unroll
+      for (int j = 0; j < kTT; ++j) acc[i][j] = -0.0;  // fma(a,b,-0) == a*b exactly, sign included
+    constexpr int XS = kRouterKC + 1;  // padded fp64 x row
     for (int c = 0; c < nch; ++c) {
       const int b = c & 1;
       nbar_sync(1 + b, nbar);
       if (active) {
-        const double* dx = f64 + (size_t)b * (fx + fw);
-        const double* dw = dx + fx + el;
-        const double* xr = dx + (size_t)(tgi * kTG) * (kRouterKC + 1);
+        const double* dx = f64 + (size_t)b * (fx + fw) + (size_t)tg * XS;
+        const double* dw = f64 + (size_t)b * (fx + fw) + fx + eg;
+        const int xstep = n_tg * XS;
         const int kvalid = min(kRouterKC, p.d - c * kRouterKC);
         if (kvalid == kRouterKC) {
-#pragma unroll 16
-          for (int kk = 0; kk < kRouterKC; ++kk) {
-            const double w = dw[kk * p.expc];
+          double xa[kTT][U], wa[kTE][U], xb[kTT][U], wb[kTE][U];
+#define MOE_RLOAD(KK, XV, WV)                                                           \
+  _Pragma("unroll") for (int u = 0; u < U; ++u) {                                       \
+    _Pragma("unroll") for (int j = 0; j < kTT; ++j) XV[j][u] = dx[j * xstep + (KK) + u]; \
+    _Pragma("unroll") for (int i = 0; i < kTE; ++i) WV[i][u] = dw[((KK) + u) * p.expc + i * n_eg]; \
+  }
+#define MOE_RFMA(XV, WV)                                                                \
+  _Pragma("unroll") for (int u = 0; u < U; ++u)                                         \
+    _Pragma("unroll") for (int i = 0; i < kTE; ++i)                                     \
+      _Pragma("unroll") for (int j = 0; j < kTT; ++j) acc[i][j] = __fma_rn(XV[j][u], WV[i][u], acc[i][j]);
+          MOE_RLOAD(0, xa, wa);
 #pragma unroll
-            for (int i = 0; i < kTG; ++i) acc[i] = __fma_rn(xr[i * (kRouterKC + 1) + kk], w, acc[i]);
+          for (int kk = 0; kk < kRouterKC; kk += 2 * U) {
+            MOE_RLOAD(kk + U, xb, wb);
+            MOE_RFMA(xa, wa);
+            if (kk + 2 * U < kRouterKC) { MOE_RLOAD(kk + 2 * U, xa, wa); }
+            MOE_RFMA(xb, wb);
           }
+#undef MOE_RLOAD
+#undef MOE_RFMA
         } else {
           for (int kk = 0; kk < kvalid; ++kk) {
-            const double w = dw[kk * p.expc];
 #pragma unroll
-            for (int i = 0; i < kTG; ++i) acc[i] = __fma_rn(xr[i * (kRouterKC + 1) + kk], w, acc[i]);
+            for (int i = 0; i < kTE; ++i) {
+              const double w = dw[kk * p.expc + i * n_eg];
+#pragma unroll
+              for (int j = 0; j < kTT; ++j) acc[i][j] = __fma_rn(dx[j * xstep + kk], w, acc[i][j]);
+            }
           }
         }
       }
@@ -350,9 +377,14 @@ router_kernel(const RouterParams p) {
     }
     if (active) {
 #pragma unroll
-      for (int i = 0; i < kTG; ++i) {
-        const int t = t0 + tgi * kTG + i;
-        if (t < p.B) p.logits[(size_t)t * p.E + e0 + el] = __double2float_rn(acc[i]);
+      for (int i = 0; i < kTE; ++i) {
+        const int e = e0 + eg + i * n_eg;
+#pragma unroll
+        for (int j = 0; j < kTT; ++j) {
+          const int t = t0 + tg + j * n_tg;
+          if (t < p.B && e < p.E && eg + i * n_eg < p.expc)
+            p.logits[(size_t)t * p.E + e] = __double2float_rn(acc[i][j]);
+        }
       }
     }
   }
