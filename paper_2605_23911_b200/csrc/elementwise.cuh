@@ -73,4 +73,47 @@ combine_kernel(const float* __restrict__ ys, void* __restrict__ y, int B, int k,
   }
 }
 
+// Fused-forward combine: the down tiles wrote raw K-split partials P[s] at
+// the expanded slot.  y[t] = sum_j fl(w[t,j] * (sum_s P[s][t*k+j])),
+// ascending j and s, fp32 — the reference's out += w_j * g_j order
+// (pipeline.py:396-399) with g_j's K-split summed first.
+template <bool kBf16Out>
+__global__ void __launch_bounds__(kRowThreads)
+combine_partials_kernel(const float* __restrict__ ys, int splits, size_t split_stride,
+                        const float* __restrict__ topk_w, void* __restrict__ y, int B, int k, int d) {
+  const int vec_per_row = d / 4;
+  const long total = (long)B * vec_per_row;
+  for (long i = (long)blockIdx.x * kRowThreads + threadIdx.x; i < total;
+       i += (long)gridDim.x * kRowThreads) {
+    const int t = static_cast<int>(i / vec_per_row);
+    const int v = static_cast<int>(i % vec_per_row);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < k; ++j) {
+      const size_t row = (size_t)t * k + j;
+      const float w = __ldg(topk_w + row);
+      const float4* src = reinterpret_cast<const float4*>(ys + row * d) + v;
+      float4 g = __ldg(src);
+      for (int s = 1; s < splits; ++s) {
+        float4 a = __ldg(src + s * (split_stride / 4));
+        g.x = __fadd_rn(g.x, a.x); g.y = __fadd_rn(g.y, a.y);
+        g.z = __fadd_rn(g.z, a.z); g.w = __fadd_rn(g.w, a.w);
+      }
+      acc.x = __fadd_rn(acc.x, __fmul_rn(w, g.x));
+      acc.y = __fadd_rn(acc.y, __fmul_rn(w, g.y));
+      acc.z = __fadd_rn(acc.z, __fmul_rn(w, g.z));
+      acc.w = __fadd_rn(acc.w, __fmul_rn(w, g.w));
+    }
+    if (kBf16Out) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y);
+      __nv_bfloat162 p1 = __floats2bfloat162_rn(acc.z, acc.w);
+      uint2 o;
+      o.x = *reinterpret_cast<uint32_t*>(&p0);
+      o.y = *reinterpret_cast<uint32_t*>(&p1);
+      reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(y) + (size_t)t * d)[v] = o;
+    } else {
+      reinterpret_cast<float4*>(static_cast<float*>(y) + (size_t)t * d)[v] = acc;
+    }
+  }
+}
+
 }  // namespace moe

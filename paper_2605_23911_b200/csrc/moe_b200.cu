@@ -11,7 +11,7 @@
 
 #include "common.cuh"
 #include "elementwise.cuh"
-#include "grouped_gemm.cuh"
+#include "ffn.cuh"
 #include "router.cuh"
 
 using namespace moe;
@@ -41,22 +41,41 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 constexpr size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-constexpr int kTbCap = 4096;  // max router token blocks per launch
+constexpr int kTbCap = 4096;      // max router token blocks per launch
+constexpr int kChunkCap = 8192;   // max expert row-chunks per launch
 
-// Fixed header at the start of the workspace (zeroed by workspace_init):
-//   [0] flags  [1] done_counter  [2] n_chunks  [16, 16 + kTbCap) token-block counters
-constexpr size_t kHeaderBytes = align256((16 + kTbCap) * sizeof(int32_t));
+// Fixed header at the start of the workspace (zeroed by workspace_init; every
+// kernel leaves its counters zeroed again):
+//   [0] flags  [1] router done counter  [2] n_chunks  [3] ffn work counter
+//   [4] ffn exit counter  [16, 16+kTbCap) router token-block counters
+//   [16+kTbCap, 16+kTbCap+kChunkCap) per-chunk gate+up completion counters
+constexpr int kHdrTb = 16;
+constexpr int kHdrGuDone = 16 + kTbCap;
+constexpr size_t kHeaderBytes = align256((16 + kTbCap + kChunkCap) * sizeof(int32_t));
 
 struct Layout {
   size_t logits, chunk_tab, xp, h, ys, total;
-  int max_chunks;
+  int max_chunks, splits, kb_per_split;
 };
 
 int chunk_rows_for(const moe_b200_config& c, int64_t B) {
   // Tokens per expert on average; big chunks keep one weight pass per expert
-  // (Mixtral), small chunks allow shallower TMEM use (DeepSeek / Qwen).
+  // (Mixtral), small chunks for many-expert layers (DeepSeek / Qwen).
   const int64_t T = B * c.top_k;
   return (T > 96LL * c.num_experts) ? 256 : 128;
+}
+
+// K splits of a down tile so that down tiles stream about as many weight
+// bytes as a gate+up tile (128 x d x 2 matrices): one HBM-stream granularity
+// for the dynamic queue.  Partials are reduced deterministically in combine.
+void down_splits(const moe_b200_config& c, int* splits, int* kb_per_split) {
+  const int nkb = (c.ffn_dim + kBK - 1) / kBK;
+  int s = static_cast<int>((c.ffn_dim + c.hidden_dim) / (2 * c.hidden_dim));  // round(f / 2d)
+  s = std::max(1, std::min(s, 4));
+  s = std::min(s, nkb);
+  int kps = (nkb + s - 1) / s;
+  *kb_per_split = kps;
+  *splits = (nkb + kps - 1) / kps;
 }
 
 Layout layout_for(const moe_b200_config& c, int64_t B) {
@@ -64,12 +83,13 @@ Layout layout_for(const moe_b200_config& c, int64_t B) {
   const int64_t T = B * c.top_k;
   const int bn = chunk_rows_for(c, B);
   L.max_chunks = static_cast<int>(std::min<int64_t>(c.num_experts, T) + T / bn + 1);
+  down_splits(c, &L.splits, &L.kb_per_split);
   size_t off = kHeaderBytes;
   L.logits = off;    off = align256(off + (size_t)B * c.num_experts * sizeof(float));
   L.chunk_tab = off; off = align256(off + (size_t)L.max_chunks * sizeof(int4));
   L.xp = off;        off = align256(off + (size_t)T * c.hidden_dim * 2);
   L.h = off;         off = align256(off + (size_t)T * c.ffn_dim * 2);
-  L.ys = off;        off = align256(off + (size_t)T * c.hidden_dim * sizeof(float));
+  L.ys = off;        off = align256(off + (size_t)L.splits * T * c.hidden_dim * sizeof(float));
   L.total = off;
   return L;
 }
@@ -199,14 +219,52 @@ int launch_router_x(const RouterParams& p, const RouterPlan& plan, cudaStream_t 
   return launch_router_t<kBf16, 1, 1>(p, plan, s);
 }
 
-template <int kBN, bool kGateUp>
-int launch_gemm_t(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
-                  const GemmParams& gp, int grid, cudaStream_t s) {
-  using C = GemmCfg<kBN, kGateUp>;
-  auto kern = grouped_gemm_kernel<kBN, kGateUp>;
-  MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
-  kern<<<grid, kGemmThreads, C::kSmemBytes, s>>>(a0, a1, b, gp);
-  MOE_LAUNCH_CHECK(kGateUp ? "grouped_gemm_kernel<gate_up>" : "grouped_gemm_kernel<down>");
+int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, const void* xp,
+               const void* w_gate, const void* w_up, const void* w_down, void* h, float* ys,
+               const float* topk_w, const int32_t* fwd, bool do_gu, bool do_dn, bool fused,
+               cudaStream_t s) {
+  const int E = c.num_experts, d = c.hidden_dim, f = c.ffn_dim;
+  const int64_t T = B * c.top_k;
+  CUtensorMap m_wg, m_wu, m_xp, m_wd, m_h;
+  int rc;
+  const void* any_w = do_gu ? w_gate : w_down;
+  if ((rc = make_map_bf16(&m_wg, do_gu ? w_gate : any_w, do_gu ? (uint64_t)E * d : (uint64_t)E * f,
+                          do_gu ? f : d, 64, 64))) return rc;
+  if ((rc = make_map_bf16(&m_wu, do_gu ? w_up : any_w, do_gu ? (uint64_t)E * d : (uint64_t)E * f,
+                          do_gu ? f : d, 64, 64))) return rc;
+  if ((rc = make_map_bf16(&m_wd, do_dn ? w_down : any_w, do_dn ? (uint64_t)E * f : (uint64_t)E * d,
+                          do_dn ? d : f, 64, 64))) return rc;
+  if ((rc = make_map_bf16(&m_xp, do_gu ? xp : h, T, do_gu ? d : f, 64, kBoxRows))) return rc;
+  if ((rc = make_map_bf16(&m_h, do_dn ? h : xp, T, do_dn ? f : d, 64, kBoxRows))) return rc;
+  int32_t* hdr = reinterpret_cast<int32_t*>(ws);
+  FfnParams p{};
+  p.chunk_tab = reinterpret_cast<const int4*>(static_cast<uint8_t*>(ws) + L.chunk_tab);
+  p.n_chunks = hdr + 2;
+  p.n_mt_gu = do_gu ? (f + kBM - 1) / kBM : 0;
+  p.n_mt_dn = do_dn ? (d + kBM - 1) / kBM : 0;
+  p.splits = fused ? L.splits : 1;
+  p.kb_per_split = fused ? L.kb_per_split : (f + kBK - 1) / kBK;
+  p.d = d; p.f = f; p.T = static_cast<int>(T);
+  p.h = static_cast<__nv_bfloat16*>(h);
+  p.ys = ys;
+  p.topk_w = topk_w;
+  p.fwd = fwd;
+  p.scale_by_w = fused ? 0 : 1;
+  p.gu_wait = fused ? 1 : 0;
+  p.work_counter = hdr + 3;
+  p.exit_counter = hdr + 4;
+  p.gu_done = hdr + kHdrGuDone;
+  const long max_tiles = (long)L.max_chunks * (p.n_mt_gu + p.n_mt_dn * p.splits);
+  const int grid = static_cast<int>(std::max(1L, std::min<long>(kNumSMs, max_tiles)));
+  static bool attr_set[64] = {};
+  int dev = 0;
+  MOE_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    MOE_CUDA(cudaFuncSetAttribute(ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FfnCfg::kSmemBytes));
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  ffn_kernel<<<grid, kFfnThreads, FfnCfg::kSmemBytes, s>>>(m_wg, m_wu, m_xp, m_wd, m_h, p);
+  MOE_LAUNCH_CHECK("ffn_kernel");
   return MOE_B200_OK;
 }
 
@@ -311,7 +369,7 @@ int moe_b200_route(const moe_b200_config* cfg, int64_t B, const void* x, int x_d
   p.fwd = perm_fwd; p.inv = perm_inv;
   p.chunk_tab = reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab);
   p.n_chunks = hdr + 2;
-  p.tb_counter = hdr + 16;
+  p.tb_counter = hdr + kHdrTb;
   p.done_counter = hdr + 1;
   p.flags = reinterpret_cast<uint32_t*>(hdr);
   return xb ? launch_router_x<true>(p, plan, s) : launch_router_x<false>(p, plan, s);
@@ -346,23 +404,9 @@ int moe_b200_gate_up(const moe_b200_config* cfg, int64_t B, const void* xp, cons
   Layout L;
   if ((rc = check_ws(cfg, B, ws, ws_bytes, &L))) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int E = cfg->num_experts, d = cfg->hidden_dim, f = cfg->ffn_dim;
-  const int64_t T = B * cfg->top_k;
-  CUtensorMap ma0, ma1, mb;
-  if ((rc = make_map_bf16(&ma0, w_gate, (uint64_t)E * d, f, 64, 64))) return rc;
-  if ((rc = make_map_bf16(&ma1, w_up, (uint64_t)E * d, f, 64, 64))) return rc;
-  if ((rc = make_map_bf16(&mb, xp, T, d, 64, kBoxRows))) return rc;
-  GemmParams gp{};
-  gp.chunk_tab = reinterpret_cast<const int4*>(ws8(ws) + L.chunk_tab);
-  gp.n_chunks = reinterpret_cast<const int32_t*>(ws) + 2;
-  gp.n_mtiles = (f + kBM - 1) / kBM;
-  gp.K = d;
-  gp.out_features = f;
-  gp.h = static_cast<__nv_bfloat16*>(h);
-  const long max_tiles = (long)L.max_chunks * gp.n_mtiles;
-  const int grid = static_cast<int>(std::min<long>(kNumSMs, max_tiles));
-  if (chunk_rows_for(*cfg, B) == 256) return launch_gemm_t<256, true>(ma0, ma1, mb, gp, grid, s);
-  return launch_gemm_t<128, true>(ma0, ma1, mb, gp, grid, s);
+  if (L.max_chunks > kChunkCap) return MOE_B200_ERR_UNSUPPORTED;
+  return launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, nullptr, h, nullptr, nullptr, nullptr,
+                    /*gu*/ true, /*dn*/ false, /*fused*/ false, s);
 }
 
 int moe_b200_down_scatter(const moe_b200_config* cfg, int64_t B, const void* h, const void* w_down,
@@ -375,24 +419,9 @@ int moe_b200_down_scatter(const moe_b200_config* cfg, int64_t B, const void* h, 
   Layout L;
   if ((rc = check_ws(cfg, B, ws, ws_bytes, &L))) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int E = cfg->num_experts, d = cfg->hidden_dim, f = cfg->ffn_dim;
-  const int64_t T = B * cfg->top_k;
-  CUtensorMap ma0, mb;
-  if ((rc = make_map_bf16(&ma0, w_down, (uint64_t)E * f, d, 64, 64))) return rc;
-  if ((rc = make_map_bf16(&mb, h, T, f, 64, kBoxRows))) return rc;
-  GemmParams gp{};
-  gp.chunk_tab = reinterpret_cast<const int4*>(ws8(ws) + L.chunk_tab);
-  gp.n_chunks = reinterpret_cast<const int32_t*>(ws) + 2;
-  gp.n_mtiles = (d + kBM - 1) / kBM;
-  gp.K = f;
-  gp.out_features = d;
-  gp.ys = ys;
-  gp.topk_w = topk_w;
-  gp.fwd = perm_fwd;
-  const long max_tiles = (long)L.max_chunks * gp.n_mtiles;
-  const int grid = static_cast<int>(std::min<long>(kNumSMs, max_tiles));
-  if (chunk_rows_for(*cfg, B) == 256) return launch_gemm_t<256, false>(ma0, ma0, mb, gp, grid, s);
-  return launch_gemm_t<128, false>(ma0, ma0, mb, gp, grid, s);
+  if (L.max_chunks > kChunkCap) return MOE_B200_ERR_UNSUPPORTED;
+  return launch_ffn(*cfg, B, L, ws, nullptr, nullptr, nullptr, w_down, const_cast<void*>(h), ys,
+                    topk_w, perm_fwd, /*gu*/ false, /*dn*/ true, /*fused*/ false, s);
 }
 
 int moe_b200_combine(const moe_b200_config* cfg, int64_t B, const float* ys, void* y, int y_dtype,
@@ -431,10 +460,22 @@ int moe_b200_forward(const moe_b200_config* cfg, int64_t B, const void* x, int x
   void* h = ws8(ws) + L.h;
   float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);
   if ((rc = moe_b200_permute(cfg, B, x, x_dtype, perm_fwd, xp, stream))) return rc;
-  if ((rc = moe_b200_gate_up(cfg, B, xp, w_gate, w_up, h, ws, ws_bytes, stream))) return rc;
-  if ((rc = moe_b200_down_scatter(cfg, B, h, w_down, topk_w, perm_fwd, ys, ws, ws_bytes, stream)))
+  if (L.max_chunks > kChunkCap) return MOE_B200_ERR_UNSUPPORTED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
+                       /*gu*/ true, /*dn*/ true, /*fused*/ true, s)))
     return rc;
-  return moe_b200_combine(cfg, B, ys, y, y_dtype, stream);
+  const int d = cfg->hidden_dim;
+  const int grid = grid_for_rows((long)B * (d / 4));
+  const size_t stride = (size_t)B * cfg->top_k * d;
+  if (y_dtype == MOE_B200_DTYPE_F32)
+    combine_partials_kernel<false><<<grid, kRowThreads, 0, s>>>(ys, L.splits, stride, topk_w, y, (int)B, cfg->top_k, d);
+  else if (y_dtype == MOE_B200_DTYPE_BF16)
+    combine_partials_kernel<true><<<grid, kRowThreads, 0, s>>>(ys, L.splits, stride, topk_w, y, (int)B, cfg->top_k, d);
+  else
+    return MOE_B200_ERR_INVALID_VALUE;
+  MOE_LAUNCH_CHECK("combine_partials_kernel");
+  return MOE_B200_OK;
 }
 
 }  // extern "C"
