@@ -55,7 +55,19 @@ struct FfnParams {
   int32_t* work_counter;     // self-resetting
   int32_t* exit_counter;     // self-resetting
   int32_t* gu_done;          // per-chunk completed gate+up tiles, self-resetting
+  unsigned long long* trace; // optional (debug): per tile {sm, t_fetch, t_first_load, t_done}
 };
+
+MOE_DEVICE unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+MOE_DEVICE uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 
 struct FfnCfg {
   static constexpr int kABytes = kBM * kBK * 2;  // 16 KB: one 128x64 weight tile
@@ -173,6 +185,10 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       uint32_t sphase = 0;
       while (true) {
         const int tile = atomicAdd(p.work_counter, 1);
+        if (p.trace && tile < total_tiles) {
+          p.trace[tile * 4 + 0] = smid();
+          p.trace[tile * 4 + 1] = globaltimer();
+        }
         mbar_wait(sched_empty + slot, sphase ^ 1);
         sched_tile[slot] = tile < total_tiles ? tile : -1;
         mbar_arrive(sched_full + slot);
@@ -196,6 +212,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             fence_proxy_async_global();
           }
         }
+        if (p.trace) p.trace[tile * 4 + 2] = globaltimer();
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty_bar + stage, phase ^ 1);
           uint8_t* st = smem + stage * C::kStageBytes;
@@ -338,6 +355,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         tc_fence_before();
         mbar_arrive(tmem_empty);
       }
+      if (p.trace && wq == 0 && lane == 0) p.trace[tile * 4 + 3] = globaltimer();
       acc_phase ^= 1;
     }
   }

@@ -159,6 +159,7 @@ int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 }
 
 // ------------------------------- launches --------------------------------------
+unsigned long long* g_ffn_trace = nullptr;  // debug: per-tile timeline of the next ffn launches
 struct RouterPlan {
   int expc, te, tt, tokc, n_eblocks, n_tblocks, threads;
   size_t smem;
@@ -254,6 +255,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.work_counter = hdr + 3;
   p.exit_counter = hdr + 4;
   p.gu_done = hdr + kHdrGuDone;
+  p.trace = g_ffn_trace;
   const long max_tiles = (long)L.max_chunks * (p.n_mt_gu + p.n_mt_dn * p.splits);
   const int grid = static_cast<int>(std::max(1L, std::min<long>(kNumSMs, max_tiles)));
   static bool attr_set[64] = {};
@@ -284,6 +286,10 @@ uint8_t* ws8(void* ws) { return static_cast<uint8_t*>(ws); }
 extern "C" {
 
 const char* moe_b200_version(void) { return "moe_b200 0.1.0 (sm_100a)"; }
+
+// Debug hook (not part of the public header): record a per-tile timeline of
+// subsequent ffn launches into a device buffer of 4 u64 per tile, or NULL to stop.
+void moe_b200_debug_set_ffn_trace(unsigned long long* dev_buf) { g_ffn_trace = dev_buf; }
 
 const char* moe_b200_last_error_detail(void) { return g_last_error.c_str(); }
 
