@@ -96,6 +96,14 @@ MOE_DEVICE void tma_load_2d_hint(const CUtensorMap* map, uint64_t* bar, void* ds
       : "memory");
 }
 
+// Prefetch a 2-D tile into L2 (no shared memory, no completion tracking).
+MOE_DEVICE void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 MOE_DEVICE uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

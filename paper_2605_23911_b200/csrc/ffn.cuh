@@ -36,6 +36,7 @@ constexpr int kBM = 128;        // weight rows (output features) per tile
 constexpr int kBK = 64;         // K per stage: one 128-byte swizzle row of bf16
 constexpr int kBoxRows = 32;    // token rows per TMA box
 constexpr int kSchedSlots = 4;  // tile-id ring between scheduler and consumers
+constexpr int kPrefetchBytes = 256 * 1024;  // L2 prefetch distance of the weight stream per SM
 
 struct FfnParams {
   const int4* chunk_tab;     // {expert, row0, nrows, 0} per token chunk
@@ -177,43 +178,101 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
 
   if (warp == 0) {
     // ====================== scheduler + TMA producer ========================
+    // Tile ids are fetched one tile ahead so the weight stream of the next
+    // tile is already being prefetched into L2 while this one finishes: the
+    // weight tensor is streamed with cp.async.bulk.prefetch.tensor ~kPrefetchBytes
+    // ahead of the smem TMA loads, which raises the bytes in flight per SM far
+    // beyond the 3 smem stages (HBM latency x 44 GB/s per SM).
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
       int slot = 0;
       uint32_t sphase = 0;
-      while (true) {
-        const int tile = atomicAdd(p.work_counter, 1);
-        if (p.trace && tile < total_tiles) {
-          p.trace[tile * 4 + 0] = smid();
-          p.trace[tile * 4 + 1] = globaltimer();
+      auto fetch = [&]() -> int {
+        const int t = atomicAdd(p.work_counter, 1);
+        if (p.trace && t < total_tiles) {
+          p.trace[t * 4 + 0] = smid();
+          p.trace[t * 4 + 1] = globaltimer();
         }
+        return t < total_tiles ? t : -1;
+      };
+      auto kb_range = [&](const TileInfo& ti, int& kb0, int& kb1) {
+        if (ti.is_gu) { kb0 = 0; kb1 = nkb_gu; }
+        else { kb0 = ti.split * p.kb_per_split; kb1 = min(nkb_dn, kb0 + p.kb_per_split); }
+      };
+      // L2 prefetch of the weight boxes of k-block kb of a tile
+      auto prefetch_w = [&](const TileInfo& ti, const int4& ch, int kb) {
+        const int a_col = ti.mt * kBM;
+        if (ti.is_gu) {
+          const int krow = ch.x * p.d + kb * kBK;
+          tma_prefetch_l2_2d(&tm_wg, a_col, krow);
+          tma_prefetch_l2_2d(&tm_wg, a_col + 64, krow);
+          tma_prefetch_l2_2d(&tm_wu, a_col, krow);
+          tma_prefetch_l2_2d(&tm_wu, a_col + 64, krow);
+        } else {
+          const int krow = ch.x * p.f + kb * kBK;
+          tma_prefetch_l2_2d(&tm_wd, a_col, krow);
+          tma_prefetch_l2_2d(&tm_wd, a_col + 64, krow);
+        }
+      };
+      int tile = fetch();
+      TileInfo ti{};
+      int4 ch{};
+      int kb0 = 0, kb1 = 0;
+      if (tile >= 0) {
+        ti = decode_tile(p, tile);
+        ch = __ldg(p.chunk_tab + ti.chunk);
+        kb_range(ti, kb0, kb1);
+      }
+      auto pd_for = [&](const TileInfo& t) {
+        return t.is_gu ? kPrefetchBytes / (2 * FfnCfg::kABytes) : kPrefetchBytes / FfnCfg::kABytes;
+      };
+      int pd = tile >= 0 ? pd_for(ti) : 0;  // prefetch distance (k-blocks) of the current tile
+      int pf_cur = 0;                          // blocks of the current tile already prefetched
+      while (true) {
         mbar_wait(sched_empty + slot, sphase ^ 1);
-        sched_tile[slot] = tile < total_tiles ? tile : -1;
+        sched_tile[slot] = tile;
         mbar_arrive(sched_full + slot);
         if (++slot == kSchedSlots) { slot = 0; sphase ^= 1; }
-        if (tile >= total_tiles) break;
-        const TileInfo ti = decode_tile(p, tile);
-        const int4 ch = __ldg(p.chunk_tab + ti.chunk);
+        if (tile < 0) break;
+        // the next tile is claimed only when the prefetch front reaches the end of
+        // this one, so tiles are not reserved long before a CTA can start them
+        int nxt = -2;
+        TileInfo tn{};
+        int4 cn{};
+        int nk0 = 0, nk1 = 0;
+        auto claim_next = [&]() {
+          nxt = fetch();
+          if (nxt >= 0) {
+            tn = decode_tile(p, nxt);
+            cn = __ldg(p.chunk_tab + tn.chunk);
+            kb_range(tn, nk0, nk1);
+          }
+        };
         const int n_mma = max(16, (ch.z + 15) & ~15);
         const int nbox = (n_mma + kBoxRows - 1) / kBoxRows;
         const uint32_t b_bytes = nbox * kBoxRows * kBK * 2;
         const int a_col = ti.mt * kBM;
-        int kb0, kb1;
-        if (ti.is_gu) {
-          kb0 = 0; kb1 = nkb_gu;
-        } else {
-          kb0 = ti.split * p.kb_per_split;
-          kb1 = min(nkb_dn, kb0 + p.kb_per_split);
-          if (p.gu_wait) {
-            // h rows of this chunk are complete once all its gate+up tiles released
-            while (ld_acquire_gpu(p.gu_done + ti.chunk) < p.n_mt_gu) __nanosleep(64);
-            fence_proxy_async_global();
-          }
+        if (!ti.is_gu && p.gu_wait) {
+          // h rows of this chunk are complete once all its gate+up tiles released
+          while (ld_acquire_gpu(p.gu_done + ti.chunk) < p.n_mt_gu) __nanosleep(64);
+          fence_proxy_async_global();
         }
         if (p.trace) p.trace[tile * 4 + 2] = globaltimer();
+        const int len = kb1 - kb0;
+        int pf_nxt = 0;
         for (int kb = kb0; kb < kb1; ++kb) {
+          // keep the L2 prefetch front pd blocks ahead, running into the next tile
+          const int target = kb - kb0 + pd + 1;
+          while (pf_cur < min(len, target)) prefetch_w(ti, ch, kb0 + pf_cur++);
+          if (target > len) {
+            if (nxt == -2) claim_next();
+            if (nxt >= 0) {
+              const int extra = min(min(nk1 - nk0, pd_for(tn)), target - len);
+              while (pf_nxt < extra) prefetch_w(tn, cn, nk0 + pf_nxt++);
+            }
+          }
           mbar_wait(empty_bar + stage, phase ^ 1);
           uint8_t* st = smem + stage * C::kStageBytes;
           uint8_t* sb = st + 2 * C::kABytes;
@@ -236,6 +295,14 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
+        if (nxt == -2) claim_next();
+        pf_cur = pf_nxt;
+        tile = nxt;
+        ti = tn;
+        ch = cn;
+        kb0 = nk0;
+        kb1 = nk1;
+        pd = nxt >= 0 ? pd_for(tn) : 0;
       }
     }
   } else if (warp == 1) {
