@@ -36,7 +36,6 @@ constexpr int kBM = 128;        // weight rows (output features) per tile
 constexpr int kBK = 64;         // K per stage: one 128-byte swizzle row of bf16
 constexpr int kBoxRows = 32;    // token rows per TMA box
 constexpr int kSchedSlots = 4;  // tile-id ring between scheduler and consumers
-constexpr int kPrefetchBytes = 256 * 1024;  // L2 prefetch distance of the weight stream per SM
 
 struct FfnParams {
   const int4* chunk_tab;     // {expert, row0, nrows, 0} per token chunk
@@ -70,13 +69,22 @@ MOE_DEVICE uint32_t smid() {
   return r;
 }
 
+// Shared memory: a ring of 16 KB weight slots (one 128 x 64 bf16 MN-major
+// tile each) decoupled from a ring of token slots (kBN x 64 bf16).  A
+// gate+up k-block takes two weight slots and one token slot, a down k-block
+// one of each, so the weight bytes in flight per SM (the HBM-latency x
+// bandwidth product) no longer shrink with the token tile: 8-10 slots keep
+// 128-160 KB of weights outstanding for either tile type.
+template <int kBN>
 struct FfnCfg {
-  static constexpr int kABytes = kBM * kBK * 2;  // 16 KB: one 128x64 weight tile
-  static constexpr int kBBytes = 256 * kBK * 2;  // 32 KB: up to 256 token rows
-  static constexpr int kStageBytes = 2 * kABytes + kBBytes;
-  static constexpr int kStages = 3;
-  static constexpr uint32_t kTmemCols = 512;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int kABytes = kBM * kBK * 2;      // 16 KB weight slot
+  static constexpr int kBBytes = kBN * kBK * 2;      // token slot
+  static constexpr int kAStages = kBN == 256 ? 8 : 10;
+  static constexpr int kBStages = kBN == 256 ? 3 : 4;
+  static constexpr int kRingBytes = kAStages * kABytes + kBStages * kBBytes;
+  static constexpr uint32_t kTmemCols = 2 * kBN <= 256 ? 256 : 512;
+  static constexpr int kSmemBytes = kRingBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static_assert(kSmemBytes <= 232448, "shared memory");
 };
 
 MOE_DEVICE float silu_mul(float g, float u) {
@@ -126,16 +134,21 @@ MOE_DEVICE TileInfo decode_tile(const FfnParams& p, int tile) {
   return t;
 }
 
+template <int kBN>
 __global__ void __launch_bounds__(kFfnThreads, 1)
 ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CUtensorMap tm_wu,
            const __grid_constant__ CUtensorMap tm_xp, const __grid_constant__ CUtensorMap tm_wd,
            const __grid_constant__ CUtensorMap tm_h, const FfnParams p) {
-  using C = FfnCfg;
+  using C = FfnCfg<kBN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
-  uint64_t* empty_bar = full_bar + C::kStages;
-  uint64_t* tmem_full = empty_bar + C::kStages;
+  uint8_t* a_ring = smem;
+  uint8_t* b_ring = smem + C::kAStages * C::kABytes;
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + C::kRingBytes);
+  uint64_t* a_empty = a_full + C::kAStages;
+  uint64_t* b_full = a_empty + C::kAStages;
+  uint64_t* b_empty = b_full + C::kBStages;
+  uint64_t* tmem_full = b_empty + C::kBStages;
   uint64_t* tmem_empty = tmem_full + 1;
   uint64_t* sched_full = tmem_empty + 1;
   uint64_t* sched_empty = sched_full + kSchedSlots;
@@ -153,9 +166,13 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
     tma_prefetch_desc(&tm_h);
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(full_bar + s, 1);
-      mbar_init(empty_bar + s, 1);
+    for (int s = 0; s < C::kAStages; ++s) {
+      mbar_init(a_full + s, 1);
+      mbar_init(a_empty + s, 1);
+    }
+    for (int s = 0; s < C::kBStages; ++s) {
+      mbar_init(b_full + s, 1);
+      mbar_init(b_empty + s, 1);
     }
     mbar_init(tmem_full, 1);
     mbar_init(tmem_empty, 128);
@@ -178,137 +195,80 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
 
   if (warp == 0) {
     // ====================== scheduler + TMA producer ========================
-    // Tile ids are fetched one tile ahead so the weight stream of the next
-    // tile is already being prefetched into L2 while this one finishes: the
-    // weight tensor is streamed with cp.async.bulk.prefetch.tensor ~kPrefetchBytes
-    // ahead of the smem TMA loads, which raises the bytes in flight per SM far
-    // beyond the 3 smem stages (HBM latency x 44 GB/s per SM).
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0;
+      int as = 0, bs = 0;
+      uint32_t aph = 0, bph = 0;
       int slot = 0;
       uint32_t sphase = 0;
-      auto fetch = [&]() -> int {
-        const int t = atomicAdd(p.work_counter, 1);
-        if (p.trace && t < total_tiles) {
-          p.trace[t * 4 + 0] = smid();
-          p.trace[t * 4 + 1] = globaltimer();
-        }
-        return t < total_tiles ? t : -1;
-      };
-      auto kb_range = [&](const TileInfo& ti, int& kb0, int& kb1) {
-        if (ti.is_gu) { kb0 = 0; kb1 = nkb_gu; }
-        else { kb0 = ti.split * p.kb_per_split; kb1 = min(nkb_dn, kb0 + p.kb_per_split); }
-      };
-      // L2 prefetch of the weight boxes of k-block kb of a tile
-      auto prefetch_w = [&](const TileInfo& ti, const int4& ch, int kb) {
-        const int a_col = ti.mt * kBM;
-        if (ti.is_gu) {
-          const int krow = ch.x * p.d + kb * kBK;
-          tma_prefetch_l2_2d(&tm_wg, a_col, krow);
-          tma_prefetch_l2_2d(&tm_wg, a_col + 64, krow);
-          tma_prefetch_l2_2d(&tm_wu, a_col, krow);
-          tma_prefetch_l2_2d(&tm_wu, a_col + 64, krow);
-        } else {
-          const int krow = ch.x * p.f + kb * kBK;
-          tma_prefetch_l2_2d(&tm_wd, a_col, krow);
-          tma_prefetch_l2_2d(&tm_wd, a_col + 64, krow);
-        }
-      };
-      int tile = fetch();
-      TileInfo ti{};
-      int4 ch{};
-      int kb0 = 0, kb1 = 0;
-      if (tile >= 0) {
-        ti = decode_tile(p, tile);
-        ch = __ldg(p.chunk_tab + ti.chunk);
-        kb_range(ti, kb0, kb1);
-      }
-      auto pd_for = [&](const TileInfo& t) {
-        return t.is_gu ? kPrefetchBytes / (2 * FfnCfg::kABytes) : kPrefetchBytes / FfnCfg::kABytes;
-      };
-      int pd = tile >= 0 ? pd_for(ti) : 0;  // prefetch distance (k-blocks) of the current tile
-      int pf_cur = 0;                          // blocks of the current tile already prefetched
       while (true) {
+        const int tile = atomicAdd(p.work_counter, 1);
+        if (p.trace && tile < total_tiles) {
+          p.trace[tile * 4 + 0] = smid();
+          p.trace[tile * 4 + 1] = globaltimer();
+        }
         mbar_wait(sched_empty + slot, sphase ^ 1);
-        sched_tile[slot] = tile;
+        sched_tile[slot] = tile < total_tiles ? tile : -1;
         mbar_arrive(sched_full + slot);
         if (++slot == kSchedSlots) { slot = 0; sphase ^= 1; }
-        if (tile < 0) break;
-        // the next tile is claimed only when the prefetch front reaches the end of
-        // this one, so tiles are not reserved long before a CTA can start them
-        int nxt = -2;
-        TileInfo tn{};
-        int4 cn{};
-        int nk0 = 0, nk1 = 0;
-        auto claim_next = [&]() {
-          nxt = fetch();
-          if (nxt >= 0) {
-            tn = decode_tile(p, nxt);
-            cn = __ldg(p.chunk_tab + tn.chunk);
-            kb_range(tn, nk0, nk1);
-          }
-        };
+        if (tile >= total_tiles) break;
+        const TileInfo ti = decode_tile(p, tile);
+        const int4 ch = __ldg(p.chunk_tab + ti.chunk);
         const int n_mma = max(16, (ch.z + 15) & ~15);
         const int nbox = (n_mma + kBoxRows - 1) / kBoxRows;
         const uint32_t b_bytes = nbox * kBoxRows * kBK * 2;
         const int a_col = ti.mt * kBM;
-        if (!ti.is_gu && p.gu_wait) {
-          // h rows of this chunk are complete once all its gate+up tiles released
-          while (ld_acquire_gpu(p.gu_done + ti.chunk) < p.n_mt_gu) __nanosleep(64);
-          fence_proxy_async_global();
+        int kb0, kb1;
+        if (ti.is_gu) {
+          kb0 = 0; kb1 = nkb_gu;
+        } else {
+          kb0 = ti.split * p.kb_per_split;
+          kb1 = min(nkb_dn, kb0 + p.kb_per_split);
+          if (p.gu_wait) {
+            // h rows of this chunk are complete once all its gate+up tiles released
+            while (ld_acquire_gpu(p.gu_done + ti.chunk) < p.n_mt_gu) __nanosleep(64);
+            fence_proxy_async_global();
+          }
         }
         if (p.trace) p.trace[tile * 4 + 2] = globaltimer();
-        const int len = kb1 - kb0;
-        int pf_nxt = 0;
         for (int kb = kb0; kb < kb1; ++kb) {
-          // keep the L2 prefetch front pd blocks ahead, running into the next tile
-          const int target = kb - kb0 + pd + 1;
-          while (pf_cur < min(len, target)) prefetch_w(ti, ch, kb0 + pf_cur++);
-          if (target > len) {
-            if (nxt == -2) claim_next();
-            if (nxt >= 0) {
-              const int extra = min(min(nk1 - nk0, pd_for(tn)), target - len);
-              while (pf_nxt < extra) prefetch_w(tn, cn, nk0 + pf_nxt++);
-            }
-          }
-          mbar_wait(empty_bar + stage, phase ^ 1);
-          uint8_t* st = smem + stage * C::kStageBytes;
-          uint8_t* sb = st + 2 * C::kABytes;
           if (ti.is_gu) {
-            mbar_arrive_expect_tx(full_bar + stage, 2 * C::kABytes + b_bytes);
             const int krow = ch.x * p.d + kb * kBK;
-            tma_load_2d_hint(&tm_wg, full_bar + stage, st, a_col, krow, pol_w);
-            tma_load_2d_hint(&tm_wg, full_bar + stage, st + C::kABytes / 2, a_col + 64, krow, pol_w);
-            tma_load_2d_hint(&tm_wu, full_bar + stage, st + C::kABytes, a_col, krow, pol_w);
-            tma_load_2d_hint(&tm_wu, full_bar + stage, st + C::kABytes + C::kABytes / 2, a_col + 64, krow, pol_w);
-            for (int b = 0; b < nbox; ++b)
-              tma_load_2d(&tm_xp, full_bar + stage, sb + b * kBoxRows * kBK * 2, kb * kBK, ch.y + b * kBoxRows);
+            mbar_wait(a_empty + as, aph ^ 1);
+            mbar_arrive_expect_tx(a_full + as, C::kABytes);
+            uint8_t* sa = a_ring + as * C::kABytes;
+            tma_load_2d_hint(&tm_wg, a_full + as, sa, a_col, krow, pol_w);
+            tma_load_2d_hint(&tm_wg, a_full + as, sa + C::kABytes / 2, a_col + 64, krow, pol_w);
+            if (++as == C::kAStages) { as = 0; aph ^= 1; }
+            mbar_wait(a_empty + as, aph ^ 1);
+            mbar_arrive_expect_tx(a_full + as, C::kABytes);
+            sa = a_ring + as * C::kABytes;
+            tma_load_2d_hint(&tm_wu, a_full + as, sa, a_col, krow, pol_w);
+            tma_load_2d_hint(&tm_wu, a_full + as, sa + C::kABytes / 2, a_col + 64, krow, pol_w);
+            if (++as == C::kAStages) { as = 0; aph ^= 1; }
           } else {
-            mbar_arrive_expect_tx(full_bar + stage, C::kABytes + b_bytes);
             const int krow = ch.x * p.f + kb * kBK;
-            tma_load_2d_hint(&tm_wd, full_bar + stage, st, a_col, krow, pol_w);
-            tma_load_2d_hint(&tm_wd, full_bar + stage, st + C::kABytes / 2, a_col + 64, krow, pol_w);
-            for (int b = 0; b < nbox; ++b)
-              tma_load_2d(&tm_h, full_bar + stage, sb + b * kBoxRows * kBK * 2, kb * kBK, ch.y + b * kBoxRows);
+            mbar_wait(a_empty + as, aph ^ 1);
+            mbar_arrive_expect_tx(a_full + as, C::kABytes);
+            uint8_t* sa = a_ring + as * C::kABytes;
+            tma_load_2d_hint(&tm_wd, a_full + as, sa, a_col, krow, pol_w);
+            tma_load_2d_hint(&tm_wd, a_full + as, sa + C::kABytes / 2, a_col + 64, krow, pol_w);
+            if (++as == C::kAStages) { as = 0; aph ^= 1; }
           }
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          mbar_wait(b_empty + bs, bph ^ 1);
+          mbar_arrive_expect_tx(b_full + bs, b_bytes);
+          uint8_t* sb = b_ring + bs * C::kBBytes;
+          const CUtensorMap* tb = ti.is_gu ? &tm_xp : &tm_h;
+          for (int b = 0; b < nbox; ++b)
+            tma_load_2d(tb, b_full + bs, sb + b * kBoxRows * kBK * 2, kb * kBK, ch.y + b * kBoxRows);
+          if (++bs == C::kBStages) { bs = 0; bph ^= 1; }
         }
-        if (nxt == -2) claim_next();
-        pf_cur = pf_nxt;
-        tile = nxt;
-        ti = tn;
-        ch = cn;
-        kb0 = nk0;
-        kb1 = nk1;
-        pd = nxt >= 0 ? pd_for(tn) : 0;
       }
     }
   } else if (warp == 1) {
     // ============================== MMA issuer ==============================
-    int stage = 0;
-    uint32_t phase = 0;
+    int as = 0, bs = 0;
+    uint32_t aph = 0, bph = 0;
     uint32_t acc_phase = 0;
     int slot = 0;
     uint32_t sphase = 0;
@@ -333,27 +293,39 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       mbar_wait(tmem_empty, acc_phase ^ 1);
       tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(full_bar + stage, phase);
+        const int as0 = as;
+        mbar_wait(a_full + as, aph);
+        if (++as == C::kAStages) { as = 0; aph ^= 1; }
+        int as1 = -1;
+        if (ti.is_gu) {
+          as1 = as;
+          mbar_wait(a_full + as, aph);
+          if (++as == C::kAStages) { as = 0; aph ^= 1; }
+        }
+        mbar_wait(b_full + bs, bph);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t st = smem_u32(smem + stage * C::kStageBytes);
-          const uint32_t sb = st + 2 * C::kABytes;
+          const uint32_t sa0 = smem_u32(a_ring + as0 * C::kABytes);
+          const uint32_t sb = smem_u32(b_ring + bs * C::kBBytes);
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
             const uint64_t bdesc = make_smem_desc_sw128(sb + kk * 32, 16, 1024);
-            const uint64_t adesc0 = make_smem_desc_sw128(st + kk * 2048, C::kABytes / 2, 1024);
+            const uint64_t adesc0 = make_smem_desc_sw128(sa0 + kk * 2048, C::kABytes / 2, 1024);
             const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
             mma_bf16(tmem_base, adesc0, bdesc, idesc, acc);
             if (ti.is_gu) {
-              const uint64_t adesc1 = make_smem_desc_sw128(st + C::kABytes + kk * 2048, C::kABytes / 2, 1024);
-              mma_bf16(tmem_base + 256, adesc1, bdesc, idesc, acc);
+              const uint32_t sa1 = smem_u32(a_ring + as1 * C::kABytes);
+              const uint64_t adesc1 = make_smem_desc_sw128(sa1 + kk * 2048, C::kABytes / 2, 1024);
+              mma_bf16(tmem_base + kBN, adesc1, bdesc, idesc, acc);
             }
           }
-          mma_commit(empty_bar + stage);
+          mma_commit(a_empty + as0);
+          if (ti.is_gu) mma_commit(a_empty + as1);
+          mma_commit(b_empty + bs);
           if (kb == kb1 - 1) mma_commit(tmem_full);
         }
         __syncwarp();
-        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        if (++bs == C::kBStages) { bs = 0; bph ^= 1; }
       }
       acc_phase ^= 1;
     }
@@ -381,7 +353,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         for (int c0 = 0; c0 < ch.z; c0 += 32) {
           uint32_t g[32], u[32];
           tmem_ld_32x32b_x32(tmem_base + lane_base + c0, g);
-          tmem_ld_32x32b_x32(tmem_base + lane_base + 256 + c0, u);
+          tmem_ld_32x32b_x32(tmem_base + lane_base + kBN + c0, u);
           tmem_wait_ld();
           if (ok) {
             __nv_bfloat16* hp = p.h + (size_t)(ch.y + c0) * p.f + feat;

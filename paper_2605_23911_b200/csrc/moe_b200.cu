@@ -258,14 +258,22 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.trace = g_ffn_trace;
   const long max_tiles = (long)L.max_chunks * (p.n_mt_gu + p.n_mt_dn * p.splits);
   const int grid = static_cast<int>(std::max(1L, std::min<long>(kNumSMs, max_tiles)));
-  static bool attr_set[64] = {};
+  const int bn = chunk_rows_for(c, B);
+  static bool attr_set[2][64] = {};
   int dev = 0;
   MOE_CUDA(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-    MOE_CUDA(cudaFuncSetAttribute(ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FfnCfg::kSmemBytes));
-    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  const int which = bn == 256 ? 1 : 0;
+  if (dev < 0 || dev >= 64 || !attr_set[which][dev]) {
+    if (bn == 256)
+      MOE_CUDA(cudaFuncSetAttribute(ffn_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, FfnCfg<256>::kSmemBytes));
+    else
+      MOE_CUDA(cudaFuncSetAttribute(ffn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, FfnCfg<128>::kSmemBytes));
+    if (dev >= 0 && dev < 64) attr_set[which][dev] = true;
   }
-  ffn_kernel<<<grid, kFfnThreads, FfnCfg::kSmemBytes, s>>>(m_wg, m_wu, m_xp, m_wd, m_h, p);
+  if (bn == 256)
+    ffn_kernel<256><<<grid, kFfnThreads, FfnCfg<256>::kSmemBytes, s>>>(m_wg, m_wu, m_xp, m_wd, m_h, p);
+  else
+    ffn_kernel<128><<<grid, kFfnThreads, FfnCfg<128>::kSmemBytes, s>>>(m_wg, m_wu, m_xp, m_wd, m_h, p);
   MOE_LAUNCH_CHECK("ffn_kernel");
   return MOE_B200_OK;
 }
