@@ -41,7 +41,7 @@ struct FfnParams {
   const int4* chunk_tab;     // {expert, row0, nrows, 0} per token chunk
   const int32_t* n_chunks;   // device count of chunks
   int n_mt_gu;               // gate+up tiles per chunk (ceil(f/128)); 0 = none
-  int n_mt_dn;               // down tiles per chunk (ceil(d/128)); 0 = none
+  int n_mt_dn;               // down tiles per chunk (ceil(d/256): pairs of 128 rows); 0 = none
   int splits;                // K splits of a down tile
   int kb_per_split;          // k-blocks per down split
   int d, f;
@@ -217,7 +217,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         const int n_mma = max(16, (ch.z + 15) & ~15);
         const int nbox = (n_mma + kBoxRows - 1) / kBoxRows;
         const uint32_t b_bytes = nbox * kBoxRows * kBK * 2;
-        const int a_col = ti.mt * kBM;
+        const int a_col = ti.is_gu ? ti.mt * kBM : ti.mt * 2 * kBM;
         int kb0, kb1;
         if (ti.is_gu) {
           kb0 = 0; kb1 = nkb_gu;
@@ -247,13 +247,17 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             tma_load_2d_hint(&tm_wu, a_full + as, sa + C::kABytes / 2, a_col + 64, krow, pol_w);
             if (++as == C::kAStages) { as = 0; aph ^= 1; }
           } else {
+            // a down tile is a PAIR of 128-row hidden tiles sharing the token slot
             const int krow = ch.x * p.f + kb * kBK;
-            mbar_wait(a_empty + as, aph ^ 1);
-            mbar_arrive_expect_tx(a_full + as, C::kABytes);
-            uint8_t* sa = a_ring + as * C::kABytes;
-            tma_load_2d_hint(&tm_wd, a_full + as, sa, a_col, krow, pol_w);
-            tma_load_2d_hint(&tm_wd, a_full + as, sa + C::kABytes / 2, a_col + 64, krow, pol_w);
-            if (++as == C::kAStages) { as = 0; aph ^= 1; }
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              mbar_wait(a_empty + as, aph ^ 1);
+              mbar_arrive_expect_tx(a_full + as, C::kABytes);
+              uint8_t* sa = a_ring + as * C::kABytes;
+              tma_load_2d_hint(&tm_wd, a_full + as, sa, a_col + half * kBM, krow, pol_w);
+              tma_load_2d_hint(&tm_wd, a_full + as, sa + C::kABytes / 2, a_col + half * kBM + 64, krow, pol_w);
+              if (++as == C::kAStages) { as = 0; aph ^= 1; }
+            }
           }
           mbar_wait(b_empty + bs, bph ^ 1);
           mbar_arrive_expect_tx(b_full + bs, b_bytes);
@@ -296,12 +300,9 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         const int as0 = as;
         mbar_wait(a_full + as, aph);
         if (++as == C::kAStages) { as = 0; aph ^= 1; }
-        int as1 = -1;
-        if (ti.is_gu) {
-          as1 = as;
-          mbar_wait(a_full + as, aph);
-          if (++as == C::kAStages) { as = 0; aph ^= 1; }
-        }
+        const int as1 = as;  // second weight slot: up (gate+up) or hidden rows +128 (down)
+        mbar_wait(a_full + as, aph);
+        if (++as == C::kAStages) { as = 0; aph ^= 1; }
         mbar_wait(b_full + bs, bph);
         tc_fence_after();
         if (elect_one()) {
@@ -313,14 +314,12 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             const uint64_t adesc0 = make_smem_desc_sw128(sa0 + kk * 2048, C::kABytes / 2, 1024);
             const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
             mma_bf16(tmem_base, adesc0, bdesc, idesc, acc);
-            if (ti.is_gu) {
-              const uint32_t sa1 = smem_u32(a_ring + as1 * C::kABytes);
-              const uint64_t adesc1 = make_smem_desc_sw128(sa1 + kk * 2048, C::kABytes / 2, 1024);
-              mma_bf16(tmem_base + kBN, adesc1, bdesc, idesc, acc);
-            }
+            const uint32_t sa1 = smem_u32(a_ring + as1 * C::kABytes);
+            const uint64_t adesc1 = make_smem_desc_sw128(sa1 + kk * 2048, C::kABytes / 2, 1024);
+            mma_bf16(tmem_base + kBN, adesc1, bdesc, idesc, acc);
           }
           mma_commit(a_empty + as0);
-          if (ti.is_gu) mma_commit(a_empty + as1);
+          mma_commit(a_empty + as1);
           mma_commit(b_empty + bs);
           if (kb == kb1 - 1) mma_commit(tmem_full);
         }
@@ -373,20 +372,24 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           if (wq == 0 && lane == 0) red_release_gpu_add(p.gu_done + ti.chunk, 1);
         }
       } else {
-        const bool ok = feat < p.d;
         float* out = p.ys + (size_t)ti.split * p.T * p.d;
-        for (int c0 = 0; c0 < ch.z; c0 += 32) {
-          uint32_t a[32];
-          tmem_ld_32x32b_x32(tmem_base + lane_base + c0, a);
-          tmem_wait_ld();
-          if (ok) {
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          const int fd = ti.mt * 2 * kBM + half * kBM + wq * 32 + lane;
+          const bool ok = fd < p.d;
+          for (int c0 = 0; c0 < ch.z; c0 += 32) {
+            uint32_t a[32];
+            tmem_ld_32x32b_x32(tmem_base + lane_base + half * kBN + c0, a);
+            tmem_wait_ld();
+            if (ok) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              if (c0 + c < ch.z) {
-                const int xid = __ldg(p.fwd + ch.y + c0 + c);
-                float v = __uint_as_float(a[c]);
-                if (p.scale_by_w) v = __fmul_rn(v, __ldg(p.topk_w + xid));
-                out[(size_t)xid * p.d + feat] = v;
+              for (int c = 0; c < 32; ++c) {
+                if (c0 + c < ch.z) {
+                  const int xid = __ldg(p.fwd + ch.y + c0 + c);
+                  float v = __uint_as_float(a[c]);
+                  if (p.scale_by_w) v = __fmul_rn(v, __ldg(p.topk_w + xid));
+                  out[(size_t)xid * p.d + fd] = v;
+                }
               }
             }
           }

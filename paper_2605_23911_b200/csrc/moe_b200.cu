@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -65,13 +66,15 @@ int chunk_rows_for(const moe_b200_config& c, int64_t B) {
   return (T > 96LL * c.num_experts) ? 256 : 128;
 }
 
-// K splits of a down tile so that down tiles stream about as many weight
-// bytes as a gate+up tile (128 x d x 2 matrices): one HBM-stream granularity
-// for the dynamic queue.  Partials are reduced deterministically in combine.
+// K splits of a down tile (a pair of 128-row hidden tiles) so that down
+// tiles stream about as many weight bytes as a gate+up tile (2 x 128 x d):
+// one HBM-stream granularity for the dynamic queue.  Partials are reduced
+// deterministically in combine.  MOE_B200_DOWN_SPLITS overrides (tuning).
 void down_splits(const moe_b200_config& c, int* splits, int* kb_per_split) {
   const int nkb = (c.ffn_dim + kBK - 1) / kBK;
-  int s = static_cast<int>((c.ffn_dim + c.hidden_dim) / (2 * c.hidden_dim));  // round(f / 2d)
-  s = std::max(1, std::min(s, 4));
+  int s = static_cast<int>((c.ffn_dim + c.hidden_dim / 2) / c.hidden_dim);  // round(f / d)
+  if (const char* env = getenv("MOE_B200_DOWN_SPLITS")) s = atoi(env);
+  s = std::max(1, std::min(s, 8));
   s = std::min(s, nkb);
   int kps = (nkb + s - 1) / s;
   *kb_per_split = kps;
@@ -242,7 +245,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.chunk_tab = reinterpret_cast<const int4*>(static_cast<uint8_t*>(ws) + L.chunk_tab);
   p.n_chunks = hdr + 2;
   p.n_mt_gu = do_gu ? (f + kBM - 1) / kBM : 0;
-  p.n_mt_dn = do_dn ? (d + kBM - 1) / kBM : 0;
+  p.n_mt_dn = do_dn ? (d + 2 * kBM - 1) / (2 * kBM) : 0;
   p.splits = fused ? L.splits : 1;
   p.kb_per_split = fused ? L.kb_per_split : (f + kBK - 1) / kBK;
   p.d = d; p.f = f; p.T = static_cast<int>(T);
