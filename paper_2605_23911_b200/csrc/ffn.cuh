@@ -55,7 +55,7 @@ struct FfnParams {
   int32_t* work_counter;     // self-resetting
   int32_t* exit_counter;     // self-resetting
   int32_t* gu_done;          // per-chunk completed gate+up tiles, self-resetting
-  unsigned long long* trace; // optional (debug): per tile {sm, t_fetch, t_first_load, t_done}
+  unsigned long long* trace; // optional (debug): 8 u64 per tile {sm, fetch, first load, epi done, epi start, mma start}
 };
 
 MOE_DEVICE unsigned long long globaltimer() {
@@ -204,8 +204,8 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       while (true) {
         const int tile = atomicAdd(p.work_counter, 1);
         if (p.trace && tile < total_tiles) {
-          p.trace[tile * 4 + 0] = smid();
-          p.trace[tile * 4 + 1] = globaltimer();
+          p.trace[tile * 8 + 0] = smid();
+          p.trace[tile * 8 + 1] = globaltimer();
         }
         mbar_wait(sched_empty + slot, sphase ^ 1);
         sched_tile[slot] = tile < total_tiles ? tile : -1;
@@ -230,7 +230,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             fence_proxy_async_global();
           }
         }
-        if (p.trace) p.trace[tile * 4 + 2] = globaltimer();
+        if (p.trace) p.trace[tile * 8 + 2] = globaltimer();
         for (int kb = kb0; kb < kb1; ++kb) {
           if (ti.is_gu) {
             const int krow = ch.x * p.d + kb * kBK;
@@ -296,6 +296,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       }
       mbar_wait(tmem_empty, acc_phase ^ 1);
       tc_fence_after();
+      if (p.trace && lane == 0) p.trace[tile * 8 + 5] = globaltimer();
       for (int kb = kb0; kb < kb1; ++kb) {
         const int as0 = as;
         mbar_wait(a_full + as, aph);
@@ -347,6 +348,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       const int feat = ti.mt * kBM + wq * 32 + lane;  // output feature of this thread
       mbar_wait(tmem_full, acc_phase);
       tc_fence_after();
+      if (p.trace && wq == 0 && lane == 0) p.trace[tile * 8 + 4] = globaltimer();
       if (ti.is_gu) {
         const bool ok = feat < p.f;
         for (int c0 = 0; c0 < ch.z; c0 += 32) {
@@ -397,7 +399,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         tc_fence_before();
         mbar_arrive(tmem_empty);
       }
-      if (p.trace && wq == 0 && lane == 0) p.trace[tile * 4 + 3] = globaltimer();
+      if (p.trace && wq == 0 && lane == 0) p.trace[tile * 8 + 3] = globaltimer();
       acc_phase ^= 1;
     }
   }

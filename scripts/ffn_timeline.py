@@ -7,6 +7,7 @@ from paper_2605_23911_b200 import _lib
 from bench import CONFIGS
 
 name = sys.argv[1] if len(sys.argv) > 1 else "mixtral"
+tag = sys.argv[2] if len(sys.argv) > 2 else name
 E, k, d, f, gating, B, _ = CONFIGS[name]
 gen = torch.Generator(device="cuda").manual_seed(1234)
 x = torch.randn((B, d), generator=gen, device="cuda").to(torch.bfloat16)
@@ -18,7 +19,7 @@ layer = P.MoELayer(P.ModelConfig(E, k, d, f, P.Gating(gating)), P.ExpertWeights(
 for _ in range(3):
     layer.forward(x)
 lib = _lib.load()
-buf = torch.zeros(4 * 200000, dtype=torch.int64, device="cuda")
+buf = torch.zeros(8 * 200000, dtype=torch.int64, device="cuda")
 lib.moe_b200_debug_set_ffn_trace.argtypes = [ctypes.c_void_p]
 lib.moe_b200_debug_set_ffn_trace(buf.data_ptr())
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda"); flush.zero_()
@@ -26,13 +27,14 @@ torch.cuda.synchronize()
 layer.forward(x)
 torch.cuda.synchronize()
 lib.moe_b200_debug_set_ffn_trace(None)
-t = buf.view(-1, 4).cpu().numpy()
+t = buf.view(-1, 8).cpu().numpy()
 n = int((t[:, 1] > 0).sum())
 t = t[:n]
 t0 = t[:, 1].min()
 rel = (t[:, 1:] - t0) / 1e3
 out = {"config": name, "counts": layer.counts.tolist(), "tiles": n,
-       "sm": t[:, 0].tolist(), "fetch_us": rel[:, 0].tolist(), "load_us": rel[:, 1].tolist(), "done_us": rel[:, 2].tolist()}
+       "sm": t[:, 0].tolist(), "fetch_us": rel[:, 0].tolist(), "load_us": rel[:, 1].tolist(), "done_us": rel[:, 2].tolist(),
+       "epi_start_us": rel[:, 3].tolist(), "mma_start_us": rel[:, 4].tolist()}
 os.makedirs("gpurun_out", exist_ok=True)
-json.dump(out, open(f"gpurun_out/timeline_{name}.json", "w"))
+json.dump(out, open(f"gpurun_out/timeline_{tag}.json", "w"))
 print(name, "tiles", n, "span_us", rel[:, 2].max())

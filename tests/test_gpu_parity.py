@@ -91,9 +91,10 @@ def test_forward_golden_cases(pkg, golden):
         bits_equal(_np(st["inverse"]).astype(np.int64), golden[p + "inverse"])
         err = O.max_rel_error(_np(st["y"]), golden[p + "y"])
         assert err <= TOL, (name, err)
-        # the one-call forward gives the same bits as the staged path
+        # the one-call fused forward (K-split down partials) agrees with the staged path
         y1 = layer.forward(torch.from_numpy(tokens).cuda())
-        bits_equal(_np(y1), _np(st["y"]))
+        assert O.max_rel_error(_np(y1), golden[p + "y"]) <= TOL, name
+        assert O.max_rel_error(_np(y1), _np(st["y"])) <= 1e-5, name
 
 
 def test_dropin_moe_forward_numpy_roundtrip(pkg, golden):
