@@ -55,6 +55,7 @@ struct FfnParams {
   int32_t* work_counter;     // self-resetting
   int32_t* exit_counter;     // self-resetting
   int32_t* gu_done;          // per-chunk completed gate+up tiles, self-resetting
+  int dbg;                   // debug/experiment bits (0 in production)
   unsigned long long* trace; // optional (debug): 8 u64 per tile {sm, fetch, first load, epi done, epi start, mma start}
 };
 
@@ -356,7 +357,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           tmem_ld_32x32b_x32(tmem_base + lane_base + c0, g);
           tmem_ld_32x32b_x32(tmem_base + lane_base + kBN + c0, u);
           tmem_wait_ld();
-          if (ok) {
+          if (ok && !(p.dbg & 1)) {
             __nv_bfloat16* hp = p.h + (size_t)(ch.y + c0) * p.f + feat;
 #pragma unroll
             for (int c = 0; c < 32; ++c)
@@ -383,11 +384,11 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             uint32_t a[32];
             tmem_ld_32x32b_x32(tmem_base + lane_base + half * kBN + c0, a);
             tmem_wait_ld();
-            if (ok) {
+            if (ok && !(p.dbg & 1)) {
 #pragma unroll
               for (int c = 0; c < 32; ++c) {
                 if (c0 + c < ch.z) {
-                  const int xid = __ldg(p.fwd + ch.y + c0 + c);
+                  const int xid = (p.dbg & 2) ? ch.y + c0 + c : __ldg(p.fwd + ch.y + c0 + c);
                   float v = __uint_as_float(a[c]);
                   if (p.scale_by_w) v = __fmul_rn(v, __ldg(p.topk_w + xid));
                   out[(size_t)xid * p.d + fd] = v;

@@ -259,6 +259,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.exit_counter = hdr + 4;
   p.gu_done = hdr + kHdrGuDone;
   p.trace = g_ffn_trace;
+  if (const char* env = getenv("MOE_B200_FFN_DEBUG")) p.dbg = atoi(env);
   const long max_tiles = (long)L.max_chunks * (p.n_mt_gu + p.n_mt_dn * p.splits);
   const int grid = static_cast<int>(std::max(1L, std::min<long>(kNumSMs, max_tiles)));
   const int bn = chunk_rows_for(c, B);
