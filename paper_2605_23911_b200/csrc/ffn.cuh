@@ -76,17 +76,39 @@ MOE_DEVICE uint32_t smid() {
 // one of each, so the weight bytes in flight per SM (the HBM-latency x
 // bandwidth product) no longer shrink with the token tile: 8-10 slots keep
 // 128-160 KB of weights outstanding for either tile type.
-template <int kBN>
+// Epilogue stores go through shared-memory staging buffers and asynchronous
+// bulk copies (one 256 B / 512 B row segment per copy, issued by one lane),
+// so the output stream never competes with the weight stream as thousands of
+// scattered STGs.  kV selects the ring/staging split (tuning).
+template <int kBN, int kV>
 struct FfnCfg {
   static constexpr int kABytes = kBM * kBK * 2;      // 16 KB weight slot
   static constexpr int kBBytes = kBN * kBK * 2;      // token slot
-  static constexpr int kAStages = kBN == 256 ? 8 : 10;
-  static constexpr int kBStages = kBN == 256 ? 3 : 4;
+  static constexpr int kStgBytes = 32 * kBM * 4;     // 32 rows x 128 fp32 (16 KB)
+  static constexpr int kStgBufs = kV == 1 ? 1 : 2;
+  static constexpr int kAStages = kBN == 256 ? (kV == 1 ? 7 : kV == 2 ? 6 : 8) : 8;
+  static constexpr int kBStages = kBN == 256 ? (kV == 3 ? 2 : 3) : 4;
   static constexpr int kRingBytes = kAStages * kABytes + kBStages * kBBytes;
+  static constexpr int kDataBytes = kRingBytes + kStgBufs * kStgBytes;
   static constexpr uint32_t kTmemCols = 2 * kBN <= 256 ? 256 : 512;
-  static constexpr int kSmemBytes = kRingBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int kSmemBytes = kDataBytes + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(kSmemBytes <= 232448, "shared memory");
 };
+
+MOE_DEVICE void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+MOE_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+MOE_DEVICE void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+MOE_DEVICE void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+MOE_DEVICE void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 MOE_DEVICE float silu_mul(float g, float u) {
   // silu(g) * u in fp32 (fast exp; tolerance path, pipeline.py:294)
@@ -135,17 +157,18 @@ MOE_DEVICE TileInfo decode_tile(const FfnParams& p, int tile) {
   return t;
 }
 
-template <int kBN>
+template <int kBN, int kV>
 __global__ void __launch_bounds__(kFfnThreads, 1)
 ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CUtensorMap tm_wu,
            const __grid_constant__ CUtensorMap tm_xp, const __grid_constant__ CUtensorMap tm_wd,
            const __grid_constant__ CUtensorMap tm_h, const FfnParams p) {
-  using C = FfnCfg<kBN>;
+  using C = FfnCfg<kBN, kV>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* a_ring = smem;
   uint8_t* b_ring = smem + C::kAStages * C::kABytes;
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + C::kRingBytes);
+  uint8_t* stg = smem + C::kRingBytes;  // epilogue staging buffers
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + C::kDataBytes);
   uint64_t* a_empty = a_full + C::kAStages;
   uint64_t* b_full = a_empty + C::kAStages;
   uint64_t* b_empty = b_full + C::kBStages;
@@ -346,59 +369,93 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       if (tile < 0) break;
       const TileInfo ti = decode_tile(p, tile);
       const int4 ch = __ldg(p.chunk_tab + ti.chunk);
-      const int feat = ti.mt * kBM + wq * 32 + lane;  // output feature of this thread
       mbar_wait(tmem_full, acc_phase);
       tc_fence_after();
       if (p.trace && wq == 0 && lane == 0) p.trace[tile * 8 + 4] = globaltimer();
+      // Staged store protocol, per 32-row chunk: (issuer) make the staging
+      // buffer free -> barrier -> every thread writes its feature column ->
+      // proxy fence -> barrier -> issuer (warp 4 lane 0) bulk-copies each row.
+      const bool issuer = (wq == 0 && lane == 0);
       if (ti.is_gu) {
-        const bool ok = feat < p.f;
-        for (int c0 = 0; c0 < ch.z; c0 += 32) {
+        const int f0 = ti.mt * kBM;
+        const int nvalid_f = min(kBM, p.f - f0);
+        int nchunk = 0;
+        for (int c0 = 0; c0 < ch.z; c0 += 32, ++nchunk) {
           uint32_t g[32], u[32];
           tmem_ld_32x32b_x32(tmem_base + lane_base + c0, g);
           tmem_ld_32x32b_x32(tmem_base + lane_base + kBN + c0, u);
           tmem_wait_ld();
-          if (ok && !(p.dbg & 1)) {
-            __nv_bfloat16* hp = p.h + (size_t)(ch.y + c0) * p.f + feat;
+          if (c0 + 32 >= ch.z) {  // all accumulator reads of this tile done: release TMEM
+            tc_fence_before();
+            mbar_arrive(tmem_empty);
+          }
+          __nv_bfloat16* sbuf = reinterpret_cast<__nv_bfloat16*>(stg + (nchunk % C::kStgBufs) * C::kStgBytes);
+          if (issuer) bulk_wait_read<C::kStgBufs - 1>();
+          epi_bar_sync();
+          const int fl = wq * 32 + lane;  // feature within the tile
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-              if (c0 + c < ch.z)
-                hp[(size_t)c * p.f] = __float2bfloat16_rn(silu_mul(__uint_as_float(g[c]), __uint_as_float(u[c])));
+          for (int c = 0; c < 32; ++c)
+            sbuf[c * kBM + fl] = __float2bfloat16_rn(silu_mul(__uint_as_float(g[c]), __uint_as_float(u[c])));
+          fence_proxy_async_smem();
+          epi_bar_sync();
+          if (issuer) {
+            const int rows = min(32, ch.z - c0);
+            for (int c = 0; c < rows; ++c)
+              bulk_store(p.h + (size_t)(ch.y + c0 + c) * p.f + f0, sbuf + c * kBM, nvalid_f * 2);
+            bulk_commit();
           }
         }
-        tc_fence_before();
-        mbar_arrive(tmem_empty);
         if (p.gu_wait) {
-          // publish: every epilogue thread's h stores, then one release increment
-          __threadfence();
-          fence_proxy_async_global();
-          epi_bar_sync();
-          if (wq == 0 && lane == 0) red_release_gpu_add(p.gu_done + ti.chunk, 1);
+          // publish the chunk's h rows: bulk writes complete, then one release increment
+          if (issuer) {
+            bulk_wait_all();
+            fence_proxy_async_global();
+            __threadfence();
+            red_release_gpu_add(p.gu_done + ti.chunk, 1);
+          }
         }
       } else {
         float* out = p.ys + (size_t)ti.split * p.T * p.d;
+        int nchunk = 0;
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
-          const int fd = ti.mt * 2 * kBM + half * kBM + wq * 32 + lane;
-          const bool ok = fd < p.d;
-          for (int c0 = 0; c0 < ch.z; c0 += 32) {
+          const int d0 = ti.mt * 2 * kBM + half * kBM;
+          const int nvalid_d = min(kBM, p.d - d0);
+          for (int c0 = 0; c0 < ch.z; c0 += 32, ++nchunk) {
             uint32_t a[32];
             tmem_ld_32x32b_x32(tmem_base + lane_base + half * kBN + c0, a);
             tmem_wait_ld();
-            if (ok && !(p.dbg & 1)) {
+            if (half == 1 && c0 + 32 >= ch.z) {
+              tc_fence_before();
+              mbar_arrive(tmem_empty);
+            }
+            float* sbuf = reinterpret_cast<float*>(stg + (nchunk % C::kStgBufs) * C::kStgBytes);
+            if (issuer) bulk_wait_read<C::kStgBufs - 1>();
+            epi_bar_sync();
+            const int fl = wq * 32 + lane;
 #pragma unroll
-              for (int c = 0; c < 32; ++c) {
-                if (c0 + c < ch.z) {
-                  const int xid = (p.dbg & 2) ? ch.y + c0 + c : __ldg(p.fwd + ch.y + c0 + c);
-                  float v = __uint_as_float(a[c]);
-                  if (p.scale_by_w) v = __fmul_rn(v, __ldg(p.topk_w + xid));
-                  out[(size_t)xid * p.d + fd] = v;
-                }
+            for (int c = 0; c < 32; ++c) sbuf[c * kBM + fl] = __uint_as_float(a[c]);
+            fence_proxy_async_smem();
+            epi_bar_sync();
+            if (wq == 0 && nvalid_d > 0) {
+              // lane c looks up row c's expanded slot; lane 0 issues all copies (scatter)
+              const int rows = min(32, ch.z - c0);
+              const int xid = lane < rows ? __ldg(p.fwd + ch.y + c0 + lane) : 0;
+              if (p.scale_by_w && lane < rows) {
+                const float w = __ldg(p.topk_w + xid);
+                for (int q = 0; q < kBM; ++q) sbuf[lane * kBM + q] = __fmul_rn(sbuf[lane * kBM + q], w);
+                fence_proxy_async_smem();
               }
+              __syncwarp();
+              for (int c = 0; c < rows; ++c) {
+                const int xc = __shfl_sync(0xffffffffu, xid, c);
+                if (lane == 0) bulk_store(out + (size_t)xc * p.d + d0, sbuf + c * kBM, nvalid_d * 4);
+              }
+              if (lane == 0) bulk_commit();
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(tmem_empty);
+        if (issuer) bulk_wait_all();
       }
       if (p.trace && wq == 0 && lane == 0) p.trace[tile * 8 + 3] = globaltimer();
       acc_phase ^= 1;

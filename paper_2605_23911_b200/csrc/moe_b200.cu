@@ -223,6 +223,35 @@ int launch_router_x(const RouterParams& p, const RouterPlan& plan, cudaStream_t 
   return launch_router_t<kBf16, 1, 1>(p, plan, s);
 }
 
+template <int kBN, int kV>
+int launch_ffn_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm, const CUtensorMap& dm,
+                 const CUtensorMap& e, const FfnParams& p, int grid, cudaStream_t s) {
+  using C = FfnCfg<kBN, kV>;
+  static bool attr_set[64] = {};
+  int dev = 0;
+  MOE_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    MOE_CUDA(cudaFuncSetAttribute(ffn_kernel<kBN, kV>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  ffn_kernel<kBN, kV><<<grid, kFfnThreads, C::kSmemBytes, s>>>(a, b, cm, dm, e, p);
+  MOE_LAUNCH_CHECK("ffn_kernel");
+  return MOE_B200_OK;
+}
+
+int launch_ffn_kernel(int bn, int variant, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm,
+                      const CUtensorMap& dm, const CUtensorMap& e, const FfnParams& p, int grid,
+                      cudaStream_t s) {
+  if (bn == 256) {
+    switch (variant) {
+      case 1: return launch_ffn_t<256, 1>(a, b, cm, dm, e, p, grid, s);
+      case 3: return launch_ffn_t<256, 3>(a, b, cm, dm, e, p, grid, s);
+      default: return launch_ffn_t<256, 2>(a, b, cm, dm, e, p, grid, s);
+    }
+  }
+  return launch_ffn_t<128, 2>(a, b, cm, dm, e, p, grid, s);
+}
+
 int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, const void* xp,
                const void* w_gate, const void* w_up, const void* w_down, void* h, float* ys,
                const float* topk_w, const int32_t* fwd, bool do_gu, bool do_dn, bool fused,
@@ -263,23 +292,9 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   const long max_tiles = (long)L.max_chunks * (p.n_mt_gu + p.n_mt_dn * p.splits);
   const int grid = static_cast<int>(std::max(1L, std::min<long>(kNumSMs, max_tiles)));
   const int bn = chunk_rows_for(c, B);
-  static bool attr_set[2][64] = {};
-  int dev = 0;
-  MOE_CUDA(cudaGetDevice(&dev));
-  const int which = bn == 256 ? 1 : 0;
-  if (dev < 0 || dev >= 64 || !attr_set[which][dev]) {
-    if (bn == 256)
-      MOE_CUDA(cudaFuncSetAttribute(ffn_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, FfnCfg<256>::kSmemBytes));
-    else
-      MOE_CUDA(cudaFuncSetAttribute(ffn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, FfnCfg<128>::kSmemBytes));
-    if (dev >= 0 && dev < 64) attr_set[which][dev] = true;
-  }
-  if (bn == 256)
-    ffn_kernel<256><<<grid, kFfnThreads, FfnCfg<256>::kSmemBytes, s>>>(m_wg, m_wu, m_xp, m_wd, m_h, p);
-  else
-    ffn_kernel<128><<<grid, kFfnThreads, FfnCfg<128>::kSmemBytes, s>>>(m_wg, m_wu, m_xp, m_wd, m_h, p);
-  MOE_LAUNCH_CHECK("ffn_kernel");
-  return MOE_B200_OK;
+  int variant = 2;
+  if (const char* env = getenv("MOE_B200_FFN_VARIANT")) variant = atoi(env);
+  return launch_ffn_kernel(bn, variant, m_wg, m_wu, m_xp, m_wd, m_h, p, grid, s);
 }
 
 int grid_for_rows(long total_vec) {
