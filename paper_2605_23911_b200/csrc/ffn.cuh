@@ -417,26 +417,34 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       } else {
         float* out = p.ys + (size_t)ti.split * p.T * p.d;
         int nchunk = 0;
+        long long t_ld = 0, t_b1 = 0, t_sts = 0, t_b2 = 0;
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
           const int d0 = ti.mt * 2 * kBM + half * kBM;
           const int nvalid_d = min(kBM, p.d - d0);
           for (int c0 = 0; c0 < ch.z; c0 += 32, ++nchunk) {
             uint32_t a[32];
+            const long long tq0 = clock64();
             tmem_ld_32x32b_x32(tmem_base + lane_base + half * kBN + c0, a);
             tmem_wait_ld();
+            t_ld += clock64() - tq0;
             if (half == 1 && c0 + 32 >= ch.z) {
               tc_fence_before();
               mbar_arrive(tmem_empty);
             }
             float* sbuf = reinterpret_cast<float*>(stg + (nchunk % C::kStgBufs) * C::kStgBytes);
+            const long long tq1 = clock64();
             if (issuer) bulk_wait_read<C::kStgBufs - 1>();
             epi_bar_sync();
+            const long long tq2 = clock64();
             const int fl = wq * 32 + lane;
 #pragma unroll
             for (int c = 0; c < 32; ++c) sbuf[c * kBM + fl] = __uint_as_float(a[c]);
             fence_proxy_async_smem();
+            const long long tq3 = clock64();
             epi_bar_sync();
+            const long long tq4 = clock64();
+            t_b1 += tq2 - tq1; t_sts += tq3 - tq2; t_b2 += tq4 - tq3;
             if (wq == 0 && nvalid_d > 0) {
               // lane c looks up row c's expanded slot; lane 0 issues all copies (scatter)
               const int rows = min(32, ch.z - c0);
@@ -449,19 +457,26 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
               __syncwarp();
               for (int c = 0; c < rows; ++c) {
                 const int xc = __shfl_sync(0xffffffffu, xid, c);
-                if (lane == 0) bulk_store(out + (size_t)xc * p.d + d0, sbuf + c * kBM, nvalid_d * 4);
+                const size_t orow = (p.dbg & 4) ? (size_t)(c & 31) : (size_t)xc;
+                if (lane == 0) bulk_store(out + orow * p.d + d0, sbuf + c * kBM, nvalid_d * 4);
               }
               if (lane == 0) bulk_commit();
             }
           }
         }
-        if (issuer) bulk_wait_all();
+        if (issuer && !(p.dbg & 8)) bulk_wait_all();
+        if (p.trace && issuer) {
+          p.trace[tile * 8 + 5] = (unsigned long long)t_ld;
+          p.trace[tile * 8 + 6] = (unsigned long long)t_b1;
+          p.trace[tile * 8 + 7] = ((unsigned long long)t_sts << 32) | (unsigned long long)t_b2;
+        }
       }
       if (p.trace && wq == 0 && lane == 0) p.trace[tile * 8 + 3] = globaltimer();
       acc_phase ^= 1;
     }
   }
 
+  if (warp == 4 && lane == 0) bulk_wait_all();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {

@@ -38,3 +38,6 @@ out = {"config": name, "counts": layer.counts.tolist(), "tiles": n,
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(out, open(f"gpurun_out/timeline_{tag}.json", "w"))
 print(name, "tiles", n, "span_us", rel[:, 2].max())
+raw = buf.view(-1, 8).cpu().numpy()[:n]
+if len(sys.argv) > 3:
+    np.save(f"gpurun_out/timeline_raw_{tag}.npy", raw)
