@@ -116,4 +116,58 @@ combine_partials_kernel(const float* __restrict__ ys, int splits, size_t split_s
   }
 }
 
+// Fused-forward combine over the tiled down partials
+//   ys[s][feat/256][(feat/128)%2][prow][feat%128]   (prow = padded permuted row)
+// y[t] = sum_j fl(w[t,j] * (sum_s P_s)), ascending j and s, fp32 — the
+// reference's out += w_j * g_j order (pipeline.py:396-399).  Each warp reads
+// one contiguous 512 B row segment per (slot, split).
+template <bool kBf16Out>
+__global__ void __launch_bounds__(kRowThreads)
+combine_tiled_kernel(const float* __restrict__ ys, int splits, int n_dp, int T_pad,
+                     const int32_t* __restrict__ prow, const float* __restrict__ topk_w,
+                     void* __restrict__ y, int B, int k, int d) {
+  const int vec_per_row = d / 4;
+  const long total = (long)B * vec_per_row;
+  const size_t half_stride = (size_t)T_pad * 128;
+  for (long i = (long)blockIdx.x * kRowThreads + threadIdx.x; i < total;
+       i += (long)gridDim.x * kRowThreads) {
+    const int t = static_cast<int>(i / vec_per_row);
+    const int v = static_cast<int>(i % vec_per_row);
+    const int feat = v * 4;
+    const size_t blk = (size_t)(feat >> 8) * 2 + ((feat >> 7) & 1);  // (d-pair, half)
+    const int col = feat & 127;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < k; ++j) {
+      const int x = t * k + j;
+      const float w = __ldg(topk_w + x);
+      const size_t row = (size_t)__ldg(prow + x);
+      float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 0; s < splits; ++s) {
+        const float* src = ys + ((size_t)s * n_dp * 2 + blk) * half_stride + row * 128 + col;
+        const float4 a = __ldg(reinterpret_cast<const float4*>(src));
+        if (s == 0) {
+          g = a;
+        } else {
+          g.x = __fadd_rn(g.x, a.x); g.y = __fadd_rn(g.y, a.y);
+          g.z = __fadd_rn(g.z, a.z); g.w = __fadd_rn(g.w, a.w);
+        }
+      }
+      acc.x = __fadd_rn(acc.x, __fmul_rn(w, g.x));
+      acc.y = __fadd_rn(acc.y, __fmul_rn(w, g.y));
+      acc.z = __fadd_rn(acc.z, __fmul_rn(w, g.z));
+      acc.w = __fadd_rn(acc.w, __fmul_rn(w, g.w));
+    }
+    if (kBf16Out) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y);
+      __nv_bfloat162 p1 = __floats2bfloat162_rn(acc.z, acc.w);
+      uint2 o;
+      o.x = *reinterpret_cast<uint32_t*>(&p0);
+      o.y = *reinterpret_cast<uint32_t*>(&p1);
+      reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(y) + (size_t)t * d)[v] = o;
+    } else {
+      reinterpret_cast<float4*>(static_cast<float*>(y) + (size_t)t * d)[v] = acc;
+    }
+  }
+}
+
 }  // namespace moe

@@ -56,6 +56,8 @@ struct FfnParams {
   int32_t* exit_counter;     // self-resetting
   int32_t* gu_done;          // per-chunk completed gate+up tiles, self-resetting
   int dbg;                   // debug/experiment bits (0 in production)
+  int tiled;                 // 1: h / ys in the tiled padded-row layouts (fused forward)
+  int T_pad;                 // padded-row capacity of the tiled layouts
   unsigned long long* trace; // optional (debug): 8 u64 per tile {sm, fetch, first load, epi done, epi start, mma start}
 };
 
@@ -286,9 +288,16 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           mbar_wait(b_empty + bs, bph ^ 1);
           mbar_arrive_expect_tx(b_full + bs, b_bytes);
           uint8_t* sb = b_ring + bs * C::kBBytes;
-          const CUtensorMap* tb = ti.is_gu ? &tm_xp : &tm_h;
-          for (int b = 0; b < nbox; ++b)
-            tma_load_2d(tb, b_full + bs, sb + b * kBoxRows * kBK * 2, kb * kBK, ch.y + b * kBoxRows);
+          if (ti.is_gu || !p.tiled) {
+            const CUtensorMap* tb = ti.is_gu ? &tm_xp : &tm_h;
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d(tb, b_full + bs, sb + b * kBoxRows * kBK * 2, kb * kBK, ch.y + b * kBoxRows);
+          } else {
+            // tiled h: [f-tile][padded row][128]; k-block kb lives in f-tile kb/2, column half kb%2
+            const int hrow = (kb >> 1) * p.T_pad + ch.w;
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d(&tm_h, b_full + bs, sb + b * kBoxRows * kBK * 2, (kb & 1) * kBK, hrow + b * kBoxRows);
+          }
           if (++bs == C::kBStages) { bs = 0; bph ^= 1; }
         }
       }
@@ -400,8 +409,13 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           epi_bar_sync();
           if (issuer) {
             const int rows = min(32, ch.z - c0);
-            for (int c = 0; c < rows; ++c)
-              bulk_store(p.h + (size_t)(ch.y + c0 + c) * p.f + f0, sbuf + c * kBM, nvalid_f * 2);
+            if (p.tiled) {
+              // one contiguous block: rows x 128 features of this f-tile
+              bulk_store(p.h + ((size_t)ti.mt * p.T_pad + ch.w + c0) * kBM, sbuf, rows * kBM * 2);
+            } else {
+              for (int c = 0; c < rows; ++c)
+                bulk_store(p.h + (size_t)(ch.y + c0 + c) * p.f + f0, sbuf + c * kBM, nvalid_f * 2);
+            }
             bulk_commit();
           }
         }
@@ -415,7 +429,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           }
         }
       } else {
-        float* out = p.ys + (size_t)ti.split * p.T * p.d;
+        float* out = p.ys;  // row layout (stage API): S == 1, slot rows
         int nchunk = 0;
         long long t_ld = 0, t_b1 = 0, t_sts = 0, t_b2 = 0;
 #pragma unroll 1
@@ -445,7 +459,15 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             epi_bar_sync();
             const long long tq4 = clock64();
             t_b1 += tq2 - tq1; t_sts += tq3 - tq2; t_b2 += tq4 - tq3;
-            if (wq == 0 && nvalid_d > 0) {
+            if (p.tiled) {
+              // one contiguous block in ys[split][d-pair][half][padded row][128]
+              if (issuer) {
+                const int rows = min(32, ch.z - c0);
+                float* dst = p.ys + ((((size_t)ti.split * p.n_mt_dn + ti.mt) * 2 + half) * p.T_pad + ch.w + c0) * kBM;
+                bulk_store(dst, sbuf, rows * kBM * 4);
+                bulk_commit();
+              }
+            } else if (wq == 0 && nvalid_d > 0) {
               // lane c looks up row c's expanded slot; lane 0 issues all copies (scatter)
               const int rows = min(32, ch.z - c0);
               const int xid = lane < rows ? __ldg(p.fwd + ch.y + c0 + lane) : 0;

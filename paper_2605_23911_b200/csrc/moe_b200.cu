@@ -55,8 +55,8 @@ constexpr int kHdrGuDone = 16 + kTbCap;
 constexpr size_t kHeaderBytes = align256((16 + kTbCap + kChunkCap) * sizeof(int32_t));
 
 struct Layout {
-  size_t logits, chunk_tab, xp, h, ys, total;
-  int max_chunks, splits, kb_per_split;
+  size_t logits, chunk_tab, prow, xp, h, ys, total;
+  int max_chunks, splits, kb_per_split, T_pad, n_ft, n_dp;
 };
 
 int chunk_rows_for(const moe_b200_config& c, int64_t B) {
@@ -87,12 +87,20 @@ Layout layout_for(const moe_b200_config& c, int64_t B) {
   const int bn = chunk_rows_for(c, B);
   L.max_chunks = static_cast<int>(std::min<int64_t>(c.num_experts, T) + T / bn + 1);
   down_splits(c, &L.splits, &L.kb_per_split);
+  // tiled layouts: experts start 16-row aligned in a padded row space
+  L.T_pad = static_cast<int>(((T + 15LL * std::min<int64_t>(c.num_experts, T)) + 15) / 16 * 16);
+  L.n_ft = (c.ffn_dim + kBM - 1) / kBM;
+  L.n_dp = (c.hidden_dim + 2 * kBM - 1) / (2 * kBM);
+  const size_t h_rows = (size_t)T * c.ffn_dim * 2;
+  const size_t h_tiled = (size_t)L.n_ft * L.T_pad * kBM * 2;
+  const size_t ys_tiled = (size_t)L.splits * L.n_dp * 2 * L.T_pad * kBM * sizeof(float);
   size_t off = kHeaderBytes;
   L.logits = off;    off = align256(off + (size_t)B * c.num_experts * sizeof(float));
   L.chunk_tab = off; off = align256(off + (size_t)L.max_chunks * sizeof(int4));
+  L.prow = off;      off = align256(off + (size_t)T * sizeof(int32_t));
   L.xp = off;        off = align256(off + (size_t)T * c.hidden_dim * 2);
-  L.h = off;         off = align256(off + (size_t)T * c.ffn_dim * 2);
-  L.ys = off;        off = align256(off + (size_t)L.splits * T * c.hidden_dim * sizeof(float));
+  L.h = off;         off = align256(off + std::max(h_rows, h_tiled));
+  L.ys = off;        off = align256(off + std::max((size_t)T * c.hidden_dim * sizeof(float), ys_tiled));
   L.total = off;
   return L;
 }
@@ -268,7 +276,12 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   if ((rc = make_map_bf16(&m_wd, do_dn ? w_down : any_w, do_dn ? (uint64_t)E * f : (uint64_t)E * d,
                           do_dn ? d : f, 64, 64))) return rc;
   if ((rc = make_map_bf16(&m_xp, do_gu ? xp : h, T, do_gu ? d : f, 64, kBoxRows))) return rc;
-  if ((rc = make_map_bf16(&m_h, do_dn ? h : xp, T, do_dn ? f : d, 64, kBoxRows))) return rc;
+  if (fused) {
+    // tiled h: [n_ft * T_pad rows][128 cols]
+    if ((rc = make_map_bf16(&m_h, h, (uint64_t)L.n_ft * L.T_pad, kBM, 64, kBoxRows))) return rc;
+  } else if ((rc = make_map_bf16(&m_h, do_dn ? h : xp, T, do_dn ? f : d, 64, kBoxRows))) {
+    return rc;
+  }
   int32_t* hdr = reinterpret_cast<int32_t*>(ws);
   FfnParams p{};
   p.chunk_tab = reinterpret_cast<const int4*>(static_cast<uint8_t*>(ws) + L.chunk_tab);
@@ -287,6 +300,8 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.work_counter = hdr + 3;
   p.exit_counter = hdr + 4;
   p.gu_done = hdr + kHdrGuDone;
+  p.tiled = fused ? 1 : 0;
+  p.T_pad = L.T_pad;
   p.trace = g_ffn_trace;
   if (const char* env = getenv("MOE_B200_FFN_DEBUG")) p.dbg = atoi(env);
   const long max_tiles = (long)L.max_chunks * (p.n_mt_gu + p.n_mt_dn * p.splits);
@@ -401,6 +416,7 @@ int moe_b200_route(const moe_b200_config* cfg, int64_t B, const void* x, int x_d
   p.topk_idx = topk_idx; p.topk_w = topk_w; p.counts = counts; p.offsets = offsets;
   p.fwd = perm_fwd; p.inv = perm_inv;
   p.chunk_tab = reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab);
+  p.prow = reinterpret_cast<int32_t*>(ws8(ws) + L.prow);
   p.n_chunks = hdr + 2;
   p.tb_counter = hdr + kHdrTb;
   p.done_counter = hdr + 1;
@@ -500,14 +516,14 @@ int moe_b200_forward(const moe_b200_config* cfg, int64_t B, const void* x, int x
     return rc;
   const int d = cfg->hidden_dim;
   const int grid = grid_for_rows((long)B * (d / 4));
-  const size_t stride = (size_t)B * cfg->top_k * d;
+  const int32_t* prow = reinterpret_cast<const int32_t*>(ws8(ws) + L.prow);
   if (y_dtype == MOE_B200_DTYPE_F32)
-    combine_partials_kernel<false><<<grid, kRowThreads, 0, s>>>(ys, L.splits, stride, topk_w, y, (int)B, cfg->top_k, d);
+    combine_tiled_kernel<false><<<grid, kRowThreads, 0, s>>>(ys, L.splits, L.n_dp, L.T_pad, prow, topk_w, y, (int)B, cfg->top_k, d);
   else if (y_dtype == MOE_B200_DTYPE_BF16)
-    combine_partials_kernel<true><<<grid, kRowThreads, 0, s>>>(ys, L.splits, stride, topk_w, y, (int)B, cfg->top_k, d);
+    combine_tiled_kernel<true><<<grid, kRowThreads, 0, s>>>(ys, L.splits, L.n_dp, L.T_pad, prow, topk_w, y, (int)B, cfg->top_k, d);
   else
     return MOE_B200_ERR_INVALID_VALUE;
-  MOE_LAUNCH_CHECK("combine_partials_kernel");
+  MOE_LAUNCH_CHECK("combine_tiled_kernel");
   return MOE_B200_OK;
 }
 

@@ -46,7 +46,8 @@ struct RouterParams {
   int32_t* offsets;     // (E+1)
   int32_t* fwd;         // (T)
   int32_t* inv;         // (T)
-  int4* chunk_tab;      // (max_chunks) {expert, row0, nrows, 0}
+  int4* chunk_tab;      // (max_chunks) {expert, row0, nrows, padded row0}
+  int32_t* prow;        // (T) expanded id -> padded permuted row (experts start 16-aligned)
   int32_t* n_chunks;    // [1]
   int32_t* tb_counter;  // (n_tblocks) self-resetting
   int32_t* done_counter;// [1] self-resetting
@@ -195,7 +196,7 @@ struct RouterSmem {
     size_t ph1 = kRouterStages * raw_stage_bytes(tokc, expc, xb) +
                  2 * (f64_x_elems(tokc) + f64_w_elems(expc)) * sizeof(double);
     size_t ph2 = (size_t)(nthreads / 32) * E * sizeof(double);
-    size_t ph3 = ((size_t)(nthreads / 32) + 4) * E * sizeof(int32_t) + 256;
+    size_t ph3 = ((size_t)(nthreads / 32) + 5) * E * sizeof(int32_t) + 512;
     size_t m = ph1 > ph2 ? ph1 : ph2;
     return m > ph3 ? m : ph3;
   }
@@ -512,6 +513,7 @@ router_kernel(const RouterParams p) {
     int32_t* s_cnt = hist + (size_t)nw * E;                  // [E]
     int32_t* s_off = s_cnt + E;                              // [E+1]
     int32_t* s_cpre = s_off + E + 1;                         // [E+1] chunk prefix
+    int32_t* s_off16 = s_cpre + E + 1;                       // [E+1] 16-padded offsets
     for (int i = tid; i < nw * E; i += nthreads) hist[i] = 0;
     __syncthreads();
     const int seg = (T + nw - 1) / nw;
@@ -533,28 +535,33 @@ router_kernel(const RouterParams p) {
     if (warp == 0) {
       const int per = (E + 31) / 32;
       const int lo = lane * per, hi = min(E, lo + per);
-      int sum_c = 0, sum_ch = 0;
+      int sum_c = 0, sum_ch = 0, sum_16 = 0;
       for (int e = lo; e < hi; ++e) {
         sum_c += s_cnt[e];
         sum_ch += (s_cnt[e] + p.chunk_rows - 1) / p.chunk_rows;
+        sum_16 += (s_cnt[e] + 15) & ~15;
       }
-      int inc_c = sum_c, inc_ch = sum_ch;
+      int inc_c = sum_c, inc_ch = sum_ch, inc_16 = sum_16;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         int a = __shfl_up_sync(0xffffffffu, inc_c, o);
         int b = __shfl_up_sync(0xffffffffu, inc_ch, o);
-        if (lane >= o) { inc_c += a; inc_ch += b; }
+        int c = __shfl_up_sync(0xffffffffu, inc_16, o);
+        if (lane >= o) { inc_c += a; inc_ch += b; inc_16 += c; }
       }
-      int run_c = inc_c - sum_c, run_ch = inc_ch - sum_ch;
+      int run_c = inc_c - sum_c, run_ch = inc_ch - sum_ch, run_16 = inc_16 - sum_16;
       for (int e = lo; e < hi; ++e) {
         s_off[e] = run_c;
         s_cpre[e] = run_ch;
+        s_off16[e] = run_16;
         run_c += s_cnt[e];
         run_ch += (s_cnt[e] + p.chunk_rows - 1) / p.chunk_rows;
+        run_16 += (s_cnt[e] + 15) & ~15;
       }
       if (lane == 31) {
         s_off[E] = inc_c;
         s_cpre[E] = inc_ch;
+        s_off16[E] = inc_16;
       }
     }
     __syncthreads();
@@ -565,7 +572,7 @@ router_kernel(const RouterParams p) {
       const int nchunk = (n_e + p.chunk_rows - 1) / p.chunk_rows;
       for (int c = 0; c < nchunk; ++c) {
         int r0 = c * p.chunk_rows;
-        p.chunk_tab[s_cpre[e] + c] = make_int4(e, s_off[e] + r0, min(p.chunk_rows, n_e - r0), 0);
+        p.chunk_tab[s_cpre[e] + c] = make_int4(e, s_off[e] + r0, min(p.chunk_rows, n_e - r0), s_off16[e] + r0);
       }
     }
     if (tid == 0) {
@@ -584,6 +591,7 @@ router_kernel(const RouterParams p) {
         int pos = s_off[e] + hist[warp * E + e] + rank;
         p.fwd[pos] = i;
         p.inv[i] = pos;
+        if (p.prow) p.prow[i] = s_off16[e] + (pos - s_off[e]);
       }
       __syncwarp();
       if (valid && (__ffs(peers) - 1) == static_cast<int>(lane)) hist[warp * E + e] += __popc(peers);
