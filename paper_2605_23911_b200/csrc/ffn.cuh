@@ -388,35 +388,57 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       if (ti.is_gu) {
         const int f0 = ti.mt * kBM;
         const int nvalid_f = min(kBM, p.f - f0);
-        int nchunk = 0;
-        for (int c0 = 0; c0 < ch.z; c0 += 32, ++nchunk) {
-          uint32_t g[32], u[32];
-          tmem_ld_32x32b_x32(tmem_base + lane_base + c0, g);
-          tmem_ld_32x32b_x32(tmem_base + lane_base + kBN + c0, u);
-          tmem_wait_ld();
-          if (c0 + 32 >= ch.z) {  // all accumulator reads of this tile done: release TMEM
-            tc_fence_before();
-            mbar_arrive(tmem_empty);
-          }
-          __nv_bfloat16* sbuf = reinterpret_cast<__nv_bfloat16*>(stg + (nchunk % C::kStgBufs) * C::kStgBytes);
-          if (issuer) bulk_wait_read<C::kStgBufs - 1>();
-          epi_bar_sync();
-          const int fl = wq * 32 + lane;  // feature within the tile
+        // Phase 1 (TMEM critical path): drain both accumulators, apply SiLU(g)*u and
+        // keep h as packed bf16 pairs in registers, then release TMEM so the next
+        // tile's MMAs start while this tile's h is still being written out.
+        constexpr int kMaxChunks = kBN / 32;
+        uint32_t hp[kMaxChunks][16];
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            sbuf[c * kBM + fl] = __float2bfloat16_rn(silu_mul(__uint_as_float(g[c]), __uint_as_float(u[c])));
-          fence_proxy_async_smem();
-          epi_bar_sync();
-          if (issuer) {
-            const int rows = min(32, ch.z - c0);
-            if (p.tiled) {
-              // one contiguous block: rows x 128 features of this f-tile
-              bulk_store(p.h + ((size_t)ti.mt * p.T_pad + ch.w + c0) * kBM, sbuf, rows * kBM * 2);
-            } else {
-              for (int c = 0; c < rows; ++c)
-                bulk_store(p.h + (size_t)(ch.y + c0 + c) * p.f + f0, sbuf + c * kBM, nvalid_f * 2);
+        for (int q = 0; q < kMaxChunks; ++q) {
+          if (q * 32 < ch.z) {
+            uint32_t g[32], u[32];
+            tmem_ld_32x32b_x32(tmem_base + lane_base + q * 32, g);
+            tmem_ld_32x32b_x32(tmem_base + lane_base + kBN + q * 32, u);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float h0 = silu_mul(__uint_as_float(g[2 * i]), __uint_as_float(u[2 * i]));
+              const float h1 = silu_mul(__uint_as_float(g[2 * i + 1]), __uint_as_float(u[2 * i + 1]));
+              __nv_bfloat162 pk = __floats2bfloat162_rn(h0, h1);
+              hp[q][i] = *reinterpret_cast<uint32_t*>(&pk);
             }
-            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(tmem_empty);
+        // Phase 2: stage 32-row chunks in smem and bulk-copy them out.
+        const int fl = wq * 32 + lane;  // feature within the tile
+#pragma unroll
+        for (int q = 0; q < kMaxChunks; ++q) {
+          const int c0 = q * 32;
+          if (c0 < ch.z) {
+            __nv_bfloat16* sbuf = reinterpret_cast<__nv_bfloat16*>(stg + (q % C::kStgBufs) * C::kStgBytes);
+            if (issuer) bulk_wait_read<C::kStgBufs - 1>();
+            epi_bar_sync();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const uint32_t w = hp[q][i];
+              reinterpret_cast<uint16_t*>(sbuf)[(2 * i) * kBM + fl] = static_cast<uint16_t>(w & 0xFFFFu);
+              reinterpret_cast<uint16_t*>(sbuf)[(2 * i + 1) * kBM + fl] = static_cast<uint16_t>(w >> 16);
+            }
+            fence_proxy_async_smem();
+            epi_bar_sync();
+            if (issuer) {
+              const int rows = min(32, ch.z - c0);
+              if (p.tiled) {
+                // one contiguous block: rows x 128 features of this f-tile
+                bulk_store(p.h + ((size_t)ti.mt * p.T_pad + ch.w + c0) * kBM, sbuf, rows * kBM * 2);
+              } else {
+                for (int c = 0; c < rows; ++c)
+                  bulk_store(p.h + (size_t)(ch.y + c0 + c) * p.f + f0, sbuf + c * kBM, nvalid_f * 2);
+              }
+              bulk_commit();
+            }
           }
         }
         if (p.gu_wait) {
