@@ -411,6 +411,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         }
         tc_fence_before();
         mbar_arrive(tmem_empty);
+        if (p.trace && issuer) p.trace[tile * 8 + 6] = globaltimer();
         // Phase 2: stage 32-row chunks in smem and bulk-copy them out.
         const int fl = wq * 32 + lane;  // feature within the tile
 #pragma unroll
@@ -510,9 +511,8 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         }
         if (issuer && !(p.dbg & 8)) bulk_wait_all();
         if (p.trace && issuer) {
-          p.trace[tile * 8 + 5] = (unsigned long long)t_ld;
-          p.trace[tile * 8 + 6] = (unsigned long long)t_b1;
-          p.trace[tile * 8 + 7] = ((unsigned long long)t_sts << 32) | (unsigned long long)t_b2;
+          p.trace[tile * 8 + 6] = (unsigned long long)t_ld;
+          p.trace[tile * 8 + 7] = (unsigned long long)(t_b1 + t_sts + t_b2);
         }
       }
       if (p.trace && wq == 0 && lane == 0) p.trace[tile * 8 + 3] = globaltimer();

@@ -34,7 +34,7 @@ t0 = t[:, 1].min()
 rel = (t[:, 1:] - t0) / 1e3
 out = {"config": name, "counts": layer.counts.tolist(), "tiles": n,
        "sm": t[:, 0].tolist(), "fetch_us": rel[:, 0].tolist(), "load_us": rel[:, 1].tolist(), "done_us": rel[:, 2].tolist(),
-       "epi_start_us": rel[:, 3].tolist(), "mma_start_us": rel[:, 4].tolist()}
+       "epi_start_us": rel[:, 3].tolist(), "mma_start_us": rel[:, 4].tolist(), "gu_release_us": rel[:, 5].tolist()}
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(out, open(f"gpurun_out/timeline_{tag}.json", "w"))
 print(name, "tiles", n, "span_us", rel[:, 2].max())
