@@ -55,7 +55,7 @@ constexpr int kHdrGuDone = 16 + kTbCap;
 constexpr size_t kHeaderBytes = align256((16 + kTbCap + kChunkCap) * sizeof(int32_t));
 
 struct Layout {
-  size_t logits, chunk_tab, prow, xp, h, ys, total;
+  size_t logits, w64, chunk_tab, prow, xp, h, ys, total;
   int max_chunks, splits, kb_per_split, T_pad, n_ft, n_dp;
 };
 
@@ -96,6 +96,12 @@ Layout layout_for(const moe_b200_config& c, int64_t B) {
   const size_t ys_tiled = (size_t)L.splits * L.n_dp * 2 * L.T_pad * kBM * sizeof(float);
   size_t off = kHeaderBytes;
   L.logits = off;    off = align256(off + (size_t)B * c.num_experts * sizeof(float));
+  {
+    const int expc = std::min(c.num_experts, 32);
+    const size_t neb = (c.num_experts + expc - 1) / expc;
+    const size_t d_pad = (c.hidden_dim + kRouterKC - 1) / kRouterKC * kRouterKC;
+    L.w64 = off;     off = align256(off + neb * d_pad * expc * sizeof(double));
+  }
   L.chunk_tab = off; off = align256(off + (size_t)L.max_chunks * sizeof(int4));
   L.prow = off;      off = align256(off + (size_t)T * sizeof(int32_t));
   L.xp = off;        off = align256(off + (size_t)T * c.hidden_dim * 2);
@@ -172,47 +178,36 @@ int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 // ------------------------------- launches --------------------------------------
 unsigned long long* g_ffn_trace = nullptr;  // debug: per-tile timeline of the next ffn launches
 struct RouterPlan {
-  int expc, te, tt, tokc, n_eblocks, n_tblocks, threads;
+  int expc, te, tt, tokc, n_eblocks, n_tblocks, threads, d_pad;
   size_t smem;
 };
 
 // Router CTA shape: expc experts x tokc tokens; each compute thread owns a
 // te x tt register tile of sequential fp64 chains; 4 producer warps stage
-// operands.  Large B*E (DeepSeek) is fp64-throughput bound: 2x2 tiles keep
-// shared-memory traffic under the DFMA rate.  Small B*E (Mixtral, Qwen) is
-// chain-latency bound: 1x1 tiles and few tokens per CTA spread the chains
-// over >= ~120 SMs.
+// operands.  Large B*E (DeepSeek) is fp64-throughput bound: 2x4 tiles keep
+// shared-memory wavefronts under the DFMA rate.  Small B*E (Mixtral, Qwen)
+// is chain-latency bound (d x 8.2 cycles): 1x1 tiles and few tokens per CTA
+// spread the chains over >= ~120 SMs.
 RouterPlan plan_router(const moe_b200_config& c, int64_t B, int x_bf16) {
   RouterPlan r{};
   const int E = c.num_experts;
-  const int xb = x_bf16 ? 2 : 4;
   r.expc = std::min(E, 32);
   r.n_eblocks = (E + r.expc - 1) / r.expc;
+  r.d_pad = (c.hidden_dim + kRouterKC - 1) / kRouterKC * kRouterKC;
   const int64_t target = (kNumSMs * 4) / 5;
-  auto threads_for = [&](int tokc, int te, int tt) {
-    return ((r.expc / te) * (tokc / tt) + 31) / 32 * 32 + kRouterProducers;
-  };
-  auto smem_for = [&](int tokc, int te, int tt) {
-    return RouterSmem::total_bytes(tokc, r.expc, xb, E, threads_for(tokc, te, tt));
-  };
-  const size_t smem_cap = 200 * 1024;
   const int64_t chains = B * (int64_t)E;
   if (chains >= 64LL * 1024 && r.expc % 2 == 0) {
-    r.te = 2; r.tt = 2;
-    int tokc = 32;
-    while (tokc > 2 && (smem_for(tokc, 2, 2) > smem_cap || threads_for(tokc, 2, 2) > 384)) tokc /= 2;
-    r.tokc = tokc;
+    r.te = 2; r.tt = 4; r.tokc = 32;
   } else {
     r.te = 1; r.tt = 1;
     int g = 1;
-    while (g * 2 <= 256 / r.expc && ((B + g * 2 - 1) / (g * 2)) * r.n_eblocks >= target &&
-           smem_for(g * 2, 1, 1) <= smem_cap)
-      g *= 2;
+    while (g * 2 * r.expc <= 256 && g * 2 <= 64 && ((B + g * 2 - 1) / (g * 2)) * r.n_eblocks >= target) g *= 2;
     r.tokc = g;
   }
-  r.threads = threads_for(r.tokc, r.te, r.tt);
+  const int compute = ((r.expc / r.te) * (r.tokc / r.tt) + 31) / 32 * 32;
+  r.threads = compute + kRouterProducers;
   r.n_tblocks = static_cast<int>((B + r.tokc - 1) / r.tokc);
-  r.smem = smem_for(r.tokc, r.te, r.tt);
+  r.smem = RouterSmem::total_bytes(r.tokc, r.expc, x_bf16 ? 2 : 4, E, r.threads);
   return r;
 }
 
@@ -227,7 +222,7 @@ int launch_router_t(const RouterParams& p, const RouterPlan& plan, cudaStream_t 
 
 template <bool kBf16>
 int launch_router_x(const RouterParams& p, const RouterPlan& plan, cudaStream_t s) {
-  if (plan.te == 2) return launch_router_t<kBf16, 2, 2>(p, plan, s);
+  if (plan.te == 2) return launch_router_t<kBf16, 2, 4>(p, plan, s);
   return launch_router_t<kBf16, 1, 1>(p, plan, s);
 }
 
@@ -406,7 +401,16 @@ int moe_b200_route(const moe_b200_config* cfg, int64_t B, const void* x, int x_d
   RouterPlan plan = plan_router(*cfg, B, xb);
   if (plan.n_tblocks > kTbCap) return MOE_B200_ERR_UNSUPPORTED;
   RouterParams p{};
-  p.x = x; p.wr = w_router; p.x_bf16 = xb;
+  double* w64 = reinterpret_cast<double*>(ws8(ws) + L.w64);
+  {
+    // exact fp32 -> fp64 widening of W_r into the chunked expert-block layout
+    const long total = (long)plan.n_eblocks * plan.d_pad * plan.expc;
+    const int grid = static_cast<int>(std::min<long>((total + 255) / 256, (long)kNumSMs * 8));
+    router_prep_kernel<<<grid, 256, 0, s>>>(w_router, w64, cfg->hidden_dim, cfg->num_experts, plan.expc,
+                                           plan.d_pad, plan.n_eblocks, reinterpret_cast<uint32_t*>(hdr));
+    MOE_LAUNCH_CHECK("router_prep_kernel");
+  }
+  p.x = x; p.wr = w_router; p.w64 = w64; p.x_bf16 = xb;
   p.B = static_cast<int>(B); p.d = cfg->hidden_dim; p.E = cfg->num_experts; p.k = cfg->top_k;
   p.gating = cfg->gating;
   p.tokc = plan.tokc; p.expc = plan.expc;

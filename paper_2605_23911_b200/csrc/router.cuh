@@ -27,13 +27,13 @@
 
 namespace moe {
 
-constexpr int kRouterKC = 128;     // k-chunk staged per pipeline step
-constexpr int kRouterStages = 3;   // cp.async ring depth
+constexpr int kRouterKC = 64;      // k-chunk staged per pipeline step
 constexpr int kMaxExperts = 1024;
 
 struct RouterParams {
   const void* x;        // (B, d) fp32 or bf16
   const float* wr;      // (d, E) fp32
+  const double* w64;    // prepared W64[eb][d_pad][expc] (router_prep_kernel)
   int x_bf16;
   int B, d, E, k, gating;
   int tokc, expc;       // CTA tile: tokc tokens x expc experts
@@ -165,36 +165,53 @@ MOE_DEVICE void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// ---------------------------------------------------------------------------
-// Named barriers (ids 1..5; 0 is __syncthreads)
-// ---------------------------------------------------------------------------
-MOE_DEVICE void nbar_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-MOE_DEVICE void nbar_arrive(int id, int count) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-constexpr int kRouterProducers = 128;  // 4 warps: cp.async ring + fp64 conversion
+constexpr int kRouterProducers = 128;  // 4 warps: W bulk copies + x fp64 conversion
+constexpr int kRouterStagesV4 = 4;
 
 // ---------------------------------------------------------------------------
-// Shared-memory carve-up for phase 1
-//   raw ring : kRouterStages x {x chunk (tokc x KC, x dtype), w chunk (KC x expc fp32)}
-//   f64 bufs : 2 x {x (tokc x (KC+1)) fp64, w (KC x expc) fp64}
+// Router weight preparation (once per weight): W64[eb][k][expc] fp64, the
+// exact widening of the fp32 router weight, zero-padded to whole k-chunks and
+// expert blocks, so a chunk of an expert block is ONE contiguous bulk copy.
+// Non-finite entries set flag bit 2 (NonFiniteInput on router_weight).
+// ---------------------------------------------------------------------------
+__global__ void router_prep_kernel(const float* __restrict__ wr, double* __restrict__ w64, int d, int E,
+                                   int expc, int d_pad, int n_eblocks, uint32_t* flags) {
+  const long total = (long)n_eblocks * d_pad * expc;
+  bool bad = false;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int el = static_cast<int>(i % expc);
+    const long r = i / expc;
+    const int k = static_cast<int>(r % d_pad);
+    const int eb = static_cast<int>(r / d_pad);
+    const int e = eb * expc + el;
+    float v = 0.0f;
+    if (k < d && e < E) {
+      v = __ldg(wr + (size_t)k * E + e);
+      if (!isfinite(v)) bad = true;
+    }
+    w64[i] = static_cast<double>(v);
+  }
+  if (bad) atomicOr(flags, 2u);
+}
+
+MOE_DEVICE void bulk_load_smem(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Shared memory of phase 1: kRouterStagesV4 x {W chunk (KC x expc fp64),
+// x chunk (tokc x (KC+1) fp64)} + mbarriers full[s], empty[s].
 // ---------------------------------------------------------------------------
 struct RouterSmem {
-  static __host__ __device__ size_t raw_x_bytes(int tokc, int xb) { return (size_t)tokc * kRouterKC * xb; }
-  static __host__ __device__ size_t raw_w_bytes(int expc) {
-    return ((size_t)kRouterKC * expc * 4 + 15) / 16 * 16;
-  }
-  static __host__ __device__ size_t raw_stage_bytes(int tokc, int expc, int xb) {
-    return raw_x_bytes(tokc, xb) + raw_w_bytes(expc);
-  }
-  static __host__ __device__ size_t f64_x_elems(int tokc) { return (size_t)tokc * (kRouterKC + 1); }
-  static __host__ __device__ size_t f64_w_elems(int expc) { return (size_t)kRouterKC * expc; }
+  static __host__ __device__ size_t w_bytes(int expc) { return (size_t)kRouterKC * expc * 8; }
+  static __host__ __device__ size_t x_bytes(int tokc) { return ((size_t)tokc * (kRouterKC + 1) * 8 + 127) / 128 * 128; }
+  static __host__ __device__ size_t stage_bytes(int tokc, int expc) { return w_bytes(expc) + x_bytes(tokc); }
   static __host__ __device__ size_t total_bytes(int tokc, int expc, int xb, int E, int nthreads) {
-    size_t ph1 = kRouterStages * raw_stage_bytes(tokc, expc, xb) +
-                 2 * (f64_x_elems(tokc) + f64_w_elems(expc)) * sizeof(double);
+    (void)xb;
+    size_t ph1 = kRouterStagesV4 * stage_bytes(tokc, expc) + 2 * kRouterStagesV4 * 8;
     size_t ph2 = (size_t)(nthreads / 32) * E * sizeof(double);
     size_t ph3 = ((size_t)(nthreads / 32) + 5) * E * sizeof(int32_t) + 512;
     size_t m = ph1 > ph2 ? ph1 : ph2;
@@ -202,50 +219,11 @@ struct RouterSmem {
   }
 };
 
-// Producer-side: issue the cp.async copies of k-chunk `c` into ring slot `slot`.
-template <bool kXBf16>
-MOE_DEVICE void router_issue_chunk(const RouterParams& p, uint8_t* raw, int slot, int c, int t0,
-                                   int e0, int ptid) {
-  const int xb = kXBf16 ? 2 : 4;
-  uint8_t* sx = raw + (size_t)slot * RouterSmem::raw_stage_bytes(p.tokc, p.expc, xb);
-  uint8_t* sw = sx + RouterSmem::raw_x_bytes(p.tokc, xb);
-  const int k0 = c * kRouterKC;
-  constexpr int x_ppr = kRouterKC * (kXBf16 ? 2 : 4) / 16;  // 16-byte pieces per x row
-  const int x_pieces = p.tokc * x_ppr;
-  const uint8_t* xg = static_cast<const uint8_t*>(p.x);
-  for (int i = ptid; i < x_pieces; i += kRouterProducers) {
-    const int row = i / x_ppr, pc = i % x_ppr;
-    const int t = t0 + row;
-    const int kk = k0 + pc * (16 / xb);
-    const bool valid = (t < p.B) && (kk < p.d);
-    const uint8_t* src = valid ? xg + ((size_t)t * p.d + kk) * xb : xg;
-    cp_async_16(sx + (size_t)i * 16, src, valid);
-  }
-  if ((p.E % 4) == 0 && (p.expc % 4) == 0) {
-    const int w_ppr = p.expc / 4;
-    const int w_pieces = kRouterKC * w_ppr;
-    for (int i = ptid; i < w_pieces; i += kRouterProducers) {
-      const int kr = i / w_ppr, pc = i % w_ppr;
-      const int kk = k0 + kr;
-      const int e = e0 + pc * 4;
-      const bool valid = (kk < p.d) && (e < p.E);
-      const float* src = valid ? p.wr + (size_t)kk * p.E + e : p.wr;
-      cp_async_16(sw + (size_t)(kr * p.expc + pc * 4) * 4, src, valid);
-    }
-  } else {
-    float* swf = reinterpret_cast<float*>(sw);
-    for (int i = ptid; i < kRouterKC * p.expc; i += kRouterProducers) {
-      const int kr = i / p.expc, el = i % p.expc;
-      const int kk = k0 + kr, e = e0 + el;
-      swf[i] = (kk < p.d && e < p.E) ? __ldg(p.wr + (size_t)kk * p.E + e) : 0.0f;
-    }
-  }
-}
-
-// Launch shape: blockDim = n_compute + kRouterProducers.  Compute threads
-// [0, n_compute) own (expert lane, token group) chains; producer warps stage
-// and convert the operands one chunk ahead, synchronised by named barriers
-// FULL[b] (ids 1,2) and EMPTY[b] (ids 3,4); id 5 syncs the producers.
+// Launch shape: blockDim = n_compute + kRouterProducers.  Compute threads own a
+// kTE x kTT register tile of independent sequential fp64 chains; the producer
+// warps fill stage s: one elected thread bulk-copies the W64 chunk (tx-count on
+// full[s]), all 128 convert the x chunk to fp64 (one arrival each).  Compute
+// warps release stages through empty[s] (one arrival per warp).
 template <bool kXBf16, int kTE, int kTT>
 __global__ void __launch_bounds__(384)
 router_kernel(const RouterParams p) {
@@ -253,75 +231,64 @@ router_kernel(const RouterParams p) {
   const int tid = threadIdx.x;
   const int nthreads = blockDim.x;
   const int n_compute = nthreads - kRouterProducers;
+  const int n_cwarps = n_compute / 32;
   const int tb = blockIdx.x / p.n_eblocks;
   const int eb = blockIdx.x % p.n_eblocks;
   const int t0 = tb * p.tokc;
   const int e0 = eb * p.expc;
-  const int xb = kXBf16 ? 2 : 4;
 
   // ------------------------------- phase 1: logits ---------------------------
-  uint8_t* raw = smem;
-  const size_t raw_total = kRouterStages * RouterSmem::raw_stage_bytes(p.tokc, p.expc, xb);
-  double* f64 = reinterpret_cast<double*>(smem + raw_total);
-  const size_t fx = RouterSmem::f64_x_elems(p.tokc), fw = RouterSmem::f64_w_elems(p.expc);
+  const size_t wbytes = RouterSmem::w_bytes(p.expc);
+  const size_t sbytes = RouterSmem::stage_bytes(p.tokc, p.expc);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRouterStagesV4 * sbytes);
+  uint64_t* empty = full + kRouterStagesV4;
   const int nch = (p.d + kRouterKC - 1) / kRouterKC;
-  const int nbar = nthreads;
+  const int d_pad = nch * kRouterKC;
+  if (tid == 0) {
+    for (int s = 0; s < kRouterStagesV4; ++s) {
+      mbar_init(full + s, kRouterProducers + 1);
+      mbar_init(empty + s, n_cwarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
 
   if (tid >= n_compute) {
     // ============================ producers ================================
     const int ptid = tid - n_compute;
-    bool nonfinite_x = false, nonfinite_w = false;
-    for (int s = 0; s < kRouterStages - 1; ++s) {
-      if (s < nch) router_issue_chunk<kXBf16>(p, raw, s, s, t0, e0, ptid);
-      cp_async_commit();
-    }
+    bool nonfinite_x = false;
+    const double* wsrc = p.w64 + (size_t)eb * d_pad * p.expc;
+    const int nx = p.tokc * kRouterKC;
     for (int c = 0; c < nch; ++c) {
-      cp_async_wait<kRouterStages - 2>();
-      nbar_sync(5, kRouterProducers);  // chunk c landed for every producer thread
-      const int b = c & 1;
-      if (c >= 2) nbar_sync(3 + b, nbar);  // consumers released buffer b (chunk c-2)
-      const uint8_t* sx = raw + (size_t)(c % kRouterStages) * RouterSmem::raw_stage_bytes(p.tokc, p.expc, xb);
-      const float* sw = reinterpret_cast<const float*>(sx + RouterSmem::raw_x_bytes(p.tokc, xb));
-      double* dx = f64 + (size_t)b * (fx + fw);
-      double* dw = dx + fx;
-      const int kvalid = min(kRouterKC, p.d - c * kRouterKC);
-      const int nx = p.tokc * kRouterKC;
-#pragma unroll 4
+      const int s = c % kRouterStagesV4;
+      const uint32_t ph = (c / kRouterStagesV4) & 1;
+      mbar_wait(empty + s, ph ^ 1);
+      uint8_t* st = smem + s * sbytes;
+      if (ptid == 0) {
+        mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(wbytes));
+        bulk_load_smem(st, wsrc + (size_t)c * kRouterKC * p.expc, static_cast<uint32_t>(wbytes), full + s);
+      }
+      double* dx = reinterpret_cast<double*>(st + wbytes);
+      const int k0 = c * kRouterKC;
       for (int i = ptid; i < nx; i += kRouterProducers) {
         const int row = i / kRouterKC, kk = i % kRouterKC;
-        float v;
-        if (kXBf16) v = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(sx)[i]);
-        else v = reinterpret_cast<const float*>(sx)[i];
-        if (kk < kvalid && t0 + row < p.B && !isfinite(v)) nonfinite_x = true;
+        const int t = t0 + row, k = k0 + kk;
+        float v = 0.0f;
+        if (t < p.B && k < p.d) {
+          if (kXBf16) v = __bfloat162float(static_cast<const __nv_bfloat16*>(p.x)[(size_t)t * p.d + k]);
+          else v = __ldg(static_cast<const float*>(p.x) + (size_t)t * p.d + k);
+          if (!isfinite(v)) nonfinite_x = true;
+        }
         dx[row * (kRouterKC + 1) + kk] = static_cast<double>(v);
       }
-      const int nw = kRouterKC * p.expc;
-#pragma unroll 4
-      for (int i = ptid; i < nw; i += kRouterProducers) {
-        const float v = sw[i];
-        const int kk = i / p.expc, e = i % p.expc;
-        if (kk < kvalid && e0 + e < p.E && !isfinite(v)) nonfinite_w = true;
-        dw[i] = static_cast<double>(v);
-      }
-      nbar_arrive(1 + b, nbar);  // buffer b full
-      // refill the raw slot of chunk c-1 (every producer converted it before
-      // the barrier at the top of this iteration) with chunk c + S - 1
-      const int nc = c + kRouterStages - 1;
-      if (nc < nch) router_issue_chunk<kXBf16>(p, raw, nc % kRouterStages, nc, t0, e0, ptid);
-      cp_async_commit();
+      mbar_arrive(full + s);
     }
-    cp_async_wait<0>();
-    // balance the consumers' final EMPTY arrivals
-    for (int c = max(nch - 2, 0); c < nch; ++c) nbar_sync(3 + (c & 1), nbar);
     if (nonfinite_x) atomicOr(p.flags, 1u);
-    if (nonfinite_w) atomicOr(p.flags, 2u);
   } else {
     // ============================ compute chains ===========================
-    // Thread tile: kTE experts x kTT tokens of independent sequential chains.
-    // Experts e0 + eg + i*n_eg, tokens t0 + tg + j*n_tg: the warp's w loads are
-    // contiguous and its x loads near-broadcast, so shared-memory wavefronts
-    // stay below the fp64 FMA rate; operands are register double-buffered
-    // U steps ahead of the dependent FMA chain.
+    // Experts e0 + eg + i*n_eg, tokens t0 + tg + j*n_tg: the warp's W loads are
+    // contiguous and its x loads near-broadcast; operands are register
+    // double-buffered U steps ahead of the dependent FMA chain.
     constexpr int U = 8;
     const int n_eg = p.expc / kTE;
     const int n_tg = p.tokc / kTT;
@@ -334,16 +301,18 @@ router_kernel(const RouterParams p) {
 #pragma unroll
       for (int j = 0; j < kTT; ++j) acc[i][j] = -0.0;  // fma(a,b,-0) == a*b exactly, sign included
     constexpr int XS = kRouterKC + 1;  // padded fp64 x row
+    const int lane = tid & 31;
     for (int c = 0; c < nch; ++c) {
-      const int b = c & 1;
-      nbar_sync(1 + b, nbar);
+      const int s = c % kRouterStagesV4;
+      const uint32_t ph = (c / kRouterStagesV4) & 1;
+      mbar_wait(full + s, ph);
       if (active) {
-        const double* dx = f64 + (size_t)b * (fx + fw) + (size_t)tg * XS;
-        const double* dw = f64 + (size_t)b * (fx + fw) + fx + eg;
+        const uint8_t* st = smem + s * sbytes;
+        const double* dw = reinterpret_cast<const double*>(st) + eg;
+        const double* dx = reinterpret_cast<const double*>(st + wbytes) + (size_t)tg * XS;
         const int xstep = n_tg * XS;
-        const int kvalid = min(kRouterKC, p.d - c * kRouterKC);
-        if (kvalid == kRouterKC) {
-          double xa[kTT][U], wa[kTE][U], xb[kTT][U], wb[kTE][U];
+        // the last chunk may be partial: only k < d is folded, like the reference
+        double xa[kTT][U], wa[kTE][U], xb[kTT][U], wb[kTE][U];
 #define MOE_RLOAD(KK, XV, WV)                                                           \
   _Pragma("unroll") for (int u = 0; u < U; ++u) {                                       \
     _Pragma("unroll") for (int j = 0; j < kTT; ++j) XV[j][u] = dx[j * xstep + (KK) + u]; \
@@ -353,6 +322,8 @@ router_kernel(const RouterParams p) {
   _Pragma("unroll") for (int u = 0; u < U; ++u)                                         \
     _Pragma("unroll") for (int i = 0; i < kTE; ++i)                                     \
       _Pragma("unroll") for (int j = 0; j < kTT; ++j) acc[i][j] = __fma_rn(XV[j][u], WV[i][u], acc[i][j]);
+        const int kvalid = min(kRouterKC, p.d - c * kRouterKC);
+        if (kvalid == kRouterKC) {
           MOE_RLOAD(0, xa, wa);
 #pragma unroll
           for (int kk = 0; kk < kRouterKC; kk += 2 * U) {
@@ -361,8 +332,6 @@ router_kernel(const RouterParams p) {
             if (kk + 2 * U < kRouterKC) { MOE_RLOAD(kk + 2 * U, xa, wa); }
             MOE_RFMA(xb, wb);
           }
-#undef MOE_RLOAD
-#undef MOE_RFMA
         } else {
           for (int kk = 0; kk < kvalid; ++kk) {
 #pragma unroll
@@ -373,8 +342,11 @@ router_kernel(const RouterParams p) {
             }
           }
         }
+#undef MOE_RLOAD
+#undef MOE_RFMA
       }
-      nbar_arrive(3 + b, nbar);  // buffer b free
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
     }
     if (active) {
 #pragma unroll
