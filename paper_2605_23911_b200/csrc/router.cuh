@@ -208,10 +208,12 @@ MOE_DEVICE void bulk_load_smem(void* dst, const void* src, uint32_t bytes, uint6
 struct RouterSmem {
   static __host__ __device__ size_t w_bytes(int expc) { return (size_t)kRouterKC * expc * 8; }
   static __host__ __device__ size_t x_bytes(int tokc) { return ((size_t)tokc * (kRouterKC + 1) * 8 + 127) / 128 * 128; }
-  static __host__ __device__ size_t stage_bytes(int tokc, int expc) { return w_bytes(expc) + x_bytes(tokc); }
+  static __host__ __device__ size_t raw_bytes(int tokc, int xb) { return ((size_t)tokc * kRouterKC * xb + 127) / 128 * 128; }
+  static __host__ __device__ size_t stage_bytes(int tokc, int expc, int xb) {
+    return w_bytes(expc) + x_bytes(tokc) + raw_bytes(tokc, xb);
+  }
   static __host__ __device__ size_t total_bytes(int tokc, int expc, int xb, int E, int nthreads) {
-    (void)xb;
-    size_t ph1 = kRouterStagesV4 * stage_bytes(tokc, expc) + 2 * kRouterStagesV4 * 8;
+    size_t ph1 = kRouterStagesV4 * stage_bytes(tokc, expc, xb) + 3 * kRouterStagesV4 * 8;
     size_t ph2 = (size_t)(nthreads / 32) * E * sizeof(double);
     size_t ph3 = ((size_t)(nthreads / 32) + 5) * E * sizeof(int32_t) + 512;
     size_t m = ph1 > ph2 ? ph1 : ph2;
@@ -238,16 +240,21 @@ router_kernel(const RouterParams p) {
   const int e0 = eb * p.expc;
 
   // ------------------------------- phase 1: logits ---------------------------
+  const int xb = kXBf16 ? 2 : 4;
   const size_t wbytes = RouterSmem::w_bytes(p.expc);
-  const size_t sbytes = RouterSmem::stage_bytes(p.tokc, p.expc);
+  const size_t xbytes = RouterSmem::x_bytes(p.tokc);
+  const size_t sbytes = RouterSmem::stage_bytes(p.tokc, p.expc, xb);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRouterStagesV4 * sbytes);
   uint64_t* empty = full + kRouterStagesV4;
+  uint64_t* rawfull = empty + kRouterStagesV4;
   const int nch = (p.d + kRouterKC - 1) / kRouterKC;
   const int d_pad = nch * kRouterKC;
+  const int ntok = min(p.tokc, p.B - t0);  // valid token rows of this block
   if (tid == 0) {
     for (int s = 0; s < kRouterStagesV4; ++s) {
       mbar_init(full + s, kRouterProducers + 1);
       mbar_init(empty + s, n_cwarps);
+      mbar_init(rawfull + s, 1);
     }
     fence_barrier_init();
   }
@@ -255,33 +262,52 @@ router_kernel(const RouterParams p) {
 
   if (tid >= n_compute) {
     // ============================ producers ================================
+    // The elected producer keeps kRouterStagesV4-1 chunks of async copies in
+    // flight (W64 chunk -> full[s], raw x rows -> rawfull[s]); all producers
+    // convert each landed raw x chunk to fp64 and arrive on full[s].
     const int ptid = tid - n_compute;
     bool nonfinite_x = false;
     const double* wsrc = p.w64 + (size_t)eb * d_pad * p.expc;
-    const int nx = p.tokc * kRouterKC;
-    for (int c = 0; c < nch; ++c) {
+    const uint8_t* xsrc = static_cast<const uint8_t*>(p.x);
+    auto issue = [&](int c) {
       const int s = c % kRouterStagesV4;
       const uint32_t ph = (c / kRouterStagesV4) & 1;
       mbar_wait(empty + s, ph ^ 1);
       uint8_t* st = smem + s * sbytes;
-      if (ptid == 0) {
-        mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(wbytes));
-        bulk_load_smem(st, wsrc + (size_t)c * kRouterKC * p.expc, static_cast<uint32_t>(wbytes), full + s);
-      }
-      double* dx = reinterpret_cast<double*>(st + wbytes);
+      mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(wbytes));
+      bulk_load_smem(st, wsrc + (size_t)c * kRouterKC * p.expc, static_cast<uint32_t>(wbytes), full + s);
       const int k0 = c * kRouterKC;
+      const int kv = min(kRouterKC, p.d - k0);
+      const uint32_t rowb = static_cast<uint32_t>(kv * xb);
+      mbar_arrive_expect_tx(rawfull + s, rowb * ntok);
+      uint8_t* raw = st + wbytes + xbytes;
+      for (int r = 0; r < ntok; ++r)
+        bulk_load_smem(raw + (size_t)r * kRouterKC * xb, xsrc + ((size_t)(t0 + r) * p.d + k0) * xb, rowb, rawfull + s);
+    };
+    if (ptid == 0)
+      for (int c = 0; c < min(nch, kRouterStagesV4 - 1); ++c) issue(c);
+    const int nx = p.tokc * kRouterKC;
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % kRouterStagesV4;
+      const uint32_t ph = (c / kRouterStagesV4) & 1;
+      mbar_wait(rawfull + s, ph);
+      uint8_t* st = smem + s * sbytes;
+      double* dx = reinterpret_cast<double*>(st + wbytes);
+      const uint8_t* raw = st + wbytes + xbytes;
+      const int kv = min(kRouterKC, p.d - c * kRouterKC);
       for (int i = ptid; i < nx; i += kRouterProducers) {
         const int row = i / kRouterKC, kk = i % kRouterKC;
-        const int t = t0 + row, k = k0 + kk;
         float v = 0.0f;
-        if (t < p.B && k < p.d) {
-          if (kXBf16) v = __bfloat162float(static_cast<const __nv_bfloat16*>(p.x)[(size_t)t * p.d + k]);
-          else v = __ldg(static_cast<const float*>(p.x) + (size_t)t * p.d + k);
+        if (row < ntok && kk < kv) {
+          if (kXBf16) v = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(raw)[i]);
+          else v = reinterpret_cast<const float*>(raw)[i];
           if (!isfinite(v)) nonfinite_x = true;
         }
         dx[row * (kRouterKC + 1) + kk] = static_cast<double>(v);
       }
       mbar_arrive(full + s);
+      // refill: chunk c+S-1 goes into the stage of chunk c-1 once compute released it
+      if (ptid == 0 && c + kRouterStagesV4 - 1 < nch) issue(c + kRouterStagesV4 - 1);
     }
     if (nonfinite_x) atomicOr(p.flags, 1u);
   } else {
