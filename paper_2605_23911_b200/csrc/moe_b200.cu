@@ -177,6 +177,7 @@ int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 
 // ------------------------------- launches --------------------------------------
 unsigned long long* g_ffn_trace = nullptr;  // debug: per-tile timeline of the next ffn launches
+unsigned long long* g_router_trace = nullptr;  // debug: CTA-0 per-chunk router timeline
 struct RouterPlan {
   int expc, te, tt, tokc, n_eblocks, n_tblocks, threads, d_pad;
   size_t smem;
@@ -327,6 +328,7 @@ const char* moe_b200_version(void) { return "moe_b200 0.1.0 (sm_100a)"; }
 // Debug hook (not part of the public header): record a per-tile timeline of
 // subsequent ffn launches into a device buffer of 4 u64 per tile, or NULL to stop.
 void moe_b200_debug_set_ffn_trace(unsigned long long* dev_buf) { g_ffn_trace = dev_buf; }
+void moe_b200_debug_set_router_trace(unsigned long long* dev_buf) { g_router_trace = dev_buf; }
 
 const char* moe_b200_last_error_detail(void) { return g_last_error.c_str(); }
 
@@ -411,6 +413,7 @@ int moe_b200_route(const moe_b200_config* cfg, int64_t B, const void* x, int x_d
     MOE_LAUNCH_CHECK("router_prep_kernel");
   }
   p.x = x; p.wr = w_router; p.w64 = w64; p.x_bf16 = xb;
+  p.trace = g_router_trace;
   p.B = static_cast<int>(B); p.d = cfg->hidden_dim; p.E = cfg->num_experts; p.k = cfg->top_k;
   p.gating = cfg->gating;
   p.tokc = plan.tokc; p.expc = plan.expc;

@@ -52,6 +52,7 @@ struct RouterParams {
   int32_t* tb_counter;  // (n_tblocks) self-resetting
   int32_t* done_counter;// [1] self-resetting
   uint32_t* flags;      // [1]
+  unsigned long long* trace;  // debug: CTA 0 per-chunk {issue, rawfull seen, full seen, compute done}
 };
 
 // ---------------------------------------------------------------------------
@@ -275,6 +276,7 @@ router_kernel(const RouterParams p) {
       mbar_wait(empty + s, ph ^ 1);
       uint8_t* st = smem + s * sbytes;
       mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(wbytes));
+      if (p.trace && blockIdx.x == 0) p.trace[c * 4 + 0] = clock64();
       bulk_load_smem(st, wsrc + (size_t)c * kRouterKC * p.expc, static_cast<uint32_t>(wbytes), full + s);
       const int k0 = c * kRouterKC;
       const int kv = min(kRouterKC, p.d - k0);
@@ -291,6 +293,7 @@ router_kernel(const RouterParams p) {
       const int s = c % kRouterStagesV4;
       const uint32_t ph = (c / kRouterStagesV4) & 1;
       mbar_wait(rawfull + s, ph);
+      if (p.trace && blockIdx.x == 0 && ptid == 0) p.trace[c * 4 + 1] = clock64();
       uint8_t* st = smem + s * sbytes;
       double* dx = reinterpret_cast<double*>(st + wbytes);
       const uint8_t* raw = st + wbytes + xbytes;
@@ -332,6 +335,7 @@ router_kernel(const RouterParams p) {
       const int s = c % kRouterStagesV4;
       const uint32_t ph = (c / kRouterStagesV4) & 1;
       mbar_wait(full + s, ph);
+      if (p.trace && blockIdx.x == 0 && tid == 0) p.trace[c * 4 + 2] = clock64();
       if (active) {
         const uint8_t* st = smem + s * sbytes;
         const double* dw = reinterpret_cast<const double*>(st) + eg;
@@ -373,6 +377,7 @@ router_kernel(const RouterParams p) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
+      if (p.trace && blockIdx.x == 0 && tid == 0) p.trace[c * 4 + 3] = clock64();
     }
     if (active) {
 #pragma unroll
