@@ -139,6 +139,12 @@ MOE_DEVICE float np_expf(float x) {
   return __double2float_rn(static_cast<double>(p) * ldexp(1.0, static_cast<int>(q)));
 }
 
+MOE_DEVICE unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 MOE_DEVICE float np_sigmoid(float x) {
   float t = np_expf(-fabsf(x));
   float den = __fadd_rn(1.0f, t);
@@ -251,6 +257,7 @@ router_kernel(const RouterParams p) {
   const int nch = (p.d + kRouterKC - 1) / kRouterKC;
   const int d_pad = nch * kRouterKC;
   const int ntok = min(p.tokc, p.B - t0);  // valid token rows of this block
+  if (p.trace && threadIdx.x == 0) p.trace[4096 * 4 + 2048 * 4 + blockIdx.x] = globaltimer_ns();
   if (tid == 0) {
     for (int s = 0; s < kRouterStagesV4; ++s) {
       mbar_init(full + s, kRouterProducers + 1);
@@ -393,6 +400,7 @@ router_kernel(const RouterParams p) {
     }
   }
 
+  if (p.trace && tid == 0) p.trace[4096 * 4 + blockIdx.x * 4 + 0] = globaltimer_ns();
   // --------------------- phase 2: scores + top-k (last CTA of block) --------
   __shared__ int s_flag;
   __threadfence();
@@ -495,6 +503,7 @@ router_kernel(const RouterParams p) {
     }
   }
 
+  if (p.trace && tid == 0) p.trace[4096 * 4 + blockIdx.x * 4 + 1] = globaltimer_ns();
   // -------------------- phase 3: scheduler (last token block) ---------------
   __threadfence();
   __syncthreads();
@@ -601,6 +610,10 @@ router_kernel(const RouterParams p) {
       __syncwarp();
     }
     if (tid == 0) *p.done_counter = 0;
+    if (p.trace && tid == 0) {
+      p.trace[4096 * 4 + blockIdx.x * 4 + 2] = 1;
+      p.trace[4096 * 4 + blockIdx.x * 4 + 3] = globaltimer_ns();
+    }
   }
 }
 
