@@ -37,6 +37,7 @@ struct RouterParams {
   int x_bf16;
   int B, d, E, k, gating;
   int tokc, expc;       // CTA tile: tokc tokens x expc experts
+  int stages;           // smem pipeline depth
   int n_eblocks, n_tblocks;
   int chunk_rows;       // GEMM row-chunk cap (BN)
   float* logits;        // (B, E) fp32
@@ -136,7 +137,8 @@ MOE_DEVICE float np_expf(float x) {
   den = __fmaf_rn(den, r, 1.0f);
   float p = __fdiv_rn(num, den);
   // p * 2^q with a single rounding (scalef): exact in fp64, then one fp32 rounding.
-  return __double2float_rn(static_cast<double>(p) * ldexp(1.0, static_cast<int>(q)));
+  const long long qe = static_cast<long long>(static_cast<int>(q) + 1023) << 52;  // 2^q, q in [-150, 128]
+  return __double2float_rn(static_cast<double>(p) * __longlong_as_double(qe));
 }
 
 MOE_DEVICE unsigned long long globaltimer_ns() {
@@ -173,7 +175,7 @@ MOE_DEVICE void cp_async_wait() {
 }
 
 constexpr int kRouterProducers = 128;  // 4 warps: W bulk copies + x fp64 conversion
-constexpr int kRouterStagesV4 = 4;
+constexpr int kRouterMaxStages = 12;
 
 // ---------------------------------------------------------------------------
 // Router weight preparation (once per weight): W64[eb][k][expc] fp64, the
@@ -209,7 +211,7 @@ MOE_DEVICE void bulk_load_smem(void* dst, const void* src, uint32_t bytes, uint6
 }
 
 // ---------------------------------------------------------------------------
-// Shared memory of phase 1: kRouterStagesV4 x {W chunk (KC x expc fp64),
+// Shared memory of phase 1: p.stages x {W chunk (KC x expc fp64),
 // x chunk (tokc x (KC+1) fp64)} + mbarriers full[s], empty[s].
 // ---------------------------------------------------------------------------
 struct RouterSmem {
@@ -219,8 +221,8 @@ struct RouterSmem {
   static __host__ __device__ size_t stage_bytes(int tokc, int expc, int xb) {
     return w_bytes(expc) + x_bytes(tokc) + raw_bytes(tokc, xb);
   }
-  static __host__ __device__ size_t total_bytes(int tokc, int expc, int xb, int E, int nthreads) {
-    size_t ph1 = kRouterStagesV4 * stage_bytes(tokc, expc, xb) + 3 * kRouterStagesV4 * 8;
+  static __host__ __device__ size_t total_bytes(int tokc, int expc, int xb, int E, int nthreads, int stages) {
+    size_t ph1 = stages * stage_bytes(tokc, expc, xb) + 3 * stages * 8;
     size_t ph2 = (size_t)(nthreads / 32) * E * sizeof(double);
     size_t ph3 = ((size_t)(nthreads / 32) + 5) * E * sizeof(int32_t) + 512;
     size_t m = ph1 > ph2 ? ph1 : ph2;
@@ -235,7 +237,7 @@ struct RouterSmem {
 // warps release stages through empty[s] (one arrival per warp).
 template <bool kXBf16, int kTE, int kTT>
 __global__ void __launch_bounds__(384)
-router_kernel(const RouterParams p) {
+router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x;
   const int nthreads = blockDim.x;
@@ -251,15 +253,15 @@ router_kernel(const RouterParams p) {
   const size_t wbytes = RouterSmem::w_bytes(p.expc);
   const size_t xbytes = RouterSmem::x_bytes(p.tokc);
   const size_t sbytes = RouterSmem::stage_bytes(p.tokc, p.expc, xb);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRouterStagesV4 * sbytes);
-  uint64_t* empty = full + kRouterStagesV4;
-  uint64_t* rawfull = empty + kRouterStagesV4;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * sbytes);
+  uint64_t* empty = full + p.stages;
+  uint64_t* rawfull = empty + p.stages;
   const int nch = (p.d + kRouterKC - 1) / kRouterKC;
   const int d_pad = nch * kRouterKC;
   const int ntok = min(p.tokc, p.B - t0);  // valid token rows of this block
   if (p.trace && threadIdx.x == 0) p.trace[4096 * 4 + 2048 * 4 + blockIdx.x] = globaltimer_ns();
   if (tid == 0) {
-    for (int s = 0; s < kRouterStagesV4; ++s) {
+    for (int s = 0; s < p.stages; ++s) {
       mbar_init(full + s, kRouterProducers + 1);
       mbar_init(empty + s, n_cwarps);
       mbar_init(rawfull + s, 1);
@@ -270,35 +272,30 @@ router_kernel(const RouterParams p) {
 
   if (tid >= n_compute) {
     // ============================ producers ================================
-    // The elected producer keeps kRouterStagesV4-1 chunks of async copies in
+    // The elected producer keeps p.stages-1 chunks of async copies in
     // flight (W64 chunk -> full[s], raw x rows -> rawfull[s]); all producers
     // convert each landed raw x chunk to fp64 and arrive on full[s].
     const int ptid = tid - n_compute;
     bool nonfinite_x = false;
     const double* wsrc = p.w64 + (size_t)eb * d_pad * p.expc;
-    const uint8_t* xsrc = static_cast<const uint8_t*>(p.x);
     auto issue = [&](int c) {
-      const int s = c % kRouterStagesV4;
-      const uint32_t ph = (c / kRouterStagesV4) & 1;
+      const int s = c % p.stages;
+      const uint32_t ph = (c / p.stages) & 1;
       mbar_wait(empty + s, ph ^ 1);
       uint8_t* st = smem + s * sbytes;
       mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(wbytes));
       if (p.trace && blockIdx.x == 0) p.trace[c * 4 + 0] = clock64();
       bulk_load_smem(st, wsrc + (size_t)c * kRouterKC * p.expc, static_cast<uint32_t>(wbytes), full + s);
-      const int k0 = c * kRouterKC;
-      const int kv = min(kRouterKC, p.d - k0);
-      const uint32_t rowb = static_cast<uint32_t>(kv * xb);
-      mbar_arrive_expect_tx(rawfull + s, rowb * ntok);
-      uint8_t* raw = st + wbytes + xbytes;
-      for (int r = 0; r < ntok; ++r)
-        bulk_load_smem(raw + (size_t)r * kRouterKC * xb, xsrc + ((size_t)(t0 + r) * p.d + k0) * xb, rowb, rawfull + s);
+      // one 2-D TMA tile (KC x tokc, OOB rows/cols zero-filled) per chunk
+      mbar_arrive_expect_tx(rawfull + s, static_cast<uint32_t>(p.tokc * kRouterKC * xb));
+      tma_load_2d(&tm_x, rawfull + s, st + wbytes + xbytes, c * kRouterKC, t0);
     };
     if (ptid == 0)
-      for (int c = 0; c < min(nch, kRouterStagesV4 - 1); ++c) issue(c);
+      for (int c = 0; c < min(nch, p.stages - 1); ++c) issue(c);
     const int nx = p.tokc * kRouterKC;
     for (int c = 0; c < nch; ++c) {
-      const int s = c % kRouterStagesV4;
-      const uint32_t ph = (c / kRouterStagesV4) & 1;
+      const int s = c % p.stages;
+      const uint32_t ph = (c / p.stages) & 1;
       mbar_wait(rawfull + s, ph);
       if (p.trace && blockIdx.x == 0 && ptid == 0) p.trace[c * 4 + 1] = clock64();
       uint8_t* st = smem + s * sbytes;
@@ -317,7 +314,7 @@ router_kernel(const RouterParams p) {
       }
       mbar_arrive(full + s);
       // refill: chunk c+S-1 goes into the stage of chunk c-1 once compute released it
-      if (ptid == 0 && c + kRouterStagesV4 - 1 < nch) issue(c + kRouterStagesV4 - 1);
+      if (ptid == 0 && c + p.stages - 1 < nch) issue(c + p.stages - 1);
     }
     if (nonfinite_x) atomicOr(p.flags, 1u);
   } else {
@@ -325,7 +322,6 @@ router_kernel(const RouterParams p) {
     // Experts e0 + eg + i*n_eg, tokens t0 + tg + j*n_tg: the warp's W loads are
     // contiguous and its x loads near-broadcast; operands are register
     // double-buffered U steps ahead of the dependent FMA chain.
-    constexpr int U = 8;
     const int n_eg = p.expc / kTE;
     const int n_tg = p.tokc / kTT;
     const int eg = tid % n_eg;
@@ -339,8 +335,8 @@ router_kernel(const RouterParams p) {
     constexpr int XS = kRouterKC + 1;  // padded fp64 x row
     const int lane = tid & 31;
     for (int c = 0; c < nch; ++c) {
-      const int s = c % kRouterStagesV4;
-      const uint32_t ph = (c / kRouterStagesV4) & 1;
+      const int s = c % p.stages;
+      const uint32_t ph = (c / p.stages) & 1;
       mbar_wait(full + s, ph);
       if (p.trace && blockIdx.x == 0 && tid == 0) p.trace[c * 4 + 2] = clock64();
       if (active) {
@@ -349,25 +345,18 @@ router_kernel(const RouterParams p) {
         const double* dx = reinterpret_cast<const double*>(st + wbytes) + (size_t)tg * XS;
         const int xstep = n_tg * XS;
         // the last chunk may be partial: only k < d is folded, like the reference
-        double xa[kTT][U], wa[kTE][U], xb[kTT][U], wb[kTE][U];
-#define MOE_RLOAD(KK, XV, WV)                                                           \
-  _Pragma("unroll") for (int u = 0; u < U; ++u) {                                       \
-    _Pragma("unroll") for (int j = 0; j < kTT; ++j) XV[j][u] = dx[j * xstep + (KK) + u]; \
-    _Pragma("unroll") for (int i = 0; i < kTE; ++i) WV[i][u] = dw[((KK) + u) * p.expc + i * n_eg]; \
-  }
-#define MOE_RFMA(XV, WV)                                                                \
-  _Pragma("unroll") for (int u = 0; u < U; ++u)                                         \
-    _Pragma("unroll") for (int i = 0; i < kTE; ++i)                                     \
-      _Pragma("unroll") for (int j = 0; j < kTT; ++j) acc[i][j] = __fma_rn(XV[j][u], WV[i][u], acc[i][j]);
+        // plain loop: the compiler keeps operand loads ~6 steps ahead of the chain
+        // without register-reuse (WAR) stalls (probe: 10.3 vs 13.9 cycles/step)
         const int kvalid = min(kRouterKC, p.d - c * kRouterKC);
         if (kvalid == kRouterKC) {
-          MOE_RLOAD(0, xa, wa);
+#pragma unroll 16
+          for (int kk = 0; kk < kRouterKC; ++kk) {
 #pragma unroll
-          for (int kk = 0; kk < kRouterKC; kk += 2 * U) {
-            MOE_RLOAD(kk + U, xb, wb);
-            MOE_RFMA(xa, wa);
-            if (kk + 2 * U < kRouterKC) { MOE_RLOAD(kk + 2 * U, xa, wa); }
-            MOE_RFMA(xb, wb);
+            for (int i = 0; i < kTE; ++i) {
+              const double w = dw[kk * p.expc + i * n_eg];
+#pragma unroll
+              for (int j = 0; j < kTT; ++j) acc[i][j] = __fma_rn(dx[j * xstep + kk], w, acc[i][j]);
+            }
           }
         } else {
           for (int kk = 0; kk < kvalid; ++kk) {
@@ -379,8 +368,6 @@ router_kernel(const RouterParams p) {
             }
           }
         }
-#undef MOE_RLOAD
-#undef MOE_RFMA
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
