@@ -179,7 +179,7 @@ int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 unsigned long long* g_ffn_trace = nullptr;  // debug: per-tile timeline of the next ffn launches
 unsigned long long* g_router_trace = nullptr;  // debug: CTA-0 per-chunk router timeline
 struct RouterPlan {
-  int expc, te, tt, tokc, n_eblocks, n_tblocks, threads, d_pad, stages;
+  int expc, te, tt, tokc, n_eblocks, n_tblocks, threads, d_pad, stages, kc;
   size_t smem;
 };
 
@@ -209,16 +209,19 @@ RouterPlan plan_router(const moe_b200_config& c, int64_t B, int x_bf16) {
   r.threads = compute + kRouterProducers;
   r.n_tblocks = static_cast<int>((B + r.tokc - 1) / r.tokc);
   const int xb = x_bf16 ? 2 : 4;
-  // deep pipelines for small stages (latency regime), >= 4 stages otherwise
-  r.stages = static_cast<int>(std::min<size_t>(kRouterMaxStages, (160u * 1024) / RouterSmem::stage_bytes(r.tokc, r.expc, xb)));
-  r.stages = std::max(r.stages, 4);
-  r.smem = RouterSmem::total_bytes(r.tokc, r.expc, xb, E, r.threads, r.stages);
+  // latency regime: long k-chunks amortise the per-chunk barrier cost;
+  // throughput regime: 64-wide chunks keep >= 4 stages of 2x4-tile operands
+  r.kc = r.te == 1 ? 128 : 64;
+  const size_t sb = RouterSmem::stage_bytes(r.tokc, r.expc, xb, r.kc);
+  r.stages = static_cast<int>(std::min<size_t>(kRouterMaxStages, (180u * 1024) / sb));
+  r.stages = std::max(r.stages, 2);
+  r.smem = RouterSmem::total_bytes(r.tokc, r.expc, xb, E, r.threads, r.stages, r.kc);
   return r;
 }
 
-template <bool kBf16, int kTE, int kTT>
+template <bool kBf16, int kTE, int kTT, int kKC>
 int launch_router_t(const CUtensorMap& tmx, const RouterParams& p, const RouterPlan& plan, cudaStream_t s) {
-  auto kern = router_kernel<kBf16, kTE, kTT>;
+  auto kern = router_kernel<kBf16, kTE, kTT, kKC>;
   MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
   kern<<<plan.n_tblocks * plan.n_eblocks, plan.threads, plan.smem, s>>>(tmx, p);
   MOE_LAUNCH_CHECK("router_kernel");
@@ -227,8 +230,8 @@ int launch_router_t(const CUtensorMap& tmx, const RouterParams& p, const RouterP
 
 template <bool kBf16>
 int launch_router_x(const CUtensorMap& tmx, const RouterParams& p, const RouterPlan& plan, cudaStream_t s) {
-  if (plan.te == 2) return launch_router_t<kBf16, 2, 4>(tmx, p, plan, s);
-  return launch_router_t<kBf16, 1, 1>(tmx, p, plan, s);
+  if (plan.te == 2) return launch_router_t<kBf16, 2, 4, 64>(tmx, p, plan, s);
+  return launch_router_t<kBf16, 1, 1, 128>(tmx, p, plan, s);
 }
 
 template <int kBN, int kV>
@@ -439,7 +442,7 @@ int moe_b200_route(const moe_b200_config* cfg, int64_t B, const void* x, int x_d
     if (rc2) return rc2;
     cuuint64_t dims[2] = {(cuuint64_t)cfg->hidden_dim, (cuuint64_t)B};
     cuuint64_t strides[1] = {(cuuint64_t)cfg->hidden_dim * (xb ? 2 : 4)};
-    cuuint32_t box[2] = {(cuuint32_t)kRouterKC, (cuuint32_t)plan.tokc};
+    cuuint32_t box[2] = {(cuuint32_t)plan.kc, (cuuint32_t)plan.tokc};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = g_encode(&tmx, xb ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                           const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -27,7 +27,7 @@
 
 namespace moe {
 
-constexpr int kRouterKC = 64;      // k-chunk staged per pipeline step
+constexpr int kRouterKC = 128;     // W64 padding granularity (max k-chunk)
 constexpr int kMaxExperts = 1024;
 
 struct RouterParams {
@@ -215,14 +215,14 @@ MOE_DEVICE void bulk_load_smem(void* dst, const void* src, uint32_t bytes, uint6
 // x chunk (tokc x (KC+1) fp64)} + mbarriers full[s], empty[s].
 // ---------------------------------------------------------------------------
 struct RouterSmem {
-  static __host__ __device__ size_t w_bytes(int expc) { return (size_t)kRouterKC * expc * 8; }
-  static __host__ __device__ size_t x_bytes(int tokc) { return ((size_t)tokc * (kRouterKC + 1) * 8 + 127) / 128 * 128; }
-  static __host__ __device__ size_t raw_bytes(int tokc, int xb) { return ((size_t)tokc * kRouterKC * xb + 127) / 128 * 128; }
-  static __host__ __device__ size_t stage_bytes(int tokc, int expc, int xb) {
-    return w_bytes(expc) + x_bytes(tokc) + raw_bytes(tokc, xb);
+  static __host__ __device__ size_t w_bytes(int expc, int kc) { return (size_t)kc * expc * 8; }
+  static __host__ __device__ size_t x_bytes(int tokc, int kc) { return ((size_t)tokc * (kc + 1) * 8 + 127) / 128 * 128; }
+  static __host__ __device__ size_t raw_bytes(int tokc, int xb, int kc) { return ((size_t)tokc * kc * xb + 127) / 128 * 128; }
+  static __host__ __device__ size_t stage_bytes(int tokc, int expc, int xb, int kc) {
+    return w_bytes(expc, kc) + x_bytes(tokc, kc) + raw_bytes(tokc, xb, kc);
   }
-  static __host__ __device__ size_t total_bytes(int tokc, int expc, int xb, int E, int nthreads, int stages) {
-    size_t ph1 = stages * stage_bytes(tokc, expc, xb) + 3 * stages * 8;
+  static __host__ __device__ size_t total_bytes(int tokc, int expc, int xb, int E, int nthreads, int stages, int kc) {
+    size_t ph1 = stages * stage_bytes(tokc, expc, xb, kc) + 3 * stages * 8;
     size_t ph2 = (size_t)(nthreads / 32) * E * sizeof(double);
     size_t ph3 = ((size_t)(nthreads / 32) + 5) * E * sizeof(int32_t) + 512;
     size_t m = ph1 > ph2 ? ph1 : ph2;
@@ -235,7 +235,7 @@ struct RouterSmem {
 // warps fill stage s: one elected thread bulk-copies the W64 chunk (tx-count on
 // full[s]), all 128 convert the x chunk to fp64 (one arrival each).  Compute
 // warps release stages through empty[s] (one arrival per warp).
-template <bool kXBf16, int kTE, int kTT>
+template <bool kXBf16, int kTE, int kTT, int kKC>
 __global__ void __launch_bounds__(384)
 router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -250,14 +250,14 @@ router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
 
   // ------------------------------- phase 1: logits ---------------------------
   const int xb = kXBf16 ? 2 : 4;
-  const size_t wbytes = RouterSmem::w_bytes(p.expc);
-  const size_t xbytes = RouterSmem::x_bytes(p.tokc);
-  const size_t sbytes = RouterSmem::stage_bytes(p.tokc, p.expc, xb);
+  const size_t wbytes = RouterSmem::w_bytes(p.expc, kKC);
+  const size_t xbytes = RouterSmem::x_bytes(p.tokc, kKC);
+  const size_t sbytes = RouterSmem::stage_bytes(p.tokc, p.expc, xb, kKC);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * sbytes);
   uint64_t* empty = full + p.stages;
   uint64_t* rawfull = empty + p.stages;
-  const int nch = (p.d + kRouterKC - 1) / kRouterKC;
-  const int d_pad = nch * kRouterKC;
+  const int nch = (p.d + kKC - 1) / kKC;
+  const int d_pad = (p.d + kRouterKC - 1) / kRouterKC * kRouterKC;
   const int ntok = min(p.tokc, p.B - t0);  // valid token rows of this block
   if (p.trace && threadIdx.x == 0) p.trace[4096 * 4 + 2048 * 4 + blockIdx.x] = globaltimer_ns();
   if (tid == 0) {
@@ -285,14 +285,14 @@ router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
       uint8_t* st = smem + s * sbytes;
       mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(wbytes));
       if (p.trace && blockIdx.x == 0) p.trace[c * 4 + 0] = clock64();
-      bulk_load_smem(st, wsrc + (size_t)c * kRouterKC * p.expc, static_cast<uint32_t>(wbytes), full + s);
+      bulk_load_smem(st, wsrc + (size_t)c * kKC * p.expc, static_cast<uint32_t>(wbytes), full + s);
       // one 2-D TMA tile (KC x tokc, OOB rows/cols zero-filled) per chunk
-      mbar_arrive_expect_tx(rawfull + s, static_cast<uint32_t>(p.tokc * kRouterKC * xb));
-      tma_load_2d(&tm_x, rawfull + s, st + wbytes + xbytes, c * kRouterKC, t0);
+      mbar_arrive_expect_tx(rawfull + s, static_cast<uint32_t>(p.tokc * kKC * xb));
+      tma_load_2d(&tm_x, rawfull + s, st + wbytes + xbytes, c * kKC, t0);
     };
     if (ptid == 0)
       for (int c = 0; c < min(nch, p.stages - 1); ++c) issue(c);
-    const int nx = p.tokc * kRouterKC;
+    const int nx = p.tokc * kKC;
     for (int c = 0; c < nch; ++c) {
       const int s = c % p.stages;
       const uint32_t ph = (c / p.stages) & 1;
@@ -301,16 +301,16 @@ router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
       uint8_t* st = smem + s * sbytes;
       double* dx = reinterpret_cast<double*>(st + wbytes);
       const uint8_t* raw = st + wbytes + xbytes;
-      const int kv = min(kRouterKC, p.d - c * kRouterKC);
+      const int kv = min(kKC, p.d - c * kKC);
       for (int i = ptid; i < nx; i += kRouterProducers) {
-        const int row = i / kRouterKC, kk = i % kRouterKC;
+        const int row = i / kKC, kk = i % kKC;
         float v = 0.0f;
         if (row < ntok && kk < kv) {
           if (kXBf16) v = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(raw)[i]);
           else v = reinterpret_cast<const float*>(raw)[i];
           if (!isfinite(v)) nonfinite_x = true;
         }
-        dx[row * (kRouterKC + 1) + kk] = static_cast<double>(v);
+        dx[row * (kKC + 1) + kk] = static_cast<double>(v);
       }
       mbar_arrive(full + s);
       // refill: chunk c+S-1 goes into the stage of chunk c-1 once compute released it
@@ -332,7 +332,7 @@ router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
     for (int i = 0; i < kTE; ++i)
 #pragma unroll
       for (int j = 0; j < kTT; ++j) acc[i][j] = -0.0;  // fma(a,b,-0) == a*b exactly, sign included
-    constexpr int XS = kRouterKC + 1;  // padded fp64 x row
+    constexpr int XS = kKC + 1;  // padded fp64 x row
     const int lane = tid & 31;
     for (int c = 0; c < nch; ++c) {
       const int s = c % p.stages;
@@ -347,10 +347,10 @@ router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
         // the last chunk may be partial: only k < d is folded, like the reference
         // plain loop: the compiler keeps operand loads ~6 steps ahead of the chain
         // without register-reuse (WAR) stalls (probe: 10.3 vs 13.9 cycles/step)
-        const int kvalid = min(kRouterKC, p.d - c * kRouterKC);
-        if (kvalid == kRouterKC) {
+        const int kvalid = min(kKC, p.d - c * kKC);
+        if (kvalid == kKC) {
 #pragma unroll 16
-          for (int kk = 0; kk < kRouterKC; ++kk) {
+          for (int kk = 0; kk < kKC; ++kk) {
 #pragma unroll
             for (int i = 0; i < kTE; ++i) {
               const double w = dw[kk * p.expc + i * n_eg];
