@@ -5,7 +5,11 @@ import numpy as np
 cfg = {"mixtral": (8, 2, 4096, 14336), "qwen60": (60, 4, 2048, 1408), "deepseek": (256, 8, 7168, 2048),
        "skew64": (64, 2, 3584, 2560)}
 for tag in sys.argv[1:] or ["mixtral", "qwen60", "deepseek"]:
-    d = json.load(open(f"gpurun_out/timeline_{tag}.json"))
+    path = f"gpurun_out/timeline_{tag}.json"
+    import os
+    if not os.path.exists(path):
+        path = f"profiles/timeline_{tag}.json"
+    d = json.load(open(path))
     name = d["config"]
     E, k, dd, ff = cfg[name]
     f = np.array(d["fetch_us"]); e = np.array(d["done_us"]); es = np.array(d["epi_start_us"])
