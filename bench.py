@@ -17,9 +17,9 @@ independent replica per rank (the Mixtral layer does not shard: "replicas
 only", weak scaling), max over ranks.  `e2e` re-times the same forward
 through the C-ABI call with the step's tokens copied from pinned host memory
 and the output copied back inside the timed region.  `roofline` is the
-dominant kernel (fused gate+up grouped GEMM) timed live, bytes from the
-reference's minimal-traffic model (moeperf/perfmodel.py:216-249) over the
-measured HBM copy peak.  `cpu_baseline` times the oracle port of the
+dominant kernel (the fused expert-FFN launch) timed live inside the real
+forward, bytes from the reference's minimal-traffic model
+(moeperf/perfmodel.py:216-249) over the measured HBM copy peak.  `cpu_baseline` times the oracle port of the
 reference forward on the host cores.
 
 Reference arm (--impl reference): the oracle port of the reference's CPU
@@ -200,6 +200,8 @@ def ours_arm(args, cfg_name):
     E, k, d, f, gating, B0, label = CONFIGS[cfg_name]
     B = args.tokens or B0
     cfg = P.ModelConfig(E, k, d, f, P.Gating(gating))
+    if world > 1 and cfg_name == "deepseek":
+        return ep_arm(args, cfg, label, B, world, rank, dev)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     x = torch.randn((B, d), generator=gen, device=dev).to(torch.bfloat16)
     wr = (torch.randn((d, E), generator=gen, device=dev) / d ** 0.5).float()
@@ -270,8 +272,9 @@ def ours_arm(args, cfg_name):
         e_end.synchronize()
         e2e_ms += e_start.elapsed_time(e_end)
 
-    # dominant kernel (fused gate+up) timed live, per-stage split
-    stages = layer.timed_stages(x, iters=max(5, min(args.steps, 20)), flush=flush)
+    # dominant kernel (the fused expert-FFN launch) timed live inside the real
+    # forward: CUDA events recorded by the library between its launches
+    stages = layer.timed_forward(x, iters=max(5, min(args.steps, 20)), flush=flush)
     counts = layer.counts.cpu().numpy().astype(np.int64)
 
     t = torch.tensor([total_ms, e2e_ms / e2e_steps], dtype=torch.float64, device=dev)
@@ -283,14 +286,15 @@ def ours_arm(args, cfg_name):
     e2e_value = world * B / (e2e_ms_max / 1e3)
 
     hbm, tflops, peak_src = _peaks()
-    gu_bytes = stage_bytes(STAGE_GATE_UP, cfg, B, counts, element_bytes=2)
-    gu_s = stages["gate_up"] / 1e3
-    achieved = gu_bytes / gu_s / 1e9
+    from paper_2605_23911_b200.trace import STAGE_DOWN
+    ffn_bytes = (stage_bytes(STAGE_GATE_UP, cfg, B, counts, element_bytes=2)
+                 + stage_bytes(STAGE_DOWN, cfg, B, counts, element_bytes=2))
+    achieved = ffn_bytes / (stages["ffn"] / 1e3) / 1e9
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(f"{cfg_name}_{B}_gate_up")
+            traffic = json.load(open(tfile)).get(f"{cfg_name}_{B}_ffn")
         except Exception:
             traffic = None
 
@@ -310,9 +314,10 @@ def ours_arm(args, cfg_name):
                     "path": "ctypes moe_b200_forward with pinned-host tokens copied in and output copied out"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "kernel": "grouped_gemm_kernel<256,gate_up>" if B * k > 96 * E else "grouped_gemm_kernel<128,gate_up>",
-                         "bytes_per_launch": gu_bytes, "launch_ms": stages["gate_up"],
-                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"},
+                         "kernel": "ffn_kernel (fused gate+up SiLU*up and K-split down, one persistent launch)",
+                         "bytes_per_launch": ffn_bytes, "launch_ms": stages["ffn"],
+                         "bytes_model": "perfmodel.stage_bytes(GateUp)+stage_bytes(Down), element_bytes=2, actual histogram",
+                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src}, burst copy)"},
             "stages_ms": stages,
             "layer_roofline_frac": None,
             "gpu_launches": 5 * args.steps,
@@ -329,6 +334,63 @@ def ours_arm(args, cfg_name):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def ep_arm(args, cfg, label, B, world, rank, dev):
+    """DeepSeek-V3 expert parallelism: experts sharded over the ranks, the global
+    batch B sharded B/n tokens per rank, NCCL all-to-all dispatch and combine.
+    Strong scaling (fixed global batch); value = B / max-over-ranks step time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_23911_b200 as P
+    from paper_2605_23911_b200.ep import ExpertParallelMoE, expert_ranges
+
+    E, k, d, f = cfg.num_experts, cfg.top_k, cfg.hidden_dim, cfg.ffn_dim
+    lo, hi = expert_ranges(E, world)[rank]
+    El = hi - lo
+    gen = torch.Generator(device=dev).manual_seed(1234)  # same router on every rank
+    wr = (torch.randn((d, E), generator=gen, device=dev) / d ** 0.5).float()
+    gen_r = torch.Generator(device=dev).manual_seed(99 + rank)
+    b0, b1 = rank * B // world, (rank + 1) * B // world
+    x = torch.randn((b1 - b0, d), generator=gen_r, device=dev).to(torch.bfloat16)
+    gate = (torch.randn((El * d, f), generator=gen_r, device=dev) / d ** 0.5).to(torch.bfloat16)
+    up = (torch.randn((El * d, f), generator=gen_r, device=dev) / d ** 0.5).to(torch.bfloat16)
+    down = (torch.randn((El * f, d), generator=gen_r, device=dev) / f ** 0.5).to(torch.bfloat16)
+    layer = ExpertParallelMoE(cfg, wr, P.ExpertWeights(gate, up, down), max_tokens=b1 - b0, device=dev)
+    for _ in range(max(3, args.warmup)):
+        layer.forward(x)
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(_env_int("LOCAL_RANK", 0))
+    sampler.start()
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        layer.forward(x)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    clocks = sampler.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t[0]) / args.steps
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": B / (ms_per_step / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (torch CUDA Philox N(0,1) bf16 tokens; random-init bf16 expert weights; router N(0,1)/sqrt(d))",
+            "config": {"workload": f"{label}, {B} tokens global", "tokens": B, "model_shape": [E, k, d, f],
+                       "gating": cfg.gating.value, "parallelism": f"expert-parallel ep{world} (NCCL all-to-all)",
+                       "timing": "CUDA events over the step loop (one host sync per step for all-to-all sizes)"},
+            "gpu_launches": None, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
     return 0
 
 

@@ -137,6 +137,42 @@ int moe_b200_forward(const moe_b200_config* cfg, int64_t num_tokens, const void*
                      int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
                      void* ws, size_t ws_bytes, void* stream);
 
+/* Same as moe_b200_forward, recording five cudaEvent_t (events[0..4]) on
+ * `stream` around the stages: [route | permute | fused FFN | combine].  Used
+ * by the benchmark to time the dominant kernel inside the real forward. */
+int moe_b200_forward_timed(const moe_b200_config* cfg, int64_t num_tokens, const void* x, int x_dtype,
+                           const float* w_router, const void* w_gate, const void* w_up,
+                           const void* w_down, void* y, int y_dtype, int32_t* topk_idx, float* topk_w,
+                           int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
+                           void* ws, size_t ws_bytes, void* stream, void** events);
+
+/* ---------------------------- expert parallelism ------------------------------
+ * The reference has no multi-GPU path ("planned
+ * follow-up").  These two entry points are the local compute of an
+ * expert-parallel layer whose dispatch/combine all-to-alls run over NCCL
+ * (paper_2605_23911_b200/ep.py).  cfg describes the LOCAL expert slice.
+ *
+ * moe_b200_expert_ffn: rows already grouped by local expert (counts[e] rows for
+ * expert e, ascending e) -> unweighted expert outputs, fp32, same row order:
+ *   out_rows[r] = silu(x_r Wg_e) * (x_r Wu_e) @ Wd_e   (pipeline.py:250-313, 186-247)
+ * Bit-identical, row by row, to the single-GPU forward's per-slot expert output.
+ *   counts   (E_local) int32 device; xp (n_rows, d) bf16; out_rows (n_rows, d) fp32
+ * Workspace: moe_b200_workspace_size(cfg with top_k = 1, n_rows). */
+int moe_b200_expert_ffn(const moe_b200_config* cfg, int64_t n_rows, const int32_t* counts,
+                        const void* xp, const void* w_gate, const void* w_up, const void* w_down,
+                        float* out_rows, void* ws, size_t ws_bytes, void* stream);
+
+/* Row gather dst[r] = src[idx[r]] (row_bytes a multiple of 16): the reorder
+ * between the all-to-all layout (source-major) and expert-major rows. */
+int moe_b200_gather_rows(int64_t n_rows, int64_t row_bytes, const void* src, const int32_t* idx,
+                         void* dst, void* stream);
+
+/* Home-rank combine (pipeline.py:373-399): rows (B*k, d) fp32 in the local
+ * permuted order; y[t] = sum_j fl(w[t,j] * rows[perm_inv[t*k+j]]), ascending j. */
+int moe_b200_combine_rows(const moe_b200_config* cfg, int64_t num_tokens, const float* rows,
+                          const int32_t* perm_inv, const float* topk_w, void* y, int y_dtype,
+                          void* stream);
+
 /* Copy the device status flags (MOE_B200_FLAG_*) to the host and clear them.
  * Synchronises `stream`. */
 int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws,

@@ -61,6 +61,11 @@ SIGNATURES = {
     "moe_b200_down_scatter": (_INT, [_CFG, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "moe_b200_combine": (_INT, [_CFG, _I64, _P, _P, _INT, _P]),
     "moe_b200_forward": (_INT, [_CFG, _I64, _P, _INT, _P, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_forward_timed": (_INT, [_CFG, _I64, _P, _INT, _P, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _P, _P, _P, _SZ, _P,
+                                      ctypes.POINTER(ctypes.c_void_p)]),
+    "moe_b200_expert_ffn": (_INT, [_CFG, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_gather_rows": (_INT, [_I64, _I64, _P, _P, _P, _P]),
+    "moe_b200_combine_rows": (_INT, [_CFG, _I64, _P, _P, _P, _P, _INT, _P]),
     "moe_b200_read_flags": (_INT, [_CFG, _I64, _P, _SZ, ctypes.POINTER(ctypes.c_uint32), _P]),
     "moe_b200_strerror": (ctypes.c_char_p, [_INT]),
     "moe_b200_last_error_detail": (ctypes.c_char_p, []),

@@ -170,4 +170,121 @@ combine_tiled_kernel(const float* __restrict__ ys, int splits, int n_dp, int T_p
   }
 }
 
+// Expert-parallel helpers --------------------------------------------------
+
+// dst[r, :] = src[idx[r], :] for rows of `row_bytes` (multiple of 16) bytes.
+__global__ void __launch_bounds__(kRowThreads)
+gather_rows_kernel(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx,
+                   uint8_t* __restrict__ dst, int n_rows, int row_bytes) {
+  const int vec_per_row = row_bytes / 16;
+  const long total = (long)n_rows * vec_per_row;
+  for (long i = (long)blockIdx.x * kRowThreads + threadIdx.x; i < total;
+       i += (long)gridDim.x * kRowThreads) {
+    const int r = static_cast<int>(i / vec_per_row);
+    const int v = static_cast<int>(i % vec_per_row);
+    const int4 val = __ldg(reinterpret_cast<const int4*>(src + (size_t)__ldg(idx + r) * row_bytes) + v);
+    reinterpret_cast<int4*>(dst + (size_t)r * row_bytes)[v] = val;
+  }
+}
+
+// Schedule for rows that arrive already grouped by (local) expert: counts ->
+// offsets, 16-aligned padded offsets, FFN chunk table and the padded row map.
+// One CTA (E_local <= 1024).  Mirrors the scheduler half of the router kernel.
+__global__ void __launch_bounds__(256)
+schedule_from_counts_kernel(const int32_t* __restrict__ counts, int E, int chunk_rows,
+                            int32_t* __restrict__ offsets, int4* __restrict__ chunk_tab,
+                            int32_t* __restrict__ n_chunks, int32_t* __restrict__ prow) {
+  __shared__ int32_t s_off[1025], s_off16[1025], s_cpre[1025];
+  if (threadIdx.x == 0) {
+    int a = 0, b = 0, c = 0;
+    for (int e = 0; e < E; ++e) {
+      s_off[e] = a; s_off16[e] = b; s_cpre[e] = c;
+      const int n = counts[e];
+      a += n; b += (n + 15) & ~15; c += (n + chunk_rows - 1) / chunk_rows;
+    }
+    s_off[E] = a; s_off16[E] = b; s_cpre[E] = c;
+    *n_chunks = c;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) offsets[e] = s_off[e];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int n = counts[e];
+    for (int c = 0; c * chunk_rows < n; ++c) {
+      const int r0 = c * chunk_rows;
+      chunk_tab[s_cpre[e] + c] = make_int4(e, s_off[e] + r0, min(chunk_rows, n - r0), s_off16[e] + r0);
+    }
+  }
+  // padded row of every (expert-major) row
+  const int T = s_off[E];
+  for (int r = threadIdx.x; r < T; r += blockDim.x) {
+    int lo = 0, hi = E - 1;  // expert of row r: last e with off[e] <= r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_off[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    prow[r] = s_off16[lo] + (r - s_off[lo]);
+  }
+}
+
+// Unweighted per-row expert output: out[r] = sum_s P_s[prow[r]] (fp32, ascending s)
+__global__ void __launch_bounds__(kRowThreads)
+row_reduce_kernel(const float* __restrict__ ys, int splits, int n_dp, int T_pad,
+                  const int32_t* __restrict__ prow, float* __restrict__ out, int T, int d) {
+  const int vec_per_row = d / 4;
+  const long total = (long)T * vec_per_row;
+  const size_t half_stride = (size_t)T_pad * 128;
+  for (long i = (long)blockIdx.x * kRowThreads + threadIdx.x; i < total;
+       i += (long)gridDim.x * kRowThreads) {
+    const int r = static_cast<int>(i / vec_per_row);
+    const int v = static_cast<int>(i % vec_per_row);
+    const int feat = v * 4;
+    const size_t blk = (size_t)(feat >> 8) * 2 + ((feat >> 7) & 1);
+    const size_t row = (size_t)__ldg(prow + r);
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < splits; ++s) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(ys + ((size_t)s * n_dp * 2 + blk) * half_stride + row * 128 + (feat & 127)));
+      if (s == 0) { g = a; } else {
+        g.x = __fadd_rn(g.x, a.x); g.y = __fadd_rn(g.y, a.y);
+        g.z = __fadd_rn(g.z, a.z); g.w = __fadd_rn(g.w, a.w);
+      }
+    }
+    reinterpret_cast<float4*>(out + (size_t)r * d)[v] = g;
+  }
+}
+
+// Home-rank combine of expert-parallel results: rows come back in the local
+// expert-major order; y[t] = sum_j fl(w[t,j] * rows[inv[t*k+j]]), ascending j.
+template <bool kBf16Out>
+__global__ void __launch_bounds__(kRowThreads)
+combine_rows_kernel(const float* __restrict__ rows, const int32_t* __restrict__ inv,
+                    const float* __restrict__ topk_w, void* __restrict__ y, int B, int k, int d) {
+  const int vec_per_row = d / 4;
+  const long total = (long)B * vec_per_row;
+  for (long i = (long)blockIdx.x * kRowThreads + threadIdx.x; i < total;
+       i += (long)gridDim.x * kRowThreads) {
+    const int t = static_cast<int>(i / vec_per_row);
+    const int v = static_cast<int>(i % vec_per_row);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < k; ++j) {
+      const int x = t * k + j;
+      const float w = __ldg(topk_w + x);
+      const float4 g = __ldg(reinterpret_cast<const float4*>(rows + (size_t)__ldg(inv + x) * d) + v);
+      acc.x = __fadd_rn(acc.x, __fmul_rn(w, g.x));
+      acc.y = __fadd_rn(acc.y, __fmul_rn(w, g.y));
+      acc.z = __fadd_rn(acc.z, __fmul_rn(w, g.z));
+      acc.w = __fadd_rn(acc.w, __fmul_rn(w, g.w));
+    }
+    if (kBf16Out) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y);
+      __nv_bfloat162 p1 = __floats2bfloat162_rn(acc.z, acc.w);
+      uint2 o;
+      o.x = *reinterpret_cast<uint32_t*>(&p0);
+      o.y = *reinterpret_cast<uint32_t*>(&p1);
+      reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(y) + (size_t)t * d)[v] = o;
+    } else {
+      reinterpret_cast<float4*>(static_cast<float*>(y) + (size_t)t * d)[v] = acc;
+    }
+  }
+}
+
 }  // namespace moe

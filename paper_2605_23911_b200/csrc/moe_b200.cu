@@ -524,28 +524,36 @@ int moe_b200_combine(const moe_b200_config* cfg, int64_t B, const float* ys, voi
   return MOE_B200_OK;
 }
 
-int moe_b200_forward(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
+static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
                      const float* w_router, const void* w_gate, const void* w_up,
                      const void* w_down, void* y, int y_dtype, int32_t* topk_idx, float* topk_w,
                      int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
-                     void* ws, size_t ws_bytes, void* stream) {
+                     void* ws, size_t ws_bytes, void* stream, void** events) {
   int rc = check_config(cfg);
   if (rc) return rc;
   Layout L;
   if ((rc = check_ws(cfg, B, ws, ws_bytes, &L))) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto mark = [&](int i) -> int {
+    if (events) MOE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s));
+    return MOE_B200_OK;
+  };
+  if ((rc = mark(0))) return rc;
   if ((rc = moe_b200_route(cfg, B, x, x_dtype, w_router, topk_idx, topk_w, counts, offsets, perm_fwd,
                            perm_inv, nullptr, ws, ws_bytes, stream)))
     return rc;
+  if ((rc = mark(1))) return rc;
   if (B == 0) return MOE_B200_OK;
   void* xp = ws8(ws) + L.xp;
   void* h = ws8(ws) + L.h;
   float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);
   if ((rc = moe_b200_permute(cfg, B, x, x_dtype, perm_fwd, xp, stream))) return rc;
+  if ((rc = mark(2))) return rc;
   if (L.max_chunks > kChunkCap) return MOE_B200_ERR_UNSUPPORTED;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
                        /*gu*/ true, /*dn*/ true, /*fused*/ true, s)))
     return rc;
+  if ((rc = mark(3))) return rc;
   const int d = cfg->hidden_dim;
   const int grid = grid_for_rows((long)B * (d / 4));
   const int32_t* prow = reinterpret_cast<const int32_t*>(ws8(ws) + L.prow);
@@ -556,6 +564,92 @@ int moe_b200_forward(const moe_b200_config* cfg, int64_t B, const void* x, int x
   else
     return MOE_B200_ERR_INVALID_VALUE;
   MOE_LAUNCH_CHECK("combine_tiled_kernel");
+  return mark(4);
+}
+
+int moe_b200_forward(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
+                     const float* w_router, const void* w_gate, const void* w_up,
+                     const void* w_down, void* y, int y_dtype, int32_t* topk_idx, float* topk_w,
+                     int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
+                     void* ws, size_t ws_bytes, void* stream) {
+  return forward_impl(cfg, B, x, x_dtype, w_router, w_gate, w_up, w_down, y, y_dtype, topk_idx, topk_w, counts,
+                      offsets, perm_fwd, perm_inv, ws, ws_bytes, stream, nullptr);
+}
+
+int moe_b200_forward_timed(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
+                           const float* w_router, const void* w_gate, const void* w_up,
+                           const void* w_down, void* y, int y_dtype, int32_t* topk_idx, float* topk_w,
+                           int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
+                           void* ws, size_t ws_bytes, void* stream, void** events) {
+  return forward_impl(cfg, B, x, x_dtype, w_router, w_gate, w_up, w_down, y, y_dtype, topk_idx, topk_w, counts,
+                      offsets, perm_fwd, perm_inv, ws, ws_bytes, stream, events);
+}
+
+// --------------------------- expert parallelism --------------------------------
+
+int moe_b200_expert_ffn(const moe_b200_config* cfg, int64_t n_rows, const int32_t* counts,
+                        const void* xp, const void* w_gate, const void* w_up, const void* w_down,
+                        float* out_rows, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (n_rows < 0) return MOE_B200_ERR_SHAPE_MISMATCH;
+  if (n_rows == 0) return MOE_B200_OK;
+  if (!counts || !xp || !w_gate || !w_up || !w_down || !out_rows) return MOE_B200_ERR_INVALID_VALUE;
+  // the FFN works on T = n_rows rows: lay the workspace out as B = n_rows tokens with k = 1
+  moe_b200_config c1 = *cfg;
+  c1.top_k = 1;
+  Layout L;
+  if ((rc = check_ws(&c1, n_rows, ws, ws_bytes, &L))) return rc;
+  if (L.max_chunks > kChunkCap || c1.num_experts > 1024) return MOE_B200_ERR_UNSUPPORTED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* hdr = reinterpret_cast<int32_t*>(ws);
+  int32_t* offsets = reinterpret_cast<int32_t*>(ws8(ws) + L.logits);  // scratch: E+1 ints
+  int32_t* prow = reinterpret_cast<int32_t*>(ws8(ws) + L.prow);
+  schedule_from_counts_kernel<<<1, 256, 0, s>>>(counts, c1.num_experts, chunk_rows_for(c1, n_rows), offsets,
+                                                reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab), hdr + 2, prow);
+  MOE_LAUNCH_CHECK("schedule_from_counts_kernel");
+  void* h = ws8(ws) + L.h;
+  float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);
+  if ((rc = launch_ffn(c1, n_rows, L, ws, xp, w_gate, w_up, w_down, h, ys, nullptr, nullptr,
+                       /*gu*/ true, /*dn*/ true, /*fused*/ true, s)))
+    return rc;
+  const int d = c1.hidden_dim;
+  row_reduce_kernel<<<grid_for_rows((long)n_rows * (d / 4)), kRowThreads, 0, s>>>(
+      ys, L.splits, L.n_dp, L.T_pad, prow, out_rows, static_cast<int>(n_rows), d);
+  MOE_LAUNCH_CHECK("row_reduce_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_gather_rows(int64_t n_rows, int64_t row_bytes, const void* src, const int32_t* idx,
+                         void* dst, void* stream) {
+  if (n_rows < 0 || row_bytes <= 0 || row_bytes % 16) return MOE_B200_ERR_INVALID_VALUE;
+  if (n_rows == 0) return MOE_B200_OK;
+  if (!src || !idx || !dst) return MOE_B200_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  gather_rows_kernel<<<grid_for_rows((long)n_rows * (row_bytes / 16)), kRowThreads, 0, s>>>(
+      static_cast<const uint8_t*>(src), idx, static_cast<uint8_t*>(dst), static_cast<int>(n_rows),
+      static_cast<int>(row_bytes));
+  MOE_LAUNCH_CHECK("gather_rows_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_combine_rows(const moe_b200_config* cfg, int64_t B, const float* rows,
+                          const int32_t* perm_inv, const float* topk_w, void* y, int y_dtype,
+                          void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (B == 0) return MOE_B200_OK;
+  if (!rows || !perm_inv || !topk_w || !y) return MOE_B200_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int d = cfg->hidden_dim;
+  const int grid = grid_for_rows((long)B * (d / 4));
+  if (y_dtype == MOE_B200_DTYPE_F32)
+    combine_rows_kernel<false><<<grid, kRowThreads, 0, s>>>(rows, perm_inv, topk_w, y, (int)B, cfg->top_k, d);
+  else if (y_dtype == MOE_B200_DTYPE_BF16)
+    combine_rows_kernel<true><<<grid, kRowThreads, 0, s>>>(rows, perm_inv, topk_w, y, (int)B, cfg->top_k, d);
+  else
+    return MOE_B200_ERR_INVALID_VALUE;
+  MOE_LAUNCH_CHECK("combine_rows_kernel");
   return MOE_B200_OK;
 }
 

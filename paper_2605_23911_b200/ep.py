@@ -1,0 +1,199 @@
+"""Expert-parallel MoE layer (DeepSeek-V3 across the GPUs of one box).
+
+The reference has no multi-GPU path (``SPEC.md:8``; ``PAPER.md:430`` item 6).
+SURVEY.md §8e specifies the partition used here:
+
+* expert ``e`` lives on rank ``owner(e)`` — contiguous blocks of ``E/n``
+  experts (uneven blocks allowed);
+* tokens are sharded ``B/n`` per rank; the router weight is replicated, and
+  each rank routes its own tokens (rows are independent, so local routing is
+  bit-identical to global routing);
+* steps: local route → per-expert counts all-to-all → dispatch all-to-all
+  (bf16 rows, already expert-major per destination because the local
+  permutation is the reference's stable expert-major order) → reorder to
+  expert-major across sources → local expert FFN → reorder back → combine
+  all-to-all (fp32 rows) → home-rank combine in ascending slot order.
+
+The output is bitwise identical to the single-GPU layer: every row's expert
+output is computed by the same kernels with the same K order regardless of
+which other rows share its tile, and the home-rank combine runs the
+reference's ``out += w_j * g_j`` order (``pipeline.py:396-399``).
+
+Collectives go through ``torch.distributed`` (NCCL on GPUs).  The one host
+synchronisation per forward is the counts exchange that sizes the
+all-to-alls.  All row compute runs in libmoe_b200.so through ``CudaOps``; the
+host logic is written against a small ops interface so it can be exercised
+on CPU with gloo in the tests.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .types import GATING_CODE, ExpertWeights, Gating, ModelConfig
+
+
+def expert_ranges(num_experts: int, world: int):
+    """Contiguous expert blocks: rank r owns [lo_r, hi_r)  (owner(e) = floor(e*n/E))."""
+    bounds = [(r * num_experts + world - 1) // world for r in range(world + 1)]
+    # owner(e) = floor(e * n / E)  <=>  e in [ceil(r*E/n), ceil((r+1)*E/n))
+    return [(bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+def source_major_to_expert_major(recv_counts: np.ndarray) -> np.ndarray:
+    """Row order fix-up for the dispatch all-to-all.
+
+    ``recv_counts[src, e]`` rows arrive source-major (src ascending, expert
+    ascending within a source).  Returns ``idx`` with ``expert_major[r] =
+    source_major[idx[r]]`` (expert ascending, source ascending within an
+    expert — i.e. the global stable order restricted to this rank's experts).
+    """
+    n_src, n_e = recv_counts.shape
+    starts = np.zeros((n_src, n_e), dtype=np.int64)
+    flat = recv_counts.reshape(-1)
+    starts.reshape(-1)[1:] = np.cumsum(flat)[:-1]
+    out = []
+    for e in range(n_e):
+        for s in range(n_src):
+            c = int(recv_counts[s, e])
+            if c:
+                out.append(np.arange(starts[s, e], starts[s, e] + c, dtype=np.int64))
+    return np.concatenate(out) if out else np.zeros(0, dtype=np.int64)
+
+
+class CudaOps:
+    """Row compute on the GPU through the C-ABI (libmoe_b200.so)."""
+
+    def __init__(self, config: ModelConfig, local_cfg: ModelConfig, router_weight, local_weights: ExpertWeights,
+                 max_tokens: int, device):
+        from .layer import MoELayer, _ptr, _stream_ptr, upload_weights  # noqa: F401
+
+        self.device = device
+        self.lib = _lib.load()
+        # router: a full-E layer with placeholder expert stacks (routing only)
+        E, d = config.num_experts, config.hidden_dim
+        z = np.zeros((E * d, 8), np.float32)
+        self.router = MoELayer(ModelConfig(E, config.top_k, d, 8, config.gating),
+                               ExpertWeights(z, z, np.zeros((E * 8, d), np.float32)), router_weight,
+                               max_tokens=max_tokens, device=device)
+        self.w = upload_weights(local_weights, local_cfg, device)
+        self.local_cfg = local_cfg
+        self.cfg1 = _lib.config_struct(local_cfg.num_experts, 1, self.w.hidden_pad, self.w.ffn_pad,
+                                       GATING_CODE[Gating(local_cfg.gating)])
+        self.cfgk = _lib.config_struct(E, config.top_k, self.w.hidden_pad, self.w.ffn_pad, GATING_CODE[Gating(config.gating)])
+        self._ws = None
+        self._ws_bytes = 0
+        self._ptr, self._stream = _ptr, _stream_ptr
+
+    def route(self, x):
+        r = self.router.route(x)
+        return (r["indices"], r["weights"], r["counts"].clone(), r["forward"].clone(), r["inverse"].clone())
+
+    def permute(self, x, fwd, k):
+        xb = x.to(torch.bfloat16).contiguous()
+        idx = (fwd // k).to(torch.int32).contiguous()
+        return self.gather_rows(xb, idx)
+
+    def gather_rows(self, src, idx):
+        n = idx.numel()
+        dst = torch.empty((n,) + tuple(src.shape[1:]), dtype=src.dtype, device=self.device)
+        row_bytes = src[0].numel() * src.element_size() if src.shape[0] else 16
+        _lib.check(self.lib.moe_b200_gather_rows(n, row_bytes, self._ptr(src), self._ptr(idx), self._ptr(dst),
+                                                 self._stream(self.device)), "gather_rows")
+        return dst
+
+    def expert_ffn(self, counts, xp):
+        n = xp.shape[0]
+        out = torch.empty((n, self.w.hidden_pad), dtype=torch.float32, device=self.device)
+        if n == 0:
+            return out
+        need = ctypes.c_size_t(0)
+        _lib.check(self.lib.moe_b200_workspace_size(ctypes.byref(self.cfg1), n, ctypes.byref(need)), "ws")
+        if need.value > self._ws_bytes:
+            self._ws_bytes = int(need.value * 1.25)
+            self._ws = torch.empty(self._ws_bytes, dtype=torch.uint8, device=self.device)
+            _lib.check(self.lib.moe_b200_workspace_init(ctypes.byref(self.cfg1), n, self._ptr(self._ws),
+                                                        self._ws_bytes, self._stream(self.device)), "ws_init")
+        c = counts.to(torch.int32).contiguous()
+        _lib.check(self.lib.moe_b200_expert_ffn(ctypes.byref(self.cfg1), n, self._ptr(c), self._ptr(xp),
+                                                self._ptr(self.w.gate), self._ptr(self.w.up), self._ptr(self.w.down),
+                                                self._ptr(out), self._ptr(self._ws), self._ws_bytes,
+                                                self._stream(self.device)), "expert_ffn")
+        return out
+
+    def combine(self, rows, inv, w, B):
+        y = torch.empty((B, rows.shape[1]), dtype=torch.float32, device=self.device)
+        _lib.check(self.lib.moe_b200_combine_rows(ctypes.byref(self.cfgk), B, self._ptr(rows), self._ptr(inv),
+                                                  self._ptr(w), self._ptr(y), _lib.DTYPE_F32,
+                                                  self._stream(self.device)), "combine_rows")
+        return y
+
+
+class ExpertParallelMoE:
+    """One MoE layer with experts sharded over the ranks of ``group``."""
+
+    def __init__(self, config: ModelConfig, router_weight, weights_local: ExpertWeights, max_tokens: int,
+                 group=None, device=None, ops=None):
+        self.config = config
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.ranges = expert_ranges(config.num_experts, self.world)
+        lo, hi = self.ranges[self.rank]
+        self.local_cfg = ModelConfig(hi - lo, 1, config.hidden_dim, config.ffn_dim, config.gating)
+        self.device = torch.device(device or "cuda")
+        self.ops = ops or CudaOps(config, self.local_cfg, router_weight, weights_local, max_tokens, self.device)
+
+    def _a2a(self, out, inp, out_splits, in_splits):
+        if self.world == 1:
+            out.copy_(inp)
+            return
+        dist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits, group=self.group)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        cfg = self.config
+        k, E, d = cfg.top_k, cfg.num_experts, cfg.hidden_dim
+        B = x.shape[0]
+        idx, w, counts, fwd, inv = self.ops.route(x)
+        xp = self.ops.permute(x, fwd, k)  # local expert-major rows (bf16)
+        # counts exchange (the one host sync): per (src, local expert)
+        counts_h = counts.to("cpu", torch.int64).numpy() if counts.is_cuda else counts.numpy().astype(np.int64)
+        send_counts = np.concatenate([counts_h[lo:hi] for lo, hi in self.ranges])
+        recv_counts = torch.zeros(self.world * self.local_cfg.num_experts, dtype=torch.int64)
+        send_t = torch.from_numpy(send_counts)
+        if self.world > 1:
+            split = [hi - lo for lo, hi in self.ranges]
+            recv_split = [self.local_cfg.num_experts] * self.world
+            dev = self.device if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+            rc = torch.zeros(self.world * self.local_cfg.num_experts, dtype=torch.int64, device=dev)
+            dist.all_to_all_single(rc, send_t.to(dev), output_split_sizes=recv_split, input_split_sizes=split,
+                                   group=self.group)
+            recv_counts = rc.cpu()
+        else:
+            recv_counts = send_t.clone()
+        recv_counts = recv_counts.numpy().reshape(self.world, self.local_cfg.num_experts)
+        send_rows = [int(counts_h[lo:hi].sum()) for lo, hi in self.ranges]
+        recv_rows = [int(r) for r in recv_counts.sum(axis=1)]
+        # dispatch
+        recv = torch.empty((sum(recv_rows), xp.shape[1]), dtype=xp.dtype, device=xp.device)
+        self._a2a(recv, xp, recv_rows, send_rows)
+        # source-major -> expert-major, local FFN, and back
+        order = source_major_to_expert_major(recv_counts)
+        order_t = torch.from_numpy(order.astype(np.int32)).to(xp.device)
+        inv_order = np.empty_like(order)
+        inv_order[order] = np.arange(order.size)
+        inv_order_t = torch.from_numpy(inv_order.astype(np.int32)).to(xp.device)
+        xe = self.ops.gather_rows(recv, order_t)
+        local_counts = torch.from_numpy(recv_counts.sum(axis=0).astype(np.int32)).to(xp.device)
+        ye = self.ops.expert_ffn(local_counts, xe)
+        ys = self.ops.gather_rows(ye, inv_order_t)
+        # combine: rows go home in the order they were sent
+        back = torch.empty((sum(send_rows), ys.shape[1]), dtype=ys.dtype, device=ys.device)
+        self._a2a(back, ys, send_rows, recv_rows)
+        y = self.ops.combine(back, inv, w, B)
+        return y[:, :d]

@@ -226,6 +226,33 @@ class MoELayer:
         return r
 
 
+    def timed_forward(self, x: torch.Tensor, iters: int = 10, flush: torch.Tensor | None = None) -> dict:
+        """Per-stage device time (ms, mean over ``iters``) of the REAL one-call forward:
+        CUDA events recorded by the library between [route | permute | fused FFN | combine]."""
+        x, xdt = self._prep_x(x)
+        B = x.shape[0]
+        out = torch.empty((B, self.dp), dtype=self.out_dtype, device=self.device)
+        ydt = _lib.DTYPE_BF16 if out.dtype == torch.bfloat16 else _lib.DTYPE_F32
+        names = ("route", "permute", "ffn", "combine")
+        tot = dict.fromkeys(names, 0.0)
+        for _ in range(iters):
+            if flush is not None:
+                flush.zero_()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            for e in ev:
+                e.record()  # materialise the underlying cudaEvent_t (re-recorded by the library)
+            arr = (ctypes.c_void_p * 5)(*[e.cuda_event for e in ev])
+            rc = self.lib.moe_b200_forward_timed(
+                ctypes.byref(self.cfg), B, _ptr(x), xdt, _ptr(self.router_weight),
+                _ptr(self.weights.gate), _ptr(self.weights.up), _ptr(self.weights.down),
+                _ptr(out), ydt, _ptr(self.topk_idx), _ptr(self.topk_w), _ptr(self.counts), _ptr(self.offsets),
+                _ptr(self.fwd), _ptr(self.inv), _ptr(self.ws), self.ws_bytes, _stream_ptr(self.device), arr)
+            _lib.check(rc, "moe_b200_forward_timed")
+            torch.cuda.synchronize(self.device)
+            for i, n in enumerate(names):
+                tot[n] += ev[i].elapsed_time(ev[i + 1])
+        return {n: v / iters for n, v in tot.items()}
+
     def timed_stages(self, x: torch.Tensor, iters: int = 10, flush: torch.Tensor | None = None) -> dict:
         """Per-stage device time (ms, mean over ``iters``) with CUDA events between
         the five C-ABI stage calls on the current stream (optional L2 flush

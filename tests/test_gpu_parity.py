@@ -267,3 +267,21 @@ def test_sigmoid_port_matches_numpy_on_device(pkg):
     idx_ref, w_ref = O.route(x, wr, k, "sigmoid_normalized")
     bits_equal(_np(r["indices"]).astype(np.int64), idx_ref)
     bits_equal(_np(r["weights"]), w_ref)
+
+
+def test_expert_parallel_single_rank_matches_layer_bitwise(pkg):
+    """EP code path (dispatch reorder, expert_ffn, gather, combine_rows) on one
+    rank reproduces the fused single-GPU forward bit-for-bit."""
+    P = pkg
+    from paper_2605_23911_b200.ep import ExpertParallelMoE
+
+    e, k, d, f, b = 16, 4, 256, 512, 64
+    tokens, wr, gate, up, down = O.make_instance(9, e, k, d, f, b)
+    cfg = _cfg(P, e, k, d, f, "sigmoid_normalized")
+    w = P.ExpertWeights(gate, up, down)
+    layer = P.MoELayer(cfg, w, wr, max_tokens=b)
+    x = torch.from_numpy(tokens).cuda()
+    y_ref = _np(layer.forward(x))
+    ep = ExpertParallelMoE(cfg, wr, w, max_tokens=b)
+    y = _np(ep.forward(x))
+    bits_equal(y, y_ref)
