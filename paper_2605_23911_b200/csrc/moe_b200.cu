@@ -66,13 +66,14 @@ int chunk_rows_for(const moe_b200_config& c, int64_t B) {
   return (T > 96LL * c.num_experts) ? 256 : 128;
 }
 
-// K splits of a down tile (a pair of 128-row hidden tiles) so that down
-// tiles stream about as many weight bytes as a gate+up tile (2 x 128 x d):
-// one HBM-stream granularity for the dynamic queue.  Partials are reduced
+// K splits of a down tile (a pair of 128-row hidden tiles): S = round(f/2d),
+// i.e. down tiles stream about twice the weight bytes of a gate+up tile
+// (measured best on Mixtral: S=2 beats 3 and 4 once the partial-sum traffic
+// of the combine is counted).  Partials are reduced
 // deterministically in combine.  MOE_B200_DOWN_SPLITS overrides (tuning).
 void down_splits(const moe_b200_config& c, int* splits, int* kb_per_split) {
   const int nkb = (c.ffn_dim + kBK - 1) / kBK;
-  int s = static_cast<int>((c.ffn_dim + c.hidden_dim / 2) / c.hidden_dim);  // round(f / d)
+  int s = static_cast<int>((c.ffn_dim + c.hidden_dim) / (2 * c.hidden_dim));  // round(f / 2d)
   if (const char* env = getenv("MOE_B200_DOWN_SPLITS")) s = atoi(env);
   s = std::max(1, std::min(s, 8));
   s = std::min(s, nkb);
