@@ -11,5 +11,5 @@ for t in 1 32 128; do timeout 600 python bench.py --config mixtral --tokens $t -
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python scripts/run_layer.py mixtral 512 3 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_kernel -s 1 -c 1 -o gpurun_out/prof_ffn_$TAG -f python scripts/run_layer.py mixtral 512 2 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:router_kernel -s 1 -c 1 -o gpurun_out/prof_router_$TAG -f python scripts/run_layer.py mixtral 512 2 > /dev/null 2>&1
-for c in mixtral qwen60 deepseek; do python scripts/ffn_timeline.py $c timeline_${c}_$TAG > /dev/null 2>&1; done
+for c in mixtral qwen60 deepseek; do python scripts/ffn_timeline.py $c ${c}_$TAG > /dev/null 2>&1; done
 echo done
