@@ -14,6 +14,8 @@
 #include "elementwise.cuh"
 #include "ffn.cuh"
 #include "router.cuh"
+#include "router_seg.cuh"
+#include "dispatch.cuh"
 
 using namespace moe;
 
@@ -44,18 +46,21 @@ constexpr size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 constexpr int kTbCap = 4096;      // max router token blocks per launch
 constexpr int kChunkCap = 8192;   // max expert row-chunks per launch
+constexpr int kBlkCap = 16384;    // max (token block x expert block) counters (segment router)
 
 // Fixed header at the start of the workspace (zeroed by workspace_init; every
 // kernel leaves its counters zeroed again):
 //   [0] flags  [1] router done counter  [2] n_chunks  [3] ffn work counter
 //   [4] ffn exit counter  [16, 16+kTbCap) router token-block counters
 //   [16+kTbCap, 16+kTbCap+kChunkCap) per-chunk gate+up completion counters
+//   [.., +kBlkCap) segment-router (token block, expert block) counters
 constexpr int kHdrTb = 16;
 constexpr int kHdrGuDone = 16 + kTbCap;
-constexpr size_t kHeaderBytes = align256((16 + kTbCap + kChunkCap) * sizeof(int32_t));
+constexpr int kHdrBlk = 16 + kTbCap + kChunkCap;
+constexpr size_t kHeaderBytes = align256((16 + kTbCap + kChunkCap + kBlkCap) * sizeof(int32_t));
 
 struct Layout {
-  size_t logits, w64, chunk_tab, prow, xp, h, ys, total;
+  size_t logits, lbuf, gpart, w64, chunk_tab, prow, xp, h, ys, total;
   int max_chunks, splits, kb_per_split, T_pad, n_ft, n_dp;
 };
 
@@ -82,6 +87,53 @@ void down_splits(const moe_b200_config& c, int* splits, int* kb_per_split) {
   *splits = (nkb + kps - 1) / kps;
 }
 
+// ---- segment (certified split-K) router plan --------------------------------
+int seg_expc(int E) {
+  if (E <= 4) return 4;
+  if (E <= 8) return 8;
+  if (E <= 16) return 16;
+  return 32;
+}
+
+// The segment router runs up to this many tokens (B*E chains <= kSegMaxChains,
+// tunable via MOE_B200_SEG_MAX_CHAINS); larger problems use the exact kernel.
+int64_t seg_max_tokens(const moe_b200_config& c) {
+  int64_t chains = 1LL << 20;
+  if (const char* env = getenv("MOE_B200_SEG_MAX_CHAINS")) chains = atoll(env);
+  return chains / std::max(1, c.num_experts);
+}
+
+struct SegPlan {
+  int expc, n_eb, n_tb, n_kb, seg_len, kr, grid;
+  size_t smem;
+};
+
+SegPlan plan_seg(const moe_b200_config& c, int64_t B) {
+  SegPlan q{};
+  q.expc = seg_expc(c.num_experts);
+  q.n_eb = (c.num_experts + q.expc - 1) / q.expc;
+  q.n_tb = static_cast<int>((B + kSegTT - 1) / kSegTT);
+  const int G = q.expc / kSegTE;
+  const int S = kSegThreads / G;
+  // segment length: 32 steps (chain latency ~0.2 us) unless the grid is too
+  // small to fill the GPU, then shorter segments split d over more CTAs
+  q.seg_len = 32;
+  if (const char* env = getenv("MOE_B200_SEG_LEN")) q.seg_len = std::max(8, atoi(env) / 8 * 8);
+  while (q.seg_len > 8) {
+    const int kr = S * q.seg_len;
+    const long grid = (long)q.n_tb * q.n_eb * ((c.hidden_dim + kr - 1) / kr);
+    if (grid >= kNumSMs / 2) break;
+    q.seg_len /= 2;
+  }
+  q.kr = S * q.seg_len;
+  q.n_kb = (c.hidden_dim + q.kr - 1) / q.kr;
+  q.grid = q.n_tb * q.n_eb * q.n_kb;
+  const size_t part = (size_t)(kSegThreads / 32) * kSegTT * q.expc * 16 + 64;  // warp partials
+  const size_t ph2 = (size_t)(kSegThreads / 32) * (c.num_experts * 16 + 256);
+  q.smem = std::max(part, ph2);
+  return q;
+}
+
 Layout layout_for(const moe_b200_config& c, int64_t B) {
   Layout L{};
   const int64_t T = B * c.top_k;
@@ -97,6 +149,16 @@ Layout layout_for(const moe_b200_config& c, int64_t B) {
   const size_t ys_tiled = (size_t)L.splits * L.n_dp * 2 * L.T_pad * kBM * sizeof(float);
   size_t off = kHeaderBytes;
   L.logits = off;    off = align256(off + (size_t)B * c.num_experts * sizeof(float));
+  L.lbuf = off;      off = align256(off + (size_t)B * c.num_experts * sizeof(float2));
+  {
+    // segment router partials: (B rounded to token blocks) x (E rounded to
+    // expert blocks) chains x at most ceil(d / 256) k-blocks (S >= 32, L >= 8)
+    const int64_t bseg = (std::min<int64_t>(B, seg_max_tokens(c)) + kSegTT - 1) / kSegTT * kSegTT;
+    const int expc = seg_expc(c.num_experts);
+    const int64_t epad = (c.num_experts + expc - 1) / expc * expc;
+    const int64_t nkb = (c.hidden_dim + 255) / 256;
+    L.gpart = off;   off = align256(off + (size_t)(bseg * epad * nkb) * 16);
+  }
   {
     const int expc = std::min(c.num_experts, 32);
     const size_t neb = (c.num_experts + expc - 1) / expc;
@@ -326,6 +388,66 @@ int grid_for_rows(long total_vec) {
 
 uint8_t* ws8(void* ws) { return static_cast<uint8_t*>(ws); }
 
+int launch_router_exact(const moe_b200_config& c, int64_t B, const void* x, int xb, const float* w_router,
+                        const Layout& L, void* ws, RouterParams& p, cudaStream_t s) {
+  const moe_b200_config* cfg = &c;
+  int32_t* hdr = reinterpret_cast<int32_t*>(ws);
+  RouterPlan plan = plan_router(c, B, xb);
+  if (plan.n_tblocks > kTbCap) return MOE_B200_ERR_UNSUPPORTED;
+  double* w64 = reinterpret_cast<double*>(ws8(ws) + L.w64);
+  {
+    // exact fp32 -> fp64 widening of W_r into the chunked expert-block layout
+    const long total = (long)plan.n_eblocks * plan.d_pad * plan.expc;
+    const int grid = static_cast<int>(std::min<long>((total + 255) / 256, (long)kNumSMs * 8));
+    router_prep_kernel<<<grid, 256, 0, s>>>(w_router, w64, cfg->hidden_dim, cfg->num_experts, plan.expc,
+                                           plan.d_pad, plan.n_eblocks, reinterpret_cast<uint32_t*>(hdr));
+    MOE_LAUNCH_CHECK("router_prep_kernel");
+  }
+  p.w64 = w64;
+  p.tokc = plan.tokc; p.expc = plan.expc;
+  p.n_eblocks = plan.n_eblocks; p.n_tblocks = plan.n_tblocks;
+  p.stages = plan.stages;
+  CUtensorMap tmx;
+  {
+    int rc2 = get_encoder();
+    if (rc2) return rc2;
+    cuuint64_t dims[2] = {(cuuint64_t)cfg->hidden_dim, (cuuint64_t)B};
+    cuuint64_t strides[1] = {(cuuint64_t)cfg->hidden_dim * (xb ? 2 : 4)};
+    cuuint32_t box[2] = {(cuuint32_t)plan.kc, (cuuint32_t)plan.tokc};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode(&tmx, xb ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                          const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      g_last_error = "cuTensorMapEncodeTiled(x) failed";
+      return MOE_B200_ERR_CUDA;
+    }
+  }
+  return xb ? launch_router_x<true>(tmx, p, plan, s) : launch_router_x<false>(tmx, p, plan, s);
+}
+
+
+int launch_dispatch(const moe_b200_config& c, int64_t B, const void* x, int xb, const int32_t* topk_idx,
+                    int32_t* counts, int32_t* offsets, int32_t* fwd, int32_t* inv, int32_t* prow, int4* chunk_tab,
+                    int32_t* n_chunks, void* xp, cudaStream_t s) {
+  DispatchParams q{};
+  q.topk_idx = topk_idx;
+  q.T = static_cast<int>(B * c.top_k); q.k = c.top_k; q.E = c.num_experts; q.d = c.hidden_dim;
+  q.chunk_rows = chunk_rows_for(c, B);
+  q.x = x; q.xp = static_cast<__nv_bfloat16*>(xp);
+  q.counts = counts; q.offsets = offsets; q.fwd = fwd; q.inv = inv; q.prow = prow;
+  q.chunk_tab = chunk_tab; q.n_chunks = n_chunks;
+  const int grid = (q.T + kDispRows - 1) / kDispRows;
+  const size_t smem = (size_t)(5 * c.num_experts + 3) * sizeof(int32_t);
+  auto kern = xb ? dispatch_kernel<true> : dispatch_kernel<false>;
+  if (smem > 48 * 1024) MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, kDispThreads, smem, s>>>(q);
+  MOE_LAUNCH_CHECK("dispatch_kernel");
+  return MOE_B200_OK;
+}
+
+
 }  // namespace
 
 // ================================ C ABI =======================================
@@ -387,10 +509,11 @@ int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws
   return MOE_B200_OK;
 }
 
-int moe_b200_route(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
-                   const float* w_router, int32_t* topk_idx, float* topk_w, int32_t* counts,
-                   int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv, float* logits,
-                   void* ws, size_t ws_bytes, void* stream) {
+// route + dispatch; xp != nullptr also gathers the permuted bf16 tokens
+static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
+                      const float* w_router, int32_t* topk_idx, float* topk_w, int32_t* counts,
+                      int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv, float* logits,
+                      void* ws, size_t ws_bytes, void* stream, void* xp, void* mid_event = nullptr) {
   int rc = check_config(cfg);
   if (rc) return rc;
   if (B < 0) return MOE_B200_ERR_SHAPE_MISMATCH;
@@ -408,55 +531,57 @@ int moe_b200_route(const moe_b200_config* cfg, int64_t B, const void* x, int x_d
   if (!x || !w_router || !topk_idx || !topk_w || !counts || !offsets || !perm_fwd || !perm_inv)
     return MOE_B200_ERR_INVALID_VALUE;
   const int xb = x_dtype == MOE_B200_DTYPE_BF16;
-  RouterPlan plan = plan_router(*cfg, B, xb);
-  if (plan.n_tblocks > kTbCap) return MOE_B200_ERR_UNSUPPORTED;
   RouterParams p{};
-  double* w64 = reinterpret_cast<double*>(ws8(ws) + L.w64);
-  {
-    // exact fp32 -> fp64 widening of W_r into the chunked expert-block layout
-    const long total = (long)plan.n_eblocks * plan.d_pad * plan.expc;
-    const int grid = static_cast<int>(std::min<long>((total + 255) / 256, (long)kNumSMs * 8));
-    router_prep_kernel<<<grid, 256, 0, s>>>(w_router, w64, cfg->hidden_dim, cfg->num_experts, plan.expc,
-                                           plan.d_pad, plan.n_eblocks, reinterpret_cast<uint32_t*>(hdr));
-    MOE_LAUNCH_CHECK("router_prep_kernel");
-  }
-  p.x = x; p.wr = w_router; p.w64 = w64; p.x_bf16 = xb;
-  p.trace = g_router_trace;
+  p.x = x; p.wr = w_router; p.x_bf16 = xb;
   p.B = static_cast<int>(B); p.d = cfg->hidden_dim; p.E = cfg->num_experts; p.k = cfg->top_k;
   p.gating = cfg->gating;
-  p.tokc = plan.tokc; p.expc = plan.expc;
-  p.n_eblocks = plan.n_eblocks; p.n_tblocks = plan.n_tblocks;
   p.chunk_rows = chunk_rows_for(*cfg, B);
-  p.logits = logits ? logits : reinterpret_cast<float*>(ws8(ws) + L.logits);
+  p.logits = logits;
+  p.want_logits = logits != nullptr;
+  if (const char* env = getenv("MOE_B200_ROUTER_FORCE_EXACT")) p.force_exact = atoi(env);
+  p.lbuf = reinterpret_cast<float2*>(ws8(ws) + L.lbuf);
   p.topk_idx = topk_idx; p.topk_w = topk_w; p.counts = counts; p.offsets = offsets;
   p.fwd = perm_fwd; p.inv = perm_inv;
   p.chunk_tab = reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab);
   p.prow = reinterpret_cast<int32_t*>(ws8(ws) + L.prow);
   p.n_chunks = hdr + 2;
   p.tb_counter = hdr + kHdrTb;
-  p.done_counter = hdr + 1;
   p.flags = reinterpret_cast<uint32_t*>(hdr);
-  p.stages = plan.stages;
-  CUtensorMap tmx;
-  {
-    int rc2 = get_encoder();
-    if (rc2) return rc2;
-    cuuint64_t dims[2] = {(cuuint64_t)cfg->hidden_dim, (cuuint64_t)B};
-    cuuint64_t strides[1] = {(cuuint64_t)cfg->hidden_dim * (xb ? 2 : 4)};
-    cuuint32_t box[2] = {(cuuint32_t)plan.kc, (cuuint32_t)plan.tokc};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = g_encode(&tmx, xb ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                          const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      g_last_error = "cuTensorMapEncodeTiled(x) failed";
-      return MOE_B200_ERR_CUDA;
-    }
+  p.trace = g_router_trace;
+
+  if (B <= seg_max_tokens(*cfg)) {
+    // latency regime: certified split-K segments (router_seg.cuh)
+    const SegPlan q = plan_seg(*cfg, B);
+    if (q.n_tb > kTbCap || (long)q.n_tb * q.n_eb > kBlkCap) return MOE_B200_ERR_UNSUPPORTED;
+    p.tokc = kSegTT; p.expc = q.expc;
+    p.n_eblocks = q.n_eb; p.n_tblocks = q.n_tb;
+    p.kr = q.kr; p.seg_len = q.seg_len; p.n_kb = q.n_kb;
+    p.blk_counter = hdr + kHdrBlk;
+    p.gpart = ws8(ws) + L.gpart;
+    const bool wvec = (cfg->num_experts % 4) == 0;
+    void (*kern)(RouterParams) = xb ? (wvec ? router_seg_kernel<true, true> : router_seg_kernel<true, false>)
+                                    : (wvec ? router_seg_kernel<false, true> : router_seg_kernel<false, false>);
+    MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q.smem));
+    kern<<<q.grid, kSegThreads, q.smem, s>>>(p);
+    MOE_LAUNCH_CHECK("router_seg_kernel");
+  } else if ((rc = launch_router_exact(*cfg, B, x, xb, w_router, L, ws, p, s))) {
+    return rc;
   }
-  return xb ? launch_router_x<true>(tmx, p, plan, s) : launch_router_x<false>(tmx, p, plan, s);
+  if (mid_event) MOE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(mid_event), s));
+  return launch_dispatch(*cfg, B, x, xb, topk_idx, counts, offsets, perm_fwd, perm_inv,
+                         reinterpret_cast<int32_t*>(ws8(ws) + L.prow), reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab),
+                         hdr + 2, xp, s);
 }
 
+int moe_b200_route(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
+                   const float* w_router, int32_t* topk_idx, float* topk_w, int32_t* counts,
+                   int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv, float* logits,
+                   void* ws, size_t ws_bytes, void* stream) {
+  return route_impl(cfg, B, x, x_dtype, w_router, topk_idx, topk_w, counts, offsets, perm_fwd, perm_inv,
+                    logits, ws, ws_bytes, stream, nullptr);
+}
+
+// throughput regime: exact sequential chains, register-tiled (router.cuh)
 int moe_b200_permute(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
                      const int32_t* perm_fwd, void* xp, void* stream) {
   int rc = check_config(cfg);
@@ -540,15 +665,14 @@ static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, in
     return MOE_B200_OK;
   };
   if ((rc = mark(0))) return rc;
-  if ((rc = moe_b200_route(cfg, B, x, x_dtype, w_router, topk_idx, topk_w, counts, offsets, perm_fwd,
-                           perm_inv, nullptr, ws, ws_bytes, stream)))
-    return rc;
-  if ((rc = mark(1))) return rc;
-  if (B == 0) return MOE_B200_OK;
   void* xp = ws8(ws) + L.xp;
   void* h = ws8(ws) + L.h;
   float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);
-  if ((rc = moe_b200_permute(cfg, B, x, x_dtype, perm_fwd, xp, stream))) return rc;
+  // router, then dispatch (scheduler + permute gather) — events[1] between them
+  if ((rc = route_impl(cfg, B, x, x_dtype, w_router, topk_idx, topk_w, counts, offsets, perm_fwd, perm_inv,
+                       nullptr, ws, ws_bytes, stream, xp, events ? events[1] : nullptr)))
+    return rc;
+  if (B == 0) return events ? mark(1) : MOE_B200_OK;
   if ((rc = mark(2))) return rc;
   if (L.max_chunks > kChunkCap) return MOE_B200_ERR_UNSUPPORTED;
   if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,

@@ -11,16 +11,17 @@
 //             == k largest keys (score desc, index asc) (router.py:99-107)
 //   sigmoid renormalisation by the fp32 pairwise sum, 1/k on zero sum
 //                                                 (router.py:108-112)
-//   histogram / offsets / stable permutation    (scheduler.py:78-103)
-//   block schedule (device tile table)          (scheduler.py:106-117)
+//   (histogram / offsets / stable permutation / schedule: dispatch.cuh)
 //
-// Launch structure: grid = (token blocks) x (expert blocks).  Phase 1: every
-// CTA runs TOKC x EXPC sequential fp64 FMA chains (TG chains per thread for
-// ILP), staging x / W_r chunks through a cp.async ring and an fp64 smem
-// buffer.  Phase 2: the last CTA to finish a token block (atomic counter)
-// computes scores and top-k for it, one warp per token.  Phase 3: the last
-// token block to finish builds counts, offsets, the stable permutation and
-// the GEMM tile table in one CTA.  All counters self-reset.
+// Two phase-1 kernels produce certified logit intervals (lbuf):
+//  * router_kernel (this file, throughput regime): grid = (token blocks) x
+//    (expert blocks); every CTA runs TOKC x EXPC exact sequential fp64 FMA
+//    chains (register tiles for ILP), staging x / W_r chunks through an
+//    mbarrier ring and an fp64 smem buffer; intervals have zero width.
+//  * router_seg_kernel (router_seg.cuh, latency regime): certified split-K.
+// Phase 2 (route_scores_tokens): the last CTA to finish a token block (atomic
+// counter) computes scores and top-k for it, one warp per token.  All
+// counters self-reset.
 #pragma once
 
 #include "common.cuh"
@@ -40,7 +41,13 @@ struct RouterParams {
   int stages;           // smem pipeline depth
   int n_eblocks, n_tblocks;
   int chunk_rows;       // GEMM row-chunk cap (BN)
-  float* logits;        // (B, E) fp32
+  float* logits;        // (B, E) fp32 exact logits, written only when want_logits
+  float2* lbuf;         // (B, E) certified logit interval {lo, hi} (fp32); lo = NaN: unknown
+  int want_logits;      // 1: resolve every logit exactly and write `logits`
+  int force_exact;      // test hook: certificates report "unknown" (exact fallback for every logit)
+  int kr, seg_len, n_kb;// segment kernel: k-range per CTA, segment length, k-blocks
+  int32_t* blk_counter; // (n_tblocks * n_eblocks) self-resetting (segment kernel)
+  void* gpart;          // segment kernel: per (block, k-block, chain) {C_b, A_b} fp64
   int32_t* topk_idx;    // (B, k)
   float* topk_w;        // (B, k)
   int32_t* counts;      // (E)
@@ -51,7 +58,6 @@ struct RouterParams {
   int32_t* prow;        // (T) expanded id -> padded permuted row (experts start 16-aligned)
   int32_t* n_chunks;    // [1]
   int32_t* tb_counter;  // (n_tblocks) self-resetting
-  int32_t* done_counter;// [1] self-resetting
   uint32_t* flags;      // [1]
   unsigned long long* trace;  // debug: CTA 0 per-chunk {issue, rawfull seen, full seen, compute done}
 };
@@ -141,6 +147,12 @@ MOE_DEVICE float np_expf(float x) {
   return __double2float_rn(static_cast<double>(p) * __longlong_as_double(qe));
 }
 
+MOE_DEVICE uint32_t smid_u32() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
 MOE_DEVICE unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -223,12 +235,289 @@ struct RouterSmem {
   }
   static __host__ __device__ size_t total_bytes(int tokc, int expc, int xb, int E, int nthreads, int stages, int kc) {
     size_t ph1 = stages * stage_bytes(tokc, expc, xb, kc) + 3 * stages * 8;
-    size_t ph2 = (size_t)(nthreads / 32) * E * sizeof(double);
-    size_t ph3 = ((size_t)(nthreads / 32) + 5) * E * sizeof(int32_t) + 512;
-    size_t m = ph1 > ph2 ? ph1 : ph2;
-    return m > ph3 ? m : ph3;
+    size_t ph2 = (size_t)(nthreads / 32) * (E * 16 + 256);  // scores row (fp64) + logit interval + window
+    return ph1 > ph2 ? ph1 : ph2;
   }
 };
+
+// ---------------------------------------------------------------------------
+// Operand helpers: 8 consecutive x values of one token row as fp32.
+// ---------------------------------------------------------------------------
+MOE_DEVICE void unpack_bf16x8(const uint4& v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+template <bool kXBf16>
+MOE_DEVICE void load_x8(const void* x, size_t off, float (&f)[8]) {
+  if constexpr (kXBf16) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(x) + off));
+    unpack_bf16x8(v, f);
+  } else {
+    const float4* q = reinterpret_cast<const float4*>(static_cast<const float*>(x) + off);
+    const float4 a = __ldg(q), b = __ldg(q + 1);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  }
+}
+
+// Last-arriver election across CTAs: every thread's prior global writes are
+// ordered before thread 0's release (bar.sync + fence.acq_rel.gpu, as in a
+// cooperative grid sync); the last CTA's reads follow its acquire and go
+// through L2 (__ldcg).  Returns true in the CTA that arrives n-th.
+MOE_DEVICE bool cta_arrive_last(int32_t* counter, int n) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    const int prev = atomicAdd(counter, 1);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    s_last = (prev == n - 1);
+  }
+  __syncthreads();
+  return s_last != 0;
+}
+
+// Exact logit: ONE sequential fp64 FMA chain in ascending k, rounded once to
+// fp32 (linalg.py:45-57 dot_accumulate; fp32 x fp32 products are exact in
+// fp64, so fma == the reference's multiply-then-add).  Used by the certified
+// segment path only for the rare logits whose certificate is inconclusive.
+// Warp-cooperative: lanes stream 32-step windows of x[t, :] and
+// W_r[:, e] (4 windows in flight, hiding L2 latency), every lane runs the same
+// dependent fold on shuffled operands (identical result in all lanes).
+template <bool kXBf16>
+MOE_DEVICE float exact_chain_logit_warp(const RouterParams& p, int t, int e, int lane, double* win) {
+  // fma(x, w, a) == fl(x*w + a) because x*w is exact in fp64: lane j forms the
+  // product of step j of a 32-step window, the window goes through shared
+  // memory, and every lane folds it with broadcast loads (one DADD per step).
+  const size_t xrow = (size_t)t * p.d;
+  const int nwin = (p.d + 31) / 32;
+  auto ld = [&](int w, float& xv, float& wv) {
+    const int k = w * 32 + lane;
+    xv = 0.0f;
+    wv = 0.0f;
+    if (w < nwin && k < p.d) {
+      if constexpr (kXBf16) xv = __bfloat162float(static_cast<const __nv_bfloat16*>(p.x)[xrow + k]);
+      else xv = __ldg(static_cast<const float*>(p.x) + xrow + k);
+      wv = __ldg(p.wr + (size_t)k * p.E + e);
+    }
+  };
+  float x0, x1, x2, x3, w0, w1, w2, w3;
+  ld(0, x0, w0); ld(1, x1, w1); ld(2, x2, w2); ld(3, x3, w3);
+  double acc = -0.0;  // fl(p + -0) == p, sign included, like fma(x, w, -0)
+  for (int w = 0; w < nwin; ++w) {
+    float x4, w4;
+    ld(w + 4, x4, w4);
+    __syncwarp();
+    win[lane] = static_cast<double>(x0) * static_cast<double>(w0);
+    __syncwarp();
+    const int n = min(32, p.d - w * 32);
+    if (n == 32) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc = __dadd_rn(acc, win[j]);
+    } else {
+      for (int j = 0; j < n; ++j) acc = __dadd_rn(acc, win[j]);
+    }
+    x0 = x1; x1 = x2; x2 = x3; x3 = x4;
+    w0 = w1; w1 = w2; w2 = w3; w3 = w4;
+  }
+  __syncwarp();
+  return __double2float_rn(acc);
+}
+
+MOE_DEVICE bool same_bits(float a, float b) { return __float_as_uint(a) == __float_as_uint(b); }
+
+// ---------------------------------------------------------------------------
+// Phase 2 (one warp per token): scores + top-k + sigmoid renormalisation from
+// the certified logit intervals.  A logit interval [lo, hi] holds every fp32
+// value the reference's sequential fold can round to.  Only the quantities
+// the outputs depend on must be certain:
+//   softmax: m = max logit, and s_e = fp32(l_e - m) for every e
+//            (router.py:78-83; exp64 and the division are then fixed);
+//   sigmoid: score_e = sigmoid32(l_e)                (linalg.py:71-80).
+// Both are checked over the interval (subtraction is monotone; the sigmoid is
+// evaluated at every candidate, at most 8), and any logit that still matters
+// is recomputed with the exact sequential chain.  want_logits resolves all.
+// ---------------------------------------------------------------------------
+template <bool kXBf16>
+MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_end, uint8_t* smem) {
+  const int tid = threadIdx.x;
+  const int nwarps = blockDim.x / 32;
+  const int warp = tid / 32, lane = tid % 32;
+  uint8_t* base = smem + (size_t)warp * (p.E * 16 + 256);
+  double* row = reinterpret_cast<double*>(base);
+  float* lo = reinterpret_cast<float*>(base + (size_t)p.E * 8);
+  float* hi = lo + p.E;
+  double* win = reinterpret_cast<double*>(base + (size_t)p.E * 16);  // exact-chain window
+  for (int t = t_begin + warp; t < t_end; t += nwarps) {
+    const float2* lb = p.lbuf + (size_t)t * p.E;
+    for (int e = lane; e < p.E; e += 32) {
+      const float2 v = __ldcg(lb + e);
+      lo[e] = v.x;
+      hi[e] = v.y;
+    }
+    __syncwarp();
+    // ---- certification; `round` 0: unknown (+ everything if want_logits),
+    //      1: whatever the outputs still depend on
+    float m = 0.0f;
+    for (int round = 0; round < 2; ++round) {
+      bool any = false;
+      for (int e0 = 0; e0 < p.E; e0 += 32) {
+        const int e = e0 + lane;
+        bool nd = false;
+        if (e < p.E) {
+          const float a = lo[e], b = hi[e];
+          const bool unsure = !same_bits(a, b);
+          if (round == 0) {
+            nd = isnan(a) || (p.want_logits && unsure);
+          } else if (unsure) {
+            if (p.gating == 0) {
+              nd = !same_bits(__fsub_rn(a, m), __fsub_rn(b, m));
+            } else {
+              const float sa = np_sigmoid(a);
+              float c = a;
+              int steps = 0;
+              while (!nd && !same_bits(c, b)) {
+                c = nextafterf(c, b);
+                nd = (++steps > 8) || !same_bits(np_sigmoid(c), sa);
+              }
+            }
+          }
+        }
+        // resolve the flagged logits of this 32-wide slice one at a time, warp-wide
+        uint32_t todo = __ballot_sync(0xffffffffu, nd);
+        while (todo) {
+          const int j = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const float v = exact_chain_logit_warp<kXBf16>(p, t, e0 + j, lane, win);
+          if (lane == j) {
+            lo[e] = v;
+            hi[e] = v;
+          }
+          if (p.trace && p.seg_len && lane == 0) atomicAdd(p.trace + (size_t)blockIdx.x * 16 + 11, 1ull);
+        }
+        any |= nd;
+      }
+      __syncwarp();
+      if (round == 0 && p.gating == 0) {
+        // the row max must be certain; otherwise resolve every unsure logit
+        float mlo = -__int_as_float(0x7f800000), mhi = mlo;
+        for (int e = lane; e < p.E; e += 32) {
+          mlo = fmaxf(mlo, lo[e]);
+          mhi = fmaxf(mhi, hi[e]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          mlo = fmaxf(mlo, __shfl_xor_sync(0xffffffffu, mlo, o));
+          mhi = fmaxf(mhi, __shfl_xor_sync(0xffffffffu, mhi, o));
+        }
+        if (mlo != mhi) {
+          for (int e0 = 0; e0 < p.E; e0 += 32) {
+            const int e = e0 + lane;
+            uint32_t todo = __ballot_sync(0xffffffffu, e < p.E && !same_bits(lo[e], hi[e]));
+            while (todo) {
+              const int j = __ffs(todo) - 1;
+              todo &= todo - 1;
+              const float v = exact_chain_logit_warp<kXBf16>(p, t, e0 + j, lane, win);
+              if (lane == j) {
+                lo[e] = v;
+                hi[e] = v;
+              }
+              if (p.trace && p.seg_len && lane == 0) atomicAdd(p.trace + (size_t)blockIdx.x * 16 + 12, 1ull);
+            }
+          }
+          __syncwarp();
+          mlo = -__int_as_float(0x7f800000);
+          for (int e = lane; e < p.E; e += 32) mlo = fmaxf(mlo, lo[e]);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) mlo = fmaxf(mlo, __shfl_xor_sync(0xffffffffu, mlo, o));
+        }
+        m = mlo;
+      }
+      (void)any;
+    }
+    if (p.want_logits)
+      for (int e = lane; e < p.E; e += 32) p.logits[(size_t)t * p.E + e] = lo[e];
+    // ---- scores (lo is a representative: every candidate gives the same bits)
+    if (p.gating == 0) {
+      for (int e = lane; e < p.E; e += 32) row[e] = exp(static_cast<double>(__fsub_rn(lo[e], m)));
+      __syncwarp();
+      double S = 0.0;
+      if (lane == 0) S = pairwise_sum<double>(row, p.E);
+      S = __shfl_sync(0xffffffffu, S, 0);
+      __syncwarp();
+      for (int e = lane; e < p.E; e += 32) {
+        float sc = __double2float_rn(__ddiv_rn(row[e], S));
+        row[e] = static_cast<double>(sc);
+      }
+    } else {
+      for (int e = lane; e < p.E; e += 32) row[e] = static_cast<double>(np_sigmoid(lo[e]));
+    }
+    __syncwarp();
+      // top-k over keys (score bits desc, index asc); scores are >= +0.
+      float wsel = 0.0f;
+      int isel = 0;
+      for (int j = 0; j < p.k; ++j) {
+        uint64_t best = 0;
+        for (int e = lane; e < p.E; e += 32) {
+          float sc = static_cast<float>(row[e]);
+          if (sc < 0.0f) continue;  // already selected (marked -1)
+          uint32_t bits = (sc == 0.0f) ? 0u : __float_as_uint(sc);
+          uint64_t key = (static_cast<uint64_t>(bits) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(e));
+          best = key > best ? key : best;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          uint64_t other = shfl_xor_u64(best, o);
+          best = other > best ? other : best;
+        }
+        int e_best = static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFu));
+        float s_best = __uint_as_float(static_cast<uint32_t>(best >> 32));
+        __syncwarp();
+        if (lane == (e_best & 31)) row[e_best] = -1.0;
+        __syncwarp();
+        if (lane == j) { wsel = s_best; isel = e_best; }
+        if (j >= 32) {  // k > 32: write directly (rare)
+          if (lane == 0) {
+            p.topk_idx[(size_t)t * p.k + j] = e_best;
+            p.topk_w[(size_t)t * p.k + j] = s_best;
+          }
+        }
+      }
+      __syncwarp();
+      if (p.gating == 1) {
+        // renormalise over the selected k with numpy's fp32 pairwise sum
+        float* wrow = reinterpret_cast<float*>(row);
+        if (lane < p.k && lane < 32) wrow[lane] = wsel;
+        __syncwarp();
+        if (p.k > 32 && lane == 0) {
+          for (int j = 32; j < p.k; ++j) wrow[j] = p.topk_w[(size_t)t * p.k + j];
+        }
+        __syncwarp();
+        float S = 0.0f;
+        if (lane == 0) S = pairwise_sum<float>(wrow, p.k);
+        S = __shfl_sync(0xffffffffu, S, 0);
+        const float uni = __double2float_rn(1.0 / static_cast<double>(p.k));
+        if (lane < p.k) wsel = (S == 0.0f) ? uni : __fdiv_rn(wsel, S);
+        if (p.k > 32 && lane == 0) {
+          for (int j = 32; j < p.k; ++j) {
+            float v = wrow[j];
+            p.topk_w[(size_t)t * p.k + j] = (S == 0.0f) ? uni : __fdiv_rn(v, S);
+          }
+        }
+        __syncwarp();
+      }
+      if (lane < p.k) {
+        p.topk_idx[(size_t)t * p.k + lane] = isel;
+        p.topk_w[(size_t)t * p.k + lane] = wsel;
+      }
+      __syncwarp();
+    }
+}
 
 // Launch shape: blockDim = n_compute + kRouterProducers.  Compute threads own a
 // kTE x kTT register tile of independent sequential fp64 chains; the producer
@@ -380,8 +669,10 @@ router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
 #pragma unroll
         for (int j = 0; j < kTT; ++j) {
           const int t = t0 + tg + j * n_tg;
-          if (t < p.B && e < p.E && eg + i * n_eg < p.expc)
-            p.logits[(size_t)t * p.E + e] = __double2float_rn(acc[i][j]);
+          if (t < p.B && e < p.E && eg + i * n_eg < p.expc) {
+            const float l = __double2float_rn(acc[i][j]);
+            p.lbuf[(size_t)t * p.E + e] = make_float2(l, l);  // exact: a zero-width interval
+          }
         }
       }
     }
@@ -389,219 +680,14 @@ router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
 
   if (p.trace && tid == 0) p.trace[4096 * 4 + blockIdx.x * 4 + 0] = globaltimer_ns();
   // --------------------- phase 2: scores + top-k (last CTA of block) --------
-  __shared__ int s_flag;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    int prev = atomicAdd(p.tb_counter + tb, 1);
-    s_flag = (prev == p.n_eblocks - 1);
+  if (p.n_eblocks > 1) {
+    if (!cta_arrive_last(p.tb_counter + tb, p.n_eblocks)) return;
+    if (tid == 0) p.tb_counter[tb] = 0;  // every CTA of this block has arrived: reset for the next launch
+  } else {
+    __syncthreads();
   }
-  __syncthreads();
-  if (!s_flag) return;
-  __threadfence();
-
-  {
-    const int warp = tid / 32, lane = tid % 32;
-    double* row = reinterpret_cast<double*>(smem) + (size_t)warp * p.E;
-    const int tend = min(t0 + p.tokc, p.B);
-    for (int t = t0 + warp; t < tend; t += nthreads / 32) {
-      const float* lg = p.logits + (size_t)t * p.E;
-      // scores -> row (as double for softmax, float bits stored in double for sigmoid)
-      if (p.gating == 0) {
-        float m = -__int_as_float(0x7f800000);
-        for (int e = lane; e < p.E; e += 32) m = fmaxf(m, __ldcg(lg + e));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        for (int e = lane; e < p.E; e += 32) {
-          float s = __fsub_rn(__ldcg(lg + e), m);
-          row[e] = exp(static_cast<double>(s));
-        }
-        __syncwarp();
-        double S = 0.0;
-        if (lane == 0) S = pairwise_sum<double>(row, p.E);
-        S = __shfl_sync(0xffffffffu, S, 0);
-        __syncwarp();
-        for (int e = lane; e < p.E; e += 32) {
-          float sc = __double2float_rn(__ddiv_rn(row[e], S));
-          row[e] = static_cast<double>(sc);
-        }
-      } else {
-        for (int e = lane; e < p.E; e += 32) row[e] = static_cast<double>(np_sigmoid(__ldcg(lg + e)));
-      }
-      __syncwarp();
-      // top-k over keys (score bits desc, index asc); scores are >= +0.
-      float wsel = 0.0f;
-      int isel = 0;
-      for (int j = 0; j < p.k; ++j) {
-        uint64_t best = 0;
-        for (int e = lane; e < p.E; e += 32) {
-          float sc = static_cast<float>(row[e]);
-          if (sc < 0.0f) continue;  // already selected (marked -1)
-          uint32_t bits = (sc == 0.0f) ? 0u : __float_as_uint(sc);
-          uint64_t key = (static_cast<uint64_t>(bits) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(e));
-          best = key > best ? key : best;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          uint64_t other = shfl_xor_u64(best, o);
-          best = other > best ? other : best;
-        }
-        int e_best = static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFu));
-        float s_best = __uint_as_float(static_cast<uint32_t>(best >> 32));
-        __syncwarp();
-        if (lane == (e_best & 31)) row[e_best] = -1.0;
-        __syncwarp();
-        if (lane == j) { wsel = s_best; isel = e_best; }
-        if (j >= 32) {  // k > 32: write directly (rare)
-          if (lane == 0) {
-            p.topk_idx[(size_t)t * p.k + j] = e_best;
-            p.topk_w[(size_t)t * p.k + j] = s_best;
-          }
-        }
-      }
-      __syncwarp();
-      if (p.gating == 1) {
-        // renormalise over the selected k with numpy's fp32 pairwise sum
-        float* wrow = reinterpret_cast<float*>(row);
-        if (lane < p.k && lane < 32) wrow[lane] = wsel;
-        __syncwarp();
-        if (p.k > 32 && lane == 0) {
-          for (int j = 32; j < p.k; ++j) wrow[j] = p.topk_w[(size_t)t * p.k + j];
-        }
-        __syncwarp();
-        float S = 0.0f;
-        if (lane == 0) S = pairwise_sum<float>(wrow, p.k);
-        S = __shfl_sync(0xffffffffu, S, 0);
-        const float uni = __double2float_rn(1.0 / static_cast<double>(p.k));
-        if (lane < p.k) wsel = (S == 0.0f) ? uni : __fdiv_rn(wsel, S);
-        if (p.k > 32 && lane == 0) {
-          for (int j = 32; j < p.k; ++j) {
-            float v = wrow[j];
-            p.topk_w[(size_t)t * p.k + j] = (S == 0.0f) ? uni : __fdiv_rn(v, S);
-          }
-        }
-        __syncwarp();
-      }
-      if (lane < p.k) {
-        p.topk_idx[(size_t)t * p.k + lane] = isel;
-        p.topk_w[(size_t)t * p.k + lane] = wsel;
-      }
-      __syncwarp();
-    }
-  }
-
+  route_scores_tokens<kXBf16>(p, t0, min(t0 + p.tokc, p.B), smem);
   if (p.trace && tid == 0) p.trace[4096 * 4 + blockIdx.x * 4 + 1] = globaltimer_ns();
-  // -------------------- phase 3: scheduler (last token block) ---------------
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    p.tb_counter[tb] = 0;  // every CTA of this block has arrived: reset for the next launch
-    int prev = atomicAdd(p.done_counter, 1);
-    s_flag = (prev == p.n_tblocks - 1);
-  }
-  __syncthreads();
-  if (!s_flag) return;
-  __threadfence();
-
-  {
-    const int nw = nthreads / 32;
-    const int warp = tid / 32, lane = tid % 32;
-    const int T = p.B * p.k;
-    const int E = p.E;
-    int32_t* hist = reinterpret_cast<int32_t*>(smem);       // [nw][E] -> per-warp base
-    int32_t* s_cnt = hist + (size_t)nw * E;                  // [E]
-    int32_t* s_off = s_cnt + E;                              // [E+1]
-    int32_t* s_cpre = s_off + E + 1;                         // [E+1] chunk prefix
-    int32_t* s_off16 = s_cpre + E + 1;                       // [E+1] 16-padded offsets
-    for (int i = tid; i < nw * E; i += nthreads) hist[i] = 0;
-    __syncthreads();
-    const int seg = (T + nw - 1) / nw;
-    const int s0 = warp * seg, s1 = min(T, s0 + seg);
-    for (int i = s0 + lane; i < s1; i += 32) atomicAdd(&hist[warp * E + __ldcg(p.topk_idx + i)], 1);
-    __syncthreads();
-    // per-expert totals and per-warp exclusive bases
-    for (int e = tid; e < E; e += nthreads) {
-      int run = 0;
-      for (int w = 0; w < nw; ++w) {
-        int h = hist[w * E + e];
-        hist[w * E + e] = run;
-        run += h;
-      }
-      s_cnt[e] = run;
-    }
-    __syncthreads();
-    // warp 0: exclusive scans of counts and of chunk counts
-    if (warp == 0) {
-      const int per = (E + 31) / 32;
-      const int lo = lane * per, hi = min(E, lo + per);
-      int sum_c = 0, sum_ch = 0, sum_16 = 0;
-      for (int e = lo; e < hi; ++e) {
-        sum_c += s_cnt[e];
-        sum_ch += (s_cnt[e] + p.chunk_rows - 1) / p.chunk_rows;
-        sum_16 += (s_cnt[e] + 15) & ~15;
-      }
-      int inc_c = sum_c, inc_ch = sum_ch, inc_16 = sum_16;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int a = __shfl_up_sync(0xffffffffu, inc_c, o);
-        int b = __shfl_up_sync(0xffffffffu, inc_ch, o);
-        int c = __shfl_up_sync(0xffffffffu, inc_16, o);
-        if (lane >= o) { inc_c += a; inc_ch += b; inc_16 += c; }
-      }
-      int run_c = inc_c - sum_c, run_ch = inc_ch - sum_ch, run_16 = inc_16 - sum_16;
-      for (int e = lo; e < hi; ++e) {
-        s_off[e] = run_c;
-        s_cpre[e] = run_ch;
-        s_off16[e] = run_16;
-        run_c += s_cnt[e];
-        run_ch += (s_cnt[e] + p.chunk_rows - 1) / p.chunk_rows;
-        run_16 += (s_cnt[e] + 15) & ~15;
-      }
-      if (lane == 31) {
-        s_off[E] = inc_c;
-        s_cpre[E] = inc_ch;
-        s_off16[E] = inc_16;
-      }
-    }
-    __syncthreads();
-    for (int e = tid; e < E; e += nthreads) {
-      p.counts[e] = s_cnt[e];
-      p.offsets[e] = s_off[e];
-      const int n_e = s_cnt[e];
-      const int nchunk = (n_e + p.chunk_rows - 1) / p.chunk_rows;
-      for (int c = 0; c < nchunk; ++c) {
-        int r0 = c * p.chunk_rows;
-        p.chunk_tab[s_cpre[e] + c] = make_int4(e, s_off[e] + r0, min(p.chunk_rows, n_e - r0), s_off16[e] + r0);
-      }
-    }
-    if (tid == 0) {
-      p.offsets[E] = s_off[E];
-      p.n_chunks[0] = s_cpre[E];
-    }
-    // stable counting sort: warp w walks its segment in id order
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    for (int base = s0; base < s1; base += 32) {
-      int i = base + lane;
-      bool valid = i < s1;
-      int e = valid ? __ldcg(p.topk_idx + i) : -1 - lane;  // unique sentinel per invalid lane
-      uint32_t peers = __match_any_sync(0xffffffffu, e);
-      if (valid) {
-        int rank = __popc(peers & lt_mask);
-        int pos = s_off[e] + hist[warp * E + e] + rank;
-        p.fwd[pos] = i;
-        p.inv[i] = pos;
-        if (p.prow) p.prow[i] = s_off16[e] + (pos - s_off[e]);
-      }
-      __syncwarp();
-      if (valid && (__ffs(peers) - 1) == static_cast<int>(lane)) hist[warp * E + e] += __popc(peers);
-      __syncwarp();
-    }
-    if (tid == 0) *p.done_counter = 0;
-    if (p.trace && tid == 0) {
-      p.trace[4096 * 4 + blockIdx.x * 4 + 2] = 1;
-      p.trace[4096 * 4 + blockIdx.x * 4 + 3] = globaltimer_ns();
-    }
-  }
 }
 
 }  // namespace moe

@@ -49,8 +49,22 @@ def _np(t):
 # routing: bit-exact against the reference goldens
 # ---------------------------------------------------------------------------
 
-def test_route_bitexact_golden_full_shapes(pkg, golden):
+ROUTER_MODES = {
+    "auto": {},
+    # certificate disabled: every logit goes through the exact fallback chain
+    "fallback": {"MOE_B200_ROUTER_FORCE_EXACT": "1"},
+    # throughput-regime kernel (exact sequential chains) for every size
+    "exact_kernel": {"MOE_B200_SEG_MAX_CHAINS": "0"},
+    # segment kernel for every size, shortest segments (most k-blocks)
+    "seg_short": {"MOE_B200_SEG_LEN": "8"},
+}
+
+
+@pytest.mark.parametrize("mode", sorted(ROUTER_MODES))
+def test_route_bitexact_golden_full_shapes(pkg, golden, mode, monkeypatch):
     P = pkg
+    for k_, v_ in ROUTER_MODES[mode].items():
+        monkeypatch.setenv(k_, v_)
     for _, name, seed, e, k, d, scaled, b, g, bf16 in [m for m in golden_meta(golden) if m[0] == "route"]:
         tokens, wr = O.make_router_instance(seed, b, d, e, scaled=bool(scaled), bf16_tokens=bool(bf16))
         cfg = _cfg(P, e, k, d, 8, g)
