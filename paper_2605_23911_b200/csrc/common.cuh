@@ -38,6 +38,16 @@ MOE_DEVICE bool elect_one() {
 }
 
 // ----------------------------------------------------------------------------
+// Programmatic dependent launch (PDL): the kernels of one forward are chained
+// with cudaLaunchAttributeProgrammaticStreamSerialization; each runs its
+// prologue, then pdl_wait() before touching its predecessor's outputs (a no-op
+// when launched without the attribute).  pdl_launch_dependents() lets the next
+// kernel's CTAs be scheduled once every CTA of this grid has issued it.
+// ----------------------------------------------------------------------------
+MOE_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+MOE_DEVICE void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ----------------------------------------------------------------------------
 // mbarrier
 // ----------------------------------------------------------------------------
 MOE_DEVICE void mbar_init(uint64_t* bar, uint32_t count) {

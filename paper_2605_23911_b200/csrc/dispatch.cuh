@@ -82,6 +82,8 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
       if (v < nvec) pre[u] = load_bf16x8<kXBf16>(p.x, (size_t)((r0 + v / vpr) / p.k), p.d, v % vpr);
     }
   }
+  pdl_launch_dependents();
+  pdl_wait();  // routing indices of the router grid
   __syncthreads();
   // histogram of all rows and of the rows before r0 (warp-aggregated smem
   // atomics); four index loads in flight per thread

@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(kRowThreads)
 combine_tiled_kernel(const float* __restrict__ ys, int splits, int n_dp, int T_pad,
                      const int32_t* __restrict__ prow, const float* __restrict__ topk_w,
                      void* __restrict__ y, int B, int k, int d) {
+  pdl_wait();
   const int vec_per_row = d / 4;
   const long total = (long)B * vec_per_row;
   const size_t half_stride = (size_t)T_pad * 128;
@@ -156,6 +157,73 @@ combine_tiled_kernel(const float* __restrict__ ys, int splits, int n_dp, int T_p
       acc.y = __fadd_rn(acc.y, __fmul_rn(w, g.y));
       acc.z = __fadd_rn(acc.z, __fmul_rn(w, g.z));
       acc.w = __fadd_rn(acc.w, __fmul_rn(w, g.w));
+    }
+    if (kBf16Out) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y);
+      __nv_bfloat162 p1 = __floats2bfloat162_rn(acc.z, acc.w);
+      uint2 o;
+      o.x = *reinterpret_cast<uint32_t*>(&p0);
+      o.y = *reinterpret_cast<uint32_t*>(&p1);
+      reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(y) + (size_t)t * d)[v] = o;
+    } else {
+      reinterpret_cast<float4*>(static_cast<float*>(y) + (size_t)t * d)[v] = acc;
+    }
+  }
+}
+
+// Fused-forward combine, one CTA per token: the k slots' padded rows and
+// routing weights are read once into shared memory, and every thread keeps
+// all k x S partial loads of its 16-byte columns in flight.
+//   y[t] = sum_j fl(w[t,j] * (sum_s P_s[prow(t*k+j)])), ascending j and s,
+// fp32 from +0 — the reference's out += w_j * g_j (pipeline.py:396-399).
+constexpr int kCombineMaxKS = 16;  // k * S register budget (else the generic loop)
+template <bool kBf16Out, int kS>
+__global__ void __launch_bounds__(kRowThreads)
+combine_token_kernel(const float* __restrict__ ys, int n_dp, int T_pad,
+                     const int32_t* __restrict__ prow, const float* __restrict__ topk_w,
+                     void* __restrict__ y, int B, int k, int d) {
+  pdl_wait();  // partials of the FFN grid
+  __shared__ int32_t s_row[kCombineMaxKS];
+  __shared__ float s_w[kCombineMaxKS];
+  const int t = blockIdx.x;
+  if (threadIdx.x < k) {
+    s_row[threadIdx.x] = __ldg(prow + (size_t)t * k + threadIdx.x);
+    s_w[threadIdx.x] = __ldg(topk_w + (size_t)t * k + threadIdx.x);
+  }
+  __syncthreads();
+  const size_t half_stride = (size_t)T_pad * 128;
+  constexpr int kMaxK = kCombineMaxKS / kS;
+  const int ks = k * kS;
+  for (int v = threadIdx.x; v < d / 4; v += kRowThreads) {
+    const int feat = v * 4;
+    const size_t blk = (size_t)(feat >> 8) * 2 + ((feat >> 7) & 1);  // (d-pair, half)
+    const int col = feat & 127;
+    float4 a[kCombineMaxKS];
+#pragma unroll
+    for (int i = 0; i < kCombineMaxKS; ++i) {
+      if (i < ks) {
+        const int j = i / kS, s = i % kS;
+        const float* src = ys + ((size_t)s * n_dp * 2 + blk) * half_stride + (size_t)s_row[j] * 128 + col;
+        a[i] = __ldg(reinterpret_cast<const float4*>(src));
+      }
+    }
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+      if (j < k) {
+        float4 g = a[j * kS];
+#pragma unroll
+        for (int s = 1; s < kS; ++s) {
+          const float4 b = a[j * kS + s];
+          g.x = __fadd_rn(g.x, b.x); g.y = __fadd_rn(g.y, b.y);
+          g.z = __fadd_rn(g.z, b.z); g.w = __fadd_rn(g.w, b.w);
+        }
+        const float w = s_w[j];
+        acc.x = __fadd_rn(acc.x, __fmul_rn(w, g.x));
+        acc.y = __fadd_rn(acc.y, __fmul_rn(w, g.y));
+        acc.z = __fadd_rn(acc.z, __fmul_rn(w, g.z));
+        acc.w = __fadd_rn(acc.w, __fmul_rn(w, g.w));
+      }
     }
     if (kBf16Out) {
       __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y);

@@ -21,8 +21,11 @@
 // between 8-row K groups).  Tokens (rows x K, K-contiguous) are the K-major
 // B operand.
 //
-// Roles (256 threads): warp 0 = scheduler + TMA producer, warp 1 = MMA
-// issuer (one lane), warp 2 = TMEM allocator, warps 4-7 = epilogue.
+// Roles (384 threads): warp 0 = scheduler + TMA producer, warp 1 = MMA
+// issuer (one lane), warp 2 = TMEM allocator, warps 4-11 = epilogue in two
+// groups of four (warp w reads TMEM lanes 32*(w%4)..+31); 32-row token chunks
+// alternate between the groups so the TMEM drain (SiLU on MUFU) runs on 8
+// warps and the next tile's MMAs start sooner.
 // Gate+up keeps two TMEM accumulators fed from the SAME staged token tile
 // and applies SiLU(g)*u in registers before the bf16 store (pipeline.py:289-296).
 #pragma once
@@ -31,7 +34,9 @@
 
 namespace moe {
 
-constexpr int kFfnThreads = 256;
+constexpr int kFfnThreads = 384;
+constexpr int kEpiWarps = 8;    // warps 4..11: two groups of 4 (one warp per TMEM lane quadrant)
+constexpr int kEpiGroups = 2;   // 32-row chunks alternate between the groups
 constexpr int kBM = 128;        // weight rows (output features) per tile
 constexpr int kBK = 64;         // K per stage: one 128-byte swizzle row of bf16
 constexpr int kBoxRows = 32;    // token rows per TMA box
@@ -87,9 +92,9 @@ struct FfnCfg {
   static constexpr int kABytes = kBM * kBK * 2;      // 16 KB weight slot
   static constexpr int kBBytes = kBN * kBK * 2;      // token slot
   static constexpr int kStgBytes = 32 * kBM * 4;     // 32 rows x 128 fp32 (16 KB)
-  static constexpr int kStgBufs = kV == 1 ? 1 : 2;
-  static constexpr int kAStages = kBN == 256 ? (kV == 1 ? 7 : kV == 2 ? 6 : 8) : 8;
-  static constexpr int kBStages = kBN == 256 ? (kV == 3 ? 2 : 3) : 4;
+  static constexpr int kStgBufs = kEpiGroups;  // one staging buffer per epilogue group
+  static constexpr int kAStages = kBN == 256 ? 6 : 8;
+  static constexpr int kBStages = kBN == 256 ? 3 : 4;
   static constexpr int kRingBytes = kAStages * kABytes + kBStages * kBBytes;
   static constexpr int kDataBytes = kRingBytes + kStgBufs * kStgBytes;
   static constexpr uint32_t kTmemCols = 2 * kBN <= 256 ? 256 : 512;
@@ -112,9 +117,16 @@ MOE_DEVICE void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+MOE_DEVICE float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 MOE_DEVICE float silu_mul(float g, float u) {
-  // silu(g) * u in fp32 (fast exp; tolerance path, pipeline.py:294)
-  return __fdividef(g, 1.0f + __expf(-g)) * u;
+  // silu(g) * u = g * sigmoid(g) * u, sigmoid(g) = 0.5 + 0.5 tanh(g/2): one
+  // MUFU op per element (tolerance path, pipeline.py:294; h is rounded to bf16)
+  const float hg = 0.5f * g;
+  return hg * u * (1.0f + tanh_approx(hg));
 }
 
 MOE_DEVICE int ld_acquire_gpu(const int32_t* p) {
@@ -128,8 +140,8 @@ MOE_DEVICE void red_release_gpu_add(int32_t* p, int v) {
 MOE_DEVICE void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-MOE_DEVICE void epi_bar_sync() {  // the 128 epilogue threads only
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+MOE_DEVICE void epi_bar_sync(int group) {  // the 128 threads of one epilogue group
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory");
 }
 
 struct TileInfo {
@@ -201,10 +213,10 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       mbar_init(b_empty + s, 1);
     }
     mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, 128);
+    mbar_init(tmem_empty, 32 * kEpiWarps);
     for (int s = 0; s < kSchedSlots; ++s) {
       mbar_init(sched_full + s, 1);
-      mbar_init(sched_empty + s, 1 + 4);  // MMA lane + one lane per epilogue warp
+      mbar_init(sched_empty + s, 1 + kEpiWarps);  // MMA lane + one lane per epilogue warp
     }
     fence_barrier_init();
   }
@@ -213,6 +225,10 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
+  // prologue done: let the combine grid queue up, then wait for the dispatch
+  // (chunk table, permuted tokens) to be complete and visible
+  pdl_launch_dependents();
+  pdl_wait();
 
   const int nch = __ldg(p.n_chunks);
   const int total_tiles = nch * (p.n_mt_gu + p.n_mt_dn * p.splits);
@@ -252,7 +268,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           kb1 = min(nkb_dn, kb0 + p.kb_per_split);
           if (p.gu_wait) {
             // h rows of this chunk are complete once all its gate+up tiles released
-            while (ld_acquire_gpu(p.gu_done + ti.chunk) < p.n_mt_gu) __nanosleep(64);
+            while (ld_acquire_gpu(p.gu_done + ti.chunk) < p.n_mt_gu * kEpiGroups) __nanosleep(64);
             fence_proxy_async_global();
           }
         }
@@ -364,8 +380,11 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
     }
   } else if (warp >= 4) {
     // =============================== epilogue ===============================
-    const int wq = warp & 3;
+    const int wq = warp & 3;                 // TMEM lane quadrant
+    const int grp = (warp - 4) >> 2;         // chunk group: 32-row chunks q with q % 2 == grp
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+    const bool issuer = (wq == 0 && lane == 0);  // one bulk-copy issuer per group
+    uint8_t* stg_g = stg + grp * C::kStgBytes;
     uint32_t acc_phase = 0;
     int slot = 0;
     uint32_t sphase = 0;
@@ -380,21 +399,21 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       const int4 ch = __ldg(p.chunk_tab + ti.chunk);
       mbar_wait(tmem_full, acc_phase);
       tc_fence_after();
-      if (p.trace && wq == 0 && lane == 0) p.trace[tile * 8 + 4] = globaltimer();
-      // Staged store protocol, per 32-row chunk: (issuer) make the staging
-      // buffer free -> barrier -> every thread writes its feature column ->
-      // proxy fence -> barrier -> issuer (warp 4 lane 0) bulk-copies each row.
-      const bool issuer = (wq == 0 && lane == 0);
+      if (p.trace && warp == 4 && lane == 0) p.trace[tile * 8 + 4] = globaltimer();
+      // Staged store protocol, per 32-row chunk of this group: (issuer) make the
+      // staging buffer free -> group barrier -> every thread writes its feature
+      // column -> proxy fence -> group barrier -> issuer bulk-copies the rows.
       if (ti.is_gu) {
         const int f0 = ti.mt * kBM;
         const int nvalid_f = min(kBM, p.f - f0);
         // Phase 1 (TMEM critical path): drain both accumulators, apply SiLU(g)*u and
         // keep h as packed bf16 pairs in registers, then release TMEM so the next
         // tile's MMAs start while this tile's h is still being written out.
-        constexpr int kMaxChunks = kBN / 32;
+        constexpr int kMaxChunks = kBN / 32 / kEpiGroups;
         uint32_t hp[kMaxChunks][16];
 #pragma unroll
-        for (int q = 0; q < kMaxChunks; ++q) {
+        for (int qq = 0; qq < kMaxChunks; ++qq) {
+          const int q = qq * kEpiGroups + grp;
           if (q * 32 < ch.z) {
             uint32_t g[32], u[32];
             tmem_ld_32x32b_x32(tmem_base + lane_base + q * 32, g);
@@ -405,30 +424,31 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
               const float h0 = silu_mul(__uint_as_float(g[2 * i]), __uint_as_float(u[2 * i]));
               const float h1 = silu_mul(__uint_as_float(g[2 * i + 1]), __uint_as_float(u[2 * i + 1]));
               __nv_bfloat162 pk = __floats2bfloat162_rn(h0, h1);
-              hp[q][i] = *reinterpret_cast<uint32_t*>(&pk);
+              hp[qq][i] = *reinterpret_cast<uint32_t*>(&pk);
             }
           }
         }
         tc_fence_before();
         mbar_arrive(tmem_empty);
-        if (p.trace && issuer) p.trace[tile * 8 + 6] = globaltimer();
+        if (p.trace && warp == 4 && lane == 0) p.trace[tile * 8 + 6] = globaltimer();
         // Phase 2: stage 32-row chunks in smem and bulk-copy them out.
         const int fl = wq * 32 + lane;  // feature within the tile
 #pragma unroll
-        for (int q = 0; q < kMaxChunks; ++q) {
+        for (int qq = 0; qq < kMaxChunks; ++qq) {
+          const int q = qq * kEpiGroups + grp;
           const int c0 = q * 32;
           if (c0 < ch.z) {
-            __nv_bfloat16* sbuf = reinterpret_cast<__nv_bfloat16*>(stg + (q % C::kStgBufs) * C::kStgBytes);
-            if (issuer) bulk_wait_read<C::kStgBufs - 1>();
-            epi_bar_sync();
+            __nv_bfloat16* sbuf = reinterpret_cast<__nv_bfloat16*>(stg_g);
+            if (issuer) bulk_wait_read<0>();
+            epi_bar_sync(grp);
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              const uint32_t w = hp[q][i];
+              const uint32_t w = hp[qq][i];
               reinterpret_cast<uint16_t*>(sbuf)[(2 * i) * kBM + fl] = static_cast<uint16_t>(w & 0xFFFFu);
               reinterpret_cast<uint16_t*>(sbuf)[(2 * i + 1) * kBM + fl] = static_cast<uint16_t>(w >> 16);
             }
             fence_proxy_async_smem();
-            epi_bar_sync();
+            epi_bar_sync(grp);
             if (issuer) {
               const int rows = min(32, ch.z - c0);
               if (p.tiled) {
@@ -442,46 +462,38 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             }
           }
         }
-        if (p.gu_wait) {
-          // publish the chunk's h rows: bulk writes complete, then one release increment
-          if (issuer) {
-            bulk_wait_all();
-            fence_proxy_async_global();
-            __threadfence();
-            red_release_gpu_add(p.gu_done + ti.chunk, 1);
-          }
+        if (p.gu_wait && issuer) {
+          // publish this group's h rows: bulk writes complete, then one release increment
+          bulk_wait_all();
+          fence_proxy_async_global();
+          __threadfence();
+          red_release_gpu_add(p.gu_done + ti.chunk, 1);
         }
       } else {
-        float* out = p.ys;  // row layout (stage API): S == 1, slot rows
-        int nchunk = 0;
-        long long t_ld = 0, t_b1 = 0, t_sts = 0, t_b2 = 0;
+        // down tile: two 128-row halves; 32-row chunks alternate between the groups
+        const int nq = (ch.z + 31) / 32;
+        const int my_last = (nq - 1 - grp) >= 0 ? (nq - 1 - ((nq - 1 - grp) % kEpiGroups)) : -1;
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
           const int d0 = ti.mt * 2 * kBM + half * kBM;
           const int nvalid_d = min(kBM, p.d - d0);
-          for (int c0 = 0; c0 < ch.z; c0 += 32, ++nchunk) {
+          for (int q = grp; q < nq; q += kEpiGroups) {
+            const int c0 = q * 32;
             uint32_t a[32];
-            const long long tq0 = clock64();
             tmem_ld_32x32b_x32(tmem_base + lane_base + half * kBN + c0, a);
             tmem_wait_ld();
-            t_ld += clock64() - tq0;
-            if (half == 1 && c0 + 32 >= ch.z) {
+            if (half == 1 && q == my_last) {
               tc_fence_before();
               mbar_arrive(tmem_empty);
             }
-            float* sbuf = reinterpret_cast<float*>(stg + (nchunk % C::kStgBufs) * C::kStgBytes);
-            const long long tq1 = clock64();
-            if (issuer) bulk_wait_read<C::kStgBufs - 1>();
-            epi_bar_sync();
-            const long long tq2 = clock64();
+            float* sbuf = reinterpret_cast<float*>(stg_g);
+            if (issuer) bulk_wait_read<0>();
+            epi_bar_sync(grp);
             const int fl = wq * 32 + lane;
 #pragma unroll
             for (int c = 0; c < 32; ++c) sbuf[c * kBM + fl] = __uint_as_float(a[c]);
             fence_proxy_async_smem();
-            const long long tq3 = clock64();
-            epi_bar_sync();
-            const long long tq4 = clock64();
-            t_b1 += tq2 - tq1; t_sts += tq3 - tq2; t_b2 += tq4 - tq3;
+            epi_bar_sync(grp);
             if (p.tiled) {
               // one contiguous block in ys[split][d-pair][half][padded row][128]
               if (issuer) {
@@ -496,31 +508,30 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
               const int xid = lane < rows ? __ldg(p.fwd + ch.y + c0 + lane) : 0;
               if (p.scale_by_w && lane < rows) {
                 const float w = __ldg(p.topk_w + xid);
-                for (int q = 0; q < kBM; ++q) sbuf[lane * kBM + q] = __fmul_rn(sbuf[lane * kBM + q], w);
+                for (int qv = 0; qv < kBM; ++qv) sbuf[lane * kBM + qv] = __fmul_rn(sbuf[lane * kBM + qv], w);
                 fence_proxy_async_smem();
               }
               __syncwarp();
               for (int c = 0; c < rows; ++c) {
                 const int xc = __shfl_sync(0xffffffffu, xid, c);
-                const size_t orow = (p.dbg & 4) ? (size_t)(c & 31) : (size_t)xc;
-                if (lane == 0) bulk_store(out + orow * p.d + d0, sbuf + c * kBM, nvalid_d * 4);
+                if (lane == 0) bulk_store(p.ys + (size_t)xc * p.d + d0, sbuf + c * kBM, nvalid_d * 4);
               }
               if (lane == 0) bulk_commit();
             }
           }
         }
-        if (issuer && !(p.dbg & 8)) bulk_wait_all();
-        if (p.trace && issuer) {
-          p.trace[tile * 8 + 6] = (unsigned long long)t_ld;
-          p.trace[tile * 8 + 7] = (unsigned long long)(t_b1 + t_sts + t_b2);
+        if (my_last < 0) {  // this group had no chunk: still release TMEM
+          tc_fence_before();
+          mbar_arrive(tmem_empty);
         }
+        if (issuer) bulk_wait_all();
       }
-      if (p.trace && wq == 0 && lane == 0) p.trace[tile * 8 + 3] = globaltimer();
+      if (p.trace && warp == 4 && lane == 0) p.trace[tile * 8 + 3] = globaltimer();
       acc_phase ^= 1;
     }
   }
 
-  if (warp == 4 && lane == 0) bulk_wait_all();
+  if ((warp == 4 || warp == 8) && lane == 0) bulk_wait_all();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {

@@ -4,11 +4,13 @@
 
 #include <cudaTypedefs.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
 
 #include "common.cuh"
 #include "elementwise.cuh"
@@ -129,7 +131,7 @@ SegPlan plan_seg(const moe_b200_config& c, int64_t B) {
   q.n_kb = (c.hidden_dim + q.kr - 1) / q.kr;
   q.grid = q.n_tb * q.n_eb * q.n_kb;
   const size_t part = (size_t)(kSegThreads / 32) * kSegTT * q.expc * 16 + 64;  // warp partials
-  const size_t ph2 = (size_t)(kSegThreads / 32) * (c.num_experts * 16 + 256);
+  const size_t ph2 = (size_t)(kSegThreads / 32) * (c.num_experts * 16 + kChainWin * 8);
   q.smem = std::max(part, ph2);
   return q;
 }
@@ -239,6 +241,27 @@ int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 }
 
 // ------------------------------- launches --------------------------------------
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor finishes; it calls pdl_wait() before reading the
+// predecessor's outputs (common.cuh).  MOE_B200_NO_PDL=1 disables it.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  const char* env = getenv("MOE_B200_NO_PDL");
+  const bool disabled = env && atoi(env);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = disabled ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+
 unsigned long long* g_ffn_trace = nullptr;  // debug: per-tile timeline of the next ffn launches
 unsigned long long* g_router_trace = nullptr;  // debug: CTA-0 per-chunk router timeline
 struct RouterPlan {
@@ -308,21 +331,16 @@ int launch_ffn_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& 
     MOE_CUDA(cudaFuncSetAttribute(ffn_kernel<kBN, kV>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
-  ffn_kernel<kBN, kV><<<grid, kFfnThreads, C::kSmemBytes, s>>>(a, b, cm, dm, e, p);
-  MOE_LAUNCH_CHECK("ffn_kernel");
+  cudaError_t err = launch_pdl(ffn_kernel<kBN, kV>, dim3(grid), dim3(kFfnThreads), C::kSmemBytes, s, a, b, cm, dm, e, p);
+  if (err != cudaSuccess) return cuda_fail(err, "ffn launch");
   return MOE_B200_OK;
 }
 
 int launch_ffn_kernel(int bn, int variant, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm,
                       const CUtensorMap& dm, const CUtensorMap& e, const FfnParams& p, int grid,
                       cudaStream_t s) {
-  if (bn == 256) {
-    switch (variant) {
-      case 1: return launch_ffn_t<256, 1>(a, b, cm, dm, e, p, grid, s);
-      case 3: return launch_ffn_t<256, 3>(a, b, cm, dm, e, p, grid, s);
-      default: return launch_ffn_t<256, 2>(a, b, cm, dm, e, p, grid, s);
-    }
-  }
+  (void)variant;
+  if (bn == 256) return launch_ffn_t<256, 2>(a, b, cm, dm, e, p, grid, s);
   return launch_ffn_t<128, 2>(a, b, cm, dm, e, p, grid, s);
 }
 
@@ -428,6 +446,34 @@ int launch_router_exact(const moe_b200_config& c, int64_t B, const void* x, int 
 }
 
 
+int launch_combine(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, const float* topk_w, void* y,
+                   int y_dtype, cudaStream_t s) {
+  if (y_dtype != MOE_B200_DTYPE_F32 && y_dtype != MOE_B200_DTYPE_BF16) return MOE_B200_ERR_INVALID_VALUE;
+  const int d = c.hidden_dim, k = c.top_k;
+  const float* ys = reinterpret_cast<const float*>(ws8(ws) + L.ys);
+  const int32_t* prow = reinterpret_cast<const int32_t*>(ws8(ws) + L.prow);
+  const bool bf = y_dtype == MOE_B200_DTYPE_BF16;
+  const int S = L.splits;
+  cudaError_t e;
+  if (S <= 4 && k * S <= kCombineMaxKS) {
+    using K = void (*)(const float*, int, int, const int32_t*, const float*, void*, int, int, int);
+    K kern;
+    switch (S) {
+      case 1: kern = bf ? combine_token_kernel<true, 1> : combine_token_kernel<false, 1>; break;
+      case 2: kern = bf ? combine_token_kernel<true, 2> : combine_token_kernel<false, 2>; break;
+      case 3: kern = bf ? combine_token_kernel<true, 3> : combine_token_kernel<false, 3>; break;
+      default: kern = bf ? combine_token_kernel<true, 4> : combine_token_kernel<false, 4>; break;
+    }
+    e = launch_pdl(kern, dim3((unsigned)B), dim3(kRowThreads), 0, s, ys, L.n_dp, L.T_pad, prow, topk_w, y, (int)B, k, d);
+  } else {
+    const int grid = grid_for_rows((long)B * (d / 4));
+    e = launch_pdl(bf ? combine_tiled_kernel<true> : combine_tiled_kernel<false>, dim3(grid), dim3(kRowThreads), 0, s,
+                   ys, S, L.n_dp, L.T_pad, prow, topk_w, y, (int)B, k, d);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "combine launch");
+  return MOE_B200_OK;
+}
+
 int launch_dispatch(const moe_b200_config& c, int64_t B, const void* x, int xb, const int32_t* topk_idx,
                     int32_t* counts, int32_t* offsets, int32_t* fwd, int32_t* inv, int32_t* prow, int4* chunk_tab,
                     int32_t* n_chunks, void* xp, cudaStream_t s) {
@@ -442,8 +488,8 @@ int launch_dispatch(const moe_b200_config& c, int64_t B, const void* x, int xb, 
   const size_t smem = (size_t)(5 * c.num_experts + 3) * sizeof(int32_t);
   auto kern = xb ? dispatch_kernel<true> : dispatch_kernel<false>;
   if (smem > 48 * 1024) MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<grid, kDispThreads, smem, s>>>(q);
-  MOE_LAUNCH_CHECK("dispatch_kernel");
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kDispThreads), smem, s, q);
+  if (e != cudaSuccess) return cuda_fail(e, "dispatch launch");
   return MOE_B200_OK;
 }
 
@@ -461,6 +507,12 @@ void moe_b200_debug_set_ffn_trace(unsigned long long* dev_buf) { g_ffn_trace = d
 void moe_b200_debug_set_router_trace(unsigned long long* dev_buf) { g_router_trace = dev_buf; }
 
 const char* moe_b200_last_error_detail(void) { return g_last_error.c_str(); }
+
+// Debug hook (not part of the public header): byte offset of the certified
+// logit-interval buffer (float2 per (token, expert)) inside the workspace.
+size_t moe_b200_debug_lbuf_offset(const moe_b200_config* cfg, int64_t max_tokens) {
+  return layout_for(*cfg, max_tokens).lbuf;
+}
 
 const char* moe_b200_strerror(int status) {
   switch (status) {
@@ -556,6 +608,7 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
     p.tokc = kSegTT; p.expc = q.expc;
     p.n_eblocks = q.n_eb; p.n_tblocks = q.n_tb;
     p.kr = q.kr; p.seg_len = q.seg_len; p.n_kb = q.n_kb;
+    p.cert_coef = ldexp((2.0 + 12.0 / q.seg_len) * (1.0 + ldexp(1.0, -20)), -53);
     p.blk_counter = hdr + kHdrBlk;
     p.gpart = ws8(ws) + L.gpart;
     const bool wvec = (cfg->num_experts % 4) == 0;
@@ -679,16 +732,7 @@ static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, in
                        /*gu*/ true, /*dn*/ true, /*fused*/ true, s)))
     return rc;
   if ((rc = mark(3))) return rc;
-  const int d = cfg->hidden_dim;
-  const int grid = grid_for_rows((long)B * (d / 4));
-  const int32_t* prow = reinterpret_cast<const int32_t*>(ws8(ws) + L.prow);
-  if (y_dtype == MOE_B200_DTYPE_F32)
-    combine_tiled_kernel<false><<<grid, kRowThreads, 0, s>>>(ys, L.splits, L.n_dp, L.T_pad, prow, topk_w, y, (int)B, cfg->top_k, d);
-  else if (y_dtype == MOE_B200_DTYPE_BF16)
-    combine_tiled_kernel<true><<<grid, kRowThreads, 0, s>>>(ys, L.splits, L.n_dp, L.T_pad, prow, topk_w, y, (int)B, cfg->top_k, d);
-  else
-    return MOE_B200_ERR_INVALID_VALUE;
-  MOE_LAUNCH_CHECK("combine_tiled_kernel");
+  if ((rc = launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s))) return rc;
   return mark(4);
 }
 

@@ -30,6 +30,7 @@ namespace moe {
 
 constexpr int kRouterKC = 128;     // W64 padding granularity (max k-chunk)
 constexpr int kMaxExperts = 1024;
+constexpr int kChainWin = 128;  // exact fallback: steps per shared-memory product window
 
 struct RouterParams {
   const void* x;        // (B, d) fp32 or bf16
@@ -45,6 +46,7 @@ struct RouterParams {
   float2* lbuf;         // (B, E) certified logit interval {lo, hi} (fp32); lo = NaN: unknown
   int want_logits;      // 1: resolve every logit exactly and write `logits`
   int force_exact;      // test hook: certificates report "unknown" (exact fallback for every logit)
+  double cert_coef;     // segment kernel: D = A * cert_coef = u (2 + 12/L)(1 + 2^-20)
   int kr, seg_len, n_kb;// segment kernel: k-range per CTA, segment length, k-blocks
   int32_t* blk_counter; // (n_tblocks * n_eblocks) self-resetting (segment kernel)
   void* gpart;          // segment kernel: per (block, k-block, chain) {C_b, A_b} fp64
@@ -235,7 +237,7 @@ struct RouterSmem {
   }
   static __host__ __device__ size_t total_bytes(int tokc, int expc, int xb, int E, int nthreads, int stages, int kc) {
     size_t ph1 = stages * stage_bytes(tokc, expc, xb, kc) + 3 * stages * 8;
-    size_t ph2 = (size_t)(nthreads / 32) * (E * 16 + 256);  // scores row (fp64) + logit interval + window
+    size_t ph2 = (size_t)(nthreads / 32) * (E * 16 + kChainWin * 8);  // scores row (fp64) + logit interval + window
     return ph1 > ph2 ? ph1 : ph2;
   }
 };
@@ -291,39 +293,51 @@ MOE_DEVICE bool cta_arrive_last(int32_t* counter, int n) {
 // dependent fold on shuffled operands (identical result in all lanes).
 template <bool kXBf16>
 MOE_DEVICE float exact_chain_logit_warp(const RouterParams& p, int t, int e, int lane, double* win) {
-  // fma(x, w, a) == fl(x*w + a) because x*w is exact in fp64: lane j forms the
-  // product of step j of a 32-step window, the window goes through shared
-  // memory, and every lane folds it with broadcast loads (one DADD per step).
+  // fma(x, w, a) == fl(x*w + a) because x*w is exact in fp64: the lanes form
+  // the products of a 128-step window (4 each, operands loaded one window
+  // ahead), the window goes through shared memory, and every lane folds it
+  // with broadcast loads — one dependent DADD per step.
   const size_t xrow = (size_t)t * p.d;
-  const int nwin = (p.d + 31) / 32;
-  auto ld = [&](int w, float& xv, float& wv) {
-    const int k = w * 32 + lane;
-    xv = 0.0f;
-    wv = 0.0f;
-    if (w < nwin && k < p.d) {
-      if constexpr (kXBf16) xv = __bfloat162float(static_cast<const __nv_bfloat16*>(p.x)[xrow + k]);
-      else xv = __ldg(static_cast<const float*>(p.x) + xrow + k);
-      wv = __ldg(p.wr + (size_t)k * p.E + e);
+  const int nwin = (p.d + kChainWin - 1) / kChainWin;
+  // volatile loads with a memory clobber: issued where written (one window
+  // ahead), never sunk below the shared-memory fold of the current window
+  auto ld = [&](int w, float (&xv)[4], float (&wv)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = min(w * kChainWin + i * 32 + lane, p.d - 1);
+      if constexpr (kXBf16) {
+        unsigned short b;
+        asm volatile("ld.global.nc.u16 %0, [%1];"
+                     : "=h"(b) : "l"(static_cast<const __nv_bfloat16*>(p.x) + xrow + k) : "memory");
+        xv[i] = __uint_as_float(static_cast<uint32_t>(b) << 16);
+      } else {
+        asm volatile("ld.global.nc.f32 %0, [%1];"
+                     : "=f"(xv[i]) : "l"(static_cast<const float*>(p.x) + xrow + k) : "memory");
+      }
+      asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(wv[i]) : "l"(p.wr + (size_t)k * p.E + e) : "memory");
     }
   };
-  float x0, x1, x2, x3, w0, w1, w2, w3;
-  ld(0, x0, w0); ld(1, x1, w1); ld(2, x2, w2); ld(3, x3, w3);
+  float xa[4], wa[4], xb[4], wb[4];
+  ld(0, xa, wa);
   double acc = -0.0;  // fl(p + -0) == p, sign included, like fma(x, w, -0)
   for (int w = 0; w < nwin; ++w) {
-    float x4, w4;
-    ld(w + 4, x4, w4);
+    if (w + 1 < nwin) ld(w + 1, xb, wb);
     __syncwarp();
-    win[lane] = static_cast<double>(x0) * static_cast<double>(w0);
-    __syncwarp();
-    const int n = min(32, p.d - w * 32);
-    if (n == 32) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) acc = __dadd_rn(acc, win[j]);
+    for (int i = 0; i < 4; ++i) {
+      // steps past d (clamped loads) are never folded: n below stops at d
+      win[i * 32 + lane] = static_cast<double>(xa[i]) * static_cast<double>(wa[i]);
+    }
+    __syncwarp();
+    const int n = min(kChainWin, p.d - w * kChainWin);
+    if (n == kChainWin) {
+#pragma unroll
+      for (int j = 0; j < kChainWin; ++j) acc = __dadd_rn(acc, win[j]);
     } else {
       for (int j = 0; j < n; ++j) acc = __dadd_rn(acc, win[j]);
     }
-    x0 = x1; x1 = x2; x2 = x3; x3 = x4;
-    w0 = w1; w1 = w2; w2 = w3; w3 = w4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { xa[i] = xb[i]; wa[i] = wb[i]; }
   }
   __syncwarp();
   return __double2float_rn(acc);
@@ -348,7 +362,7 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
   const int tid = threadIdx.x;
   const int nwarps = blockDim.x / 32;
   const int warp = tid / 32, lane = tid % 32;
-  uint8_t* base = smem + (size_t)warp * (p.E * 16 + 256);
+  uint8_t* base = smem + (size_t)warp * (p.E * 16 + kChainWin * 8);
   double* row = reinterpret_cast<double*>(base);
   float* lo = reinterpret_cast<float*>(base + (size_t)p.E * 8);
   float* hi = lo + p.E;
@@ -549,6 +563,7 @@ router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
   const int d_pad = (p.d + kRouterKC - 1) / kRouterKC * kRouterKC;
   const int ntok = min(p.tokc, p.B - t0);  // valid token rows of this block
   if (p.trace && threadIdx.x == 0) p.trace[4096 * 4 + 2048 * 4 + blockIdx.x] = globaltimer_ns();
+  pdl_launch_dependents();
   if (tid == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(full + s, kRouterProducers + 1);

@@ -13,9 +13,15 @@
 // with C_s the prefix of the segment totals; the segment sums themselves err
 // by at most u * m_s.  Hence with
 //   A = sum_s (L_s |C_s| + m_s),   s^ = sum_s c_s
-// the reference value lies in [s^ - D, s^ + D] for D = 2^-50 (A + |s^|)
-// (a > 2x margin over the worst-case first-order bound; second-order terms
-// are O(d u) relative).  The fp32 rounding of every point of that interval
+// the reference value lies in [s^ - D, s^ + D] for D = u A (2 + 12/L)(1 + 2^-20):
+//   u A        bounds the reference fold's own rounding (|a_i| <= |C_s| + |b_j|),
+//   u sum m_s  (<= u A) the segment folds' rounding,
+//   u sum |C_node| over the merge tree (<= 5 warp-tree levels plus the
+//              sequential cross-warp / cross-k-block prefixes, each level
+//              <= 2A/L) the merges' rounding,
+// and (1 + 2^-20) covers the O(d u) second-order terms and the rounding of A
+// itself (tests/test_certificate.py restates this arithmetic in numpy and
+// checks it on random and adversarial inputs).  The fp32 rounding of every point of that interval
 // is the certified logit interval {lo, hi}; lo == hi almost always.  Phase 2
 // (router.cuh route_scores_tokens) checks whether the outputs depend on the
 // remaining uncertainty and recomputes only those logits with the exact
@@ -47,7 +53,7 @@ MOE_DEVICE void seg_finalize(const RouterParams& p, int t, int e, double s, doub
   if (!(A > 0.0) || !isfinite(s) || p.force_exact) {
     r = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));  // unknown: recompute exactly
   } else {
-    const double D = __dmul_ru(__dadd_ru(A, fabs(s)), 0x1p-50);
+    const double D = __dmul_ru(A, p.cert_coef);
     r = make_float2(__double2float_rn(__dsub_rd(s, D)), __double2float_rn(__dadd_ru(s, D)));
   }
   p.lbuf[(size_t)t * p.E + e] = r;
@@ -74,6 +80,8 @@ __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const Router
   const long long c_start = clock64();
   auto stamp = [&](int i) { if (tr && threadIdx.x == 0) tr[i] = clock64() - c_start; };
   if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[10] = smid_u32(); }
+
+  pdl_launch_dependents();  // the dispatch grid may queue up (it waits for this grid)
 
   // ------------------------------ phase 1 -----------------------------------
   double acc[TT][TE], mag[TT][TE];

@@ -23,27 +23,16 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(3):
     layer.forward(x, out)
 torch.cuda.synchronize()
-s = torch.cuda.Stream()
-# graph with the library's stage events inside
-lib = layer.lib
-ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-for e in ev:
-    e.record()
-torch.cuda.synchronize()
-arr = (ctypes.c_void_p * 5)(*[e.cuda_event for e in ev])
-xp, xdt = layer._prep_x(x)
-def fwd_timed():
-    rc = lib.moe_b200_forward_timed(ctypes.byref(layer.cfg), B, xp.data_ptr(), xdt, layer.router_weight.data_ptr(),
-        layer.weights.gate.data_ptr(), layer.weights.up.data_ptr(), layer.weights.down.data_ptr(), out.data_ptr(), 0,
-        layer.topk_idx.data_ptr(), layer.topk_w.data_ptr(), layer.counts.data_ptr(), layer.offsets.data_ptr(),
-        layer.fwd.data_ptr(), layer.inv.data_ptr(), layer.ws.data_ptr(), layer.ws_bytes, torch.cuda.current_stream().cuda_stream, arr)
-    assert rc == 0, rc
-g_plain = torch.cuda.CUDAGraph()
-with torch.cuda.graph(g_plain):
-    layer.forward(x, out)
-g_timed = torch.cuda.CUDAGraph()
-with torch.cuda.graph(g_timed):
-    fwd_timed()
+def capture(env):
+    for k_, v_ in env.items():
+        os.environ[k_] = v_
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        layer.forward(x, out)
+    for k_ in env:
+        os.environ.pop(k_, None)
+    return g
+variants = {"pdl": capture({}), "no_pdl": capture({"MOE_B200_NO_PDL": "1"})}
 torch.cuda.synchronize()
 def run(graph, n, do_flush):
     st = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
@@ -53,15 +42,12 @@ def run(graph, n, do_flush):
         st[i].record(); graph.replay(); en[i].record()
     torch.cuda.synchronize()
     return np.array([a.elapsed_time(b) for a, b in zip(st, en)]) * 1e3
-for _ in range(2):
-    a = run(g_plain, 30, True); b = run(g_plain, 30, False)
-    print(f"{name} B={B}: graph step us: flush med {np.median(a):.1f} min {a.min():.1f} | no-flush med {np.median(b):.1f} min {b.min():.1f}")
-names = ["route", "dispatch", "ffn", "combine"]
-acc = np.zeros(4)
-n = 20
-for i in range(n):
-    flush.zero_()
-    g_timed.replay()
-    torch.cuda.synchronize()
-    acc += np.array([ev[j].elapsed_time(ev[j + 1]) for j in range(4)]) * 1e3
-print("  in-graph stages us: " + " ".join(f"{nm}={v/n:.1f}" for nm, v in zip(names, acc)) + f" sum={acc.sum()/n:.1f}")
+res = {k: [] for k in variants}
+for rnd in range(8):  # alternate variants to cancel drift in clocks / power
+    for kname, g in variants.items():
+        res[kname].append(run(g, 10, True))
+line = f"{name} B={B}: graph step us (flush, alternating A/B):"
+for kname, v in res.items():
+    v = np.concatenate(v)
+    line += f" {kname} med {np.median(v):.1f} min {v.min():.1f} |"
+print(line)

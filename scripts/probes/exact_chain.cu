@@ -5,7 +5,7 @@
 #include "../../paper_2605_23911_b200/csrc/router.cuh"
 using namespace moe;
 __global__ void probe(RouterParams p, long long* cyc, float* out) {
-  __shared__ double win[32];
+  __shared__ double win[kChainWin];
   const int lane = threadIdx.x;
   long long t0 = clock64();
   float v = exact_chain_logit_warp<true>(p, 3, 5, lane, win);
