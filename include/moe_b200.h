@@ -146,6 +146,43 @@ int moe_b200_forward_timed(const moe_b200_config* cfg, int64_t num_tokens, const
                            int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
                            void* ws, size_t ws_bytes, void* stream, void** events);
 
+/* --------------------- host-buffer (end-to-end) forward ---------------------
+ * The reference API takes and returns host arrays (pipeline.py:572-578:
+ * numpy in, numpy out).  An I/O context owns double-buffered device staging
+ * for x and y and two copy streams, so that consecutive calls overlap the
+ * host<->device copies of one batch with the compute of its neighbours:
+ *   copy-in stream:  x_host -> x_dev[i % 2]      (waits for batch i-2's dispatch)
+ *   compute stream:  moe_b200_forward(x_dev, y_dev[i % 2])  (waits for copy-in
+ *                    and for batch i-2's copy-out of y_dev)
+ *   copy-out stream: y_dev[i % 2] -> y_host       (waits for the compute)
+ * x_host / y_host should be pinned (page-locked) for the copies to be
+ * asynchronous; the caller keeps them untouched until moe_b200_io_sync.
+ * The context allocates its staging buffers once (moe_b200_io_create); the
+ * forward path itself never allocates. */
+typedef struct moe_b200_io moe_b200_io;
+
+int moe_b200_io_create(const moe_b200_config* cfg, int64_t max_tokens, int x_dtype, int y_dtype,
+                       moe_b200_io** io);
+int moe_b200_io_destroy(moe_b200_io* io);
+
+/* Asynchronous: returns once the copies and launches are enqueued. */
+int moe_b200_forward_host(moe_b200_io* io, int64_t num_tokens, const void* x_host, void* y_host,
+                          const float* w_router, const void* w_gate, const void* w_up,
+                          const void* w_down, int32_t* topk_idx, float* topk_w, int32_t* counts,
+                          int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv, void* ws,
+                          size_t ws_bytes, void* stream);
+
+/* Record `event` (a cudaEvent_t) on the copy-out stream after the last
+ * enqueued batch's y copy; make both copy streams wait for `event` (e.g. a
+ * timing start recorded on the compute stream); wait for everything. */
+int moe_b200_io_record(moe_b200_io* io, void* event);
+int moe_b200_io_wait(moe_b200_io* io, void* event);
+int moe_b200_io_sync(moe_b200_io* io);
+
+/* Number of kernel launches one moe_b200_forward of `num_tokens` tokens makes
+ * (router [+ weight prep], dispatch, FFN, combine). */
+int moe_b200_launches_per_forward(const moe_b200_config* cfg, int64_t num_tokens);
+
 /* ---------------------------- expert parallelism ------------------------------
  * The reference has no multi-GPU path ("planned
  * follow-up").  These two entry points are the local compute of an

@@ -47,7 +47,7 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # Device-facing symbols import torch lazily so host-only users (trace,
     # types) do not pay for it.
-    if name in ("MoELayer", "DeviceExpertWeights", "upload_weights", "moe_forward", "route"):
+    if name in ("MoELayer", "HostPipeline", "DeviceExpertWeights", "upload_weights", "moe_forward", "route"):
         from . import layer
 
         return getattr(layer, name)

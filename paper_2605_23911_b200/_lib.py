@@ -67,6 +67,13 @@ SIGNATURES = {
     "moe_b200_gather_rows": (_INT, [_I64, _I64, _P, _P, _P, _P]),
     "moe_b200_combine_rows": (_INT, [_CFG, _I64, _P, _P, _P, _P, _INT, _P]),
     "moe_b200_read_flags": (_INT, [_CFG, _I64, _P, _SZ, ctypes.POINTER(ctypes.c_uint32), _P]),
+    "moe_b200_io_create": (_INT, [_CFG, _I64, _INT, _INT, ctypes.POINTER(ctypes.c_void_p)]),
+    "moe_b200_io_destroy": (_INT, [_P]),
+    "moe_b200_forward_host": (_INT, [_P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_io_record": (_INT, [_P, _P]),
+    "moe_b200_io_wait": (_INT, [_P, _P]),
+    "moe_b200_launches_per_forward": (_INT, [_CFG, _I64]),
+    "moe_b200_io_sync": (_INT, [_P]),
     "moe_b200_strerror": (ctypes.c_char_p, [_INT]),
     "moe_b200_last_error_detail": (ctypes.c_char_p, []),
     "moe_b200_version": (ctypes.c_char_p, []),

@@ -714,7 +714,7 @@ static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, in
   if ((rc = check_ws(cfg, B, ws, ws_bytes, &L))) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto mark = [&](int i) -> int {
-    if (events) MOE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s));
+    if (events && events[i]) MOE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s));
     return MOE_B200_OK;
   };
   if ((rc = mark(0))) return rc;
@@ -752,6 +752,132 @@ int moe_b200_forward_timed(const moe_b200_config* cfg, int64_t B, const void* x,
                            void* ws, size_t ws_bytes, void* stream, void** events) {
   return forward_impl(cfg, B, x, x_dtype, w_router, w_gate, w_up, w_down, y, y_dtype, topk_idx, topk_w, counts,
                       offsets, perm_fwd, perm_inv, ws, ws_bytes, stream, events);
+}
+
+// ----------------------- host-buffer (end-to-end) forward -----------------------
+
+}  // extern "C"
+
+struct moe_b200_io {
+  moe_b200_config cfg;
+  int64_t max_tokens;
+  int x_dtype, y_dtype;
+  size_t x_bytes, y_bytes;
+  void* x_dev[2];
+  void* y_dev[2];
+  cudaStream_t s_in, s_out;
+  cudaEvent_t in_done[2], disp_done[2], comp_done[2], out_done[2];
+  int64_t count;
+};
+
+extern "C" {
+
+int moe_b200_io_create(const moe_b200_config* cfg, int64_t max_tokens, int x_dtype, int y_dtype,
+                       moe_b200_io** io_out) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (!io_out || max_tokens < 1) return MOE_B200_ERR_INVALID_VALUE;
+  if ((x_dtype != MOE_B200_DTYPE_F32 && x_dtype != MOE_B200_DTYPE_BF16) ||
+      (y_dtype != MOE_B200_DTYPE_F32 && y_dtype != MOE_B200_DTYPE_BF16))
+    return MOE_B200_ERR_INVALID_VALUE;
+  moe_b200_io* io = new moe_b200_io{};
+  io->cfg = *cfg;
+  io->max_tokens = max_tokens;
+  io->x_dtype = x_dtype;
+  io->y_dtype = y_dtype;
+  io->x_bytes = (size_t)max_tokens * cfg->hidden_dim * (x_dtype == MOE_B200_DTYPE_BF16 ? 2 : 4);
+  io->y_bytes = (size_t)max_tokens * cfg->hidden_dim * (y_dtype == MOE_B200_DTYPE_BF16 ? 2 : 4);
+  auto fail = [&](cudaError_t e, const char* what) {
+    moe_b200_io_destroy(io);
+    return cuda_fail(e, what);
+  };
+  cudaError_t e;
+  for (int i = 0; i < 2; ++i) {
+    if ((e = cudaMalloc(&io->x_dev[i], io->x_bytes)) != cudaSuccess) return fail(e, "io x staging");
+    if ((e = cudaMalloc(&io->y_dev[i], io->y_bytes)) != cudaSuccess) return fail(e, "io y staging");
+    for (cudaEvent_t* ev : {&io->in_done[i], &io->disp_done[i], &io->comp_done[i], &io->out_done[i]})
+      if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e, "io event");
+  }
+  if ((e = cudaStreamCreateWithFlags(&io->s_in, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "io stream");
+  if ((e = cudaStreamCreateWithFlags(&io->s_out, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "io stream");
+  *io_out = io;
+  return MOE_B200_OK;
+}
+
+int moe_b200_io_destroy(moe_b200_io* io) {
+  if (!io) return MOE_B200_OK;
+  if (io->s_in) cudaStreamSynchronize(io->s_in);
+  if (io->s_out) cudaStreamSynchronize(io->s_out);
+  for (int i = 0; i < 2; ++i) {
+    if (io->x_dev[i]) cudaFree(io->x_dev[i]);
+    if (io->y_dev[i]) cudaFree(io->y_dev[i]);
+    for (cudaEvent_t ev : {io->in_done[i], io->disp_done[i], io->comp_done[i], io->out_done[i]})
+      if (ev) cudaEventDestroy(ev);
+  }
+  if (io->s_in) cudaStreamDestroy(io->s_in);
+  if (io->s_out) cudaStreamDestroy(io->s_out);
+  delete io;
+  return MOE_B200_OK;
+}
+
+int moe_b200_forward_host(moe_b200_io* io, int64_t B, const void* x_host, void* y_host, const float* w_router,
+                          const void* w_gate, const void* w_up, const void* w_down, int32_t* topk_idx,
+                          float* topk_w, int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
+                          void* ws, size_t ws_bytes, void* stream) {
+  if (!io) return MOE_B200_ERR_INVALID_VALUE;
+  if (B < 0 || B > io->max_tokens) return MOE_B200_ERR_SHAPE_MISMATCH;
+  if (B > 0 && (!x_host || !y_host)) return MOE_B200_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int slot = static_cast<int>(io->count & 1);
+  const size_t xb = (size_t)B * io->cfg.hidden_dim * (io->x_dtype == MOE_B200_DTYPE_BF16 ? 2 : 4);
+  const size_t yb = (size_t)B * io->cfg.hidden_dim * (io->y_dtype == MOE_B200_DTYPE_BF16 ? 2 : 4);
+  const bool reuse = io->count >= 2;  // this slot's buffers were used by batch count-2
+  // copy-in: x_dev[slot] is free once batch count-2's router + dispatch read it
+  if (reuse) MOE_CUDA(cudaStreamWaitEvent(io->s_in, io->disp_done[slot], 0));
+  if (xb) MOE_CUDA(cudaMemcpyAsync(io->x_dev[slot], x_host, xb, cudaMemcpyHostToDevice, io->s_in));
+  MOE_CUDA(cudaEventRecord(io->in_done[slot], io->s_in));
+  // compute: after the copy-in, and after batch count-2's copy-out released y_dev[slot]
+  MOE_CUDA(cudaStreamWaitEvent(s, io->in_done[slot], 0));
+  if (reuse) MOE_CUDA(cudaStreamWaitEvent(s, io->out_done[slot], 0));
+  // events[2] is recorded after the dispatch (the last reader of x)
+  void* evs[5] = {nullptr, nullptr, io->disp_done[slot], nullptr, nullptr};
+  int rc = forward_impl(&io->cfg, B, io->x_dev[slot], io->x_dtype, w_router, w_gate, w_up, w_down,
+                        io->y_dev[slot], io->y_dtype, topk_idx, topk_w, counts, offsets, perm_fwd, perm_inv, ws,
+                        ws_bytes, stream, evs);
+  if (rc) return rc;
+  MOE_CUDA(cudaEventRecord(io->comp_done[slot], s));
+  // copy-out
+  MOE_CUDA(cudaStreamWaitEvent(io->s_out, io->comp_done[slot], 0));
+  if (yb) MOE_CUDA(cudaMemcpyAsync(y_host, io->y_dev[slot], yb, cudaMemcpyDeviceToHost, io->s_out));
+  MOE_CUDA(cudaEventRecord(io->out_done[slot], io->s_out));
+  ++io->count;
+  return MOE_B200_OK;
+}
+
+int moe_b200_io_record(moe_b200_io* io, void* event) {
+  if (!io || !event) return MOE_B200_ERR_INVALID_VALUE;
+  MOE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(event), io->s_out));
+  return MOE_B200_OK;
+}
+
+int moe_b200_io_wait(moe_b200_io* io, void* event) {
+  if (!io || !event) return MOE_B200_ERR_INVALID_VALUE;
+  MOE_CUDA(cudaStreamWaitEvent(io->s_in, static_cast<cudaEvent_t>(event), 0));
+  MOE_CUDA(cudaStreamWaitEvent(io->s_out, static_cast<cudaEvent_t>(event), 0));
+  return MOE_B200_OK;
+}
+
+int moe_b200_launches_per_forward(const moe_b200_config* cfg, int64_t B) {
+  if (check_config(cfg)) return -1;
+  if (B <= 0) return 0;
+  return B <= seg_max_tokens(*cfg) ? 4 : 5;  // segment router | weight prep + exact router
+}
+
+int moe_b200_io_sync(moe_b200_io* io) {
+  if (!io) return MOE_B200_ERR_INVALID_VALUE;
+  MOE_CUDA(cudaStreamSynchronize(io->s_in));
+  MOE_CUDA(cudaStreamSynchronize(io->s_out));
+  return MOE_B200_OK;
 }
 
 // --------------------------- expert parallelism --------------------------------

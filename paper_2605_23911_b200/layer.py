@@ -171,6 +171,16 @@ class MoELayer:
 
     __call__ = forward
 
+    # -- host buffers in, host buffers out (pipelined across calls) -------------
+    def host_pipeline(self, x_dtype=torch.bfloat16, y_dtype=None) -> "HostPipeline":
+        """I/O context for ``forward_host``: the reference API's numpy-in /
+        numpy-out contract (``pipeline.py:572-578``) with the host<->device
+        copies of consecutive batches overlapped with the compute."""
+        return HostPipeline(self, x_dtype, y_dtype or self.out_dtype)
+
+    def launches_per_forward(self, num_tokens: int) -> int:
+        return int(self.lib.moe_b200_launches_per_forward(ctypes.byref(self.cfg), int(num_tokens)))
+
     def read_flags(self) -> int:
         """Device non-finite flags (synchronises); clears them."""
         v = ctypes.c_uint32(0)
@@ -292,6 +302,66 @@ class MoELayer:
             for i, n in enumerate(names):
                 tot[n] += ev[i].elapsed_time(ev[i + 1])
         return {n: v / iters for n, v in tot.items()}
+
+
+class HostPipeline:
+    """Double-buffered host-buffer forward over ``moe_b200_forward_host``.
+
+    ``submit(x_host, y_host)`` enqueues: copy x (pinned host, (B, d)) in on a
+    copy stream, run the layer on the current stream, copy y out on a second
+    copy stream; it returns immediately.  Batch i's copies overlap batch i+-1's
+    compute.  ``sync()`` waits for every submitted batch.  Keep x_host/y_host
+    untouched until ``sync``.
+    """
+
+    def __init__(self, layer: "MoELayer", x_dtype, y_dtype):
+        self.layer = layer
+        if layer.dp != layer.d:
+            raise ShapeMismatch("host pipeline needs hidden_dim % 8 == 0 (no padding)")
+        self.x_dtype, self.y_dtype = x_dtype, y_dtype
+        xdt = _lib.DTYPE_BF16 if x_dtype == torch.bfloat16 else _lib.DTYPE_F32
+        ydt = _lib.DTYPE_BF16 if y_dtype == torch.bfloat16 else _lib.DTYPE_F32
+        h = ctypes.c_void_p(0)
+        _lib.check(layer.lib.moe_b200_io_create(ctypes.byref(layer.cfg), layer.max_tokens, xdt, ydt,
+                                                ctypes.byref(h)), "io_create")
+        self._io = h
+
+    def submit(self, x_host: torch.Tensor, y_host: torch.Tensor) -> None:
+        L = self.layer
+        if x_host.dim() != 2 or x_host.shape[1] != L.d or x_host.dtype != self.x_dtype:
+            raise ShapeMismatch(f"x_host must be (B, {L.d}) {self.x_dtype}")
+        B = x_host.shape[0]
+        if tuple(y_host.shape) != (B, L.d) or y_host.dtype != self.y_dtype:
+            raise ShapeMismatch(f"y_host must be ({B}, {L.d}) {self.y_dtype}")
+        rc = L.lib.moe_b200_forward_host(
+            self._io, B, _ptr(x_host), _ptr(y_host), _ptr(L.router_weight), _ptr(L.weights.gate),
+            _ptr(L.weights.up), _ptr(L.weights.down), _ptr(L.topk_idx), _ptr(L.topk_w), _ptr(L.counts),
+            _ptr(L.offsets), _ptr(L.fwd), _ptr(L.inv), _ptr(L.ws), L.ws_bytes, _stream_ptr(L.device))
+        _lib.check(rc, "moe_b200_forward_host")
+
+    def record(self, event: torch.cuda.Event) -> None:
+        """Record ``event`` after the last submitted batch's output copy."""
+        if not event.cuda_event:
+            event.record()  # materialise the underlying cudaEvent_t (re-recorded below)
+        _lib.check(self.layer.lib.moe_b200_io_record(self._io, event.cuda_event), "io_record")
+
+    def wait(self, event: torch.cuda.Event) -> None:
+        """Make the copy streams wait for ``event`` (e.g. a timing start)."""
+        _lib.check(self.layer.lib.moe_b200_io_wait(self._io, event.cuda_event), "io_wait")
+
+    def sync(self) -> None:
+        _lib.check(self.layer.lib.moe_b200_io_sync(self._io), "io_sync")
+
+    def close(self) -> None:
+        if self._io:
+            self.layer.lib.moe_b200_io_destroy(self._io)
+            self._io = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 from .types import Gating  # noqa: E402  (used in MoELayer.__init__)

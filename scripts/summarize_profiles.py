@@ -45,7 +45,7 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__cycles_elapsed.avg.per_second", "launch__grid_size", "launch__block_size",
            "launch__registers_per_thread", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"]
 traffic = {}
-for kern in ("ffn", "router"):
+for kern in ("ffn", "router", "router_seg", "dispatch", "combine_token"):
     rep = os.path.join(G, f"prof_{kern}_{tag}.ncu-rep")
     if not os.path.exists(rep):
         continue

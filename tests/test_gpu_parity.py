@@ -299,3 +299,27 @@ def test_expert_parallel_single_rank_matches_layer_bitwise(pkg):
     ep = ExpertParallelMoE(cfg, wr, w, max_tokens=b)
     y = _np(ep.forward(x))
     bits_equal(y, y_ref)
+
+
+def test_host_pipeline_matches_device_forward_bitwise(pkg):
+    """moe_b200_forward_host (pinned host buffers, copies overlapped with the
+    neighbouring batches' compute) returns exactly the device forward's bits,
+    batch after batch, including a short final batch."""
+    P = pkg
+    e, k, d, f = 8, 2, 512, 1024
+    cfg = _cfg(P, e, k, d, f, "softmax")
+    tokens, wr, gate, up, down = O.make_instance(5, e, k, d, f, 64)
+    layer = _layer(P, cfg, wr, gate, up, down, 64)
+    pipe = layer.host_pipeline(x_dtype=torch.bfloat16, y_dtype=torch.float32)
+    gen = torch.Generator().manual_seed(11)
+    sizes = [64, 64, 37, 64, 1]
+    xs = [torch.randn((b, d), generator=gen).to(torch.bfloat16).pin_memory() for b in sizes]
+    ys = [torch.empty((b, d), dtype=torch.float32).pin_memory() for b in sizes]
+    for x, y in zip(xs, ys):
+        pipe.submit(x, y)
+    pipe.sync()
+    for x, y in zip(xs, ys):
+        ref = layer.forward(x.cuda())
+        torch.cuda.synchronize()
+        bits_equal(y.numpy(), _np(ref))
+    pipe.close()
