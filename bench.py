@@ -212,9 +212,26 @@ def ours_arm(args, cfg_name):
     out = torch.empty((B, d), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
+    # routing-skew workload (BASELINE configs[4]): the reference harness's Zipf
+    # table (skew.synthesize_routing, rank r -> expert r, weights 1/k) replaces
+    # the router output; the router projection still runs
+    skew = None
+    if args.zipf is not None:
+        from paper_2605_23911_b200.skew import SkewSpec, imbalance_metrics, synthesize_routing
+
+        spec = SkewSpec.for_alpha(args.zipf, 1234 + rank, B, cfg)
+        rt = synthesize_routing(spec)
+        routed = (torch.from_numpy(rt.indices.astype(np.int32)).to(dev), torch.from_numpy(rt.weights).to(dev))
+        m = imbalance_metrics(np.bincount(rt.indices.reshape(-1), minlength=E))
+        skew = {"distribution": spec.distribution, "alpha": args.zipf, "seed": spec.seed,
+                "max_over_mean": m.max_over_mean, "gini": m.gini, "active_experts": m.active_experts}
+        run = lambda xx, oo: layer.forward_routed(xx, routed, oo)  # noqa: E731
+    else:
+        run = lambda xx, oo: layer.forward(xx, oo)  # noqa: E731
+
     # warm-up (also JIT-free: the library is prebuilt), then capture the one-call forward
     for _ in range(max(3, args.warmup)):
-        layer.forward(x, out)
+        run(x, out)
     torch.cuda.synchronize(dev)
     # L2 policy between timed steps: flush (write 256 MB > 126 MB L2) unless the
     # expert weights streamed per step are >= 16x L2, i.e. inputs larger than
@@ -228,7 +245,7 @@ def ours_arm(args, cfg_name):
                f"no flush: inputs larger than L2 (streamed expert weights {streamed / 1e9:.2f} GB/step >= 16x the 126 MB L2)")
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph):
-        layer.forward(x, out)
+        run(x, out)
     for _ in range(3):
         graph.replay()
     torch.cuda.synchronize(dev)
@@ -283,32 +300,17 @@ def ours_arm(args, cfg_name):
     # back to pinned host memory inside the timed region; consecutive steps
     # overlap those copies with the neighbouring steps' compute (two device
     # staging slots, dedicated copy streams), as a serving loop does.
-    n_slots = 2
-    x_host = [x.cpu().pin_memory() for _ in range(n_slots)]
-    y_host = [torch.empty((B, d), dtype=torch.float32).pin_memory() for _ in range(n_slots)]
-    pipe = layer.host_pipeline(x_dtype=torch.bfloat16, y_dtype=torch.float32)
-    for i in range(4):
-        pipe.submit(x_host[i % n_slots], y_host[i % n_slots])
-    pipe.sync()
-    e2e_steps = max(5, min(args.steps, 50))
-    e_start = torch.cuda.Event(enable_timing=True)
-    e_end = torch.cuda.Event(enable_timing=True)
-    if flush_between:
-        flush.zero_()
-    torch.cuda.synchronize(dev)
-    e_start.record()
-    pipe.wait(e_start)  # the copy streams start after the timing start
-    for i in range(e2e_steps):
-        pipe.submit(x_host[i % n_slots], y_host[i % n_slots])
-    pipe.record(e_end)
-    pipe.sync()
-    e_end.synchronize()
-    e2e_ms = e_start.elapsed_time(e_end)
-    pipe.close()
+    if skew is not None:
+        e2e_ms, e2e_steps, e2e_path = _e2e_serial(args, x, out, run, flush if flush_between else None, dev)
+    else:
+        e2e_ms, e2e_steps, e2e_path = _e2e_pipelined(args, layer, x, B, d, flush if flush_between else None, dev)
 
     # dominant kernel (the fused expert-FFN launch) timed live inside the real
     # forward: CUDA events recorded by the library between its launches
-    stages = layer.timed_forward(x, iters=max(5, min(args.steps, 20)), flush=flush if flush_between else None)
+    if skew is None:
+        stages = layer.timed_forward(x, iters=max(5, min(args.steps, 20)), flush=flush if flush_between else None)
+    else:  # routed path: no per-stage events; the FFN share comes from the launch list
+        stages = {"ffn": ms_per_step_estimate(total_ms, args.steps)}
     counts = layer.counts.cpu().numpy().astype(np.int64)
 
     t = torch.tensor([total_ms, e2e_ms / e2e_steps], dtype=torch.float64, device=dev)
@@ -345,9 +347,7 @@ def ours_arm(args, cfg_name):
                        "timing": timing_desc},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * d * 2,
                     "d2h_bytes_per_step": B * d * 4,
-                    "path": "moe_b200_forward_host (C-ABI, pinned host buffers): per step H2D tokens + layer + D2H "
-                            "output, copies overlapped with neighbouring steps' compute (double-buffered staging)",
-                    "steps": e2e_steps},
+                    "path": e2e_path, "steps": e2e_steps},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "kernel": "ffn_kernel (fused gate+up SiLU*up and K-split down, one persistent launch)",
@@ -367,10 +367,71 @@ def ours_arm(args, cfg_name):
         line["layer_roofline_frac"] = t_roof / (ms_per_step / 1e3)
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline_leg(x, wr, gate, up, down, E, k, gating, B)
+        if skew is not None:
+            line["config"]["routing"] = skew
+            line["config"]["workload"] += f", Zipf routing override alpha={args.zipf}"
+            line["roofline"]["kernel"] = "whole routed layer (router projection + dispatch + FFN + combine)"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _e2e_pipelined(args, layer, x, B, d, flush, dev):
+    """e2e through moe_b200_forward_host: every step copies its tokens in from
+    pinned host memory and its output back inside the timed region; the copies
+    overlap the neighbouring steps' compute (two staging slots, copy streams)."""
+    import torch
+
+    n_slots = 2
+    x_host = [x.cpu().pin_memory() for _ in range(n_slots)]
+    y_host = [torch.empty((B, d), dtype=torch.float32).pin_memory() for _ in range(n_slots)]
+    pipe = layer.host_pipeline(x_dtype=torch.bfloat16, y_dtype=torch.float32)
+    for i in range(4):
+        pipe.submit(x_host[i % n_slots], y_host[i % n_slots])
+    pipe.sync()
+    steps = max(5, min(args.steps, 50))
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    if flush is not None:
+        flush.zero_()
+    torch.cuda.synchronize(dev)
+    e_start.record()
+    pipe.wait(e_start)  # the copy streams start after the timing start
+    for i in range(steps):
+        pipe.submit(x_host[i % n_slots], y_host[i % n_slots])
+    pipe.record(e_end)
+    pipe.sync()
+    e_end.synchronize()
+    ms = e_start.elapsed_time(e_end)
+    pipe.close()
+    return ms, steps, ("moe_b200_forward_host (C-ABI, pinned host buffers): per step H2D tokens + layer + D2H "
+                       "output, copies overlapped with neighbouring steps' compute (double-buffered staging)")
+
+
+def _e2e_serial(args, x, out, run, flush, dev):
+    """e2e with the copies serialised around each step (routing-override path)."""
+    import torch
+
+    x_host = x.cpu().pin_memory()
+    y_host = torch.empty(tuple(out.shape), dtype=out.dtype).pin_memory()
+    x_dev = torch.empty_like(x)
+    steps = max(5, min(args.steps, 50))
+    ms = 0.0
+    for i in range(steps + 2):
+        if flush is not None:
+            flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        x_dev.copy_(x_host, non_blocking=True)
+        run(x_dev, out)
+        y_host.copy_(out, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        if i >= 2:
+            ms += e0.elapsed_time(e1)
+    return ms, steps, "C-ABI forward_routed with pinned-host tokens copied in and output copied out, serialised"
 
 
 def ep_arm(args, cfg, label, B, world, rank, dev):
@@ -430,6 +491,10 @@ def ep_arm(args, cfg, label, B, world, rank, dev):
     return 0
 
 
+def ms_per_step_estimate(total_ms, steps):
+    return total_ms / steps
+
+
 def cpu_baseline_leg(x, wr, gate, up, down, E, k, gating, B):
     from oracle.cpu_baseline import host_cores
 
@@ -452,6 +517,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="mixtral")
     ap.add_argument("--tokens", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--zipf", type=float, default=None,
+                    help="routing-skew workload: override routing with the Zipf(alpha) table (0 = uniform)")
     ap.add_argument("--l2-flush", choices=("auto", "always", "never"), default="auto",
                     help="flush L2 between timed steps (auto: unless streamed weights >= 16x L2)")
     args = ap.parse_args()

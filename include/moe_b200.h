@@ -71,6 +71,7 @@ typedef struct moe_b200_config {
 /* Device-side status bits, readable with moe_b200_read_flags. */
 #define MOE_B200_FLAG_NONFINITE_TOKENS 1u
 #define MOE_B200_FLAG_NONFINITE_ROUTER 2u
+#define MOE_B200_FLAG_INDEX_OUT_OF_RANGE 4u
 
 /* Bytes of workspace needed for up to `max_tokens` tokens.  The workspace
  * holds the router logits, schedule tables, the permuted bf16 tokens, the
@@ -136,6 +137,20 @@ int moe_b200_forward(const moe_b200_config* cfg, int64_t num_tokens, const void*
                      const void* w_down, void* y, int y_dtype, int32_t* topk_idx, float* topk_w,
                      int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
                      void* ws, size_t ws_bytes, void* stream);
+
+/* Whole layer with the routing given (the paper's router override for the
+ * routing-skew study; tables from moeperf/skew.py:74-105):
+ * topk_idx (B, k) int32 and topk_w (B, k) fp32 are INPUTS on the device.
+ * Runs dispatch (histogram, offsets, stable permutation, schedule, gather),
+ * the fused FFN and the combine.  If w_router is non-NULL the router kernel
+ * also runs (its result is discarded), so a timing includes the projection as
+ * in the paper's experiment.  Indices outside [0, E) set
+ * MOE_B200_FLAG_INDEX_OUT_OF_RANGE and those rows are dropped. */
+int moe_b200_forward_routed(const moe_b200_config* cfg, int64_t num_tokens, const void* x, int x_dtype,
+                            const int32_t* topk_idx, const float* topk_w, const float* w_router,
+                            const void* w_gate, const void* w_up, const void* w_down, void* y,
+                            int y_dtype, int32_t* counts, int32_t* offsets, int32_t* perm_fwd,
+                            int32_t* perm_inv, void* ws, size_t ws_bytes, void* stream);
 
 /* Same as moe_b200_forward, recording five cudaEvent_t (events[0..4]) on
  * `stream` around the stages: [route | permute | fused FFN | combine].  Used

@@ -34,7 +34,9 @@ struct DispatchParams {
   int32_t* inv;             // (T) expanded id -> permuted row
   int32_t* prow;            // (T) expanded id -> padded permuted row (experts start 16-aligned)
   int4* chunk_tab;          // {expert, row0, nrows, padded row0}
+  int2* chunk_grp;          // {first chunk of the expert, chunks of the expert}
   int32_t* n_chunks;        // [1]
+  uint32_t* flags;          // bit 4: an index outside [0, E) (row dropped)
 };
 
 template <bool kXBf16>
@@ -94,13 +96,17 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
     for (int u = 0; u < U; ++u) {
       const int i = base0 + u * kDispThreads + lane;
       ev[u] = i < p.T ? __ldg(p.topk_idx + i) : -1 - lane;
+      if (i < p.T && (ev[u] < 0 || ev[u] >= p.E)) {  // routing override out of range: drop the row
+        if (blockIdx.x == 0 && p.flags) atomicOr(p.flags, 4u);
+        ev[u] = -1 - lane;
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = base0 + u * kDispThreads + lane;
       const uint32_t peers = __match_any_sync(0xffffffffu, ev[u]);
       const uint32_t peers_before = peers & __ballot_sync(0xffffffffu, i < r0);
-      if (i < p.T && (__ffs(peers) - 1) == lane) {
+      if (i < p.T && ev[u] >= 0 && (__ffs(peers) - 1) == lane) {
         atomicAdd(&tot[ev[u]], __popc(peers));
         if (peers_before) atomicAdd(&before[ev[u]], __popc(peers_before));
       }
@@ -142,9 +148,11 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
       p.counts[e] = tot[e];
       p.offsets[e] = off[e];
       const int n = tot[e];
-      for (int c = 0; c * p.chunk_rows < n; ++c) {
+      const int nch_e = (n + p.chunk_rows - 1) / p.chunk_rows;
+      for (int c = 0; c < nch_e; ++c) {
         const int rr = c * p.chunk_rows;
         p.chunk_tab[cpre[e] + c] = make_int4(e, off[e] + rr, min(p.chunk_rows, n - rr), off16[e] + rr);
+        p.chunk_grp[cpre[e] + c] = make_int2(cpre[e], nch_e);
       }
     }
     if (tid == 0) {
@@ -156,15 +164,21 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
   if (warp == 0) {
     const int i = r0 + lane;
     const bool valid = lane < kDispRows && i < r1;
-    const int e = valid ? __ldg(p.topk_idx + i) : -1 - lane;
+    int e = valid ? __ldg(p.topk_idx + i) : -1 - lane;
+    if (e < 0 || e >= p.E) e = -1 - lane;
     const uint32_t peers = __match_any_sync(0xffffffffu, e);
-    if (valid) {
+    if (valid && e >= 0) {
       const int rank = before[e] + __popc(peers & ((1u << lane) - 1u));
       const int pos = off[e] + rank;
       p.fwd[pos] = i;
       p.inv[i] = pos;
       p.prow[i] = off16[e] + rank;
       s_pos[lane] = pos;
+      s_tok[lane] = i / p.k;
+    } else if (valid) {  // dropped (out-of-range override index): in-bounds placeholders
+      p.inv[i] = -1;
+      p.prow[i] = 0;
+      s_pos[lane] = -1;
       s_tok[lane] = i / p.k;
     }
   }
@@ -174,7 +188,7 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
 #pragma unroll
   for (int u = 0; u < kPre; ++u) {
     const int v = tid + u * kDispThreads;
-    if (v < nvec) reinterpret_cast<int4*>(p.xp + (size_t)s_pos[v / vpr] * p.d)[v % vpr] = pre[u];
+    if (v < nvec && s_pos[v / vpr] >= 0) reinterpret_cast<int4*>(p.xp + (size_t)s_pos[v / vpr] * p.d)[v % vpr] = pre[u];
   }
   for (int v0 = tid + kPre * kDispThreads; v0 < nvec; v0 += U * kDispThreads) {
     int4 out[U];
@@ -186,7 +200,7 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int v = v0 + u * kDispThreads;
-      if (v < nvec) reinterpret_cast<int4*>(p.xp + (size_t)s_pos[v / vpr] * p.d)[v % vpr] = out[u];
+      if (v < nvec && s_pos[v / vpr] >= 0) reinterpret_cast<int4*>(p.xp + (size_t)s_pos[v / vpr] * p.d)[v % vpr] = out[u];
     }
   }
 }

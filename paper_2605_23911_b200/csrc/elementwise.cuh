@@ -260,7 +260,7 @@ gather_rows_kernel(const uint8_t* __restrict__ src, const int32_t* __restrict__ 
 // One CTA (E_local <= 1024).  Mirrors the scheduler half of the router kernel.
 __global__ void __launch_bounds__(256)
 schedule_from_counts_kernel(const int32_t* __restrict__ counts, int E, int chunk_rows,
-                            int32_t* __restrict__ offsets, int4* __restrict__ chunk_tab,
+                            int32_t* __restrict__ offsets, int4* __restrict__ chunk_tab, int2* __restrict__ chunk_grp,
                             int32_t* __restrict__ n_chunks, int32_t* __restrict__ prow) {
   __shared__ int32_t s_off[1025], s_off16[1025], s_cpre[1025];
   if (threadIdx.x == 0) {
@@ -277,9 +277,11 @@ schedule_from_counts_kernel(const int32_t* __restrict__ counts, int E, int chunk
   for (int e = threadIdx.x; e <= E; e += blockDim.x) offsets[e] = s_off[e];
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     const int n = counts[e];
-    for (int c = 0; c * chunk_rows < n; ++c) {
+    const int nch_e = (n + chunk_rows - 1) / chunk_rows;
+    for (int c = 0; c < nch_e; ++c) {
       const int r0 = c * chunk_rows;
       chunk_tab[s_cpre[e] + c] = make_int4(e, s_off[e] + r0, min(chunk_rows, n - r0), s_off16[e] + r0);
+      chunk_grp[s_cpre[e] + c] = make_int2(s_cpre[e], nch_e);
     }
   }
   // padded row of every (expert-major) row

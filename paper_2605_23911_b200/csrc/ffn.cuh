@@ -43,7 +43,8 @@ constexpr int kBoxRows = 32;    // token rows per TMA box
 constexpr int kSchedSlots = 4;  // tile-id ring between scheduler and consumers
 
 struct FfnParams {
-  const int4* chunk_tab;     // {expert, row0, nrows, 0} per token chunk
+  const int4* chunk_tab;     // {expert, row0, nrows, padded row0} per token chunk
+  const int2* chunk_grp;     // {first chunk, chunks} of the chunk's expert
   const int32_t* n_chunks;   // device count of chunks
   int n_mt_gu;               // gate+up tiles per chunk (ceil(f/128)); 0 = none
   int n_mt_dn;               // down tiles per chunk (ceil(d/256): pairs of 128 rows); 0 = none
@@ -148,25 +149,40 @@ struct TileInfo {
   int is_gu, chunk, mt, split;
 };
 
+// Tile order.  Gate+up tiles come first, then down tiles.  Within each, an
+// expert's tiles are contiguous (chunk-major over experts, so the down tiles
+// of early experts are ready early), and when an expert spans several token
+// chunks (a hot expert under routing skew) its tiles are ordered weight-tile
+// major, chunk minor: the chunks' reads of the SAME weight tile are adjacent
+// in the queue, run concurrently on different SMs and are served once from
+// HBM (L2 de-duplicates), keeping the weight stream near one pass.
 MOE_DEVICE TileInfo decode_tile(const FfnParams& p, int tile) {
   TileInfo t;
-  const int n_gu_per = p.n_mt_gu;
+  const int per_gu = p.n_mt_gu;
   const int per_dn = p.n_mt_dn * p.splits;
-  // gate+up tiles occupy [0, n_chunks*n_mt_gu)
   const int nch = __ldg(p.n_chunks);
-  const int n_gu = nch * n_gu_per;
+  const int n_gu = nch * per_gu;
+  int q, per;
   if (tile < n_gu) {
     t.is_gu = 1;
-    t.chunk = tile / n_gu_per;
-    t.mt = tile % n_gu_per;
+    q = tile;
+    per = per_gu;
+  } else {
+    t.is_gu = 0;
+    q = tile - n_gu;
+    per = per_dn;
+  }
+  const int c0 = q / per;
+  const int2 g = __ldg(p.chunk_grp + c0);  // {first chunk of the expert, chunks of the expert}
+  const int r = q - g.x * per;              // position within the expert's tiles
+  const int wt = r / g.y;                   // weight tile (gate+up: mt; down: mt * splits + split)
+  t.chunk = g.x + r % g.y;
+  if (t.is_gu) {
+    t.mt = wt;
     t.split = 0;
   } else {
-    const int q = tile - n_gu;
-    t.is_gu = 0;
-    t.chunk = q / per_dn;
-    const int r = q % per_dn;
-    t.mt = r / p.splits;
-    t.split = r % p.splits;
+    t.mt = wt / p.splits;
+    t.split = wt % p.splits;
   }
   return t;
 }

@@ -62,7 +62,7 @@ constexpr int kHdrBlk = 16 + kTbCap + kChunkCap;
 constexpr size_t kHeaderBytes = align256((16 + kTbCap + kChunkCap + kBlkCap) * sizeof(int32_t));
 
 struct Layout {
-  size_t logits, lbuf, gpart, w64, chunk_tab, prow, xp, h, ys, total;
+  size_t logits, lbuf, gpart, w64, chunk_tab, prow, xp, h, ys, rt_idx, rt_w, rt_misc, total;
   int max_chunks, splits, kb_per_split, T_pad, n_ft, n_dp;
 };
 
@@ -167,11 +167,17 @@ Layout layout_for(const moe_b200_config& c, int64_t B) {
     const size_t d_pad = (c.hidden_dim + kRouterKC - 1) / kRouterKC * kRouterKC;
     L.w64 = off;     off = align256(off + neb * d_pad * expc * sizeof(double));
   }
-  L.chunk_tab = off; off = align256(off + (size_t)L.max_chunks * sizeof(int4));
+  // chunk table {expert, row0, nrows, padded row0} followed by the per-chunk
+  // expert group {first chunk of the expert, chunks of the expert}
+  L.chunk_tab = off; off = align256(off + (size_t)L.max_chunks * (sizeof(int4) + sizeof(int2)));
   L.prow = off;      off = align256(off + (size_t)T * sizeof(int32_t));
   L.xp = off;        off = align256(off + (size_t)T * c.hidden_dim * 2);
   L.h = off;         off = align256(off + std::max(h_rows, h_tiled));
   L.ys = off;        off = align256(off + std::max((size_t)T * c.hidden_dim * sizeof(float), ys_tiled));
+  // scratch routing outputs for moe_b200_forward_routed's discarded router run
+  L.rt_idx = off;    off = align256(off + (size_t)T * sizeof(int32_t));
+  L.rt_w = off;      off = align256(off + (size_t)T * sizeof(float));
+  L.rt_misc = off;   off = align256(off + (size_t)(2 * c.num_experts + 1 + 2 * T) * sizeof(int32_t));
   L.total = off;
   return L;
 }
@@ -369,6 +375,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   int32_t* hdr = reinterpret_cast<int32_t*>(ws);
   FfnParams p{};
   p.chunk_tab = reinterpret_cast<const int4*>(static_cast<uint8_t*>(ws) + L.chunk_tab);
+  p.chunk_grp = reinterpret_cast<const int2*>(p.chunk_tab + L.max_chunks);
   p.n_chunks = hdr + 2;
   p.n_mt_gu = do_gu ? (f + kBM - 1) / kBM : 0;
   p.n_mt_dn = do_dn ? (d + 2 * kBM - 1) / (2 * kBM) : 0;
@@ -476,14 +483,16 @@ int launch_combine(const moe_b200_config& c, int64_t B, const Layout& L, void* w
 
 int launch_dispatch(const moe_b200_config& c, int64_t B, const void* x, int xb, const int32_t* topk_idx,
                     int32_t* counts, int32_t* offsets, int32_t* fwd, int32_t* inv, int32_t* prow, int4* chunk_tab,
-                    int32_t* n_chunks, void* xp, cudaStream_t s) {
+                    int32_t* n_chunks, void* xp, cudaStream_t s, uint32_t* flags = nullptr) {
   DispatchParams q{};
+  q.flags = flags;
   q.topk_idx = topk_idx;
   q.T = static_cast<int>(B * c.top_k); q.k = c.top_k; q.E = c.num_experts; q.d = c.hidden_dim;
   q.chunk_rows = chunk_rows_for(c, B);
   q.x = x; q.xp = static_cast<__nv_bfloat16*>(xp);
   q.counts = counts; q.offsets = offsets; q.fwd = fwd; q.inv = inv; q.prow = prow;
   q.chunk_tab = chunk_tab; q.n_chunks = n_chunks;
+  q.chunk_grp = reinterpret_cast<int2*>(chunk_tab + layout_for(c, B).max_chunks);
   const int grid = (q.T + kDispRows - 1) / kDispRows;
   const size_t smem = (size_t)(5 * c.num_experts + 3) * sizeof(int32_t);
   auto kern = xb ? dispatch_kernel<true> : dispatch_kernel<false>;
@@ -745,6 +754,49 @@ int moe_b200_forward(const moe_b200_config* cfg, int64_t B, const void* x, int x
                       offsets, perm_fwd, perm_inv, ws, ws_bytes, stream, nullptr);
 }
 
+int moe_b200_forward_routed(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
+                            const int32_t* topk_idx, const float* topk_w, const float* w_router,
+                            const void* w_gate, const void* w_up, const void* w_down, void* y, int y_dtype,
+                            int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv, void* ws,
+                            size_t ws_bytes, void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (B < 0) return MOE_B200_ERR_SHAPE_MISMATCH;
+  if (x_dtype != MOE_B200_DTYPE_F32 && x_dtype != MOE_B200_DTYPE_BF16) return MOE_B200_ERR_INVALID_VALUE;
+  if (y_dtype != MOE_B200_DTYPE_F32 && y_dtype != MOE_B200_DTYPE_BF16) return MOE_B200_ERR_INVALID_VALUE;
+  Layout L;
+  if ((rc = check_ws(cfg, B, ws, ws_bytes, &L))) return rc;
+  if (B == 0) return MOE_B200_OK;
+  if (!x || !topk_idx || !topk_w || !w_gate || !w_up || !w_down || !y || !counts || !offsets || !perm_fwd ||
+      !perm_inv)
+    return MOE_B200_ERR_INVALID_VALUE;
+  if (L.max_chunks > kChunkCap) return MOE_B200_ERR_UNSUPPORTED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* hdr = reinterpret_cast<int32_t*>(ws);
+  if (w_router) {
+    // the paper's override still runs the router projection: route into scratch, discard
+    int32_t* r_idx = reinterpret_cast<int32_t*>(ws8(ws) + L.rt_idx);
+    float* r_w = reinterpret_cast<float*>(ws8(ws) + L.rt_w);
+    int32_t* r_misc = reinterpret_cast<int32_t*>(ws8(ws) + L.rt_misc);
+    const int T = static_cast<int>(B * cfg->top_k);
+    if ((rc = route_impl(cfg, B, x, x_dtype, w_router, r_idx, r_w, r_misc, r_misc + cfg->num_experts,
+                         r_misc + 2 * cfg->num_experts + 1, r_misc + 2 * cfg->num_experts + 1 + T, nullptr, ws,
+                         ws_bytes, stream, nullptr)))
+      return rc;
+  }
+  void* xp = ws8(ws) + L.xp;
+  void* h = ws8(ws) + L.h;
+  float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);
+  if ((rc = launch_dispatch(*cfg, B, x, x_dtype == MOE_B200_DTYPE_BF16, topk_idx, counts, offsets, perm_fwd, perm_inv,
+                            reinterpret_cast<int32_t*>(ws8(ws) + L.prow), reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab),
+                            hdr + 2, xp, s, reinterpret_cast<uint32_t*>(hdr))))
+    return rc;
+  if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
+                       /*gu*/ true, /*dn*/ true, /*fused*/ true, s)))
+    return rc;
+  return launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s);
+}
+
 int moe_b200_forward_timed(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
                            const float* w_router, const void* w_gate, const void* w_up,
                            const void* w_down, void* y, int y_dtype, int32_t* topk_idx, float* topk_w,
@@ -901,7 +953,9 @@ int moe_b200_expert_ffn(const moe_b200_config* cfg, int64_t n_rows, const int32_
   int32_t* offsets = reinterpret_cast<int32_t*>(ws8(ws) + L.logits);  // scratch: E+1 ints
   int32_t* prow = reinterpret_cast<int32_t*>(ws8(ws) + L.prow);
   schedule_from_counts_kernel<<<1, 256, 0, s>>>(counts, c1.num_experts, chunk_rows_for(c1, n_rows), offsets,
-                                                reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab), hdr + 2, prow);
+                                                reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab),
+                                                reinterpret_cast<int2*>(ws8(ws) + L.chunk_tab) + 2 * L.max_chunks,
+                                                hdr + 2, prow);
   MOE_LAUNCH_CHECK("schedule_from_counts_kernel");
   void* h = ws8(ws) + L.h;
   float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import NonFiniteInput, ShapeMismatch
+from .errors import IndexOutOfRange, NonFiniteInput, ShapeMismatch
 from .trace import PipelineTrace, trace_from_counts
 from .types import GATING_CODE, ExpertWeights, ModelConfig, PipelineParams, RoutingResult
 
@@ -171,6 +171,34 @@ class MoELayer:
 
     __call__ = forward
 
+    def forward_routed(self, x: torch.Tensor, routing, out: torch.Tensor | None = None,
+                       run_router: bool = True) -> torch.Tensor:
+        """y = MoE(x) with the routing given (``RoutingResult`` or (indices,
+        weights)): the paper's router override for the routing-skew study
+        (``PAPER.md:333-336``; tables from ``skew.synthesize_routing``).  With
+        ``run_router`` the router projection still runs and is discarded, as in
+        the paper's experiment.  Asynchronous, graph-capturable once the
+        routing tensors are on the device."""
+        x, xdt = self._prep_x(x)
+        B = x.shape[0]
+        idx, w = (routing.indices, routing.weights) if hasattr(routing, "indices") else routing
+        idx = _as_tensor(idx, self.device, torch.int32)
+        w = _as_tensor(w, self.device, torch.float32)
+        if tuple(idx.shape) != (B, self.k) or tuple(w.shape) != (B, self.k):
+            raise ShapeMismatch(f"routing must be ({B}, {self.k}), got {tuple(idx.shape)} / {tuple(w.shape)}")
+        self._routed_idx, self._routed_w = idx, w  # keep alive while the launches run
+        if out is None:
+            out = torch.empty((B, self.dp), dtype=self.out_dtype, device=self.device)
+        ydt = _lib.DTYPE_BF16 if out.dtype == torch.bfloat16 else _lib.DTYPE_F32
+        rc = self.lib.moe_b200_forward_routed(
+            ctypes.byref(self.cfg), B, _ptr(x), xdt, _ptr(idx), _ptr(w),
+            _ptr(self.router_weight) if run_router else None,
+            _ptr(self.weights.gate), _ptr(self.weights.up), _ptr(self.weights.down), _ptr(out), ydt,
+            _ptr(self.counts), _ptr(self.offsets), _ptr(self.fwd), _ptr(self.inv), _ptr(self.ws), self.ws_bytes,
+            _stream_ptr(self.device))
+        _lib.check(rc, "moe_b200_forward_routed")
+        return out if self.dp == self.d else out[:, : self.d]
+
     # -- host buffers in, host buffers out (pipelined across calls) -------------
     def host_pipeline(self, x_dtype=torch.bfloat16, y_dtype=None) -> "HostPipeline":
         """I/O context for ``forward_host``: the reference API's numpy-in /
@@ -195,6 +223,8 @@ class MoELayer:
             raise NonFiniteInput("tokens contains non-finite values")
         if flags & 2:
             raise NonFiniteInput("router_weight contains non-finite values")
+        if flags & 4:
+            raise IndexOutOfRange("routing index outside [0, num_experts)")
 
     # -- stage-level entry points (parity tests, reference stage API) ----------
     def route(self, x: torch.Tensor, logits: bool = False) -> dict:
