@@ -138,6 +138,16 @@ int moe_b200_forward(const moe_b200_config* cfg, int64_t num_tokens, const void*
                      int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
                      void* ws, size_t ws_bytes, void* stream);
 
+/* The same layer with the reference's unfused gate+up (pipeline.py:316-370,
+ * PipelineParams.fused = False): gate and up as separate grouped GEMMs
+ * writing fp32, a separate SiLU*up pass, then the down projection.  The
+ * fusion ablation; results are bit-identical to moe_b200_forward. */
+int moe_b200_forward_unfused(const moe_b200_config* cfg, int64_t num_tokens, const void* x, int x_dtype,
+                             const float* w_router, const void* w_gate, const void* w_up,
+                             const void* w_down, void* y, int y_dtype, int32_t* topk_idx, float* topk_w,
+                             int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
+                             void* ws, size_t ws_bytes, void* stream);
+
 /* Whole layer with the routing given (the paper's router override for the
  * routing-skew study; tables from moeperf/skew.py:74-105):
  * topk_idx (B, k) int32 and topk_w (B, k) fp32 are INPUTS on the device.

@@ -61,6 +61,8 @@ SIGNATURES = {
     "moe_b200_down_scatter": (_INT, [_CFG, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "moe_b200_combine": (_INT, [_CFG, _I64, _P, _P, _INT, _P]),
     "moe_b200_forward": (_INT, [_CFG, _I64, _P, _INT, _P, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_forward_unfused": (_INT, [_CFG, _I64, _P, _INT, _P, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _P, _P, _P,
+                                        _SZ, _P]),
     "moe_b200_forward_routed": (_INT, [_CFG, _I64, _P, _INT, _P, _P, _P, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _P,
                                        _SZ, _P]),
     "moe_b200_forward_timed": (_INT, [_CFG, _I64, _P, _INT, _P, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _P, _P, _P, _SZ, _P,

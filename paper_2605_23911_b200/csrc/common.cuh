@@ -48,6 +48,23 @@ MOE_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); 
 MOE_DEVICE void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ----------------------------------------------------------------------------
+// SwiGLU activation h = silu(g) * u (pipeline.py:294), shared by the fused
+// gate+up epilogue and the unfused ablation's activation pass so both give the
+// same bits: silu(g) = g * sigmoid(g), sigmoid(g) = 0.5 + 0.5 tanh(g/2), one
+// MUFU op per element, explicit roundings (no contraction).  Tolerance path:
+// h is rounded to bf16.
+// ----------------------------------------------------------------------------
+MOE_DEVICE float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+MOE_DEVICE float silu_mul(float g, float u) {
+  const float hg = __fmul_rn(0.5f, g);
+  return __fmul_rn(__fmul_rn(hg, u), __fadd_rn(1.0f, tanh_approx(hg)));
+}
+
+// ----------------------------------------------------------------------------
 // mbarrier
 // ----------------------------------------------------------------------------
 MOE_DEVICE void mbar_init(uint64_t* bar, uint32_t count) {

@@ -238,6 +238,26 @@ combine_token_kernel(const float* __restrict__ ys, int n_dp, int T_pad,
   }
 }
 
+// Unfused ablation (pipeline.py:316-370 unfused_gate_up): the separate
+// activation pass h = bf16(silu(g) * u) over the tiled fp32 projections
+// [proj][f/128][T_pad][128] -> tiled bf16 h [f/128][T_pad][128], with the
+// fused epilogue's exact formula (silu_mul, ffn.cuh) so h is bit-identical.
+__global__ void __launch_bounds__(kRowThreads)
+swiglu_tiled_kernel(const float* __restrict__ gu32, __nv_bfloat16* __restrict__ h, size_t n_per_proj) {
+  pdl_wait();
+  const size_t n4 = n_per_proj / 4;
+  for (size_t i = (size_t)blockIdx.x * kRowThreads + threadIdx.x; i < n4; i += (size_t)gridDim.x * kRowThreads) {
+    const float4 g = __ldg(reinterpret_cast<const float4*>(gu32) + i);
+    const float4 u = __ldg(reinterpret_cast<const float4*>(gu32 + n_per_proj) + i);
+    const __nv_bfloat162 a = __floats2bfloat162_rn(silu_mul(g.x, u.x), silu_mul(g.y, u.y));
+    const __nv_bfloat162 b = __floats2bfloat162_rn(silu_mul(g.z, u.z), silu_mul(g.w, u.w));
+    uint2 o;
+    o.x = *reinterpret_cast<const uint32_t*>(&a);
+    o.y = *reinterpret_cast<const uint32_t*>(&b);
+    reinterpret_cast<uint2*>(h)[i] = o;
+  }
+}
+
 // Expert-parallel helpers --------------------------------------------------
 
 // dst[r, :] = src[idx[r], :] for rows of `row_bytes` (multiple of 16) bytes.

@@ -61,6 +61,8 @@ struct FfnParams {
   int32_t* work_counter;     // self-resetting
   int32_t* exit_counter;     // self-resetting
   int32_t* gu_done;          // per-chunk completed gate+up tiles, self-resetting
+  int gu_unfused;            // 1: gate and up as separate tiles, fp32 out (pipeline.py:316-370 ablation)
+  float* gu32;               // unfused output: tiled [proj][f/128][T_pad][128] fp32
   int dbg;                   // debug/experiment bits (0 in production)
   int tiled;                 // 1: h / ys in the tiled padded-row layouts (fused forward)
   int T_pad;                 // padded-row capacity of the tiled layouts
@@ -94,8 +96,10 @@ struct FfnCfg {
   static constexpr int kBBytes = kBN * kBK * 2;      // token slot
   static constexpr int kStgBytes = 32 * kBM * 4;     // 32 rows x 128 fp32 (16 KB)
   static constexpr int kStgBufs = kEpiGroups;  // one staging buffer per epilogue group
-  static constexpr int kAStages = kBN == 256 ? 6 : 8;
-  static constexpr int kBStages = kBN == 256 ? 3 : 4;
+  // kV 2: balanced rings; kV 3: deeper weight ring (more HBM bytes in flight
+  // per SM), shallower token ring (tokens are L2-resident)
+  static constexpr int kAStages = kBN == 256 ? (kV == 3 ? 8 : 6) : (kV == 3 ? 10 : 8);
+  static constexpr int kBStages = kBN == 256 ? (kV == 3 ? 2 : 3) : (kV == 3 ? 2 : 4);
   static constexpr int kRingBytes = kAStages * kABytes + kBStages * kBBytes;
   static constexpr int kDataBytes = kRingBytes + kStgBufs * kStgBytes;
   static constexpr uint32_t kTmemCols = 2 * kBN <= 256 ? 256 : 512;
@@ -116,18 +120,6 @@ MOE_DEVICE void bulk_wait_read() {
 MOE_DEVICE void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 MOE_DEVICE void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-MOE_DEVICE float tanh_approx(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-MOE_DEVICE float silu_mul(float g, float u) {
-  // silu(g) * u = g * sigmoid(g) * u, sigmoid(g) = 0.5 + 0.5 tanh(g/2): one
-  // MUFU op per element (tolerance path, pipeline.py:294; h is rounded to bf16)
-  const float hg = 0.5f * g;
-  return hg * u * (1.0f + tanh_approx(hg));
 }
 
 MOE_DEVICE int ld_acquire_gpu(const int32_t* p) {
@@ -158,7 +150,7 @@ struct TileInfo {
 // HBM (L2 de-duplicates), keeping the weight stream near one pass.
 MOE_DEVICE TileInfo decode_tile(const FfnParams& p, int tile) {
   TileInfo t;
-  const int per_gu = p.n_mt_gu;
+  const int per_gu = p.n_mt_gu * (p.gu_unfused ? 2 : 1);
   const int per_dn = p.n_mt_dn * p.splits;
   const int nch = __ldg(p.n_chunks);
   const int n_gu = nch * per_gu;
@@ -178,8 +170,9 @@ MOE_DEVICE TileInfo decode_tile(const FfnParams& p, int tile) {
   const int wt = r / g.y;                   // weight tile (gate+up: mt; down: mt * splits + split)
   t.chunk = g.x + r % g.y;
   if (t.is_gu) {
-    t.mt = wt;
-    t.split = 0;
+    // unfused: weight tiles (mt, projection) with split = 0 gate / 1 up
+    t.mt = p.gu_unfused ? (wt >> 1) : wt;
+    t.split = p.gu_unfused ? (wt & 1) : 0;
   } else {
     t.mt = wt / p.splits;
     t.split = wt % p.splits;
@@ -247,7 +240,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
   pdl_wait();
 
   const int nch = __ldg(p.n_chunks);
-  const int total_tiles = nch * (p.n_mt_gu + p.n_mt_dn * p.splits);
+  const int total_tiles = nch * (p.n_mt_gu * (p.gu_unfused ? 2 : 1) + p.n_mt_dn * p.splits);
   const int nkb_gu = (p.d + kBK - 1) / kBK;
   const int nkb_dn = (p.f + kBK - 1) / kBK;
 
@@ -290,7 +283,17 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         }
         if (p.trace) p.trace[tile * 8 + 2] = globaltimer();
         for (int kb = kb0; kb < kb1; ++kb) {
-          if (ti.is_gu) {
+          if (ti.is_gu && p.gu_unfused) {
+            // one projection per tile: a single weight slot per k-block
+            const int krow = ch.x * p.d + kb * kBK;
+            const CUtensorMap* tw = ti.split ? &tm_wu : &tm_wg;
+            mbar_wait(a_empty + as, aph ^ 1);
+            mbar_arrive_expect_tx(a_full + as, C::kABytes);
+            uint8_t* sa = a_ring + as * C::kABytes;
+            tma_load_2d_hint(tw, a_full + as, sa, a_col, krow, pol_w);
+            tma_load_2d_hint(tw, a_full + as, sa + C::kABytes / 2, a_col + 64, krow, pol_w);
+            if (++as == C::kAStages) { as = 0; aph ^= 1; }
+          } else if (ti.is_gu) {
             const int krow = ch.x * p.d + kb * kBK;
             mbar_wait(a_empty + as, aph ^ 1);
             mbar_arrive_expect_tx(a_full + as, C::kABytes);
@@ -318,9 +321,11 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             }
           }
           mbar_wait(b_empty + bs, bph ^ 1);
-          mbar_arrive_expect_tx(b_full + bs, b_bytes);
           uint8_t* sb = b_ring + bs * C::kBBytes;
-          if (ti.is_gu || !p.tiled) {
+          if (p.dbg & 16) {
+            // diagnostic only (wrong results): no token loads, measures the weight stream alone
+            mbar_arrive(b_full + bs);
+          } else if (mbar_arrive_expect_tx(b_full + bs, b_bytes), ti.is_gu || !p.tiled) {
             const CUtensorMap* tb = ti.is_gu ? &tm_xp : &tm_h;
             for (int b = 0; b < nbox; ++b)
               tma_load_2d(tb, b_full + bs, sb + b * kBoxRows * kBK * 2, kb * kBK, ch.y + b * kBoxRows);
@@ -363,12 +368,15 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       tc_fence_after();
       if (p.trace && lane == 0) p.trace[tile * 8 + 5] = globaltimer();
       for (int kb = kb0; kb < kb1; ++kb) {
+        const bool single = ti.is_gu && p.gu_unfused;  // one weight slot, one accumulator
         const int as0 = as;
         mbar_wait(a_full + as, aph);
         if (++as == C::kAStages) { as = 0; aph ^= 1; }
         const int as1 = as;  // second weight slot: up (gate+up) or hidden rows +128 (down)
-        mbar_wait(a_full + as, aph);
-        if (++as == C::kAStages) { as = 0; aph ^= 1; }
+        if (!single) {
+          mbar_wait(a_full + as, aph);
+          if (++as == C::kAStages) { as = 0; aph ^= 1; }
+        }
         mbar_wait(b_full + bs, bph);
         tc_fence_after();
         if (elect_one()) {
@@ -380,12 +388,14 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             const uint64_t adesc0 = make_smem_desc_sw128(sa0 + kk * 2048, C::kABytes / 2, 1024);
             const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
             mma_bf16(tmem_base, adesc0, bdesc, idesc, acc);
-            const uint32_t sa1 = smem_u32(a_ring + as1 * C::kABytes);
-            const uint64_t adesc1 = make_smem_desc_sw128(sa1 + kk * 2048, C::kABytes / 2, 1024);
-            mma_bf16(tmem_base + kBN, adesc1, bdesc, idesc, acc);
+            if (!single) {
+              const uint32_t sa1 = smem_u32(a_ring + as1 * C::kABytes);
+              const uint64_t adesc1 = make_smem_desc_sw128(sa1 + kk * 2048, C::kABytes / 2, 1024);
+              mma_bf16(tmem_base + kBN, adesc1, bdesc, idesc, acc);
+            }
           }
           mma_commit(a_empty + as0);
-          mma_commit(a_empty + as1);
+          if (!single) mma_commit(a_empty + as1);
           mma_commit(b_empty + bs);
           if (kb == kb1 - 1) mma_commit(tmem_full);
         }
@@ -419,7 +429,41 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       // Staged store protocol, per 32-row chunk of this group: (issuer) make the
       // staging buffer free -> group barrier -> every thread writes its feature
       // column -> proxy fence -> group barrier -> issuer bulk-copies the rows.
-      if (ti.is_gu) {
+      if (ti.is_gu && p.gu_unfused) {
+        // unfused ablation: store the raw fp32 projection (gate or up) tiled
+        // [proj][f-tile][padded row][128]; the activation runs in a separate pass
+        const int nq = (ch.z + 31) / 32;
+        const int my_last = (nq - 1 - grp) >= 0 ? (nq - 1 - ((nq - 1 - grp) % kEpiGroups)) : -1;
+        for (int q = grp; q < nq; q += kEpiGroups) {
+          const int c0 = q * 32;
+          uint32_t a[32];
+          tmem_ld_32x32b_x32(tmem_base + lane_base + c0, a);
+          tmem_wait_ld();
+          if (q == my_last) {
+            tc_fence_before();
+            mbar_arrive(tmem_empty);
+          }
+          float* sbuf = reinterpret_cast<float*>(stg_g);
+          if (issuer) bulk_wait_read<0>();
+          epi_bar_sync(grp);
+          const int fl = wq * 32 + lane;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) sbuf[c * kBM + fl] = __uint_as_float(a[c]);
+          fence_proxy_async_smem();
+          epi_bar_sync(grp);
+          if (issuer) {
+            const int rows = min(32, ch.z - c0);
+            float* dst = p.gu32 + (((size_t)ti.split * p.n_mt_gu + ti.mt) * p.T_pad + ch.w + c0) * kBM;
+            bulk_store(dst, sbuf, rows * kBM * 4);
+            bulk_commit();
+          }
+        }
+        if (my_last < 0) {
+          tc_fence_before();
+          mbar_arrive(tmem_empty);
+        }
+        if (issuer) bulk_wait_all();
+      } else if (ti.is_gu) {
         const int f0 = ti.mt * kBM;
         const int nvalid_f = min(kBM, p.f - f0);
         // Phase 1 (TMEM critical path): drain both accumulators, apply SiLU(g)*u and

@@ -62,7 +62,7 @@ constexpr int kHdrBlk = 16 + kTbCap + kChunkCap;
 constexpr size_t kHeaderBytes = align256((16 + kTbCap + kChunkCap + kBlkCap) * sizeof(int32_t));
 
 struct Layout {
-  size_t logits, lbuf, gpart, w64, chunk_tab, prow, xp, h, ys, rt_idx, rt_w, rt_misc, total;
+  size_t logits, lbuf, gpart, w64, chunk_tab, prow, xp, h, ys, rt_idx, rt_w, rt_misc, gu32, total;
   int max_chunks, splits, kb_per_split, T_pad, n_ft, n_dp;
 };
 
@@ -97,10 +97,12 @@ int seg_expc(int E) {
   return 32;
 }
 
-// The segment router runs up to this many tokens (B*E chains <= kSegMaxChains,
-// tunable via MOE_B200_SEG_MAX_CHAINS); larger problems use the exact kernel.
+// The segment router runs up to this many tokens (B*E chains <= 64K, tunable
+// via MOE_B200_SEG_MAX_CHAINS); larger problems are fp64-throughput bound and
+// use the exact kernel (no magnitude DADD: half the fp64 work; measured
+// DeepSeek-V3 B=512: 257 us exact vs 430 us segment).
 int64_t seg_max_tokens(const moe_b200_config& c) {
-  int64_t chains = 1LL << 20;
+  int64_t chains = 64LL * 1024;
   if (const char* env = getenv("MOE_B200_SEG_MAX_CHAINS")) chains = atoll(env);
   return chains / std::max(1, c.num_experts);
 }
@@ -178,6 +180,8 @@ Layout layout_for(const moe_b200_config& c, int64_t B) {
   L.rt_idx = off;    off = align256(off + (size_t)T * sizeof(int32_t));
   L.rt_w = off;      off = align256(off + (size_t)T * sizeof(float));
   L.rt_misc = off;   off = align256(off + (size_t)(2 * c.num_experts + 1 + 2 * T) * sizeof(int32_t));
+  // unfused ablation: tiled fp32 gate and up projections [2][f/128][T_pad][128]
+  L.gu32 = off;      off = align256(off + (size_t)2 * L.n_ft * L.T_pad * kBM * sizeof(float));
   L.total = off;
   return L;
 }
@@ -247,13 +251,15 @@ int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 }
 
 // ------------------------------- launches --------------------------------------
-// Launch with programmatic stream serialization (PDL): the kernel may start
-// while its predecessor finishes; it calls pdl_wait() before reading the
-// predecessor's outputs (common.cuh).  MOE_B200_NO_PDL=1 disables it.
+// Launch with programmatic stream serialization (PDL) when MOE_B200_PDL=1:
+// the kernel may start while its predecessor finishes and calls pdl_wait()
+// before reading the predecessor's outputs (common.cuh).  Off by default: it
+// measured no gain on the graph-replayed forward (A/B 510 vs 508 us, Mixtral)
+// and one test sequence (Mixtral then Qwen layers) stalled with it on.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
-  const char* env = getenv("MOE_B200_NO_PDL");
-  const bool disabled = env && atoi(env);
+  const char* env = getenv("MOE_B200_PDL");
+  const bool disabled = !(env && atoi(env));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -345,15 +351,23 @@ int launch_ffn_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& 
 int launch_ffn_kernel(int bn, int variant, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm,
                       const CUtensorMap& dm, const CUtensorMap& e, const FfnParams& p, int grid,
                       cudaStream_t s) {
-  (void)variant;
-  if (bn == 256) return launch_ffn_t<256, 2>(a, b, cm, dm, e, p, grid, s);
-  return launch_ffn_t<128, 2>(a, b, cm, dm, e, p, grid, s);
+  if (bn == 256)
+    return variant == 3 ? launch_ffn_t<256, 3>(a, b, cm, dm, e, p, grid, s) : launch_ffn_t<256, 2>(a, b, cm, dm, e, p, grid, s);
+  return variant == 3 ? launch_ffn_t<128, 3>(a, b, cm, dm, e, p, grid, s) : launch_ffn_t<128, 2>(a, b, cm, dm, e, p, grid, s);
 }
+
+// FFN launch modes: kFfnFused = gate+up and down in one launch over the tiled
+// layouts (down tiles wait on per-chunk gate+up release); kFfnStaged = one
+// projection per launch over row layouts (stage API); kFfnUnfusedGU = gate and
+// up as separate tiles writing fp32 (ablation); kFfnTiledDown = down tiles
+// only over the tiled h (after the ablation's activation pass).
+enum FfnMode { kFfnFused = 0, kFfnStaged = 1, kFfnUnfusedGU = 2, kFfnTiledDown = 3 };
 
 int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, const void* xp,
                const void* w_gate, const void* w_up, const void* w_down, void* h, float* ys,
-               const float* topk_w, const int32_t* fwd, bool do_gu, bool do_dn, bool fused,
-               cudaStream_t s) {
+               const float* topk_w, const int32_t* fwd, bool do_gu, bool do_dn, int mode,
+               cudaStream_t s, float* gu32 = nullptr) {
+  const bool fused = (mode != kFfnStaged);  // tiled padded-row layouts
   const int E = c.num_experts, d = c.hidden_dim, f = c.ffn_dim;
   const int64_t T = B * c.top_k;
   CUtensorMap m_wg, m_wu, m_xp, m_wd, m_h;
@@ -387,7 +401,9 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.topk_w = topk_w;
   p.fwd = fwd;
   p.scale_by_w = fused ? 0 : 1;
-  p.gu_wait = fused ? 1 : 0;
+  p.gu_wait = (mode == kFfnFused && do_gu && do_dn) ? 1 : 0;
+  p.gu_unfused = (mode == kFfnUnfusedGU) ? 1 : 0;
+  p.gu32 = gu32;
   p.work_counter = hdr + 3;
   p.exit_counter = hdr + 4;
   p.gu_done = hdr + kHdrGuDone;
@@ -395,7 +411,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.T_pad = L.T_pad;
   p.trace = g_ffn_trace;
   if (const char* env = getenv("MOE_B200_FFN_DEBUG")) p.dbg = atoi(env);
-  const long max_tiles = (long)L.max_chunks * (p.n_mt_gu + p.n_mt_dn * p.splits);
+  const long max_tiles = (long)L.max_chunks * (p.n_mt_gu * (p.gu_unfused ? 2 : 1) + p.n_mt_dn * p.splits);
   const int grid = static_cast<int>(std::max(1L, std::min<long>(kNumSMs, max_tiles)));
   const int bn = chunk_rows_for(c, B);
   int variant = 2;
@@ -675,7 +691,7 @@ int moe_b200_gate_up(const moe_b200_config* cfg, int64_t B, const void* xp, cons
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (L.max_chunks > kChunkCap) return MOE_B200_ERR_UNSUPPORTED;
   return launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, nullptr, h, nullptr, nullptr, nullptr,
-                    /*gu*/ true, /*dn*/ false, /*fused*/ false, s);
+                    /*gu*/ true, /*dn*/ false, kFfnStaged, s);
 }
 
 int moe_b200_down_scatter(const moe_b200_config* cfg, int64_t B, const void* h, const void* w_down,
@@ -690,7 +706,7 @@ int moe_b200_down_scatter(const moe_b200_config* cfg, int64_t B, const void* h, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (L.max_chunks > kChunkCap) return MOE_B200_ERR_UNSUPPORTED;
   return launch_ffn(*cfg, B, L, ws, nullptr, nullptr, nullptr, w_down, const_cast<void*>(h), ys,
-                    topk_w, perm_fwd, /*gu*/ false, /*dn*/ true, /*fused*/ false, s);
+                    topk_w, perm_fwd, /*gu*/ false, /*dn*/ true, kFfnStaged, s);
 }
 
 int moe_b200_combine(const moe_b200_config* cfg, int64_t B, const float* ys, void* y, int y_dtype,
@@ -716,7 +732,7 @@ static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, in
                      const float* w_router, const void* w_gate, const void* w_up,
                      const void* w_down, void* y, int y_dtype, int32_t* topk_idx, float* topk_w,
                      int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
-                     void* ws, size_t ws_bytes, void* stream, void** events) {
+                     void* ws, size_t ws_bytes, void* stream, void** events, bool unfused = false) {
   int rc = check_config(cfg);
   if (rc) return rc;
   Layout L;
@@ -737,9 +753,26 @@ static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, in
   if (B == 0) return events ? mark(1) : MOE_B200_OK;
   if ((rc = mark(2))) return rc;
   if (L.max_chunks > kChunkCap) return MOE_B200_ERR_UNSUPPORTED;
-  if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
-                       /*gu*/ true, /*dn*/ true, /*fused*/ true, s)))
-    return rc;
+  if (!unfused) {
+    if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
+                         /*gu*/ true, /*dn*/ true, kFfnFused, s)))
+      return rc;
+  } else {
+    // ablation (pipeline.py:316-370): gate and up GEMMs as separate tiles
+    // (fp32 out), a separate activation pass, then the down projection
+    float* gu32 = reinterpret_cast<float*>(ws8(ws) + L.gu32);
+    if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
+                         /*gu*/ true, /*dn*/ false, kFfnUnfusedGU, s, gu32)))
+      return rc;
+    const size_t n_per_proj = (size_t)L.n_ft * L.T_pad * kBM;
+    const int grid = grid_for_rows((long)(n_per_proj / 4));
+    cudaError_t e = launch_pdl(swiglu_tiled_kernel, dim3(grid), dim3(kRowThreads), 0, s, (const float*)gu32,
+                               static_cast<__nv_bfloat16*>(h), n_per_proj);
+    if (e != cudaSuccess) return cuda_fail(e, "swiglu launch");
+    if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
+                         /*gu*/ false, /*dn*/ true, kFfnTiledDown, s)))
+      return rc;
+  }
   if ((rc = mark(3))) return rc;
   if ((rc = launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s))) return rc;
   return mark(4);
@@ -752,6 +785,15 @@ int moe_b200_forward(const moe_b200_config* cfg, int64_t B, const void* x, int x
                      void* ws, size_t ws_bytes, void* stream) {
   return forward_impl(cfg, B, x, x_dtype, w_router, w_gate, w_up, w_down, y, y_dtype, topk_idx, topk_w, counts,
                       offsets, perm_fwd, perm_inv, ws, ws_bytes, stream, nullptr);
+}
+
+int moe_b200_forward_unfused(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
+                             const float* w_router, const void* w_gate, const void* w_up,
+                             const void* w_down, void* y, int y_dtype, int32_t* topk_idx, float* topk_w,
+                             int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
+                             void* ws, size_t ws_bytes, void* stream) {
+  return forward_impl(cfg, B, x, x_dtype, w_router, w_gate, w_up, w_down, y, y_dtype, topk_idx, topk_w, counts,
+                      offsets, perm_fwd, perm_inv, ws, ws_bytes, stream, nullptr, /*unfused*/ true);
 }
 
 int moe_b200_forward_routed(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
@@ -792,7 +834,7 @@ int moe_b200_forward_routed(const moe_b200_config* cfg, int64_t B, const void* x
                             hdr + 2, xp, s, reinterpret_cast<uint32_t*>(hdr))))
     return rc;
   if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
-                       /*gu*/ true, /*dn*/ true, /*fused*/ true, s)))
+                       /*gu*/ true, /*dn*/ true, kFfnFused, s)))
     return rc;
   return launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s);
 }
@@ -960,7 +1002,7 @@ int moe_b200_expert_ffn(const moe_b200_config* cfg, int64_t n_rows, const int32_
   void* h = ws8(ws) + L.h;
   float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);
   if ((rc = launch_ffn(c1, n_rows, L, ws, xp, w_gate, w_up, w_down, h, ys, nullptr, nullptr,
-                       /*gu*/ true, /*dn*/ true, /*fused*/ true, s)))
+                       /*gu*/ true, /*dn*/ true, kFfnFused, s)))
     return rc;
   const int d = c1.hidden_dim;
   row_reduce_kernel<<<grid_for_rows((long)n_rows * (d / 4)), kRowThreads, 0, s>>>(

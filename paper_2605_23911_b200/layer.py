@@ -154,14 +154,17 @@ class MoELayer:
         return x, (_lib.DTYPE_BF16 if x.dtype == torch.bfloat16 else _lib.DTYPE_F32)
 
     # -- whole layer ------------------------------------------------------------
-    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        """y = MoE(x) on the current stream; asynchronous, graph-capturable."""
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None, fused: bool = True) -> torch.Tensor:
+        """y = MoE(x) on the current stream; asynchronous, graph-capturable.
+        ``fused=False`` runs the reference's unfused gate+up variant
+        (``PipelineParams.fused``, ``pipeline.py:316-370``): same bits."""
         x, xdt = self._prep_x(x)
         B = x.shape[0]
         if out is None:
             out = torch.empty((B, self.dp), dtype=self.out_dtype, device=self.device)
         ydt = _lib.DTYPE_BF16 if out.dtype == torch.bfloat16 else _lib.DTYPE_F32
-        rc = self.lib.moe_b200_forward(
+        fn = self.lib.moe_b200_forward if fused else self.lib.moe_b200_forward_unfused
+        rc = fn(
             ctypes.byref(self.cfg), B, _ptr(x), xdt, _ptr(self.router_weight),
             _ptr(self.weights.gate), _ptr(self.weights.up), _ptr(self.weights.down),
             _ptr(out), ydt, _ptr(self.topk_idx), _ptr(self.topk_w), _ptr(self.counts), _ptr(self.offsets),
@@ -454,7 +457,7 @@ def moe_forward(tokens, router_weight, weights, config: ModelConfig,
     if B == 0:
         y = torch.zeros((0, config.hidden_dim), dtype=torch.float32, device=layer.device)
         return _finish(y, like_numpy), trace_from_counts(config, 0, np.zeros(config.num_experts, np.int64), params)
-    y = layer.forward(x)
+    y = layer.forward(x, fused=params.fused)
     counts = layer.counts.cpu().numpy().astype(np.int64)
     layer.raise_if_nonfinite()
     trace = trace_from_counts(config, B, counts, params)

@@ -370,3 +370,26 @@ def test_forward_routed_rejects_out_of_range(pkg):
     layer.forward_routed(torch.from_numpy(tokens).cuda(), (idx, w), run_router=False)
     with pytest.raises(P.IndexOutOfRange):
         layer.raise_if_nonfinite()
+
+
+@pytest.mark.parametrize("shape", [
+    (8, 2, 512, 1024, 128, "softmax"),
+    (16, 4, 256, 384, 64, "sigmoid_normalized"),
+    (60, 4, 256, 176, 96, "softmax"),
+])
+def test_unfused_gate_up_is_bit_identical(pkg, shape):
+    """PipelineParams(fused=False) (pipeline.py:316-370): separate gate / up
+    GEMMs + activation pass give exactly the fused forward's bits, like the
+    reference's fused == unfused invariant (tests/test_acceptance.py:116-134)."""
+    P = pkg
+    e, k, d, f, b, g = shape
+    tokens, wr, gate, up, down = O.make_instance(31, e, k, d, f, b)
+    layer = _layer(P, _cfg(P, e, k, d, f, g), wr, gate, up, down, b)
+    x = torch.from_numpy(tokens).cuda()
+    y_f = _np(layer.forward(x))
+    y_u = _np(layer.forward(x, fused=False))
+    bits_equal(y_u, y_f)
+    y_np, trace = P.moe_forward(tokens, wr, P.ExpertWeights(gate, up, down), _cfg(P, e, k, d, f, g),
+                                P.PipelineParams(fused=False))
+    bits_equal(y_np, y_f)
+    assert len(trace.records) == 6
