@@ -393,3 +393,25 @@ def test_unfused_gate_up_is_bit_identical(pkg, shape):
                                 P.PipelineParams(fused=False))
     bits_equal(y_np, y_f)
     assert len(trace.records) == 6
+
+
+@pytest.mark.parametrize("argv", [
+    ["--model", "Mixtral8x7B", "--trials", "3", "--batch", "16"],
+    ["--model", "DeepSeekV3", "--trials", "2", "--batch", "8"],
+    ["--experts", "60", "--top-k", "4", "--hidden-dim", "64", "--ffn-dim", "48", "--trials", "2", "--batch", "24"],
+])
+def test_gpu_verify_cli_passes(pkg, argv, tmp_path):
+    """python -m paper_2605_23911_b200 verify: the reference's verify contract
+    (cli.py:755-881) with the GPU layer under test and moeperf as the checker."""
+    pytest.importorskip("paper_2605_23911_b200.verify")
+    from paper_2605_23911_b200.verify import _import_reference, main
+    try:
+        _import_reference()
+    except RuntimeError:
+        pytest.skip("reference package not installed (baseline/_ref)")
+    out = tmp_path / "verify.json"
+    rc = main(["verify", *argv, "--format", "json", "--out", str(out)])
+    payload = __import__("json").loads(out.read_text())
+    assert rc == 0, payload
+    assert payload["status"] == "pass"
+    assert all(t["routing_exact"] and t["bitwise_fused_unfused"] and t["trace_match"] for t in payload["trials"])

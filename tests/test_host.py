@@ -156,3 +156,12 @@ def test_product_package_never_imports_the_oracle():
             if fn.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, fn)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle/", ""), fn
+
+
+def test_verify_cli_usage_errors_exit_2():
+    """Usage errors map to exit code 2 like the reference CLI (cli.py:979-992)."""
+    from paper_2605_23911_b200.verify import main
+    assert main(["verify", "--model", "NoSuchModel"]) == 2
+    assert main(["verify", "--experts", "4"]) == 2
+    assert main(["verify", "--batch", "0"]) == 2
+    assert main(["nope"]) == 2
