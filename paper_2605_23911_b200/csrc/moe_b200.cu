@@ -70,6 +70,10 @@ int chunk_rows_for(const moe_b200_config& c, int64_t B) {
   // Tokens per expert on average; big chunks keep one weight pass per expert
   // (Mixtral), small chunks for many-expert layers (DeepSeek / Qwen).
   const int64_t T = B * c.top_k;
+  if (const char* env = getenv("MOE_B200_CHUNK_ROWS")) {
+    const int v = atoi(env);
+    if (v == 128 || v == 256) return v;  // tuning hook (the FFN templates are BN 128 / 256)
+  }
   return (T > 96LL * c.num_experts) ? 256 : 128;
 }
 
@@ -636,11 +640,12 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
     p.cert_coef = ldexp((2.0 + 12.0 / q.seg_len) * (1.0 + ldexp(1.0, -20)), -53);
     p.blk_counter = hdr + kHdrBlk;
     p.gpart = ws8(ws) + L.gpart;
+    const int grid = q.grid;
     const bool wvec = (cfg->num_experts % 4) == 0;
     void (*kern)(RouterParams) = xb ? (wvec ? router_seg_kernel<true, true> : router_seg_kernel<true, false>)
                                     : (wvec ? router_seg_kernel<false, true> : router_seg_kernel<false, false>);
     MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q.smem));
-    kern<<<q.grid, kSegThreads, q.smem, s>>>(p);
+    kern<<<grid, kSegThreads, q.smem, s>>>(p);
     MOE_LAUNCH_CHECK("router_seg_kernel");
   } else if ((rc = launch_router_exact(*cfg, B, x, xb, w_router, L, ws, p, s))) {
     return rc;
