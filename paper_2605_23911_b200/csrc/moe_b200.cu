@@ -123,16 +123,15 @@ SegPlan plan_seg(const moe_b200_config& c, int64_t B) {
   q.n_tb = static_cast<int>((B + kSegTT - 1) / kSegTT);
   const int G = q.expc / kSegTE;
   const int S = kSegThreads / G;
-  // segment length: 32 steps (chain latency ~0.2 us) unless the grid is too
-  // small to fill the GPU, then shorter segments split d over more CTAs
-  q.seg_len = 32;
+  // k-blocks: one when the (token, expert) blocks alone fill >= 3/4 of the
+  // SMs (long segments amortise the per-CTA reduction / arrival overhead;
+  // a segment of L steps costs ~8L cycles of latency), otherwise enough
+  // k-blocks for ~1.5 waves, with segments of at least 8 steps
+  const long base = (long)q.n_tb * q.n_eb;
+  const int max_kb = std::max(1, (c.hidden_dim + S * 8 - 1) / (S * 8));
+  int n_kb = base * 4 >= kNumSMs * 3 ? 1 : static_cast<int>(std::min<long>(max_kb, (kNumSMs * 3 / 2 + base - 1) / base));
+  q.seg_len = ((c.hidden_dim + (long)n_kb * S - 1) / ((long)n_kb * S) + 7) / 8 * 8;
   if (const char* env = getenv("MOE_B200_SEG_LEN")) q.seg_len = std::max(8, atoi(env) / 8 * 8);
-  while (q.seg_len > 8) {
-    const int kr = S * q.seg_len;
-    const long grid = (long)q.n_tb * q.n_eb * ((c.hidden_dim + kr - 1) / kr);
-    if (grid >= kNumSMs / 2) break;
-    q.seg_len /= 2;
-  }
   q.kr = S * q.seg_len;
   q.n_kb = (c.hidden_dim + q.kr - 1) / q.kr;
   q.grid = q.n_tb * q.n_eb * q.n_kb;

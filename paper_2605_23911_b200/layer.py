@@ -296,6 +296,40 @@ class MoELayer:
                 tot[n] += ev[i].elapsed_time(ev[i + 1])
         return {n: v / iters for n, v in tot.items()}
 
+    def device_trace(self, x: torch.Tensor, iters: int = 10, flush: torch.Tensor | None = None,
+                     peak_gbs: float | None = None, peak_tflops: float | None = None) -> list:
+        """Device-measured counterpart of the reference's trace
+        (``pipeline.py:534-565`` records, ``perfmodel.py:148-249`` TileTrace
+        mode): per device launch, the CUDA-event time inside the real one-call
+        forward and the reference model's algorithmic bytes / FLOPs for the
+        stages it implements, computed from the measured expert histogram, so
+        achieved GB/s and TFLOP/s (and roofline fractions, given peaks) come
+        from measured time rather than the analytic time model."""
+        from .trace import (STAGE_DOWN, STAGE_GATE_UP, STAGE_PERMUTE, STAGE_ROUTER, STAGE_UNPERMUTE,
+                            stage_bytes, stage_flops)
+        t = self.timed_forward(x, iters=iters, flush=flush)
+        B = x.shape[0]
+        counts = self.counts.cpu().numpy().astype(np.int64)
+        groups = {"route": (STAGE_ROUTER,), "permute": (STAGE_PERMUTE,),
+                  "ffn": (STAGE_GATE_UP, STAGE_DOWN), "combine": (STAGE_UNPERMUTE,)}
+        kernels = {"route": "router (+ weight prep)", "permute": "dispatch (schedule + gather)",
+                   "ffn": "fused gate+up / down", "combine": "combine"}
+        out = []
+        for name, stages in groups.items():
+            nbytes = sum(stage_bytes(st, self.config, B, counts, element_bytes=2) for st in stages)
+            flops = sum(stage_flops(st, self.config, B) for st in stages)
+            ms = t[name]
+            rec = {"launch": kernels[name], "stages": list(stages), "time_us": ms * 1e3,
+                   "bytes": nbytes, "flops": flops,
+                   "achieved_gbs": nbytes / (ms * 1e-3) / 1e9 if ms > 0 else None,
+                   "achieved_tflops": flops / (ms * 1e-3) / 1e12 if ms > 0 else None}
+            if peak_gbs and rec["achieved_gbs"] is not None:
+                rec["hbm_frac"] = rec["achieved_gbs"] / peak_gbs
+            if peak_tflops and rec["achieved_tflops"] is not None:
+                rec["tensor_frac"] = rec["achieved_tflops"] / peak_tflops
+            out.append(rec)
+        return out
+
     def timed_stages(self, x: torch.Tensor, iters: int = 10, flush: torch.Tensor | None = None) -> dict:
         """Per-stage device time (ms, mean over ``iters``) with CUDA events between
         the five C-ABI stage calls on the current stream (optional L2 flush

@@ -415,3 +415,16 @@ def test_gpu_verify_cli_passes(pkg, argv, tmp_path):
     assert rc == 0, payload
     assert payload["status"] == "pass"
     assert all(t["routing_exact"] and t["bitwise_fused_unfused"] and t["trace_match"] for t in payload["trials"])
+
+
+def test_device_trace_records(pkg):
+    """Device-measured trace: one record per launch with the
+    reference model's bytes / FLOPs and a positive measured time."""
+    P = pkg
+    e, k, d, f, b = 8, 2, 512, 1024, 128
+    tokens, wr, gate, up, down = O.make_instance(0, e, k, d, f, b)
+    layer = _layer(P, _cfg(P, e, k, d, f, "softmax"), wr, gate, up, down, b)
+    recs = layer.device_trace(torch.from_numpy(tokens).cuda(), iters=3, peak_gbs=6500.0, peak_tflops=1650.0)
+    assert [r["launch"] for r in recs][2] == "fused gate+up / down"
+    assert all(r["time_us"] > 0 and r["bytes"] > 0 for r in recs)
+    assert recs[2]["flops"] == 6 * b * k * d * f + 5 * b * k * f  # 3 GEMMs + SiLU*up (perfmodel.py:196-213)
