@@ -63,6 +63,7 @@ struct FfnParams {
   int32_t* gu_done;          // per-chunk completed gate+up tiles, self-resetting
   int gu_unfused;            // 1: gate and up as separate tiles, fp32 out (pipeline.py:316-370 ablation)
   float* gu32;               // unfused output: tiled [proj][f/128][T_pad][128] fp32
+  int pair;                  // 1: launched as CTA pairs (clusters of 2) sharing token loads
   int dbg;                   // debug/experiment bits (0 in production)
   int tiled;                 // 1: h / ys in the tiled padded-row layouts (fused forward)
   int T_pad;                 // padded-row capacity of the tiled layouts
@@ -139,6 +140,7 @@ MOE_DEVICE void epi_bar_sync(int group) {  // the 128 threads of one epilogue gr
 
 struct TileInfo {
   int is_gu, chunk, mt, split;
+  int dummy;  // pair mode: the pair's second weight tile does not exist (odd tile count)
 };
 
 // Tile order.  Gate+up tiles come first, then down tiles.  Within each, an
@@ -148,10 +150,16 @@ struct TileInfo {
 // major, chunk minor: the chunks' reads of the SAME weight tile are adjacent
 // in the queue, run concurrently on different SMs and are served once from
 // HBM (L2 de-duplicates), keeping the weight stream near one pass.
-MOE_DEVICE TileInfo decode_tile(const FfnParams& p, int tile) {
+// Pair mode (CTA pairs sharing token loads, see ffn_kernel): a tile id names a
+// PAIR of adjacent weight tiles of the same chunk; CTA rank r takes weight
+// tile 2 * pair + r.
+MOE_DEVICE TileInfo decode_tile(const FfnParams& p, int tile, int rank = 0) {
   TileInfo t;
-  const int per_gu = p.n_mt_gu * (p.gu_unfused ? 2 : 1);
-  const int per_dn = p.n_mt_dn * p.splits;
+  t.dummy = 0;
+  const int mt_gu = p.pair ? (p.n_mt_gu + 1) / 2 : p.n_mt_gu;
+  const int mt_dn = p.pair ? (p.n_mt_dn + 1) / 2 : p.n_mt_dn;
+  const int per_gu = mt_gu * (p.gu_unfused ? 2 : 1);
+  const int per_dn = mt_dn * p.splits;
   const int nch = __ldg(p.n_chunks);
   const int n_gu = nch * per_gu;
   int q, per;
@@ -177,15 +185,27 @@ MOE_DEVICE TileInfo decode_tile(const FfnParams& p, int tile) {
     t.mt = wt / p.splits;
     t.split = wt % p.splits;
   }
+  if (p.pair) {
+    t.mt = 2 * t.mt + rank;
+    t.dummy = t.mt >= (t.is_gu ? p.n_mt_gu : p.n_mt_dn);
+  }
   return t;
 }
 
-template <int kBN, int kV>
+// kPair: the kernel runs as clusters of two CTAs that process the two halves
+// of a pair tile (adjacent weight tiles of the same token chunk).  Each CTA
+// streams its own weights, but the shared token k-blocks are loaded ONCE per
+// pair: each CTA loads half the 32-row boxes with TMA multicast into both CTAs'
+// token slots, and each MMA releases a token slot in both CTAs (multicast
+// commit), halving the token traffic per SM.  Rank 0 owns the tile queue and
+// hands each pair tile to rank 1 through distributed shared memory.
+template <int kBN, int kV, bool kPair = false>
 __global__ void __launch_bounds__(kFfnThreads, 1)
 ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CUtensorMap tm_wu,
            const __grid_constant__ CUtensorMap tm_xp, const __grid_constant__ CUtensorMap tm_wd,
            const __grid_constant__ CUtensorMap tm_h, const FfnParams p) {
   using C = FfnCfg<kBN, kV>;
+  const int rank = kPair ? static_cast<int>(cluster_ctarank()) : 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* a_ring = smem;
@@ -219,20 +239,40 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
     }
     for (int s = 0; s < C::kBStages; ++s) {
       mbar_init(b_full + s, 1);
-      mbar_init(b_empty + s, 1);
+      mbar_init(b_empty + s, kPair ? 2 : 1);  // pair: both CTAs' MMAs release the shared slot
     }
     mbar_init(tmem_full, 1);
     mbar_init(tmem_empty, 32 * kEpiWarps);
     for (int s = 0; s < kSchedSlots; ++s) {
       mbar_init(sched_full + s, 1);
-      mbar_init(sched_empty + s, 1 + kEpiWarps);  // MMA lane + one lane per epilogue warp
+      // MMA lane + one lane per epilogue warp (pair: of both CTAs, plus rank 1's producer)
+      mbar_init(sched_empty + s, kPair ? 2 * (1 + kEpiWarps) + 1 : 1 + kEpiWarps);
     }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_base_smem);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // peer barriers initialised before any remote access
+  else __syncthreads();
   tc_fence_after();
+  // pair: remote (peer-rank) addresses of the scheduler ring
+  const uint32_t peer = static_cast<uint32_t>(rank ^ 1);
+  const uint32_t r_sched_empty0 = kPair ? map_to_rank(smem_u32(sched_empty), 0) : 0;  // rank 0's ring
+  const uint32_t r_sched_full1 = kPair ? map_to_rank(smem_u32(sched_full), 1) : 0;    // rank 1's ring
+  const uint32_t r_sched_tile1 = kPair ? map_to_rank(smem_u32(sched_tile), 1) : 0;
+  (void)peer;
+  // consumer side of the scheduler ring: read slot, release it (pair: on rank 0)
+  auto sched_read = [&](int slot, uint32_t sphase, bool release_lane, bool warp_sync) -> int {
+    if (kPair && rank == 1) mbar_wait_cluster(sched_full + slot, sphase);
+    else mbar_wait(sched_full + slot, sphase);
+    const int t = sched_tile[slot];
+    if (warp_sync) __syncwarp();
+    if (release_lane) {
+      if (kPair && rank == 1) mbar_arrive_cluster(r_sched_empty0 + slot * 8);
+      else mbar_arrive(sched_empty + slot);
+    }
+    return t;
+  };
   const uint32_t tmem_base = *tmem_base_smem;
   // prologue done: let the combine grid queue up, then wait for the dispatch
   // (chunk table, permuted tokens) to be complete and visible
@@ -240,7 +280,9 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
   pdl_wait();
 
   const int nch = __ldg(p.n_chunks);
-  const int total_tiles = nch * (p.n_mt_gu * (p.gu_unfused ? 2 : 1) + p.n_mt_dn * p.splits);
+  const int mt_gu_q = kPair ? (p.n_mt_gu + 1) / 2 : p.n_mt_gu;  // queue entries per chunk
+  const int mt_dn_q = kPair ? (p.n_mt_dn + 1) / 2 : p.n_mt_dn;
+  const int total_tiles = nch * (mt_gu_q * (p.gu_unfused ? 2 : 1) + mt_dn_q * p.splits);
   const int nkb_gu = (p.d + kBK - 1) / kBK;
   const int nkb_dn = (p.f + kBK - 1) / kBK;
 
@@ -253,17 +295,28 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       int slot = 0;
       uint32_t sphase = 0;
       while (true) {
-        const int tile = atomicAdd(p.work_counter, 1);
-        if (p.trace && tile < total_tiles) {
-          p.trace[tile * 8 + 0] = smid();
-          p.trace[tile * 8 + 1] = globaltimer();
+        int tile;
+        if (!kPair || rank == 0) {
+          tile = atomicAdd(p.work_counter, 1);
+          if (p.trace && tile < total_tiles) {
+            p.trace[tile * 8 + 0] = smid();
+            p.trace[tile * 8 + 1] = globaltimer();
+          }
+          const int v = tile < total_tiles ? tile : -1;
+          mbar_wait(sched_empty + slot, sphase ^ 1);
+          sched_tile[slot] = v;
+          if constexpr (kPair) {  // hand the pair tile to rank 1 through DSMEM
+            st_cluster_u32(r_sched_tile1 + slot * 4, static_cast<uint32_t>(v));
+            mbar_arrive_cluster(r_sched_full1 + slot * 8);
+          }
+          mbar_arrive(sched_full + slot);
+        } else {
+          tile = sched_read(slot, sphase, true, false);
+          if (tile < 0) tile = total_tiles;
         }
-        mbar_wait(sched_empty + slot, sphase ^ 1);
-        sched_tile[slot] = tile < total_tiles ? tile : -1;
-        mbar_arrive(sched_full + slot);
         if (++slot == kSchedSlots) { slot = 0; sphase ^= 1; }
         if (tile >= total_tiles) break;
-        const TileInfo ti = decode_tile(p, tile);
+        const TileInfo ti = decode_tile(p, tile, rank);
         const int4 ch = __ldg(p.chunk_tab + ti.chunk);
         const int n_mma = max(16, (ch.z + 15) & ~15);
         const int nbox = (n_mma + kBoxRows - 1) / kBoxRows;
@@ -283,7 +336,10 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         }
         if (p.trace) p.trace[tile * 8 + 2] = globaltimer();
         for (int kb = kb0; kb < kb1; ++kb) {
-          if (ti.is_gu && p.gu_unfused) {
+          if (ti.dummy) {
+            // pair mode, missing second tile: no weights; still supply this
+            // CTA's half of the shared token k-block below
+          } else if (ti.is_gu && p.gu_unfused) {
             // one projection per tile: a single weight slot per k-block
             const int krow = ch.x * p.d + kb * kBK;
             const CUtensorMap* tw = ti.split ? &tm_wu : &tm_wg;
@@ -327,13 +383,25 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             mbar_arrive(b_full + bs);
           } else if (mbar_arrive_expect_tx(b_full + bs, b_bytes), ti.is_gu || !p.tiled) {
             const CUtensorMap* tb = ti.is_gu ? &tm_xp : &tm_h;
-            for (int b = 0; b < nbox; ++b)
-              tma_load_2d(tb, b_full + bs, sb + b * kBoxRows * kBK * 2, kb * kBK, ch.y + b * kBoxRows);
+            for (int b = 0; b < nbox; ++b) {
+              if constexpr (kPair) {  // this CTA's half of the boxes, into both CTAs' slot
+                if ((b & 1) == rank)
+                  tma_load_2d_mc(tb, b_full + bs, sb + b * kBoxRows * kBK * 2, kb * kBK, ch.y + b * kBoxRows, 3);
+              } else {
+                tma_load_2d(tb, b_full + bs, sb + b * kBoxRows * kBK * 2, kb * kBK, ch.y + b * kBoxRows);
+              }
+            }
           } else {
             // tiled h: [f-tile][padded row][128]; k-block kb lives in f-tile kb/2, column half kb%2
             const int hrow = (kb >> 1) * p.T_pad + ch.w;
-            for (int b = 0; b < nbox; ++b)
-              tma_load_2d(&tm_h, b_full + bs, sb + b * kBoxRows * kBK * 2, (kb & 1) * kBK, hrow + b * kBoxRows);
+            for (int b = 0; b < nbox; ++b) {
+              if constexpr (kPair) {
+                if ((b & 1) == rank)
+                  tma_load_2d_mc(&tm_h, b_full + bs, sb + b * kBoxRows * kBK * 2, (kb & 1) * kBK, hrow + b * kBoxRows, 3);
+              } else {
+                tma_load_2d(&tm_h, b_full + bs, sb + b * kBoxRows * kBK * 2, (kb & 1) * kBK, hrow + b * kBoxRows);
+              }
+            }
           }
           if (++bs == C::kBStages) { bs = 0; bph ^= 1; }
         }
@@ -347,13 +415,10 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
     int slot = 0;
     uint32_t sphase = 0;
     while (true) {
-      mbar_wait(sched_full + slot, sphase);
-      const int tile = sched_tile[slot];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(sched_empty + slot);
+      const int tile = sched_read(slot, sphase, lane == 0, true);
       if (++slot == kSchedSlots) { slot = 0; sphase ^= 1; }
       if (tile < 0) break;
-      const TileInfo ti = decode_tile(p, tile);
+      const TileInfo ti = decode_tile(p, tile, rank);
       const int4 ch = __ldg(p.chunk_tab + ti.chunk);
       const int n_mma = max(16, (ch.z + 15) & ~15);
       const uint32_t idesc = make_idesc_bf16(kBM, n_mma, /*a MN-major*/ 1, /*b K-major*/ 0);
@@ -368,6 +433,18 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       tc_fence_after();
       if (p.trace && lane == 0) p.trace[tile * 8 + 5] = globaltimer();
       for (int kb = kb0; kb < kb1; ++kb) {
+        if (ti.dummy) {
+          // pair mode, missing second tile: consume and release the shared token slot
+          mbar_wait(b_full + bs, bph);
+          tc_fence_after();
+          if (elect_one()) {
+            mma_commit_mc(b_empty + bs, 3);
+            if (kb == kb1 - 1) mma_commit(tmem_full);
+          }
+          __syncwarp();
+          if (++bs == C::kBStages) { bs = 0; bph ^= 1; }
+          continue;
+        }
         const bool single = ti.is_gu && p.gu_unfused;  // one weight slot, one accumulator
         const int as0 = as;
         mbar_wait(a_full + as, aph);
@@ -396,7 +473,8 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           }
           mma_commit(a_empty + as0);
           if (!single) mma_commit(a_empty + as1);
-          mma_commit(b_empty + bs);
+          if constexpr (kPair) mma_commit_mc(b_empty + bs, 3);  // the slot is shared by the pair
+          else mma_commit(b_empty + bs);
           if (kb == kb1 - 1) mma_commit(tmem_full);
         }
         __syncwarp();
@@ -415,16 +493,19 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
     int slot = 0;
     uint32_t sphase = 0;
     while (true) {
-      mbar_wait(sched_full + slot, sphase);
-      const int tile = sched_tile[slot];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(sched_empty + slot);
+      const int tile = sched_read(slot, sphase, lane == 0, true);
       if (++slot == kSchedSlots) { slot = 0; sphase ^= 1; }
       if (tile < 0) break;
-      const TileInfo ti = decode_tile(p, tile);
+      const TileInfo ti = decode_tile(p, tile, rank);
       const int4 ch = __ldg(p.chunk_tab + ti.chunk);
       mbar_wait(tmem_full, acc_phase);
       tc_fence_after();
+      if (ti.dummy) {  // pair mode, missing second tile: nothing to write
+        tc_fence_before();
+        mbar_arrive(tmem_empty);
+        acc_phase ^= 1;
+        continue;
+      }
       if (p.trace && warp == 4 && lane == 0) p.trace[tile * 8 + 4] = globaltimer();
       // Staged store protocol, per 32-row chunk of this group: (issuer) make the
       // staging buffer free -> group barrier -> every thread writes its feature
@@ -593,7 +674,10 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
 
   if ((warp == 4 || warp == 8) && lane == 0) bulk_wait_all();
   tc_fence_before();
-  __syncthreads();
+  // pair: neither CTA leaves while its peer may still multicast into its
+  // shared memory or arrive on its barriers
+  if constexpr (kPair) cluster_sync_all();
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem_base);

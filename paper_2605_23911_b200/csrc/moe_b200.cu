@@ -335,18 +335,37 @@ int launch_router_x(const CUtensorMap& tmx, const RouterParams& p, const RouterP
   return launch_router_t<kBf16, 1, 1, 128>(tmx, p, plan, s);
 }
 
-template <int kBN, int kV>
+template <int kBN, int kV, bool kPair = false>
 int launch_ffn_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm, const CUtensorMap& dm,
                  const CUtensorMap& e, const FfnParams& p, int grid, cudaStream_t s) {
   using C = FfnCfg<kBN, kV>;
+  auto kern = ffn_kernel<kBN, kV, kPair>;
   static bool attr_set[64] = {};
   int dev = 0;
   MOE_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-    MOE_CUDA(cudaFuncSetAttribute(ffn_kernel<kBN, kV>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+    MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
-  cudaError_t err = launch_pdl(ffn_kernel<kBN, kV>, dim3(grid), dim3(kFfnThreads), C::kSmemBytes, s, a, b, cm, dm, e, p);
+  cudaError_t err;
+  if constexpr (kPair) {
+    // clusters of two CTAs (same TPC) sharing token loads
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kFfnThreads);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    err = cudaLaunchKernelEx(&cfg, kern, a, b, cm, dm, e, p);
+  } else {
+    err = launch_pdl(kern, dim3(grid), dim3(kFfnThreads), C::kSmemBytes, s, a, b, cm, dm, e, p);
+  }
   if (err != cudaSuccess) return cuda_fail(err, "ffn launch");
   return MOE_B200_OK;
 }
@@ -354,6 +373,10 @@ int launch_ffn_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& 
 int launch_ffn_kernel(int bn, int variant, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm,
                       const CUtensorMap& dm, const CUtensorMap& e, const FfnParams& p, int grid,
                       cudaStream_t s) {
+  if (p.pair) {
+    return bn == 256 ? launch_ffn_t<256, 2, true>(a, b, cm, dm, e, p, grid, s)
+                     : launch_ffn_t<128, 2, true>(a, b, cm, dm, e, p, grid, s);
+  }
   if (bn == 256)
     return variant == 3 ? launch_ffn_t<256, 3>(a, b, cm, dm, e, p, grid, s) : launch_ffn_t<256, 2>(a, b, cm, dm, e, p, grid, s);
   return variant == 3 ? launch_ffn_t<128, 3>(a, b, cm, dm, e, p, grid, s) : launch_ffn_t<128, 2>(a, b, cm, dm, e, p, grid, s);
@@ -414,9 +437,15 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.T_pad = L.T_pad;
   p.trace = g_ffn_trace;
   if (const char* env = getenv("MOE_B200_FFN_DEBUG")) p.dbg = atoi(env);
-  const long max_tiles = (long)L.max_chunks * (p.n_mt_gu * (p.gu_unfused ? 2 : 1) + p.n_mt_dn * p.splits);
-  const int grid = static_cast<int>(std::max(1L, std::min<long>(kNumSMs, max_tiles)));
   const int bn = chunk_rows_for(c, B);
+  // CTA pairs sharing token loads: fused mode with large token chunks, where
+  // token re-reads are a real share of the L2 -> SM traffic (MOE_B200_FFN_PAIR
+  // forces it on / off)
+  p.pair = (mode == kFfnFused && bn == 256) ? 1 : 0;
+  if (const char* env = getenv("MOE_B200_FFN_PAIR")) p.pair = (atoi(env) != 0 && mode == kFfnFused) ? 1 : 0;
+  long max_tiles = (long)L.max_chunks * (p.n_mt_gu * (p.gu_unfused ? 2 : 1) + p.n_mt_dn * p.splits);
+  int grid = static_cast<int>(std::max(1L, std::min<long>(kNumSMs, max_tiles)));
+  if (p.pair) grid = std::max(2, grid & ~1);  // whole clusters
   int variant = 2;
   if (const char* env = getenv("MOE_B200_FFN_VARIANT")) variant = atoi(env);
   return launch_ffn_kernel(bn, variant, m_wg, m_wu, m_xp, m_wd, m_h, p, grid, s);
