@@ -47,8 +47,27 @@ constexpr int kSegThreads = 256;
 constexpr int kSegTT = 4;  // tokens per CTA (and per thread tile)
 constexpr int kSegTE = 4;  // experts per thread tile
 
+// Non-finite inputs (require_finite, linalg.py:38-42): finite fp32 operands
+// cannot make the fp64 fold non-finite (|x w| <= 1.2e77, d < 2^20 terms), so a
+// non-finite sum means the token row or the expert column holds an Inf / NaN.
+// Only then are both scanned to set the right flag (off the hot loop).
+template <bool kXBf16>
+MOE_DEVICE void flag_nonfinite_inputs(const RouterParams& p, int t, int e) {
+  bool bad_x = false, bad_w = false;
+  for (int k = 0; k < p.d; ++k) {
+    const float xv = kXBf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(p.x)[(size_t)t * p.d + k])
+                            : static_cast<const float*>(p.x)[(size_t)t * p.d + k];
+    bad_x |= !isfinite(xv);
+    bad_w |= !isfinite(p.wr[(size_t)k * p.E + e]);
+  }
+  if (bad_x) atomicOr(p.flags, 1u);
+  if (bad_w) atomicOr(p.flags, 2u);
+}
+
+template <bool kXBf16>
 MOE_DEVICE void seg_finalize(const RouterParams& p, int t, int e, double s, double A) {
   if (t >= p.B || e >= p.E) return;
+  if (!isfinite(s) || !isfinite(A)) flag_nonfinite_inputs<kXBf16>(p, t, e);
   float2 r;
   if (!(A > 0.0) || !isfinite(s) || p.force_exact) {
     r = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));  // unknown: recompute exactly
@@ -92,7 +111,6 @@ __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const Router
       acc[i][j] = -0.0;
       mag[i][j] = 0.0;
     }
-  bool bad_x = false, bad_w = false;
   bool tok_ok[TT];
 #pragma unroll
   for (int i = 0; i < TT; ++i) tok_ok[i] = (t0 + i) < p.B;
@@ -131,14 +149,6 @@ __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const Router
       float xn[TT][8], wn[8][TE];
       if (k + 8 < kend) load_blk(k + 8, xn, wn);
 #pragma unroll
-      for (int i = 0; i < TT; ++i)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) bad_x |= !isfinite(xc[i][q]);
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-#pragma unroll
-        for (int j = 0; j < TE; ++j) bad_w |= !isfinite(wc[r][j]);
-#pragma unroll
       for (int r = 0; r < 8; ++r) {
         double xd[TT], wd[TE];
 #pragma unroll
@@ -163,8 +173,6 @@ __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const Router
         for (int j = 0; j < TE; ++j) wc[r][j] = wn[r][j];
     }
   }
-  if (bad_x) atomicOr(p.flags, 1u);
-  if (bad_w) atomicOr(p.flags, 2u);
 
   stamp(2);
   // ---- per-chain reduction of the segment partials --------------------------
@@ -215,7 +223,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const Router
     }
     const int t = t0 + c / p.expc, e = e0 + c % p.expc;
     if (single_kb) {
-      seg_finalize(p, t, e, C, A);
+      seg_finalize<kXBf16>(p, t, e, C, A);
     } else {
       gpart[((size_t)(tb * p.n_eblocks + eb) * p.n_kb + kb) * chains + c] = make_double2(C, A);
     }
@@ -233,7 +241,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const Router
         A += v.y + static_cast<double>(Kb) * fabs(Gs);
         Gs += v.x;
       }
-      seg_finalize(p, t0 + c / p.expc, e0 + c % p.expc, Gs, A);
+      seg_finalize<kXBf16>(p, t0 + c / p.expc, e0 + c % p.expc, Gs, A);
     }
     if (tid == 0) p.blk_counter[tb * p.n_eblocks + eb] = 0;
     stamp(5);

@@ -428,3 +428,18 @@ def test_device_trace_records(pkg):
     assert [r["launch"] for r in recs][2] == "fused gate+up / down"
     assert all(r["time_us"] > 0 and r["bytes"] > 0 for r in recs)
     assert recs[2]["flops"] == 6 * b * k * d * f + 5 * b * k * f  # 3 GEMMs + SiLU*up (perfmodel.py:196-213)
+
+
+@pytest.mark.parametrize("mode", ["auto", "exact_kernel"])
+def test_nonfinite_router_weight_raises(pkg, mode, monkeypatch):
+    """require_finite on router_weight (router.py:118-130): the segment router
+    flags it from the non-finite fold, the exact kernel from its weight prep."""
+    P = pkg
+    for k_, v_ in ROUTER_MODES[mode].items():
+        monkeypatch.setenv(k_, v_)
+    e, k, d, f, b = 8, 2, 128, 64, 16
+    tokens, wr, gate, up, down = O.make_instance(4, e, k, d, f, b)
+    wr = wr.copy()
+    wr[7, 3] = np.inf
+    with pytest.raises(P.NonFiniteInput, match="router_weight"):
+        P.moe_forward(tokens, wr, P.ExpertWeights(gate, up, down), _cfg(P, e, k, d, f, "softmax"))
