@@ -219,10 +219,25 @@ int moe_b200_launches_per_forward(const moe_b200_config* cfg, int64_t num_tokens
  *   out_rows[r] = silu(x_r Wg_e) * (x_r Wu_e) @ Wd_e   (pipeline.py:250-313, 186-247)
  * Bit-identical, row by row, to the single-GPU forward's per-slot expert output.
  *   counts   (E_local) int32 device; xp (n_rows, d) bf16; out_rows (n_rows, d) fp32
- * Workspace: moe_b200_workspace_size(cfg with top_k = 1, n_rows). */
-int moe_b200_expert_ffn(const moe_b200_config* cfg, int64_t n_rows, const int32_t* counts,
+ * down_splits: the K-split count of the down projection (its fp32 partial
+ * sums are added in split order, so a row's bits depend on it).  Pass
+ * moe_b200_down_splits(global cfg, global token count) to reproduce the
+ * single-GPU forward bit for bit; 0 derives it from (cfg, n_rows).
+ * Workspace: moe_b200_expert_ffn_workspace_size(cfg, max rows, largest
+ * down_splits passed). */
+int moe_b200_expert_ffn(const moe_b200_config* cfg, int64_t n_rows, int down_splits, const int32_t* counts,
                         const void* xp, const void* w_gate, const void* w_up, const void* w_down,
                         float* out_rows, void* ws, size_t ws_bytes, void* stream);
+
+/* Workspace bytes for moe_b200_expert_ffn over up to max_rows rows with
+ * split counts up to down_splits_max (0: the count derived from cfg). */
+int moe_b200_expert_ffn_workspace_size(const moe_b200_config* cfg, int64_t max_rows, int down_splits_max,
+                                       size_t* bytes);
+
+/* The K-split count of the down projection that moe_b200_forward uses for
+ * num_tokens tokens (more splits for small batches, where few experts are
+ * active and the down tiles would otherwise not fill the SMs). */
+int moe_b200_down_splits(const moe_b200_config* cfg, int64_t num_tokens, int* splits);
 
 /* Row gather dst[r] = src[idx[r]] (row_bytes a multiple of 16): the reorder
  * between the all-to-all layout (source-major) and expert-major rows. */

@@ -67,7 +67,9 @@ SIGNATURES = {
                                        _SZ, _P]),
     "moe_b200_forward_timed": (_INT, [_CFG, _I64, _P, _INT, _P, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _P, _P, _P, _SZ, _P,
                                       ctypes.POINTER(ctypes.c_void_p)]),
-    "moe_b200_expert_ffn": (_INT, [_CFG, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_expert_ffn": (_INT, [_CFG, _I64, ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_expert_ffn_workspace_size": (_INT, [_CFG, _I64, ctypes.c_int, ctypes.POINTER(_SZ)]),
+    "moe_b200_down_splits": (_INT, [_CFG, _I64, ctypes.POINTER(ctypes.c_int)]),
     "moe_b200_gather_rows": (_INT, [_I64, _I64, _P, _P, _P, _P]),
     "moe_b200_combine_rows": (_INT, [_CFG, _I64, _P, _P, _P, _P, _INT, _P]),
     "moe_b200_read_flags": (_INT, [_CFG, _I64, _P, _SZ, ctypes.POINTER(ctypes.c_uint32), _P]),

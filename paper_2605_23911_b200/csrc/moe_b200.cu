@@ -77,17 +77,38 @@ int chunk_rows_for(const moe_b200_config& c, int64_t B) {
   return (T > 96LL * c.num_experts) ? 256 : 128;
 }
 
-// K splits of a down tile (a pair of 128-row hidden tiles): S = round(f/2d),
-// i.e. down tiles stream about twice the weight bytes of a gate+up tile
-// (measured best on Mixtral: S=2 beats 3 and 4 once the partial-sum traffic
-// of the combine is counted).  Partials are reduced
-// deterministically in combine.  MOE_B200_DOWN_SPLITS overrides (tuning).
-void down_splits(const moe_b200_config& c, int* splits, int* kb_per_split) {
+// Expected number of experts with at least one routed row under uniform top-k
+// routing: E (1 - (1 - k/E)^B).
+double expected_active_experts(const moe_b200_config& c, int64_t B) {
+  const double E = c.num_experts;
+  return std::max(1.0, E * (1.0 - std::pow(1.0 - c.top_k / E, static_cast<double>(B))));
+}
+
+// K splits of a down tile (a pair of 128-row hidden tiles).  Large batches:
+// S = round(f/2d), i.e. down tiles stream about twice the weight bytes of a
+// gate+up tile (measured best on Mixtral-512: S=2 beats 3 and 4 once the
+// partial-sum traffic of the combine is counted).  Small batches have few
+// active experts, so few down tiles: split until about 256 down tiles (~1.7
+// waves) exist, keeping >= 6 k-blocks per split (measured Mixtral B=1/2/4:
+// S=8/6/4 -> 161->131, 203->182, 248->229 us; B=16 keeps S=2; Qwen B=1/4:
+// S=4 -> 59->53, 82->76 us).  Partials are reduced deterministically in
+// combine.  MOE_B200_DOWN_SPLITS overrides (tuning).
+int down_split_count(const moe_b200_config& c, int64_t B, const char* env) {
   const int nkb = (c.ffn_dim + kBK - 1) / kBK;
+  const int n_dp = (c.hidden_dim + 2 * kBM - 1) / (2 * kBM);
   int s = static_cast<int>((c.ffn_dim + c.hidden_dim) / (2 * c.hidden_dim));  // round(f / 2d)
-  if (const char* env = getenv("MOE_B200_DOWN_SPLITS")) s = atoi(env);
-  s = std::max(1, std::min(s, 8));
-  s = std::min(s, nkb);
+  const int fill = static_cast<int>(std::lround(256.0 / (n_dp * expected_active_experts(c, B))));
+  s = std::max(s, std::min(fill, nkb / 6));
+  if (env && atoi(env) > 0) s = atoi(env);  // 0: the rule above
+  s = std::max(1, std::min(s, 16));
+  return std::min(s, nkb);
+}
+
+// s_force > 0: a caller-chosen count (the expert-parallel ranks use the global
+// layer's count so their rows match the single-GPU forward bit for bit)
+void down_splits(const moe_b200_config& c, int64_t B, int* splits, int* kb_per_split, int s_force = 0) {
+  const int nkb = (c.ffn_dim + kBK - 1) / kBK;
+  const int s = s_force > 0 ? std::min(std::min(s_force, 16), nkb) : down_split_count(c, B, getenv("MOE_B200_DOWN_SPLITS"));
   int kps = (nkb + s - 1) / s;
   *kb_per_split = kps;
   *splits = (nkb + kps - 1) / kps;
@@ -141,12 +162,12 @@ SegPlan plan_seg(const moe_b200_config& c, int64_t B) {
   return q;
 }
 
-Layout layout_for(const moe_b200_config& c, int64_t B) {
+Layout layout_for(const moe_b200_config& c, int64_t B, int s_force = 0) {
   Layout L{};
   const int64_t T = B * c.top_k;
   const int bn = chunk_rows_for(c, B);
   L.max_chunks = static_cast<int>(std::min<int64_t>(c.num_experts, T) + T / bn + 1);
-  down_splits(c, &L.splits, &L.kb_per_split);
+  down_splits(c, B, &L.splits, &L.kb_per_split, s_force);
   // tiled layouts: experts start 16-row aligned in a padded row space
   L.T_pad = static_cast<int>(((T + 15LL * std::min<int64_t>(c.num_experts, T)) + 15) / 16 * 16);
   L.n_ft = (c.ffn_dim + kBM - 1) / kBM;
@@ -200,8 +221,8 @@ int check_config(const moe_b200_config* c) {
   return MOE_B200_OK;
 }
 
-int check_ws(const moe_b200_config* c, int64_t B, void* ws, size_t ws_bytes, Layout* L) {
-  *L = layout_for(*c, B);
+int check_ws(const moe_b200_config* c, int64_t B, void* ws, size_t ws_bytes, Layout* L, int s_force = 0) {
+  *L = layout_for(*c, B, s_force);
   if (!ws || ws_bytes < L->total) {
     g_last_error = "workspace too small";
     return MOE_B200_ERR_WORKSPACE;
@@ -593,7 +614,18 @@ int moe_b200_workspace_size(const moe_b200_config* cfg, int64_t max_tokens, size
   int rc = check_config(cfg);
   if (rc) return rc;
   if (max_tokens < 0 || !bytes) return MOE_B200_ERR_INVALID_VALUE;
-  *bytes = layout_for(*cfg, max_tokens).total;
+  // the down-split count falls as B grows (down_split_count) while the padded
+  // row space grows: size for the largest B of every split count <= max_tokens
+  size_t total = layout_for(*cfg, max_tokens).total;
+  const char* env = getenv("MOE_B200_DOWN_SPLITS");
+  const int s_last = down_split_count(*cfg, max_tokens, env);
+  int s_prev = down_split_count(*cfg, 1, env);
+  for (int64_t b = 2; b <= max_tokens && s_prev > s_last; ++b) {
+    const int s_b = down_split_count(*cfg, b, env);
+    if (s_b != s_prev) total = std::max(total, layout_for(*cfg, b - 1).total);
+    s_prev = s_b;
+  }
+  *bytes = total;
   return MOE_B200_OK;
 }
 
@@ -1009,7 +1041,28 @@ int moe_b200_io_sync(moe_b200_io* io) {
 
 // --------------------------- expert parallelism --------------------------------
 
-int moe_b200_expert_ffn(const moe_b200_config* cfg, int64_t n_rows, const int32_t* counts,
+int moe_b200_down_splits(const moe_b200_config* cfg, int64_t num_tokens, int* splits) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (num_tokens < 0 || !splits) return MOE_B200_ERR_INVALID_VALUE;
+  int kps = 0;
+  down_splits(*cfg, std::max<int64_t>(num_tokens, 1), splits, &kps);
+  return MOE_B200_OK;
+}
+
+int moe_b200_expert_ffn_workspace_size(const moe_b200_config* cfg, int64_t max_rows, int down_splits_max,
+                                       size_t* bytes) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (max_rows < 0 || down_splits_max < 0 || !bytes) return MOE_B200_ERR_INVALID_VALUE;
+  moe_b200_config c1 = *cfg;
+  c1.top_k = 1;
+  if (down_splits_max == 0) return moe_b200_workspace_size(&c1, max_rows, bytes);
+  *bytes = layout_for(c1, std::max<int64_t>(max_rows, 1), down_splits_max).total;
+  return MOE_B200_OK;
+}
+
+int moe_b200_expert_ffn(const moe_b200_config* cfg, int64_t n_rows, int down_splits, const int32_t* counts,
                         const void* xp, const void* w_gate, const void* w_up, const void* w_down,
                         float* out_rows, void* ws, size_t ws_bytes, void* stream) {
   int rc = check_config(cfg);
@@ -1021,7 +1074,8 @@ int moe_b200_expert_ffn(const moe_b200_config* cfg, int64_t n_rows, const int32_
   moe_b200_config c1 = *cfg;
   c1.top_k = 1;
   Layout L;
-  if ((rc = check_ws(&c1, n_rows, ws, ws_bytes, &L))) return rc;
+  if (down_splits < 0) return MOE_B200_ERR_INVALID_VALUE;
+  if ((rc = check_ws(&c1, n_rows, ws, ws_bytes, &L, down_splits))) return rc;
   if (L.max_chunks > kChunkCap || c1.num_experts > 1024) return MOE_B200_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int32_t* hdr = reinterpret_cast<int32_t*>(ws);

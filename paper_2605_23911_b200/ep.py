@@ -107,20 +107,32 @@ class CudaOps:
                                                  self._stream(self.device)), "gather_rows")
         return dst
 
-    def expert_ffn(self, counts, xp):
+    def _down_splits(self, tokens):
+        s = ctypes.c_int(0)
+        _lib.check(self.lib.moe_b200_down_splits(ctypes.byref(self.cfgk), max(int(tokens), 1), ctypes.byref(s)),
+                   "down_splits")
+        return s.value
+
+    def expert_ffn(self, counts, xp, global_tokens):
+        """Local expert rows; the down projection uses the K-split count of the
+        single-GPU forward over ``global_tokens`` tokens, so every row is
+        bit-identical to that forward's."""
         n = xp.shape[0]
         out = torch.empty((n, self.w.hidden_pad), dtype=torch.float32, device=self.device)
         if n == 0:
             return out
+        splits = self._down_splits(global_tokens)
         need = ctypes.c_size_t(0)
-        _lib.check(self.lib.moe_b200_workspace_size(ctypes.byref(self.cfg1), n, ctypes.byref(need)), "ws")
+        # the split count falls as the batch grows: size for the largest (1 token)
+        _lib.check(self.lib.moe_b200_expert_ffn_workspace_size(ctypes.byref(self.cfg1), n, self._down_splits(1),
+                                                               ctypes.byref(need)), "ws")
         if need.value > self._ws_bytes:
             self._ws_bytes = int(need.value * 1.25)
             self._ws = torch.empty(self._ws_bytes, dtype=torch.uint8, device=self.device)
             _lib.check(self.lib.moe_b200_workspace_init(ctypes.byref(self.cfg1), n, self._ptr(self._ws),
                                                         self._ws_bytes, self._stream(self.device)), "ws_init")
         c = counts.to(torch.int32).contiguous()
-        _lib.check(self.lib.moe_b200_expert_ffn(ctypes.byref(self.cfg1), n, self._ptr(c), self._ptr(xp),
+        _lib.check(self.lib.moe_b200_expert_ffn(ctypes.byref(self.cfg1), n, splits, self._ptr(c), self._ptr(xp),
                                                 self._ptr(self.w.gate), self._ptr(self.w.up), self._ptr(self.w.down),
                                                 self._ptr(out), self._ptr(self._ws), self._ws_bytes,
                                                 self._stream(self.device)), "expert_ffn")
@@ -161,22 +173,24 @@ class ExpertParallelMoE:
         B = x.shape[0]
         idx, w, counts, fwd, inv = self.ops.route(x)
         xp = self.ops.permute(x, fwd, k)  # local expert-major rows (bf16)
-        # counts exchange (the one host sync): per (src, local expert)
+        # counts exchange (the one host sync): per (src, local expert), plus each
+        # source's token count (the global batch fixes the down K-split count)
         counts_h = counts.to("cpu", torch.int64).numpy() if counts.is_cuda else counts.numpy().astype(np.int64)
-        send_counts = np.concatenate([counts_h[lo:hi] for lo, hi in self.ranges])
-        recv_counts = torch.zeros(self.world * self.local_cfg.num_experts, dtype=torch.int64)
+        send_counts = np.concatenate([np.append(counts_h[lo:hi], B) for lo, hi in self.ranges])
         send_t = torch.from_numpy(send_counts)
+        n_loc = self.local_cfg.num_experts
         if self.world > 1:
-            split = [hi - lo for lo, hi in self.ranges]
-            recv_split = [self.local_cfg.num_experts] * self.world
+            split = [hi - lo + 1 for lo, hi in self.ranges]
+            recv_split = [n_loc + 1] * self.world
             dev = self.device if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
-            rc = torch.zeros(self.world * self.local_cfg.num_experts, dtype=torch.int64, device=dev)
+            rc = torch.zeros(self.world * (n_loc + 1), dtype=torch.int64, device=dev)
             dist.all_to_all_single(rc, send_t.to(dev), output_split_sizes=recv_split, input_split_sizes=split,
                                    group=self.group)
-            recv_counts = rc.cpu()
+            recv_all = rc.cpu().numpy().reshape(self.world, n_loc + 1)
         else:
-            recv_counts = send_t.clone()
-        recv_counts = recv_counts.numpy().reshape(self.world, self.local_cfg.num_experts)
+            recv_all = send_counts.reshape(1, n_loc + 1)
+        global_tokens = int(recv_all[:, -1].sum())
+        recv_counts = recv_all[:, :-1]
         send_rows = [int(counts_h[lo:hi].sum()) for lo, hi in self.ranges]
         recv_rows = [int(r) for r in recv_counts.sum(axis=1)]
         # dispatch
@@ -190,7 +204,7 @@ class ExpertParallelMoE:
         inv_order_t = torch.from_numpy(inv_order.astype(np.int32)).to(xp.device)
         xe = self.ops.gather_rows(recv, order_t)
         local_counts = torch.from_numpy(recv_counts.sum(axis=0).astype(np.int32)).to(xp.device)
-        ye = self.ops.expert_ffn(local_counts, xe)
+        ye = self.ops.expert_ffn(local_counts, xe, global_tokens)
         ys = self.ops.gather_rows(ye, inv_order_t)
         # combine: rows go home in the order they were sent
         back = torch.empty((sum(send_rows), ys.shape[1]), dtype=ys.dtype, device=ys.device)

@@ -26,8 +26,10 @@ up = (torch.randn((E * d, f), generator=gen, device="cuda") / d ** 0.5).to(torch
 down = (torch.randn((E * f, d), generator=gen, device="cuda") / f ** 0.5).to(torch.bfloat16)
 # workspace sized with every router path enabled (the variants may switch paths)
 os.environ["MOE_B200_SEG_MAX_CHAINS"] = str(1 << 30)
+os.environ["MOE_B200_DOWN_SPLITS"] = "16"
 layer = P.MoELayer(P.ModelConfig(E, k, d, f, P.Gating(gating)), P.ExpertWeights(gate, up, down), wr, max_tokens=B)
 os.environ.pop("MOE_B200_SEG_MAX_CHAINS")
+os.environ.pop("MOE_B200_DOWN_SPLITS")
 out = torch.empty((B, d), dtype=torch.float32, device="cuda")
 graphs = []
 for v in variants:

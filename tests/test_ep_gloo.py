@@ -42,7 +42,8 @@ class OracleOps:
     def gather_rows(self, src, idx):
         return src[idx.long()].clone()
 
-    def expert_ffn(self, counts, xp):
+    def expert_ffn(self, counts, xp, global_tokens):
+        self.global_tokens = global_tokens
         out = torch.zeros((xp.shape[0], self.d), dtype=torch.float32)
         d, f = self.d, self.f
         r = 0
@@ -83,6 +84,9 @@ def _worker(rank, world, port, case, q):
         ops = OracleOps(tokens, wr, gate, up, down, E, k, d, f, gating, lo, hi)
         layer = ExpertParallelMoE(cfg, wr, None, max_tokens=B, device="cpu", ops=ops)
         y = layer.forward(torch.from_numpy(tokens[b0:b1]))
+        # the counts exchange also carries every rank's token count: each rank
+        # sees the global batch (it fixes the down K-split count)
+        assert ops.global_tokens == B, (ops.global_tokens, B)
         q.put((rank, b0, y.numpy()))
     finally:
         dist.destroy_process_group()

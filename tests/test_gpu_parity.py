@@ -283,13 +283,20 @@ def test_sigmoid_port_matches_numpy_on_device(pkg):
     bits_equal(_np(r["weights"]), w_ref)
 
 
-def test_expert_parallel_single_rank_matches_layer_bitwise(pkg):
+@pytest.mark.parametrize("shape", [
+    (16, 4, 256, 512, 64),
+    # small batch: the down K-split count of the global layer (E=8, k=2, B=8:
+    # 4) differs from the one the local k=1 row layout would pick (5); the EP
+    # path must use the global one to stay bitwise equal
+    (8, 2, 2048, 2048, 8),
+])
+def test_expert_parallel_single_rank_matches_layer_bitwise(pkg, shape):
     """EP code path (dispatch reorder, expert_ffn, gather, combine_rows) on one
     rank reproduces the fused single-GPU forward bit-for-bit."""
     P = pkg
     from paper_2605_23911_b200.ep import ExpertParallelMoE
 
-    e, k, d, f, b = 16, 4, 256, 512, 64
+    e, k, d, f, b = shape
     tokens, wr, gate, up, down = O.make_instance(9, e, k, d, f, b)
     cfg = _cfg(P, e, k, d, f, "sigmoid_normalized")
     w = P.ExpertWeights(gate, up, down)
