@@ -20,7 +20,8 @@
 namespace moe {
 
 constexpr int kDispThreads = 256;
-constexpr int kDispRows = 8;  // expanded rows per CTA
+constexpr int kDispRows = 8;         // expanded rows per CTA
+constexpr int kDispSmemT = 8192;     // up to this many rows, every CTA stages all indices in smem
 
 struct DispatchParams {
   const int32_t* topk_idx;  // (T) expert of expanded row i = t*k + j
@@ -37,6 +38,7 @@ struct DispatchParams {
   int2* chunk_grp;          // {first chunk of the expert, chunks of the expert}
   int32_t* n_chunks;        // [1]
   uint32_t* flags;          // bit 4: an index outside [0, E) (row dropped)
+  unsigned long long* trace;  // debug: 16 u64 per CTA (globaltimer start, clock64 phase deltas)
 };
 
 template <bool kXBf16>
@@ -54,7 +56,11 @@ MOE_DEVICE int4 load_bf16x8(const void* x, size_t t, int d, int q) {
   return out;
 }
 
-template <bool kXBf16>
+// kSmemIdx (T <= kDispSmemT): all T indices are staged in shared memory with
+// one round of 16-byte loads and counted with plain shared atomics; the CTA's
+// own rows read their experts from that copy.  Otherwise they are streamed
+// (four loads in flight per thread, warp-aggregated atomics).
+template <bool kXBf16, bool kSmemIdx>
 __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchParams p) {
   extern __shared__ __align__(16) int32_t dsm[];
   int32_t* tot = dsm;                  // [E]
@@ -62,35 +68,68 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
   int32_t* off = before + p.E;         // [E+1]
   int32_t* off16 = off + p.E + 1;      // [E+1]
   int32_t* cpre = off16 + p.E + 1;     // [E+1]
-  __shared__ int32_t s_pos[kDispRows], s_tok[kDispRows];
+  int32_t* idx_s = dsm + ((5 * p.E + 3 + 3) & ~3);  // [T] (kSmemIdx), 16-byte aligned
+  __shared__ int32_t s_pos[kDispRows];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r0 = blockIdx.x * kDispRows;
   const int r1 = min(p.T, r0 + kDispRows);
+  unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 16 : nullptr;
+  const long long c_start = clock64();
+  auto stamp = [&](int i) { if (tr && threadIdx.x == 0) tr[i] = clock64() - c_start; };
+  if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[15] = smid_u32(); }
 
   for (int e = tid; e < p.E; e += kDispThreads) {
     tot[e] = 0;
     before[e] = 0;
   }
-  // the gather sources (token i / k) are known now: put the first batch of row
-  // loads in flight before the histogram, store them once positions are known
-  const int vpr = p.d / 8;
-  const int nvec = (r1 - r0) * vpr;
+  // gather: warp w copies expanded row r0 + w (token (r0 + w) / k).  The
+  // sources are known now: put the first loads of the row in flight before the
+  // histogram, store them once the positions are known
+  static_assert(kDispRows == kDispThreads / 32, "one warp per gathered row");
+  const int vpr = p.d / 8;                 // 16-byte vectors per row
+  const bool has_row = r0 + warp < r1;
+  const int src_tok = (r0 + warp) / p.k;
   constexpr int kPre = 8;
   int4 pre[kPre];
-  if (p.xp != nullptr) {
+  if (p.xp != nullptr && has_row) {
 #pragma unroll
     for (int u = 0; u < kPre; ++u) {
-      const int v = tid + u * kDispThreads;
-      if (v < nvec) pre[u] = load_bf16x8<kXBf16>(p.x, (size_t)((r0 + v / vpr) / p.k), p.d, v % vpr);
+      const int q = lane + 32 * u;
+      if (q < vpr) pre[u] = load_bf16x8<kXBf16>(p.x, (size_t)src_tok, p.d, q);
     }
   }
   pdl_launch_dependents();
   pdl_wait();  // routing indices of the router grid
+  constexpr int U = 4;
+  if (kSmemIdx) {
+    if ((reinterpret_cast<uintptr_t>(p.topk_idx) & 15) == 0) {
+      const int nv = p.T >> 2;
+#pragma unroll 4
+      for (int v = tid; v < nv; v += kDispThreads)
+        reinterpret_cast<int4*>(idx_s)[v] = __ldg(reinterpret_cast<const int4*>(p.topk_idx) + v);
+      for (int i = 4 * nv + tid; i < p.T; i += kDispThreads) idx_s[i] = __ldg(p.topk_idx + i);
+    } else {
+#pragma unroll 4
+      for (int i = tid; i < p.T; i += kDispThreads) idx_s[i] = __ldg(p.topk_idx + i);
+    }
+  }
   __syncthreads();
+  stamp(1);
+  if (kSmemIdx) {
+    // histogram of all rows and of the rows before r0 (shared atomics)
+    for (int i = tid; i < p.T; i += kDispThreads) {
+      const int e = idx_s[i];
+      if (e < 0 || e >= p.E) {  // routing override out of range: drop the row
+        if (blockIdx.x == 0 && p.flags) atomicOr(p.flags, 4u);
+        continue;
+      }
+      atomicAdd(&tot[e], 1);
+      if (i < r0) atomicAdd(&before[e], 1);
+    }
+  }
   // histogram of all rows and of the rows before r0 (warp-aggregated smem
   // atomics); four index loads in flight per thread
-  constexpr int U = 4;
-  for (int base0 = warp * 32; base0 < p.T; base0 += U * kDispThreads) {
+  for (int base0 = warp * 32; !kSmemIdx && base0 < p.T; base0 += U * kDispThreads) {
     int ev[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -113,16 +152,21 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
     }
   }
   __syncthreads();
+  stamp(2);
   // exclusive scans: offsets, 16-aligned padded offsets, chunk counts (warp 0)
+  // (cold code, run once per CTA: kept small -- instruction fetch, not
+  // arithmetic, bounds these short phases; chunk_rows is a power of two)
+  const int cshift = __ffs(p.chunk_rows) - 1;
   if (warp == 0) {
     const int per = (p.E + 31) / 32;
     const int lo = lane * per, hi = min(p.E, lo + per);
     int sc = 0, s16 = 0, sch = 0;
+#pragma unroll 1
     for (int e = lo; e < hi; ++e) {
       const int n = tot[e];
       sc += n;
       s16 += (n + 15) & ~15;
-      sch += (n + p.chunk_rows - 1) / p.chunk_rows;
+      sch += (n + p.chunk_rows - 1) >> cshift;
     }
     int ic = sc, i16 = s16, ich = sch;
 #pragma unroll
@@ -133,22 +177,27 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
       if (lane >= o) { ic += a; i16 += b; ich += c; }
     }
     int rc = ic - sc, r16 = i16 - s16, rch = ich - sch;
+#pragma unroll 1
     for (int e = lo; e < hi; ++e) {
       off[e] = rc; off16[e] = r16; cpre[e] = rch;
       const int n = tot[e];
       rc += n;
       r16 += (n + 15) & ~15;
-      rch += (n + p.chunk_rows - 1) / p.chunk_rows;
+      rch += (n + p.chunk_rows - 1) >> cshift;
     }
     if (lane == 31) { off[p.E] = ic; off16[p.E] = i16; cpre[p.E] = ich; }
   }
+  stamp(6);
   __syncthreads();
+  stamp(7);
   if (blockIdx.x == 0) {
+#pragma unroll 1
     for (int e = tid; e < p.E; e += kDispThreads) {
       p.counts[e] = tot[e];
       p.offsets[e] = off[e];
       const int n = tot[e];
-      const int nch_e = (n + p.chunk_rows - 1) / p.chunk_rows;
+      const int nch_e = (n + p.chunk_rows - 1) >> cshift;
+#pragma unroll 1
       for (int c = 0; c < nch_e; ++c) {
         const int rr = c * p.chunk_rows;
         p.chunk_tab[cpre[e] + c] = make_int4(e, off[e] + rr, min(p.chunk_rows, n - rr), off16[e] + rr);
@@ -160,11 +209,12 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
       p.n_chunks[0] = cpre[p.E];
     }
   }
+  stamp(8);
   // stable positions of this CTA's rows (one warp; kDispRows <= 32)
   if (warp == 0) {
     const int i = r0 + lane;
     const bool valid = lane < kDispRows && i < r1;
-    int e = valid ? __ldg(p.topk_idx + i) : -1 - lane;
+    int e = valid ? (kSmemIdx ? idx_s[i] : __ldg(p.topk_idx + i)) : -1 - lane;
     if (e < 0 || e >= p.E) e = -1 - lane;
     const uint32_t peers = __match_any_sync(0xffffffffu, e);
     if (valid && e >= 0) {
@@ -174,35 +224,42 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
       p.inv[i] = pos;
       p.prow[i] = off16[e] + rank;
       s_pos[lane] = pos;
-      s_tok[lane] = i / p.k;
     } else if (valid) {  // dropped (out-of-range override index): in-bounds placeholders
       p.inv[i] = -1;
       p.prow[i] = 0;
       s_pos[lane] = -1;
-      s_tok[lane] = i / p.k;
     }
   }
+  stamp(3);
   if (p.xp == nullptr) return;
   __syncthreads();
-  // gather: xp[pos(i)] = bf16(x[i / k]), 16-byte vectors
+  stamp(4);
+  // gather: xp[pos(i)] = bf16(x[i / k]), 16-byte vectors, warp w -> row r0 + w
+  const int dst_row = has_row ? s_pos[warp] : -1;
+  if (dst_row >= 0) {
+    int4* dst = reinterpret_cast<int4*>(p.xp + (size_t)dst_row * p.d);
 #pragma unroll
-  for (int u = 0; u < kPre; ++u) {
-    const int v = tid + u * kDispThreads;
-    if (v < nvec && s_pos[v / vpr] >= 0) reinterpret_cast<int4*>(p.xp + (size_t)s_pos[v / vpr] * p.d)[v % vpr] = pre[u];
-  }
-  for (int v0 = tid + kPre * kDispThreads; v0 < nvec; v0 += U * kDispThreads) {
-    int4 out[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {  // all loads first: U vectors in flight per thread
-      const int v = v0 + u * kDispThreads;
-      if (v < nvec) out[u] = load_bf16x8<kXBf16>(p.x, (size_t)s_tok[v / vpr], p.d, v % vpr);
+    for (int u = 0; u < kPre; ++u) {
+      const int q = lane + 32 * u;
+      if (q < vpr) dst[q] = pre[u];
     }
+#pragma unroll 1
+    for (int q0 = lane + 32 * kPre; q0 < vpr; q0 += 32 * U) {
+      int4 out[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int v = v0 + u * kDispThreads;
-      if (v < nvec && s_pos[v / vpr] >= 0) reinterpret_cast<int4*>(p.xp + (size_t)s_pos[v / vpr] * p.d)[v % vpr] = out[u];
+      for (int u = 0; u < U; ++u) {  // all loads first: U vectors in flight per lane
+        const int q = q0 + 32 * u;
+        if (q < vpr) out[u] = load_bf16x8<kXBf16>(p.x, (size_t)src_tok, p.d, q);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + 32 * u;
+        if (q < vpr) dst[q] = out[u];
+      }
     }
   }
+  __syncthreads();
+  stamp(5);
 }
 
 }  // namespace moe

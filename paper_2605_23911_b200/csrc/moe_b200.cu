@@ -115,10 +115,18 @@ void down_splits(const moe_b200_config& c, int64_t B, int* splits, int* kb_per_s
 }
 
 // ---- segment (certified split-K) router plan --------------------------------
-int seg_expc(int E) {
+// Experts per CTA block (a multiple of the 4-expert thread tile).  Up to 64
+// experts go in one 64-wide block (16 lanes per segment) when 32-wide blocks
+// would need more than one wave of CTAs (a 202-register CTA runs alone on an
+// SM): Qwen-60 at 512 tokens, 256 CTAs in two waves -> 128 CTAs in one.
+int seg_expc(int E, int64_t B) {
   if (E <= 4) return 4;
   if (E <= 8) return 8;
   if (E <= 16) return 16;
+  if (E <= 32) return 32;
+  const int64_t n_tb = (B + kSegTT - 1) / kSegTT;
+  const char* env = getenv("MOE_B200_SEG_WIDE");  // 0: never 64-wide (A/B)
+  if (E <= 64 && n_tb * ((E + 31) / 32) > kNumSMs && !(env && atoi(env) == 0)) return 64;
   return 32;
 }
 
@@ -139,7 +147,7 @@ struct SegPlan {
 
 SegPlan plan_seg(const moe_b200_config& c, int64_t B) {
   SegPlan q{};
-  q.expc = seg_expc(c.num_experts);
+  q.expc = seg_expc(c.num_experts, B);
   q.n_eb = (c.num_experts + q.expc - 1) / q.expc;
   q.n_tb = static_cast<int>((B + kSegTT - 1) / kSegTT);
   const int G = q.expc / kSegTE;
@@ -151,8 +159,10 @@ SegPlan plan_seg(const moe_b200_config& c, int64_t B) {
   const long base = (long)q.n_tb * q.n_eb;
   const int max_kb = std::max(1, (c.hidden_dim + S * 8 - 1) / (S * 8));
   int n_kb = base * 4 >= kNumSMs * 3 ? 1 : static_cast<int>(std::min<long>(max_kb, (kNumSMs * 3 / 2 + base - 1) / base));
+  if (q.expc > 32) n_kb = 1;  // (64-wide blocks only when they fill the SMs; keeps n_kb <= d/256)
   q.seg_len = ((c.hidden_dim + (long)n_kb * S - 1) / ((long)n_kb * S) + 7) / 8 * 8;
-  if (const char* env = getenv("MOE_B200_SEG_LEN")) q.seg_len = std::max(8, atoi(env) / 8 * 8);
+  if (const char* env = getenv("MOE_B200_SEG_LEN"))
+    if (q.expc <= 32) q.seg_len = std::max(8, atoi(env) / 8 * 8);
   q.kr = S * q.seg_len;
   q.n_kb = (c.hidden_dim + q.kr - 1) / q.kr;
   q.grid = q.n_tb * q.n_eb * q.n_kb;
@@ -182,7 +192,7 @@ Layout layout_for(const moe_b200_config& c, int64_t B, int s_force = 0) {
     // segment router partials: (B rounded to token blocks) x (E rounded to
     // expert blocks) chains x at most ceil(d / 256) k-blocks (S >= 32, L >= 8)
     const int64_t bseg = (std::min<int64_t>(B, seg_max_tokens(c)) + kSegTT - 1) / kSegTT * kSegTT;
-    const int expc = seg_expc(c.num_experts);
+    const int expc = seg_expc(c.num_experts, 1);  // 32-wide padding >= the 64-wide one (E <= 64)
     const int64_t epad = (c.num_experts + expc - 1) / expc * expc;
     const int64_t nkb = (c.hidden_dim + 255) / 256;
     L.gpart = off;   off = align256(off + (size_t)(bseg * epad * nkb) * 16);
@@ -299,6 +309,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 
 
 unsigned long long* g_ffn_trace = nullptr;  // debug: per-tile timeline of the next ffn launches
+unsigned long long* g_dispatch_trace = nullptr;  // debug: per-CTA dispatch timeline
 unsigned long long* g_router_trace = nullptr;  // debug: CTA-0 per-chunk router timeline
 struct RouterPlan {
   int expc, te, tt, tokc, n_eblocks, n_tblocks, threads, d_pad, stages, kc;
@@ -554,6 +565,7 @@ int launch_dispatch(const moe_b200_config& c, int64_t B, const void* x, int xb, 
                     int32_t* counts, int32_t* offsets, int32_t* fwd, int32_t* inv, int32_t* prow, int4* chunk_tab,
                     int32_t* n_chunks, void* xp, cudaStream_t s, uint32_t* flags = nullptr) {
   DispatchParams q{};
+  q.trace = g_dispatch_trace;
   q.flags = flags;
   q.topk_idx = topk_idx;
   q.T = static_cast<int>(B * c.top_k); q.k = c.top_k; q.E = c.num_experts; q.d = c.hidden_dim;
@@ -563,8 +575,10 @@ int launch_dispatch(const moe_b200_config& c, int64_t B, const void* x, int xb, 
   q.chunk_tab = chunk_tab; q.n_chunks = n_chunks;
   q.chunk_grp = reinterpret_cast<int2*>(chunk_tab + layout_for(c, B).max_chunks);
   const int grid = (q.T + kDispRows - 1) / kDispRows;
-  const size_t smem = (size_t)(5 * c.num_experts + 3) * sizeof(int32_t);
-  auto kern = xb ? dispatch_kernel<true> : dispatch_kernel<false>;
+  const bool smem_idx = q.T <= kDispSmemT;
+  const size_t smem = (((5 * c.num_experts + 3 + 3) & ~3) + (smem_idx ? ((q.T + 3) & ~3) : 0)) * sizeof(int32_t);
+  auto kern = xb ? (smem_idx ? dispatch_kernel<true, true> : dispatch_kernel<true, false>)
+                 : (smem_idx ? dispatch_kernel<false, true> : dispatch_kernel<false, false>);
   if (smem > 48 * 1024) MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kDispThreads), smem, s, q);
   if (e != cudaSuccess) return cuda_fail(e, "dispatch launch");
@@ -583,6 +597,7 @@ const char* moe_b200_version(void) { return "moe_b200 0.1.0 (sm_100a)"; }
 // subsequent ffn launches into a device buffer of 4 u64 per tile, or NULL to stop.
 void moe_b200_debug_set_ffn_trace(unsigned long long* dev_buf) { g_ffn_trace = dev_buf; }
 void moe_b200_debug_set_router_trace(unsigned long long* dev_buf) { g_router_trace = dev_buf; }
+void moe_b200_debug_set_dispatch_trace(unsigned long long* dev_buf) { g_dispatch_trace = dev_buf; }
 
 const char* moe_b200_last_error_detail(void) { return g_last_error.c_str(); }
 

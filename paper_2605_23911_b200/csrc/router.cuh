@@ -149,18 +149,6 @@ MOE_DEVICE float np_expf(float x) {
   return __double2float_rn(static_cast<double>(p) * __longlong_as_double(qe));
 }
 
-MOE_DEVICE uint32_t smid_u32() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-  return r;
-}
-
-MOE_DEVICE unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
 MOE_DEVICE float np_sigmoid(float x) {
   float t = np_expf(-fabsf(x));
   float den = __fadd_rn(1.0f, t);

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const Router
   const int eb = rest % p.n_eblocks;
   const int tb = rest / p.n_eblocks;
   const int t0 = tb * TT, e0 = eb * p.expc;
-  const int G = p.expc / TE;        // expert groups per segment: 1, 2, 4, 8
+  const int G = p.expc / TE;        // expert groups per segment: 1, 2, 4, 8, 16
   const int g = tid % G, s = tid / G;
   const int kbeg = kb * p.kr + s * p.seg_len;
   const int kend = min(p.d, kbeg + p.seg_len);

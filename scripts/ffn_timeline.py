@@ -9,6 +9,7 @@ from bench import CONFIGS
 name = sys.argv[1] if len(sys.argv) > 1 else "mixtral"
 tag = sys.argv[2] if len(sys.argv) > 2 else name
 E, k, d, f, gating, B, _ = CONFIGS[name]
+B = int(os.environ.get("TL_B", B))
 gen = torch.Generator(device="cuda").manual_seed(1234)
 x = torch.randn((B, d), generator=gen, device="cuda").to(torch.bfloat16)
 wr = (torch.randn((d, E), generator=gen, device="cuda") / d ** 0.5).float()

@@ -70,7 +70,7 @@ def _check(x: np.ndarray, w: np.ndarray, seg_len: int, G: int = 2):
     return abs(seq - s_hat), D
 
 
-@pytest.mark.parametrize("seg_len,G", [(8, 2), (16, 8), (32, 2), (32, 8), (64, 1)])
+@pytest.mark.parametrize("seg_len,G", [(8, 2), (16, 8), (32, 2), (32, 8), (64, 1), (128, 16)])
 def test_certificate_random(seg_len, G):
     rng = np.random.default_rng(seg_len * 10 + G)
     worst = 0.0
@@ -115,7 +115,7 @@ def test_certificate_adversarial():
     w = (rng.standard_normal(d) / np.sqrt(d)).astype(np.float32)
     cases.append((x, w))
     for x, w in cases:
-        for seg_len, G in ((8, 2), (32, 8), (128, 1)):
+        for seg_len, G in ((8, 2), (32, 8), (128, 1), (128, 16)):
             _check(x, w, seg_len, G)
 
 
