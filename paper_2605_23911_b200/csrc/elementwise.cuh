@@ -177,44 +177,57 @@ combine_tiled_kernel(const float* __restrict__ ys, int splits, int n_dp, int T_p
 //   y[t] = sum_j fl(w[t,j] * (sum_s P_s[prow(t*k+j)])), ascending j and s,
 // fp32 from +0 — the reference's out += w_j * g_j (pipeline.py:396-399).
 constexpr int kCombineMaxKS = 16;  // k * S register budget (else the generic loop)
-template <bool kBf16Out, int kS>
+// kNV: 16-byte columns per thread (k * S <= kCombineMaxKS / kNV partials each)
+template <bool kBf16Out, int kS, int kNV>
 __global__ void __launch_bounds__(kRowThreads)
 combine_token_kernel(const float* __restrict__ ys, int n_dp, int T_pad,
                      const int32_t* __restrict__ prow, const float* __restrict__ topk_w,
                      void* __restrict__ y, int B, int k, int d) {
-  pdl_wait();  // partials of the FFN grid
   __shared__ int32_t s_row[kCombineMaxKS];
   __shared__ float s_w[kCombineMaxKS];
+  // grid (B, ceil(d / 4 / (kRowThreads * kNV))): up to kNV
+  // 16-byte columns of one token per thread, every partial load issued before
+  // the first add (one L2 round trip after the row ids)
   const int t = blockIdx.x;
-  if (threadIdx.x < k) {
+  if (threadIdx.x < k) {  // row ids / weights: outputs of kernels before the FFN
     s_row[threadIdx.x] = __ldg(prow + (size_t)t * k + threadIdx.x);
     s_w[threadIdx.x] = __ldg(topk_w + (size_t)t * k + threadIdx.x);
   }
+  pdl_wait();  // partials of the FFN grid
   __syncthreads();
   const size_t half_stride = (size_t)T_pad * 128;
-  constexpr int kMaxK = kCombineMaxKS / kS;
+  constexpr int kSlots = kCombineMaxKS / kNV;
+  constexpr int kMaxK = kSlots / kS;
   const int ks = k * kS;
-  for (int v = threadIdx.x; v < d / 4; v += kRowThreads) {
+  const int v0 = blockIdx.y * kRowThreads * kNV + threadIdx.x;
+  float4 a[kNV][kSlots];
+#pragma unroll
+  for (int c = 0; c < kNV; ++c) {
+    const int v = v0 + c * kRowThreads;
     const int feat = v * 4;
     const size_t blk = (size_t)(feat >> 8) * 2 + ((feat >> 7) & 1);  // (d-pair, half)
     const int col = feat & 127;
-    float4 a[kCombineMaxKS];
 #pragma unroll
-    for (int i = 0; i < kCombineMaxKS; ++i) {
-      if (i < ks) {
+    for (int i = 0; i < kSlots; ++i) {
+      if (i < ks && v < d / 4) {
         const int j = i / kS, s = i % kS;
         const float* src = ys + ((size_t)s * n_dp * 2 + blk) * half_stride + (size_t)s_row[j] * 128 + col;
-        a[i] = __ldg(reinterpret_cast<const float4*>(src));
+        a[c][i] = __ldg(reinterpret_cast<const float4*>(src));
       }
     }
+  }
+#pragma unroll
+  for (int c = 0; c < kNV; ++c) {
+    const int v = v0 + c * kRowThreads;
+    if (v >= d / 4) continue;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int j = 0; j < kMaxK; ++j) {
       if (j < k) {
-        float4 g = a[j * kS];
+        float4 g = a[c][j * kS];
 #pragma unroll
         for (int s = 1; s < kS; ++s) {
-          const float4 b = a[j * kS + s];
+          const float4 b = a[c][j * kS + s];
           g.x = __fadd_rn(g.x, b.x); g.y = __fadd_rn(g.y, b.y);
           g.z = __fadd_rn(g.z, b.z); g.w = __fadd_rn(g.w, b.w);
         }

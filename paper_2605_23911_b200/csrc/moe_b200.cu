@@ -288,12 +288,13 @@ int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 // Launch with programmatic stream serialization (PDL) when MOE_B200_PDL=1:
 // the kernel may start while its predecessor finishes and calls pdl_wait()
 // before reading the predecessor's outputs (common.cuh).  Off by default: it
-// measured no gain on the graph-replayed forward (A/B 510 vs 508 us, Mixtral)
+// measured no gain on the graph-replayed forward (A/B 510 vs 508 us, Mixtral;
+// on the FFN -> combine edge alone 601 vs 600 us Mixtral, 209 vs 209 us Qwen)
 // and one test sequence (Mixtral then Qwen layers) stalled with it on.
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
-  const char* env = getenv("MOE_B200_PDL");
-  const bool disabled = !(env && atoi(env));
+cudaError_t launch_pdl_if(bool on, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                          Args&&... args) {
+  const bool disabled = !on;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -306,6 +307,13 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.numAttrs = disabled ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  const char* env = getenv("MOE_B200_PDL");
+  return launch_pdl_if(env && atoi(env), kern, grid, block, smem, s, std::forward<Args>(args)...);
+}
+
 
 
 unsigned long long* g_ffn_trace = nullptr;  // debug: per-tile timeline of the next ffn launches
@@ -544,14 +552,22 @@ int launch_combine(const moe_b200_config& c, int64_t B, const Layout& L, void* w
   cudaError_t e;
   if (S <= 4 && k * S <= kCombineMaxKS) {
     using K = void (*)(const float*, int, int, const int32_t*, const float*, void*, int, int, int);
+    const bool wide = k * S <= kCombineMaxKS / 4;  // 4 columns per thread
     K kern;
+#define MOE_COMBINE_PICK(SS)                                                                   \
+  kern = wide ? (bf ? combine_token_kernel<true, SS, 4> : combine_token_kernel<false, SS, 4>) \
+              : (bf ? combine_token_kernel<true, SS, 1> : combine_token_kernel<false, SS, 1>)
     switch (S) {
-      case 1: kern = bf ? combine_token_kernel<true, 1> : combine_token_kernel<false, 1>; break;
-      case 2: kern = bf ? combine_token_kernel<true, 2> : combine_token_kernel<false, 2>; break;
-      case 3: kern = bf ? combine_token_kernel<true, 3> : combine_token_kernel<false, 3>; break;
-      default: kern = bf ? combine_token_kernel<true, 4> : combine_token_kernel<false, 4>; break;
+      case 1: MOE_COMBINE_PICK(1); break;
+      case 2: MOE_COMBINE_PICK(2); break;
+      case 3: MOE_COMBINE_PICK(3); break;
+      default: MOE_COMBINE_PICK(4); break;
     }
-    e = launch_pdl(kern, dim3((unsigned)B), dim3(kRowThreads), 0, s, ys, L.n_dp, L.T_pad, prow, topk_w, y, (int)B, k, d);
+#undef MOE_COMBINE_PICK
+    const int nv = wide ? 4 : 1;
+    const unsigned col_blocks = (unsigned)((d / 4 + kRowThreads * nv - 1) / (kRowThreads * nv));
+    e = launch_pdl(kern, dim3((unsigned)B, col_blocks), dim3(kRowThreads), 0, s, ys, L.n_dp, L.T_pad, prow, topk_w, y,
+                   (int)B, k, d);
   } else {
     const int grid = grid_for_rows((long)B * (d / 4));
     e = launch_pdl(bf ? combine_tiled_kernel<true> : combine_tiled_kernel<false>, dim3(grid), dim3(kRowThreads), 0, s,
