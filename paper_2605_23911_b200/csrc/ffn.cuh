@@ -91,16 +91,18 @@ MOE_DEVICE uint32_t smid() {
 // bulk copies (one 256 B / 512 B row segment per copy, issued by one lane),
 // so the output stream never competes with the weight stream as thousands of
 // scattered STGs.  kV selects the ring/staging split (tuning).
-template <int kBN, int kV>
+template <int kBN, int kV, bool k2 = false>
 struct FfnCfg {
   static constexpr int kABytes = kBM * kBK * 2;      // 16 KB weight slot
-  static constexpr int kBBytes = kBN * kBK * 2;      // token slot
+  static constexpr int kBRows = k2 ? kBN / 2 : kBN;  // cta_group::2: each CTA holds half the token rows
+  static constexpr int kBBytes = kBRows * kBK * 2;   // token slot
   static constexpr int kStgBytes = 32 * kBM * 4;     // 32 rows x 128 fp32 (16 KB)
   static constexpr int kStgBufs = kEpiGroups;  // one staging buffer per epilogue group
   // kV 2: balanced rings; kV 3: deeper weight ring (more HBM bytes in flight
   // per SM), shallower token ring (tokens are L2-resident)
-  static constexpr int kAStages = kBN == 256 ? (kV == 3 ? 8 : 6) : (kV == 3 ? 10 : 8);
-  static constexpr int kBStages = kBN == 256 ? (kV == 3 ? 2 : 3) : (kV == 3 ? 2 : 4);
+  // k2: the halved token slots buy a deeper weight ring (8 A / 4 B for BN=256)
+  static constexpr int kAStages = k2 ? (kBN == 256 ? 8 : 10) : kBN == 256 ? (kV == 3 ? 8 : 6) : (kV == 3 ? 10 : 8);
+  static constexpr int kBStages = k2 ? 4 : kBN == 256 ? (kV == 3 ? 2 : 3) : (kV == 3 ? 2 : 4);
   static constexpr int kRingBytes = kAStages * kABytes + kBStages * kBBytes;
   static constexpr int kDataBytes = kRingBytes + kStgBufs * kStgBytes;
   static constexpr uint32_t kTmemCols = 2 * kBN <= 256 ? 256 : 512;
@@ -199,12 +201,22 @@ MOE_DEVICE TileInfo decode_tile(const FfnParams& p, int tile, int rank = 0) {
 // token slots, and each MMA releases a token slot in both CTAs (multicast
 // commit), halving the token traffic per SM.  Rank 0 owns the tile queue and
 // hands each pair tile to rank 1 through distributed shared memory.
-template <int kBN, int kV, bool kPair = false>
+//
+// kPM == 2 (cta_group::2): the pair's two weight tiles form ONE MMA of
+// M = 256 issued by rank 0; each CTA stages its own 128 weight rows and HALF
+// of the token rows (rank r: rows [r N/2, (r+1) N/2)), so every token byte is
+// fetched once per pair with no multicast, and the halved token slots buy a
+// deeper weight ring.  Both producers signal rank 0's full barriers; rank 0's
+// commits multicast to both CTAs' empty / TMEM-full barriers; both CTAs'
+// epilogue warps release rank 0's TMEM-empty barrier.
+template <int kBN, int kV, int kPM = 0>
 __global__ void __launch_bounds__(kFfnThreads, 1)
 ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CUtensorMap tm_wu,
            const __grid_constant__ CUtensorMap tm_xp, const __grid_constant__ CUtensorMap tm_wd,
            const __grid_constant__ CUtensorMap tm_h, const FfnParams p) {
-  using C = FfnCfg<kBN, kV>;
+  constexpr bool kPair = kPM != 0;
+  constexpr bool k2 = kPM == 2;
+  using C = FfnCfg<kBN, kV, k2>;
   const int rank = kPair ? static_cast<int>(cluster_ctarank()) : 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -234,15 +246,15 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::kAStages; ++s) {
-      mbar_init(a_full + s, 1);
+      mbar_init(a_full + s, k2 ? 2 : 1);  // k2 (rank 0's): both producers
       mbar_init(a_empty + s, 1);
     }
     for (int s = 0; s < C::kBStages; ++s) {
-      mbar_init(b_full + s, 1);
-      mbar_init(b_empty + s, kPair ? 2 : 1);  // pair: both CTAs' MMAs release the shared slot
+      mbar_init(b_full + s, k2 ? 2 : 1);
+      mbar_init(b_empty + s, kPM == 1 ? 2 : 1);  // pair: both CTAs' MMAs release the shared slot
     }
     mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, 32 * kEpiWarps);
+    mbar_init(tmem_empty, (k2 ? 2 : 1) * kEpiWarps);  // one arrival per epilogue warp (k2: of both CTAs)
     for (int s = 0; s < kSchedSlots; ++s) {
       mbar_init(sched_full + s, 1);
       // MMA lane + one lane per epilogue warp (pair: of both CTAs, plus rank 1's producer)
@@ -250,7 +262,10 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_base_smem);
+  if (warp == 2) {
+    if constexpr (k2) tmem_alloc2<C::kTmemCols>(tmem_base_smem);
+    else tmem_alloc<C::kTmemCols>(tmem_base_smem);
+  }
   tc_fence_before();
   if constexpr (kPair) cluster_sync_all();  // peer barriers initialised before any remote access
   else __syncthreads();
@@ -261,6 +276,10 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
   const uint32_t r_sched_full1 = kPair ? map_to_rank(smem_u32(sched_full), 1) : 0;    // rank 1's ring
   const uint32_t r_sched_tile1 = kPair ? map_to_rank(smem_u32(sched_tile), 1) : 0;
   (void)peer;
+  // k2: rank 0's full / TMEM-empty barriers (cluster addresses)
+  const uint32_t lead_a_full = k2 ? map_to_rank(smem_u32(a_full), 0) : 0;
+  const uint32_t lead_b_full = k2 ? map_to_rank(smem_u32(b_full), 0) : 0;
+  const uint32_t lead_tmem_empty = k2 ? map_to_rank(smem_u32(tmem_empty), 0) : 0;
   // consumer side of the scheduler ring: read slot, release it (pair: on rank 0)
   auto sched_read = [&](int slot, uint32_t sphase, bool release_lane, bool warp_sync) -> int {
     if (kPair && rank == 1) mbar_wait_cluster(sched_full + slot, sphase);
@@ -290,6 +309,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
     // ====================== scheduler + TMA producer ========================
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_t = policy_evict_last();  // k2 token loads: reused by the chunk's tiles
       int as = 0, bs = 0;
       uint32_t aph = 0, bph = 0;
       int slot = 0;
@@ -319,9 +339,30 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         const TileInfo ti = decode_tile(p, tile, rank);
         const int4 ch = __ldg(p.chunk_tab + ti.chunk);
         const int n_mma = max(16, (ch.z + 15) & ~15);
-        const int nbox = (n_mma + kBoxRows - 1) / kBoxRows;
+        // k2: this CTA's half of the token rows
+        const int b_row0 = k2 ? rank * (n_mma / 2) : 0;
+        const int b_rows = k2 ? n_mma / 2 : n_mma;
+        const int nbox = (b_rows + kBoxRows - 1) / kBoxRows;
         const uint32_t b_bytes = nbox * kBoxRows * kBK * 2;
-        const int a_col = ti.is_gu ? ti.mt * kBM : ti.mt * 2 * kBM;
+        // k2, missing second weight tile: stream a valid tile (results discarded)
+        const int mt_ld = (k2 && ti.dummy) ? (ti.is_gu ? p.n_mt_gu : p.n_mt_dn) - 1 : ti.mt;
+        const int a_col = ti.is_gu ? mt_ld * kBM : mt_ld * 2 * kBM;
+        // one 16 KB weight slot: two 64-column boxes
+        auto load_a = [&](const CUtensorMap* m, int col, int krow) {
+          mbar_wait(a_empty + as, aph ^ 1);
+          uint8_t* sa = a_ring + as * C::kABytes;
+          if constexpr (k2) {
+            const uint32_t bar = lead_a_full + as * 8;
+            mbar_arrive_expect_tx_cluster(bar, C::kABytes);
+            tma_load_2d_2sm(m, bar, sa, col, krow, pol_w);
+            tma_load_2d_2sm(m, bar, sa + C::kABytes / 2, col + 64, krow, pol_w);
+          } else {
+            mbar_arrive_expect_tx(a_full + as, C::kABytes);
+            tma_load_2d_hint(m, a_full + as, sa, col, krow, pol_w);
+            tma_load_2d_hint(m, a_full + as, sa + C::kABytes / 2, col + 64, krow, pol_w);
+          }
+          if (++as == C::kAStages) { as = 0; aph ^= 1; }
+        };
         int kb0, kb1;
         if (ti.is_gu) {
           kb0 = 0; kb1 = nkb_gu;
@@ -336,70 +377,50 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         }
         if (p.trace) p.trace[tile * 8 + 2] = globaltimer();
         for (int kb = kb0; kb < kb1; ++kb) {
-          if (ti.dummy) {
-            // pair mode, missing second tile: no weights; still supply this
+          if (ti.dummy && !k2) {
+            // pair mode 1, missing second tile: no weights; still supply this
             // CTA's half of the shared token k-block below
           } else if (ti.is_gu && p.gu_unfused) {
             // one projection per tile: a single weight slot per k-block
-            const int krow = ch.x * p.d + kb * kBK;
-            const CUtensorMap* tw = ti.split ? &tm_wu : &tm_wg;
-            mbar_wait(a_empty + as, aph ^ 1);
-            mbar_arrive_expect_tx(a_full + as, C::kABytes);
-            uint8_t* sa = a_ring + as * C::kABytes;
-            tma_load_2d_hint(tw, a_full + as, sa, a_col, krow, pol_w);
-            tma_load_2d_hint(tw, a_full + as, sa + C::kABytes / 2, a_col + 64, krow, pol_w);
-            if (++as == C::kAStages) { as = 0; aph ^= 1; }
+            load_a(ti.split ? &tm_wu : &tm_wg, a_col, ch.x * p.d + kb * kBK);
           } else if (ti.is_gu) {
             const int krow = ch.x * p.d + kb * kBK;
-            mbar_wait(a_empty + as, aph ^ 1);
-            mbar_arrive_expect_tx(a_full + as, C::kABytes);
-            uint8_t* sa = a_ring + as * C::kABytes;
-            tma_load_2d_hint(&tm_wg, a_full + as, sa, a_col, krow, pol_w);
-            tma_load_2d_hint(&tm_wg, a_full + as, sa + C::kABytes / 2, a_col + 64, krow, pol_w);
-            if (++as == C::kAStages) { as = 0; aph ^= 1; }
-            mbar_wait(a_empty + as, aph ^ 1);
-            mbar_arrive_expect_tx(a_full + as, C::kABytes);
-            sa = a_ring + as * C::kABytes;
-            tma_load_2d_hint(&tm_wu, a_full + as, sa, a_col, krow, pol_w);
-            tma_load_2d_hint(&tm_wu, a_full + as, sa + C::kABytes / 2, a_col + 64, krow, pol_w);
-            if (++as == C::kAStages) { as = 0; aph ^= 1; }
+            load_a(&tm_wg, a_col, krow);
+            load_a(&tm_wu, a_col, krow);
           } else {
             // a down tile is a PAIR of 128-row hidden tiles sharing the token slot
             const int krow = ch.x * p.f + kb * kBK;
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-              mbar_wait(a_empty + as, aph ^ 1);
-              mbar_arrive_expect_tx(a_full + as, C::kABytes);
-              uint8_t* sa = a_ring + as * C::kABytes;
-              tma_load_2d_hint(&tm_wd, a_full + as, sa, a_col + half * kBM, krow, pol_w);
-              tma_load_2d_hint(&tm_wd, a_full + as, sa + C::kABytes / 2, a_col + half * kBM + 64, krow, pol_w);
-              if (++as == C::kAStages) { as = 0; aph ^= 1; }
-            }
+            load_a(&tm_wd, a_col, krow);
+            load_a(&tm_wd, a_col + kBM, krow);
           }
           mbar_wait(b_empty + bs, bph ^ 1);
           uint8_t* sb = b_ring + bs * C::kBBytes;
-          if (p.dbg & 16) {
+          const bool tok_rows = ti.is_gu || !p.tiled;
+          const CUtensorMap* tb = ti.is_gu ? &tm_xp : &tm_h;
+          // token row coordinate of box 0 and the k column within the map
+          const int r0 = tok_rows ? ch.y + b_row0 : (kb >> 1) * p.T_pad + ch.w + b_row0;
+          const int kc = tok_rows ? kb * kBK : (kb & 1) * kBK;  // tiled h: [f-tile][padded row][128]
+          if constexpr (k2) {
+            const uint32_t bar = lead_b_full + bs * 8;
+            if (p.dbg & 16) {
+              // diagnostic only (wrong results): no token loads
+              mbar_arrive_cluster(bar);
+            } else {
+              mbar_arrive_expect_tx_cluster(bar, b_bytes);
+              for (int b = 0; b < nbox; ++b)
+                tma_load_2d_2sm(tb, bar, sb + b * kBoxRows * kBK * 2, kc, r0 + b * kBoxRows, pol_t);
+            }
+          } else if (p.dbg & 16) {
             // diagnostic only (wrong results): no token loads, measures the weight stream alone
             mbar_arrive(b_full + bs);
-          } else if (mbar_arrive_expect_tx(b_full + bs, b_bytes), ti.is_gu || !p.tiled) {
-            const CUtensorMap* tb = ti.is_gu ? &tm_xp : &tm_h;
+          } else {
+            mbar_arrive_expect_tx(b_full + bs, b_bytes);
             for (int b = 0; b < nbox; ++b) {
               if constexpr (kPair) {  // this CTA's half of the boxes, into both CTAs' slot
                 if ((b & 1) == rank)
-                  tma_load_2d_mc(tb, b_full + bs, sb + b * kBoxRows * kBK * 2, kb * kBK, ch.y + b * kBoxRows, 3);
+                  tma_load_2d_mc(tb, b_full + bs, sb + b * kBoxRows * kBK * 2, kc, r0 + b * kBoxRows, 3);
               } else {
-                tma_load_2d(tb, b_full + bs, sb + b * kBoxRows * kBK * 2, kb * kBK, ch.y + b * kBoxRows);
-              }
-            }
-          } else {
-            // tiled h: [f-tile][padded row][128]; k-block kb lives in f-tile kb/2, column half kb%2
-            const int hrow = (kb >> 1) * p.T_pad + ch.w;
-            for (int b = 0; b < nbox; ++b) {
-              if constexpr (kPair) {
-                if ((b & 1) == rank)
-                  tma_load_2d_mc(&tm_h, b_full + bs, sb + b * kBoxRows * kBK * 2, (kb & 1) * kBK, hrow + b * kBoxRows, 3);
-              } else {
-                tma_load_2d(&tm_h, b_full + bs, sb + b * kBoxRows * kBK * 2, (kb & 1) * kBK, hrow + b * kBoxRows);
+                tma_load_2d(tb, b_full + bs, sb + b * kBoxRows * kBK * 2, kc, r0 + b * kBoxRows);
               }
             }
           }
@@ -418,10 +439,11 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       const int tile = sched_read(slot, sphase, lane == 0, true);
       if (++slot == kSchedSlots) { slot = 0; sphase ^= 1; }
       if (tile < 0) break;
+      if (k2 && rank == 1) continue;  // k2: rank 0 issues the pair's MMAs
       const TileInfo ti = decode_tile(p, tile, rank);
       const int4 ch = __ldg(p.chunk_tab + ti.chunk);
       const int n_mma = max(16, (ch.z + 15) & ~15);
-      const uint32_t idesc = make_idesc_bf16(kBM, n_mma, /*a MN-major*/ 1, /*b K-major*/ 0);
+      const uint32_t idesc = make_idesc_bf16(k2 ? 2 * kBM : kBM, n_mma, /*a MN-major*/ 1, /*b K-major*/ 0);
       int kb0, kb1;
       if (ti.is_gu) {
         kb0 = 0; kb1 = nkb_gu;
@@ -433,28 +455,33 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       tc_fence_after();
       if (p.trace && lane == 0) p.trace[tile * 8 + 5] = globaltimer();
       for (int kb = kb0; kb < kb1; ++kb) {
-        if (ti.dummy) {
-          // pair mode, missing second tile: consume and release the shared token slot
-          mbar_wait(b_full + bs, bph);
-          tc_fence_after();
-          if (elect_one()) {
-            mma_commit_mc(b_empty + bs, 3);
-            if (kb == kb1 - 1) mma_commit(tmem_full);
+        if constexpr (!k2) {
+          if (ti.dummy) {
+            // pair mode 1, missing second tile: consume and release the shared token slot
+            mbar_wait(b_full + bs, bph);
+            tc_fence_after();
+            if (elect_one()) {
+              mma_commit_mc(b_empty + bs, 3);
+              if (kb == kb1 - 1) mma_commit(tmem_full);
+            }
+            __syncwarp();
+            if (++bs == C::kBStages) { bs = 0; bph ^= 1; }
+            continue;
           }
-          __syncwarp();
-          if (++bs == C::kBStages) { bs = 0; bph ^= 1; }
-          continue;
         }
         const bool single = ti.is_gu && p.gu_unfused;  // one weight slot, one accumulator
+        // (k2: the full barriers complete with the peer's TMA bytes too; the
+        // transaction completion makes them visible, a CTA-scope wait suffices)
+        auto wait_full = [&](uint64_t* bar, uint32_t ph) { mbar_wait(bar, ph); };
         const int as0 = as;
-        mbar_wait(a_full + as, aph);
+        wait_full(a_full + as, aph);
         if (++as == C::kAStages) { as = 0; aph ^= 1; }
         const int as1 = as;  // second weight slot: up (gate+up) or hidden rows +128 (down)
         if (!single) {
-          mbar_wait(a_full + as, aph);
+          wait_full(a_full + as, aph);
           if (++as == C::kAStages) { as = 0; aph ^= 1; }
         }
-        mbar_wait(b_full + bs, bph);
+        wait_full(b_full + bs, bph);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sa0 = smem_u32(a_ring + as0 * C::kABytes);
@@ -464,18 +491,27 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             const uint64_t bdesc = make_smem_desc_sw128(sb + kk * 32, 16, 1024);
             const uint64_t adesc0 = make_smem_desc_sw128(sa0 + kk * 2048, C::kABytes / 2, 1024);
             const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
-            mma_bf16(tmem_base, adesc0, bdesc, idesc, acc);
+            if constexpr (k2) mma_bf16_2sm(tmem_base, adesc0, bdesc, idesc, acc);
+            else mma_bf16(tmem_base, adesc0, bdesc, idesc, acc);
             if (!single) {
               const uint32_t sa1 = smem_u32(a_ring + as1 * C::kABytes);
               const uint64_t adesc1 = make_smem_desc_sw128(sa1 + kk * 2048, C::kABytes / 2, 1024);
-              mma_bf16(tmem_base + kBN, adesc1, bdesc, idesc, acc);
+              if constexpr (k2) mma_bf16_2sm(tmem_base + kBN, adesc1, bdesc, idesc, acc);
+              else mma_bf16(tmem_base + kBN, adesc1, bdesc, idesc, acc);
             }
           }
-          mma_commit(a_empty + as0);
-          if (!single) mma_commit(a_empty + as1);
-          if constexpr (kPair) mma_commit_mc(b_empty + bs, 3);  // the slot is shared by the pair
-          else mma_commit(b_empty + bs);
-          if (kb == kb1 - 1) mma_commit(tmem_full);
+          if constexpr (k2) {  // release both CTAs' slots; both epilogues start
+            mma_commit2_mc(a_empty + as0, 3);
+            if (!single) mma_commit2_mc(a_empty + as1, 3);
+            mma_commit2_mc(b_empty + bs, 3);
+            if (kb == kb1 - 1) mma_commit2_mc(tmem_full, 3);
+          } else {
+            mma_commit(a_empty + as0);
+            if (!single) mma_commit(a_empty + as1);
+            if constexpr (kPair) mma_commit_mc(b_empty + bs, 3);  // the slot is shared by the pair
+            else mma_commit(b_empty + bs);
+            if (kb == kb1 - 1) mma_commit(tmem_full);
+          }
         }
         __syncwarp();
         if (++bs == C::kBStages) { bs = 0; bph ^= 1; }
@@ -489,6 +525,15 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
     const bool issuer = (wq == 0 && lane == 0);  // one bulk-copy issuer per group
     uint8_t* stg_g = stg + grp * C::kStgBytes;
+    // release the accumulator: one arrival per warp (k2: on rank 0's barrier)
+    auto release_tmem = [&]() {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (k2) mbar_arrive_cluster(lead_tmem_empty);
+        else mbar_arrive(tmem_empty);
+      }
+    };
     uint32_t acc_phase = 0;
     int slot = 0;
     uint32_t sphase = 0;
@@ -501,8 +546,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       mbar_wait(tmem_full, acc_phase);
       tc_fence_after();
       if (ti.dummy) {  // pair mode, missing second tile: nothing to write
-        tc_fence_before();
-        mbar_arrive(tmem_empty);
+        release_tmem();
         acc_phase ^= 1;
         continue;
       }
@@ -520,10 +564,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           uint32_t a[32];
           tmem_ld_32x32b_x32(tmem_base + lane_base + c0, a);
           tmem_wait_ld();
-          if (q == my_last) {
-            tc_fence_before();
-            mbar_arrive(tmem_empty);
-          }
+          if (q == my_last) release_tmem();
           float* sbuf = reinterpret_cast<float*>(stg_g);
           if (issuer) bulk_wait_read<0>();
           epi_bar_sync(grp);
@@ -539,10 +580,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             bulk_commit();
           }
         }
-        if (my_last < 0) {
-          tc_fence_before();
-          mbar_arrive(tmem_empty);
-        }
+        if (my_last < 0) release_tmem();
         if (issuer) bulk_wait_all();
       } else if (ti.is_gu) {
         const int f0 = ti.mt * kBM;
@@ -569,8 +607,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(tmem_empty);
+        release_tmem();
         if (p.trace && warp == 4 && lane == 0) p.trace[tile * 8 + 6] = globaltimer();
         // Phase 2: stage 32-row chunks in smem and bulk-copy them out.
         const int fl = wq * 32 + lane;  // feature within the tile
@@ -623,10 +660,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             uint32_t a[32];
             tmem_ld_32x32b_x32(tmem_base + lane_base + half * kBN + c0, a);
             tmem_wait_ld();
-            if (half == 1 && q == my_last) {
-              tc_fence_before();
-              mbar_arrive(tmem_empty);
-            }
+            if (half == 1 && q == my_last) release_tmem();
             float* sbuf = reinterpret_cast<float*>(stg_g);
             if (issuer) bulk_wait_read<0>();
             epi_bar_sync(grp);
@@ -661,10 +695,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             }
           }
         }
-        if (my_last < 0) {  // this group had no chunk: still release TMEM
-          tc_fence_before();
-          mbar_arrive(tmem_empty);
-        }
+        if (my_last < 0) release_tmem();  // this group had no chunk: still release TMEM
         if (issuer) bulk_wait_all();
       }
       if (p.trace && warp == 4 && lane == 0) p.trace[tile * 8 + 3] = globaltimer();
@@ -680,7 +711,8 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
   else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<C::kTmemCols>(tmem_base);
+    if constexpr (k2) tmem_dealloc2<C::kTmemCols>(tmem_base);
+    else tmem_dealloc<C::kTmemCols>(tmem_base);
   }
   if (threadIdx.x == 0) {
     // last CTA out resets the queue and the per-chunk counters for the next launch

@@ -375,11 +375,12 @@ int launch_router_x(const CUtensorMap& tmx, const RouterParams& p, const RouterP
   return launch_router_t<kBf16, 1, 1, 128>(tmx, p, plan, s);
 }
 
-template <int kBN, int kV, bool kPair = false>
+template <int kBN, int kV, int kPM = 0>
 int launch_ffn_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm, const CUtensorMap& dm,
                  const CUtensorMap& e, const FfnParams& p, int grid, cudaStream_t s) {
-  using C = FfnCfg<kBN, kV>;
-  auto kern = ffn_kernel<kBN, kV, kPair>;
+  constexpr bool kPair = kPM != 0;
+  using C = FfnCfg<kBN, kV, kPM == 2>;
+  auto kern = ffn_kernel<kBN, kV, kPM>;
   static bool attr_set[64] = {};
   int dev = 0;
   MOE_CUDA(cudaGetDevice(&dev));
@@ -413,9 +414,13 @@ int launch_ffn_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& 
 int launch_ffn_kernel(int bn, int variant, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm,
                       const CUtensorMap& dm, const CUtensorMap& e, const FfnParams& p, int grid,
                       cudaStream_t s) {
+  if (p.pair == 2) {  // cta_group::2 pairs
+    return bn == 256 ? launch_ffn_t<256, 2, 2>(a, b, cm, dm, e, p, grid, s)
+                     : launch_ffn_t<128, 2, 2>(a, b, cm, dm, e, p, grid, s);
+  }
   if (p.pair) {
-    return bn == 256 ? launch_ffn_t<256, 2, true>(a, b, cm, dm, e, p, grid, s)
-                     : launch_ffn_t<128, 2, true>(a, b, cm, dm, e, p, grid, s);
+    return bn == 256 ? launch_ffn_t<256, 2, 1>(a, b, cm, dm, e, p, grid, s)
+                     : launch_ffn_t<128, 2, 1>(a, b, cm, dm, e, p, grid, s);
   }
   if (bn == 256)
     return variant == 3 ? launch_ffn_t<256, 3>(a, b, cm, dm, e, p, grid, s) : launch_ffn_t<256, 2>(a, b, cm, dm, e, p, grid, s);
@@ -482,7 +487,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   // token re-reads are a real share of the L2 -> SM traffic (MOE_B200_FFN_PAIR
   // forces it on / off)
   p.pair = (mode == kFfnFused && bn == 256) ? 1 : 0;
-  if (const char* env = getenv("MOE_B200_FFN_PAIR")) p.pair = (atoi(env) != 0 && mode == kFfnFused) ? 1 : 0;
+  if (const char* env = getenv("MOE_B200_FFN_PAIR")) p.pair = mode == kFfnFused ? std::min(2, std::max(0, atoi(env))) : 0;
   long max_tiles = (long)L.max_chunks * (p.n_mt_gu * (p.gu_unfused ? 2 : 1) + p.n_mt_dn * p.splits);
   int grid = static_cast<int>(std::max(1L, std::min<long>(kNumSMs, max_tiles)));
   if (p.pair) grid = std::max(2, grid & ~1);  // whole clusters

@@ -380,6 +380,31 @@ def test_forward_routed_rejects_out_of_range(pkg):
 
 
 @pytest.mark.parametrize("shape", [
+    (4, 2, 768, 1408, 512, "softmax"),          # 256-row chunks; odd gate+up / down tile counts
+    (8, 2, 512, 384, 64, "sigmoid_normalized"),  # 128-row chunks, 3 gate+up tiles
+])
+def test_ffn_cta_pair_modes_bit_identical(pkg, shape, monkeypatch):
+    """The FFN's CTA-pair variants (ffn.cuh kPM: 1 = token loads multicast to
+    both CTAs, 2 = one cta_group::2 MMA of M = 256 over the pair, each CTA
+    holding half the token rows) give exactly the single-CTA kernel's bits,
+    including pairs whose second weight tile does not exist."""
+    P = pkg
+    e, k, d, f, b, g = shape
+    tokens, wr, gate, up, down = O.make_instance(41, e, k, d, f, b)
+    layer = _layer(P, _cfg(P, e, k, d, f, g), wr, gate, up, down, b)
+    x = torch.from_numpy(tokens).cuda()
+    ys = {}
+    for mode in ("0", "1", "2"):
+        monkeypatch.setenv("MOE_B200_FFN_PAIR", mode)
+        ys[mode] = _np(layer.forward(x))
+    bits_equal(ys["1"], ys["0"])
+    bits_equal(ys["2"], ys["0"])
+    if b * d * f <= 5e7:  # (the oracle's fp64 fold is sized for small shapes)
+        ref = O.moe_forward(tokens, wr, gate, up, down, e, k, g)["y"]
+        assert np.abs(ys["2"] - ref).max() <= 2e-2 * max(np.abs(ref).max(), 1e-6)
+
+
+@pytest.mark.parametrize("shape", [
     (8, 2, 512, 1024, 128, "softmax"),
     (16, 4, 256, 384, 64, "sigmoid_normalized"),
     (60, 4, 256, 176, 96, "softmax"),
