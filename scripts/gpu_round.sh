@@ -14,4 +14,5 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_kernel -s 1 -c 1 -o gpurun_out/prof_ffn_$TAG -f python scripts/run_layer.py mixtral 512 2 > /dev/null 2>&1
 for k in router_seg dispatch combine_token; do timeout 300 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -o gpurun_out/prof_${k}_$TAG -f python scripts/run_layer.py mixtral 512 2 > /dev/null 2>&1; done
 for c in mixtral qwen60 deepseek; do python scripts/ffn_timeline.py $c ${c}_$TAG > /dev/null 2>&1; done
+timeout 300 python scripts/stage_times.py qwen60 mixtral > gpurun_out/stage_times_$TAG.log 2>&1
 echo done
