@@ -475,3 +475,64 @@ def test_nonfinite_router_weight_raises(pkg, mode, monkeypatch):
     wr[7, 3] = np.inf
     with pytest.raises(P.NonFiniteInput, match="router_weight"):
         P.moe_forward(tokens, wr, P.ExpertWeights(gate, up, down), _cfg(P, e, k, d, f, "softmax"))
+
+
+@pytest.mark.parametrize("gating", ["softmax", "sigmoid_normalized"])
+def test_top_k_equals_num_experts(pkg, gating):
+    """k = E (every expert selected; ModelConfig allows 1 <= k <= E,
+    model.py:37-48): routing bit-exact, y within tolerance of the oracle."""
+    P = pkg
+    e, k, d, f, b = 4, 4, 64, 96, 37
+    tokens, wr, gate, up, down = O.make_instance(51, e, k, d, f, b)
+    cfg = _cfg(P, e, k, d, f, gating)
+    layer = _layer(P, cfg, wr, gate, up, down, b)
+    st = layer.run_stages(torch.from_numpy(tokens).cuda())
+    ref = O.moe_forward(tokens, wr, gate, up, down, e, k, gating)
+    bits_equal(_np(st["indices"]).astype(np.int64), ref["indices"])
+    bits_equal(_np(st["weights"]), ref["weights"])
+    bits_equal(_np(st["counts"]).astype(np.int64), np.full(e, b, np.int64))
+    bits_equal(_np(st["forward"]).astype(np.int64), ref["forward"])
+    y = _np(layer.forward(torch.from_numpy(tokens).cuda()))
+    assert O.max_rel_error(y, ref["y"]) <= TOL
+
+
+def test_large_batch_streamed_dispatch(pkg):
+    """More expanded rows than the dispatch kernel stages in shared memory
+    (T > 8192: indices streamed from global memory): counts and the stable
+    permutation bit-exact against the oracle; y against a torch fp32 reference
+    on the same bf16-rounded operands."""
+    P = pkg
+    e, k, d, f, b = 8, 2, 256, 256, 4200
+    rng = np.random.default_rng(61)
+    tokens = rng.standard_normal((b, d)).astype(np.float32)
+    wr = (rng.standard_normal((d, e)) / np.sqrt(d)).astype(np.float32)
+    gate = (rng.standard_normal((e * d, f)) / np.sqrt(d)).astype(np.float32)
+    up = (rng.standard_normal((e * d, f)) / np.sqrt(d)).astype(np.float32)
+    down = (rng.standard_normal((e * f, d)) / np.sqrt(f)).astype(np.float32)
+    cfg = _cfg(P, e, k, d, f, "softmax")
+    layer = _layer(P, cfg, wr, gate, up, down, b)
+    x = torch.from_numpy(tokens).cuda()
+    y = layer.forward(x)
+    idx = _np(layer.topk_idx[:b]).astype(np.int64)
+    w = _np(layer.topk_w[:b])
+    idx_ref, w_ref = O.route(tokens, wr, k, "softmax")
+    bits_equal(idx, idx_ref)
+    bits_equal(w, w_ref)
+    bits_equal(_np(layer.counts).astype(np.int64), O.expert_histogram(idx_ref, e))
+    fwd_ref, _ = O.build_permutation(idx_ref)
+    bits_equal(_np(layer.fwd[: b * k]).astype(np.int64), fwd_ref)
+    # torch fp32 reference over bf16-rounded operands (h rounded to bf16, as the kernel stores it)
+    bf = lambda a: torch.from_numpy(a).cuda().to(torch.bfloat16).float()  # noqa: E731
+    xb, gb, ub, db = bf(tokens), bf(gate), bf(up), bf(down)
+    y_ref = torch.zeros((b, d), dtype=torch.float32, device="cuda")
+    it, iw = torch.from_numpy(idx_ref).cuda(), torch.from_numpy(w_ref).cuda()
+    for ex in range(e):
+        for j in range(k):
+            rows = (it[:, j] == ex).nonzero().flatten()
+            if rows.numel() == 0:
+                continue
+            g_ = xb[rows] @ gb[ex * d:(ex + 1) * d]
+            u_ = xb[rows] @ ub[ex * d:(ex + 1) * d]
+            h = (torch.nn.functional.silu(g_) * u_).to(torch.bfloat16).float()
+            y_ref[rows] += iw[rows, j:j + 1] * (h @ db[ex * f:(ex + 1) * f])
+    assert O.max_rel_error(_np(y), _np(y_ref)) <= TOL
