@@ -11,6 +11,7 @@
 #include <mutex>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "elementwise.cuh"
@@ -263,9 +264,49 @@ int get_encoder() {
   return MOE_B200_OK;
 }
 
+// Host cost per forward: encoded tensor maps are cached by their inputs (the
+// weight stacks and workspace regions of a layer repeat call after call), so
+// the common case is a lookup, not an encode.
+struct MapKey {
+  const void* base;
+  uint64_t rows, cols;
+  uint32_t box_cols, box_rows;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && rows == o.rows && cols == o.cols && box_cols == o.box_cols && box_rows == o.box_rows;
+  }
+};
+constexpr int kMapCache = 64;
+struct MapCache {
+  std::mutex mu;
+  MapKey key[kMapCache];
+  CUtensorMap map[kMapCache];
+  int n = 0, next = 0;
+};
+MapCache g_maps;
+
+int encode_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                    uint32_t box_rows);
+
 // Row-major bf16 matrix (rows x cols), box (box_cols x box_rows), 128B swizzle.
 int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
                   uint32_t box_cols, uint32_t box_rows) {
+  const MapKey k{base, rows, cols, box_cols, box_rows};
+  std::lock_guard<std::mutex> lock(g_maps.mu);
+  for (int i = 0; i < g_maps.n; ++i)
+    if (g_maps.key[i] == k) {
+      *m = g_maps.map[i];
+      return MOE_B200_OK;
+    }
+  const int rc = encode_map_bf16(m, base, rows, cols, box_cols, box_rows);
+  if (rc) return rc;
+  const int slot = g_maps.n < kMapCache ? g_maps.n++ : (g_maps.next++ % kMapCache);
+  g_maps.key[slot] = k;
+  g_maps.map[slot] = *m;
+  return MOE_B200_OK;
+}
+
+int encode_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                    uint32_t box_rows) {
   int rc = get_encoder();
   if (rc) return rc;
   cuuint64_t dims[2] = {cols, rows};
@@ -282,6 +323,27 @@ int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
     return MOE_B200_ERR_CUDA;
   }
   return MOE_B200_OK;
+}
+
+// Largest dynamic shared memory already granted per (kernel, device):
+// cudaFuncSetAttribute is a driver call, so it runs only when a launch needs more.
+cudaError_t ensure_dyn_smem(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, size_t>> granted;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& g : granted)
+    if (g.first.first == kern && g.first.second == dev) {
+      if (bytes <= g.second) return cudaSuccess;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+      if (e == cudaSuccess) g.second = bytes;
+      return e;
+    }
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e == cudaSuccess) granted.push_back({{kern, dev}, bytes});
+  return e;
 }
 
 // ------------------------------- launches --------------------------------------
@@ -363,7 +425,7 @@ RouterPlan plan_router(const moe_b200_config& c, int64_t B, int x_bf16) {
 template <bool kBf16, int kTE, int kTT, int kKC>
 int launch_router_t(const CUtensorMap& tmx, const RouterParams& p, const RouterPlan& plan, cudaStream_t s) {
   auto kern = router_kernel<kBf16, kTE, kTT, kKC>;
-  MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
+  MOE_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(kern), plan.smem));
   kern<<<plan.n_tblocks * plan.n_eblocks, plan.threads, plan.smem, s>>>(tmx, p);
   MOE_LAUNCH_CHECK("router_kernel");
   return MOE_B200_OK;
@@ -600,7 +662,7 @@ int launch_dispatch(const moe_b200_config& c, int64_t B, const void* x, int xb, 
   const size_t smem = (((5 * c.num_experts + 3 + 3) & ~3) + (smem_idx ? ((q.T + 3) & ~3) : 0)) * sizeof(int32_t);
   auto kern = xb ? (smem_idx ? dispatch_kernel<true, true> : dispatch_kernel<true, false>)
                  : (smem_idx ? dispatch_kernel<false, true> : dispatch_kernel<false, false>);
-  if (smem > 48 * 1024) MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > 48 * 1024) MOE_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem));
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kDispThreads), smem, s, q);
   if (e != cudaSuccess) return cuda_fail(e, "dispatch launch");
   return MOE_B200_OK;
@@ -740,7 +802,7 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
     const bool wvec = (cfg->num_experts % 4) == 0;
     void (*kern)(RouterParams) = xb ? (wvec ? router_seg_kernel<true, true> : router_seg_kernel<true, false>)
                                     : (wvec ? router_seg_kernel<false, true> : router_seg_kernel<false, false>);
-    MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q.smem));
+    MOE_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(kern), q.smem));
     kern<<<grid, kSegThreads, q.smem, s>>>(p);
     MOE_LAUNCH_CHECK("router_seg_kernel");
   } else if ((rc = launch_router_exact(*cfg, B, x, xb, w_router, L, ws, p, s))) {
