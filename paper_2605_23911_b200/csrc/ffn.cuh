@@ -64,7 +64,6 @@ struct FfnParams {
   int gu_unfused;            // 1: gate and up as separate tiles, fp32 out (pipeline.py:316-370 ablation)
   float* gu32;               // unfused output: tiled [proj][f/128][T_pad][128] fp32
   int pair;                  // 1: launched as CTA pairs (clusters of 2) sharing token loads
-  int dbg;                   // debug/experiment bits (0 in production)
   int tiled;                 // 1: h / ys in the tiled padded-row layouts (fused forward)
   int T_pad;                 // padded-row capacity of the tiled layouts
   unsigned long long* trace; // optional (debug): 8 u64 per tile {sm, fetch, first load, epi done, epi start, mma start}
@@ -402,17 +401,9 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           const int kc = tok_rows ? kb * kBK : (kb & 1) * kBK;  // tiled h: [f-tile][padded row][128]
           if constexpr (k2) {
             const uint32_t bar = lead_b_full + bs * 8;
-            if (p.dbg & 16) {
-              // diagnostic only (wrong results): no token loads
-              mbar_arrive_cluster(bar);
-            } else {
-              mbar_arrive_expect_tx_cluster(bar, b_bytes);
-              for (int b = 0; b < nbox; ++b)
-                tma_load_2d_2sm(tb, bar, sb + b * kBoxRows * kBK * 2, kc, r0 + b * kBoxRows, pol_t);
-            }
-          } else if (p.dbg & 16) {
-            // diagnostic only (wrong results): no token loads, measures the weight stream alone
-            mbar_arrive(b_full + bs);
+            mbar_arrive_expect_tx_cluster(bar, b_bytes);
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d_2sm(tb, bar, sb + b * kBoxRows * kBK * 2, kc, r0 + b * kBoxRows, pol_t);
           } else {
             mbar_arrive_expect_tx(b_full + bs, b_bytes);
             for (int b = 0; b < nbox; ++b) {

@@ -543,7 +543,6 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.tiled = fused ? 1 : 0;
   p.T_pad = L.T_pad;
   p.trace = g_ffn_trace;
-  if (const char* env = getenv("MOE_B200_FFN_DEBUG")) p.dbg = atoi(env);
   const int bn = chunk_rows_for(c, B);
   // CTA pairs sharing token loads: fused mode with large token chunks, where
   // token re-reads are a real share of the L2 -> SM traffic (MOE_B200_FFN_PAIR
