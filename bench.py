@@ -395,7 +395,15 @@ def _e2e_pipelined(args, layer, x, B, d, flush, dev):
     e_end = torch.cuda.Event(enable_timing=True)
     if flush is not None:
         flush.zero_()
-    torch.cuda.synchronize(dev)
+    # same power / clock regime as `value`: ~1 s of the same pipelined steps
+    # right before the timed ones, with no idle gap in between (a short run
+    # after an idle gap would ride the burst clocks the power cap has not yet
+    # pulled down)
+    t_warm = time.time() + 1.0
+    i = 0
+    while time.time() < t_warm:
+        pipe.submit(x_host[i % n_slots], y_host[i % n_slots])
+        i += 1
     e_start.record()
     pipe.wait(e_start)  # the copy streams start after the timing start
     for i in range(steps):
