@@ -544,10 +544,12 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.T_pad = L.T_pad;
   p.trace = g_ffn_trace;
   const int bn = chunk_rows_for(c, B);
-  // CTA pairs sharing token loads: fused mode with large token chunks, where
-  // token re-reads are a real share of the L2 -> SM traffic (MOE_B200_FFN_PAIR
-  // forces it on / off)
-  p.pair = (mode == kFfnFused && bn == 256) ? 1 : 0;
+  // CTA pairs for large token chunks, where token re-reads are a real share of
+  // the L2 -> SM traffic: one cta_group::2 MMA per pair, each CTA holding half
+  // the token rows (mode 2; under the 1 kW cap Mixtral-512 ~6% faster than the
+  // multicast pair, mode 1, from the saved data movement; a tie uncapped).
+  // MOE_B200_FFN_PAIR=0/1/2 forces a mode (all bit-identical).
+  p.pair = (mode == kFfnFused && bn == 256) ? 2 : 0;
   if (const char* env = getenv("MOE_B200_FFN_PAIR")) p.pair = mode == kFfnFused ? std::min(2, std::max(0, atoi(env))) : 0;
   long max_tiles = (long)L.max_chunks * (p.n_mt_gu * (p.gu_unfused ? 2 : 1) + p.n_mt_dn * p.splits);
   int grid = static_cast<int>(std::max(1L, std::min<long>(kNumSMs, max_tiles)));
