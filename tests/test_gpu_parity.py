@@ -536,3 +536,23 @@ def test_large_batch_streamed_dispatch(pkg):
             h = (torch.nn.functional.silu(g_) * u_).to(torch.bfloat16).float()
             y_ref[rows] += iw[rows, j:j + 1] * (h @ db[ex * f:(ex + 1) * f])
     assert O.max_rel_error(_np(y), _np(y_ref)) <= TOL
+
+
+@pytest.mark.parametrize("shape", [
+    (1, 1, 64, 128, 300, "softmax"),             # one expert: chunks of 256 + 44 rows, pair mode
+    (2, 2, 64, 128, 200, "sigmoid_normalized"),  # k = E = 2, 200 rows per expert, pair mode
+])
+def test_large_chunk_pair_path_small_expert_counts(pkg, shape):
+    """Batches with more than 96 rows per expert take 256-row chunks and the
+    CTA-pair (cta_group::2) FFN; with one or two experts that includes ragged
+    last chunks.  Routing bit-exact, y within tolerance of the oracle."""
+    P = pkg
+    e, k, d, f, b, g = shape
+    tokens, wr, gate, up, down = O.make_instance(71, e, k, d, f, b)
+    layer = _layer(P, _cfg(P, e, k, d, f, g), wr, gate, up, down, b)
+    x = torch.from_numpy(tokens).cuda()
+    y = _np(layer.forward(x))
+    ref = O.moe_forward(tokens, wr, gate, up, down, e, k, g)
+    bits_equal(_np(layer.topk_idx[:b]).astype(np.int64), ref["indices"])
+    bits_equal(_np(layer.counts).astype(np.int64), ref["counts"])
+    assert O.max_rel_error(y, ref["y"]) <= TOL
