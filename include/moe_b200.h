@@ -250,6 +250,55 @@ int moe_b200_combine_rows(const moe_b200_config* cfg, int64_t num_tokens, const 
                           const int32_t* perm_inv, const float* topk_w, void* y, int y_dtype,
                           void* stream);
 
+/* ---- expert parallelism over peer memory (NVLink P2P / CUDA IPC) ----------
+ * Replaces the library all-to-alls of the expert-parallel layer (
+ * paper_2605_23911_b200/ep.py) with direct writes into the peer ranks' buffers.
+ * Buffers are allocated with moe_b200_ipc_alloc, their handles exchanged by the
+ * caller (any host transport) and mapped with moe_b200_ipc_open.  Per rank r:
+ *   counts[r]  int32 [n][E]          all-gathered per-expert row counts
+ *   flags[r]   uint64 [3][n]         epoch flags (counts, rows, returns) per source, zeroed once
+ *   rows[r]    bf16 [R_max][d]       expert-major received rows
+ *   ids[r]     int32x2 [R_max]       {source rank, expanded id} of each received row
+ *   home[r]    fp32 [T_max][d]       returned expert outputs by expanded id
+ * `epoch` grows by one per forward; flags are never reset. */
+#define MOE_B200_EP_MAX_RANKS 16
+typedef struct {
+  void* counts[MOE_B200_EP_MAX_RANKS];
+  void* flags[MOE_B200_EP_MAX_RANKS];
+  void* rows[MOE_B200_EP_MAX_RANKS];
+  void* ids[MOE_B200_EP_MAX_RANKS];
+  void* home[MOE_B200_EP_MAX_RANKS];
+  int expert_lo[MOE_B200_EP_MAX_RANKS + 1]; /* rank r owns experts [lo[r], lo[r+1]) */
+  int n, me;
+} moe_b200_ep_peers;
+
+/* cudaMalloc + IPC handle (64 bytes, opaque) of the allocation. */
+int moe_b200_ipc_alloc(size_t bytes, void** ptr, void* handle64);
+/* Map another process's allocation from its handle. */
+int moe_b200_ipc_open(const void* handle64, void** ptr);
+int moe_b200_ipc_close(void* ptr);
+int moe_b200_ipc_free(void* ptr);
+
+/* 1. Counts all-gather: histogram of topk_idx (T = B*k entries, global expert
+ *    ids) written into counts[r][me][:] of every rank r, then flag set 0. */
+int moe_b200_ep_p2p_counts(const moe_b200_config* cfg, int64_t num_rows, const int32_t* topk_idx,
+                           const moe_b200_ep_peers* peers, uint64_t epoch, void* stream);
+/* Wait (on the device) until flag set `set` of every source reached `epoch`. */
+int moe_b200_ep_p2p_wait(const moe_b200_ep_peers* peers, int set, uint64_t epoch, void* stream);
+/* 2. Dispatch: the local permuted rows (perm_fwd / offsets of the local
+ *    route) of x (bf16, num_tokens x d) go into the owners' rows / ids at the
+ *    single-GPU permutation's expert-major order, then flag set 1.  Waits for
+ *    flag set 0 itself.  done_counter: one int32 of device memory, zeroed once. */
+int moe_b200_ep_p2p_dispatch(const moe_b200_config* cfg, int64_t num_tokens, const void* x_bf16,
+                             const int32_t* topk_idx, const int32_t* perm_fwd, const int32_t* offsets,
+                             const moe_b200_ep_peers* peers, int32_t* done_counter, uint64_t epoch,
+                             void* stream);
+/* 3. Return: the num_rows received rows' outputs (fp32, num_rows x d) into
+ *    home[source][expanded id], then flag set 2 of every source. */
+int moe_b200_ep_p2p_return(const moe_b200_config* cfg, int64_t num_rows, const float* out_rows,
+                           const moe_b200_ep_peers* peers, int32_t* done_counter, uint64_t epoch,
+                           void* stream);
+
 /* Copy the device status flags (MOE_B200_FLAG_*) to the host and clear them.
  * Synchronises `stream`. */
 int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws,

@@ -45,6 +45,23 @@ class Config(ctypes.Structure):
     ]
 
 
+EP_MAX_RANKS = 16
+
+
+class EpPeers(ctypes.Structure):
+    """moe_b200_ep_peers: per-rank buffer pointers mapped in this process."""
+    _fields_ = [
+        ("counts", ctypes.c_void_p * EP_MAX_RANKS),
+        ("flags", ctypes.c_void_p * EP_MAX_RANKS),
+        ("rows", ctypes.c_void_p * EP_MAX_RANKS),
+        ("ids", ctypes.c_void_p * EP_MAX_RANKS),
+        ("home", ctypes.c_void_p * EP_MAX_RANKS),
+        ("expert_lo", ctypes.c_int32 * (EP_MAX_RANKS + 1)),
+        ("n", ctypes.c_int32),
+        ("me", ctypes.c_int32),
+    ]
+
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _INT = ctypes.c_int
@@ -52,7 +69,17 @@ _CFG = ctypes.POINTER(Config)
 _SZ = ctypes.c_size_t
 
 #: symbol -> (restype, argtypes); every symbol declared in include/moe_b200.h
+_PEERS = ctypes.POINTER(EpPeers)
+_U64 = ctypes.c_uint64
 SIGNATURES = {
+    "moe_b200_ipc_alloc": (_INT, [_SZ, ctypes.POINTER(_P), _P]),
+    "moe_b200_ipc_open": (_INT, [_P, ctypes.POINTER(_P)]),
+    "moe_b200_ipc_close": (_INT, [_P]),
+    "moe_b200_ipc_free": (_INT, [_P]),
+    "moe_b200_ep_p2p_counts": (_INT, [_CFG, _I64, _P, _PEERS, _U64, _P]),
+    "moe_b200_ep_p2p_wait": (_INT, [_PEERS, _INT, _U64, _P]),
+    "moe_b200_ep_p2p_dispatch": (_INT, [_CFG, _I64, _P, _P, _P, _P, _PEERS, _P, _U64, _P]),
+    "moe_b200_ep_p2p_return": (_INT, [_CFG, _I64, _P, _PEERS, _P, _U64, _P]),
     "moe_b200_workspace_size": (_INT, [_CFG, _I64, ctypes.POINTER(_SZ)]),
     "moe_b200_workspace_init": (_INT, [_CFG, _I64, _P, _SZ, _P]),
     "moe_b200_route": (_INT, [_CFG, _I64, _P, _INT, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),

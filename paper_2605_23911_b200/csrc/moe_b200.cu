@@ -19,6 +19,7 @@
 #include "router.cuh"
 #include "router_seg.cuh"
 #include "dispatch.cuh"
+#include "ep_p2p.cuh"
 
 using namespace moe;
 
@@ -1207,6 +1208,111 @@ int moe_b200_gather_rows(int64_t n_rows, int64_t row_bytes, const void* src, con
       static_cast<const uint8_t*>(src), idx, static_cast<uint8_t*>(dst), static_cast<int>(n_rows),
       static_cast<int>(row_bytes));
   MOE_LAUNCH_CHECK("gather_rows_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_ipc_alloc(size_t bytes, void** ptr, void* handle64) {
+  if (!ptr || !handle64 || bytes == 0) return MOE_B200_ERR_INVALID_VALUE;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  MOE_CUDA(cudaMalloc(ptr, bytes));
+  MOE_CUDA(cudaMemset(*ptr, 0, bytes));
+  cudaIpcMemHandle_t h;
+  MOE_CUDA(cudaIpcGetMemHandle(&h, *ptr));
+  memcpy(handle64, &h, sizeof(h));
+  return MOE_B200_OK;
+}
+
+int moe_b200_ipc_open(const void* handle64, void** ptr) {
+  if (!ptr || !handle64) return MOE_B200_ERR_INVALID_VALUE;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  MOE_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return MOE_B200_OK;
+}
+
+int moe_b200_ipc_close(void* ptr) {
+  MOE_CUDA(cudaIpcCloseMemHandle(ptr));
+  return MOE_B200_OK;
+}
+
+int moe_b200_ipc_free(void* ptr) {
+  MOE_CUDA(cudaFree(ptr));
+  return MOE_B200_OK;
+}
+
+static int ep_peers_from(const moe_b200_ep_peers* in, moe::EpPeers* out) {
+  if (!in || in->n < 1 || in->n > kEpMaxRanks || in->me < 0 || in->me >= in->n) return MOE_B200_ERR_INVALID_VALUE;
+  for (int r = 0; r < in->n; ++r) {
+    out->counts[r] = static_cast<int32_t*>(in->counts[r]);
+    out->flags[r] = static_cast<unsigned long long*>(in->flags[r]);
+    out->rows[r] = static_cast<__nv_bfloat16*>(in->rows[r]);
+    out->ids[r] = static_cast<int2*>(in->ids[r]);
+    out->home[r] = static_cast<float*>(in->home[r]);
+  }
+  for (int r = 0; r <= in->n; ++r) out->expert_lo[r] = in->expert_lo[r];
+  out->n = in->n;
+  out->me = in->me;
+  return MOE_B200_OK;
+}
+
+int moe_b200_ep_p2p_counts(const moe_b200_config* cfg, int64_t num_rows, const int32_t* topk_idx,
+                           const moe_b200_ep_peers* peers, uint64_t epoch, void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  moe::EpPeers P{};
+  if ((rc = ep_peers_from(peers, &P))) return rc;
+  if (num_rows < 0 || (num_rows > 0 && !topk_idx)) return MOE_B200_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t smem = (size_t)cfg->num_experts * sizeof(int32_t);
+  ep_counts_kernel<<<1, 256, smem, s>>>(topk_idx, static_cast<int>(num_rows), cfg->num_experts, P, epoch);
+  MOE_LAUNCH_CHECK("ep_counts_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_ep_p2p_wait(const moe_b200_ep_peers* peers, int set, uint64_t epoch, void* stream) {
+  moe::EpPeers P{};
+  int rc;
+  if ((rc = ep_peers_from(peers, &P))) return rc;
+  if (set < 0 || set >= kEpFlagSets) return MOE_B200_ERR_INVALID_VALUE;
+  ep_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(P.flags[P.me], set, P.n, epoch);
+  MOE_LAUNCH_CHECK("ep_wait_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_ep_p2p_dispatch(const moe_b200_config* cfg, int64_t num_tokens, const void* x_bf16,
+                             const int32_t* topk_idx, const int32_t* perm_fwd, const int32_t* offsets,
+                             const moe_b200_ep_peers* peers, int32_t* done_counter, uint64_t epoch,
+                             void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  moe::EpPeers P{};
+  if ((rc = ep_peers_from(peers, &P))) return rc;
+  if (!done_counter || (num_tokens > 0 && (!x_bf16 || !topk_idx || !perm_fwd || !offsets)))
+    return MOE_B200_ERR_INVALID_VALUE;
+  if (cfg->hidden_dim % 8) return MOE_B200_ERR_UNSUPPORTED;
+  const int T = static_cast<int>(num_tokens * cfg->top_k);
+  const int grid = std::max(1, std::min((T + 7) / 8, kNumSMs));
+  const size_t smem = (size_t)cfg->num_experts * sizeof(int32_t);
+  ep_dispatch_kernel<<<grid, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(x_bf16), topk_idx, perm_fwd, offsets, T, cfg->top_k, cfg->num_experts,
+      cfg->hidden_dim, P, done_counter, epoch);
+  MOE_LAUNCH_CHECK("ep_dispatch_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_ep_p2p_return(const moe_b200_config* cfg, int64_t num_rows, const float* out_rows,
+                           const moe_b200_ep_peers* peers, int32_t* done_counter, uint64_t epoch,
+                           void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  moe::EpPeers P{};
+  if ((rc = ep_peers_from(peers, &P))) return rc;
+  if (!done_counter || (num_rows > 0 && !out_rows)) return MOE_B200_ERR_INVALID_VALUE;
+  if (cfg->hidden_dim % 4) return MOE_B200_ERR_UNSUPPORTED;
+  const int grid = std::max(1, std::min<int>(static_cast<int>((num_rows + 7) / 8), kNumSMs));
+  ep_return_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      out_rows, P.ids[P.me], static_cast<int>(num_rows), cfg->hidden_dim, P, done_counter, epoch);
+  MOE_LAUNCH_CHECK("ep_return_kernel");
   return MOE_B200_OK;
 }
 

@@ -150,7 +150,9 @@ class ExpertParallelMoE:
     """One MoE layer with experts sharded over the ranks of ``group``."""
 
     def __init__(self, config: ModelConfig, router_weight, weights_local: ExpertWeights, max_tokens: int,
-                 group=None, device=None, ops=None):
+                 group=None, device=None, ops=None, transport: str = "collective"):
+        """``transport``: "collective" (torch.distributed all-to-alls) or "p2p"
+        (rows written straight into the peers' buffers, PeerExchange)."""
         self.config = config
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -160,6 +162,9 @@ class ExpertParallelMoE:
         self.local_cfg = ModelConfig(hi - lo, 1, config.hidden_dim, config.ffn_dim, config.gating)
         self.device = torch.device(device or "cuda")
         self.ops = ops or CudaOps(config, self.local_cfg, router_weight, weights_local, max_tokens, self.device)
+        if transport not in ("collective", "p2p"):
+            raise ValueError(f"transport must be 'collective' or 'p2p', got {transport!r}")
+        self.p2p = PeerExchange(self, max_tokens) if transport == "p2p" else None
 
     def _a2a(self, out, inp, out_splits, in_splits):
         if self.world == 1:
@@ -168,6 +173,8 @@ class ExpertParallelMoE:
         dist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits, group=self.group)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if self.p2p is not None:
+            return self.p2p.forward(x)
         cfg = self.config
         k, E, d = cfg.top_k, cfg.num_experts, cfg.hidden_dim
         B = x.shape[0]
@@ -211,3 +218,129 @@ class ExpertParallelMoE:
         self._a2a(back, ys, send_rows, recv_rows)
         y = self.ops.combine(back, inv, w, B)
         return y[:, :d]
+
+
+class PeerExchange:
+    """The expert-parallel exchanges over peer memory (libmoe_b200 ``ep_p2p``).
+
+    Each rank allocates its exchange buffers (counts, epoch flags, received
+    rows and ids, returned outputs) with CUDA IPC handles; the handles are
+    all-gathered over ``group`` once, and every rank maps every peer's
+    buffers.  A forward then writes rows straight into the owners' buffers
+    (dispatch fused with the local gather) and the expert outputs straight
+    back into the home ranks' buffers, with device-side epoch flags instead
+    of library all-to-alls.  The one host synchronisation per forward reads
+    the all-gathered counts to size the local expert FFN, as in the NCCL
+    path.
+    """
+
+    def __init__(self, ep: "ExpertParallelMoE", max_tokens: int):
+        ops = ep.ops
+        self.ep, self.ops, self.lib = ep, ops, ops.lib
+        n, me = ep.world, ep.rank
+        if n > _lib.EP_MAX_RANKS:
+            raise ValueError(f"at most {_lib.EP_MAX_RANKS} ranks")
+        E, k = ep.config.num_experts, ep.config.top_k
+        d = ops.w.hidden_pad
+        n_loc = ep.local_cfg.num_experts
+        self.max_tokens = max_tokens
+        # worst case: every token of every rank sends min(k, E_local) rows here
+        self.r_max = max(1, n * max_tokens * min(k, n_loc))
+        t_max = max(1, max_tokens * k)
+        sizes = {"counts": n * E * 4, "flags": 3 * n * 8, "rows": self.r_max * d * 2,
+                 "ids": self.r_max * 8, "home": t_max * d * 4}
+        self._own, handles = {}, {}
+        for name, nbytes in sizes.items():
+            p = ctypes.c_void_p()
+            h = ctypes.create_string_buffer(64)
+            _lib.check(self.lib.moe_b200_ipc_alloc(nbytes, ctypes.byref(p), h), "ipc_alloc")
+            self._own[name] = p.value
+            handles[name] = h.raw
+        gathered = [None] * n
+        if n > 1:
+            dist.all_gather_object(gathered, handles, group=ep.group)
+        else:
+            gathered = [handles]
+        self.peers = _lib.EpPeers()
+        self._opened = []
+        for r in range(n):
+            for name in sizes:
+                if r == me:
+                    ptr = self._own[name]
+                else:
+                    p = ctypes.c_void_p()
+                    _lib.check(self.lib.moe_b200_ipc_open(gathered[r][name], ctypes.byref(p)), "ipc_open")
+                    ptr = p.value
+                    self._opened.append(ptr)
+                getattr(self.peers, name)[r] = ptr
+        for r, (lo, _) in enumerate(ep.ranges):
+            self.peers.expert_lo[r] = lo
+        self.peers.expert_lo[n] = E
+        self.peers.n, self.peers.me = n, me
+        self.epoch = 0
+        dev = ep.device
+        self.done = torch.zeros(2, dtype=torch.int32, device=dev)  # dispatch / return CTA counters
+        self.inv_identity = torch.arange(t_max, dtype=torch.int32, device=dev)
+        # local views of the own buffers
+        self.counts_local = _device_view(self._own["counts"], (n, E), torch.int32, dev)
+        self.rows_local = _device_view(self._own["rows"], (self.r_max, d), torch.bfloat16, dev)
+        self.home_local = _device_view(self._own["home"], (t_max, d), torch.float32, dev)
+        if n > 1:
+            dist.barrier(group=ep.group)  # every rank mapped every buffer
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        ep, ops, lib = self.ep, self.ops, self.lib
+        cfg = ep.config
+        k, d = cfg.top_k, cfg.hidden_dim
+        B = x.shape[0]
+        if B > self.max_tokens:
+            raise ValueError(f"{B} tokens > max_tokens {self.max_tokens}")
+        s = ops._stream(ep.device)
+        peers = ctypes.byref(self.peers)
+        self.epoch += 1
+        e = self.epoch
+        r = ops.router.route(x)
+        xb = x.to(torch.bfloat16)
+        if xb.shape[1] != ops.w.hidden_pad:
+            xb = torch.nn.functional.pad(xb, (0, ops.w.hidden_pad - xb.shape[1]))
+        xb = xb.contiguous()
+        self._keep = (xb, r)  # alive while the launches run
+        _lib.check(lib.moe_b200_ep_p2p_counts(ctypes.byref(ops.cfgk), B * k, ops._ptr(r["indices"]), peers, e, s),
+                   "ep_p2p_counts")
+        _lib.check(lib.moe_b200_ep_p2p_wait(peers, 0, e, s), "ep_p2p_wait")
+        cnt = self.counts_local.cpu().numpy().astype(np.int64)  # the one host sync
+        lo, hi = ep.ranges[ep.rank]
+        local_counts = cnt[:, lo:hi].sum(axis=0)
+        n_rows = int(local_counts.sum())
+        global_tokens = int(cnt.sum()) // k
+        _lib.check(lib.moe_b200_ep_p2p_dispatch(ctypes.byref(ops.cfgk), B, ops._ptr(xb), ops._ptr(r["indices"]),
+                                                ops._ptr(r["forward"]), ops._ptr(r["offsets"]), peers,
+                                                ops._ptr(self.done[0:1]), e, s), "ep_p2p_dispatch")
+        _lib.check(lib.moe_b200_ep_p2p_wait(peers, 1, e, s), "ep_p2p_wait")
+        lc = torch.from_numpy(local_counts.astype(np.int32)).to(ep.device)
+        ye = ops.expert_ffn(lc, self.rows_local[:n_rows], global_tokens)
+        _lib.check(lib.moe_b200_ep_p2p_return(ctypes.byref(ops.cfgk), n_rows, ops._ptr(ye), peers,
+                                              ops._ptr(self.done[1:2]), e, s), "ep_p2p_return")
+        _lib.check(lib.moe_b200_ep_p2p_wait(peers, 2, e, s), "ep_p2p_wait")
+        y = ops.combine(self.home_local[: B * k], self.inv_identity[: B * k], r["weights"], B)
+        return y[:, :d]
+
+    def close(self):
+        torch.cuda.synchronize(self.ep.device)
+        for p in self._opened:
+            self.lib.moe_b200_ipc_close(ctypes.c_void_p(p))
+        self._opened = []
+        for p in self._own.values():
+            self.lib.moe_b200_ipc_free(ctypes.c_void_p(p))
+        self._own = {}
+
+
+def _device_view(ptr: int, shape, dtype, device) -> torch.Tensor:
+    """A torch tensor over library-owned device memory (no copy, not owned)."""
+    n = int(np.prod(shape))
+    nbytes = n * torch.empty((), dtype=dtype).element_size()
+    # wrap the pointer through __cuda_array_interface__ (torch does not own it)
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+    t = torch.as_tensor(_Arr(), device=device)
+    return t.view(dtype).view(*shape)

@@ -556,3 +556,91 @@ def test_large_chunk_pair_path_small_expert_counts(pkg, shape):
     bits_equal(_np(layer.topk_idx[:b]).astype(np.int64), ref["indices"])
     bits_equal(_np(layer.counts).astype(np.int64), ref["counts"])
     assert O.max_rel_error(y, ref["y"]) <= TOL
+
+
+def test_expert_parallel_p2p_single_rank_matches_layer_bitwise(pkg):
+    """EP over peer memory (PeerExchange: counts all-gather, dispatch fused with
+    the gather, return of the expert outputs, all as direct writes into the
+    ranks' buffers with epoch flags) on one rank reproduces the fused
+    single-GPU forward bit-for-bit; repeated forwards (growing epochs) too."""
+    P = pkg
+    from paper_2605_23911_b200.ep import ExpertParallelMoE
+
+    e, k, d, f, b = 16, 4, 256, 512, 64
+    tokens, wr, gate, up, down = O.make_instance(9, e, k, d, f, b)
+    cfg = _cfg(P, e, k, d, f, "sigmoid_normalized")
+    w = P.ExpertWeights(gate, up, down)
+    layer = P.MoELayer(cfg, w, wr, max_tokens=b)
+    x = torch.from_numpy(tokens).cuda()
+    y_ref = _np(layer.forward(x))
+    ep = ExpertParallelMoE(cfg, wr, w, max_tokens=b, transport="p2p")
+    for _ in range(3):
+        bits_equal(_np(ep.forward(x)), y_ref)
+    bits_equal(_np(ep.forward(x[:17])), y_ref[:17])
+    ep.p2p.close()
+
+
+def _p2p_worker(rank, world, port, case, q):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)  # both ranks on the one GPU: CUDA IPC maps the peer's buffers
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2605_23911_b200 as P
+        from paper_2605_23911_b200.ep import ExpertParallelMoE, expert_ranges
+
+        seed, e, k, d, f, b, g = case
+        tokens, wr, gate, up, down = O.make_instance(seed, e, k, d, f, b)
+        cfg = P.ModelConfig(e, k, d, f, P.Gating(g))
+        lo, hi = expert_ranges(e, world)[rank]
+        wl = P.ExpertWeights(gate[lo * d:hi * d], up[lo * d:hi * d], down[lo * f:hi * f])
+        b0, b1 = rank * b // world, (rank + 1) * b // world
+        ep = ExpertParallelMoE(cfg, wr, wl, max_tokens=b1 - b0, transport="p2p", device="cuda:0")
+        outs = []
+        for _ in range(2):
+            outs.append(ep.forward(torch.from_numpy(tokens[b0:b1]).cuda()).cpu().numpy())
+        torch.cuda.synchronize()
+        dist.barrier()
+        ep.p2p.close()
+        q.put((rank, b0, outs))
+    except Exception as exc:  # surface the failure to the parent
+        q.put((rank, -1, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_expert_parallel_p2p_two_processes_one_gpu(pkg):
+    """Two ranks (processes) sharing the GPU through CUDA IPC: the peer-memory
+    exchanges (device-side flags across processes) give every rank's token
+    shard exactly the single-GPU layer's bits."""
+    import socket
+    import torch.multiprocessing as mp
+
+    P = pkg
+    case = (13, 8, 2, 128, 256, 48, "softmax")
+    seed, e, k, d, f, b, g = case
+    tokens, wr, gate, up, down = O.make_instance(seed, e, k, d, f, b)
+    layer = P.MoELayer(P.ModelConfig(e, k, d, f, P.Gating(g)), P.ExpertWeights(gate, up, down), wr, max_tokens=b)
+    y_ref = _np(layer.forward(torch.from_numpy(tokens).cuda()))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 2
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        parts = [q.get(timeout=240) for _ in range(world)]
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    for rank, b0, outs in parts:
+        assert b0 >= 0, outs
+        for y in outs:
+            bits_equal(y, y_ref[b0:b0 + y.shape[0]])
