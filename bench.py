@@ -444,8 +444,10 @@ def _e2e_serial(args, x, out, run, flush, dev):
 
 def ep_arm(args, cfg, label, B, world, rank, dev):
     """DeepSeek-V3 expert parallelism: experts sharded over the ranks, the global
-    batch B sharded B/n tokens per rank, NCCL all-to-all dispatch and combine.
-    Strong scaling (fixed global batch); value = B / max-over-ranks step time."""
+    batch B sharded B/n tokens per rank; exchanges over peer memory (rows written
+    straight into the owners' buffers over NVLink, `--ep-transport p2p`, default)
+    or NCCL all-to-alls (`collective`).  Strong scaling (fixed global batch);
+    value = B / max-over-ranks step time."""
     import torch
     import torch.distributed as dist
 
@@ -463,7 +465,8 @@ def ep_arm(args, cfg, label, B, world, rank, dev):
     gate = (torch.randn((El * d, f), generator=gen_r, device=dev) / d ** 0.5).to(torch.bfloat16)
     up = (torch.randn((El * d, f), generator=gen_r, device=dev) / d ** 0.5).to(torch.bfloat16)
     down = (torch.randn((El * f, d), generator=gen_r, device=dev) / f ** 0.5).to(torch.bfloat16)
-    layer = ExpertParallelMoE(cfg, wr, P.ExpertWeights(gate, up, down), max_tokens=b1 - b0, device=dev)
+    layer = ExpertParallelMoE(cfg, wr, P.ExpertWeights(gate, up, down), max_tokens=b1 - b0, device=dev,
+                              transport=args.ep_transport)
     for _ in range(max(3, args.warmup)):
         layer.forward(x)
     torch.cuda.synchronize(dev)
@@ -490,7 +493,10 @@ def ep_arm(args, cfg, label, B, world, rank, dev):
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (torch CUDA Philox N(0,1) bf16 tokens; random-init bf16 expert weights; router N(0,1)/sqrt(d))",
             "config": {"workload": f"{label}, {B} tokens global", "tokens": B, "model_shape": [E, k, d, f],
-                       "gating": cfg.gating.value, "parallelism": f"expert-parallel ep{world} (NCCL all-to-all)",
+                       "gating": cfg.gating.value,
+                       "parallelism": f"expert-parallel ep{world} ("
+                                      + ("peer-memory exchanges over NVLink" if args.ep_transport == "p2p"
+                                         else "NCCL all-to-all") + ")",
                        "timing": "CUDA events over the step loop (one host sync per step for all-to-all sizes)"},
             "gpu_launches": None, "clocks": clocks,
         }
@@ -527,6 +533,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--zipf", type=float, default=None,
                     help="routing-skew workload: override routing with the Zipf(alpha) table (0 = uniform)")
+    ap.add_argument("--ep-transport", choices=("p2p", "collective"), default="p2p",
+                    help="expert-parallel exchanges (DeepSeek, --gpus > 1): peer memory or NCCL all-to-alls")
     ap.add_argument("--l2-flush", choices=("auto", "always", "never"), default="auto",
                     help="flush L2 between timed steps (auto: unless streamed weights >= 16x L2)")
     args = ap.parse_args()
