@@ -299,6 +299,16 @@ int moe_b200_ep_p2p_return(const moe_b200_config* cfg, int64_t num_rows, const f
                            const moe_b200_ep_peers* peers, int32_t* done_counter, uint64_t epoch,
                            void* stream);
 
+/* 3'. The local expert FFN over the num_rows received rows (expert-major,
+ *     counts per local expert; cfg describes the LOCAL expert slice, as for
+ *     moe_b200_expert_ffn) with the return fused into its K-split reduction:
+ *     each row's output goes straight into home[source][expanded id] of its
+ *     home rank, then flag set 2.  Workspace as moe_b200_expert_ffn. */
+int moe_b200_ep_p2p_ffn_return(const moe_b200_config* cfg, int64_t num_rows, int down_splits,
+                               const int32_t* counts, const void* xp, const void* w_gate, const void* w_up,
+                               const void* w_down, const moe_b200_ep_peers* peers, int32_t* done_counter,
+                               uint64_t epoch, void* ws, size_t ws_bytes, void* stream);
+
 /* Copy the device status flags (MOE_B200_FLAG_*) to the host and clear them.
  * Synchronises `stream`. */
 int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws,

@@ -164,4 +164,50 @@ __global__ void __launch_bounds__(256) ep_return_kernel(const float* __restrict_
   }
 }
 
+// 3'. return fused with the FFN's K-split reduction: received row p's output
+// = sum over the down splits of its partials (ascending split order, exactly
+// row_reduce_kernel's sum), written straight into home[source][id] of its
+// home rank; then flag set 2 of every source.  Partials are in the FFN's
+// tiled layout ys[split][d-pair][half][padded row][128] (prow: row -> padded row).
+__global__ void __launch_bounds__(256) ep_reduce_return_kernel(const float* __restrict__ ys, int splits, int n_dp,
+                                                               int T_pad, const int32_t* __restrict__ prow,
+                                                               const int2* __restrict__ ids, int R, int d,
+                                                               EpPeers P, int32_t* done_counter,
+                                                               unsigned long long epoch) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nwarps = gridDim.x * (blockDim.x / 32);
+  const size_t half_stride = (size_t)T_pad * 128;
+  for (int p = blockIdx.x * (blockDim.x / 32) + warp; p < R; p += nwarps) {
+    const int2 id = ids[p];
+    const size_t row = (size_t)__ldg(prow + p);
+    float4* dst = reinterpret_cast<float4*>(P.home[id.x] + (size_t)id.y * d);
+    for (int v = lane; v < d / 4; v += 32) {
+      const int feat = v * 4;
+      const size_t blk = (size_t)(feat >> 8) * 2 + ((feat >> 7) & 1);
+      float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 0; s < splits; ++s) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(ys + ((size_t)s * n_dp * 2 + blk) * half_stride +
+                                                               row * 128 + (feat & 127)));
+        if (s == 0) {
+          g = a;
+        } else {
+          g.x = __fadd_rn(g.x, a.x); g.y = __fadd_rn(g.y, a.y);
+          g.z = __fadd_rn(g.z, a.z); g.w = __fadd_rn(g.w, a.w);
+        }
+      }
+      dst[v] = g;
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(done_counter, 1);
+    if (prev == static_cast<int>(gridDim.x) - 1) {
+      __threadfence_system();
+      *done_counter = 0;
+      for (int r = 0; r < P.n; ++r) st_release_sys_u64(P.flags[r] + 2 * P.n + P.me, epoch);
+    }
+  }
+}
+
 }  // namespace moe

@@ -1198,6 +1198,52 @@ int moe_b200_expert_ffn(const moe_b200_config* cfg, int64_t n_rows, int down_spl
   return MOE_B200_OK;
 }
 
+static int ep_peers_from(const moe_b200_ep_peers* in, moe::EpPeers* out);
+
+int moe_b200_ep_p2p_ffn_return(const moe_b200_config* cfg, int64_t n_rows, int down_splits, const int32_t* counts,
+                               const void* xp, const void* w_gate, const void* w_up, const void* w_down,
+                               const moe_b200_ep_peers* peers, int32_t* done_counter, uint64_t epoch, void* ws,
+                               size_t ws_bytes, void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  moe::EpPeers P{};
+  if ((rc = ep_peers_from(peers, &P))) return rc;
+  if (n_rows < 0 || down_splits < 0) return MOE_B200_ERR_INVALID_VALUE;
+  if (!done_counter) return MOE_B200_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  moe_b200_config c1 = *cfg;
+  c1.top_k = 1;
+  const int d = c1.hidden_dim;
+  if (d % 4) return MOE_B200_ERR_UNSUPPORTED;
+  if (n_rows == 0) {  // nothing received: still publish the (empty) return
+    ep_reduce_return_kernel<<<1, 256, 0, s>>>(nullptr, 1, 1, 1, nullptr, nullptr, 0, d, P, done_counter, epoch);
+    MOE_LAUNCH_CHECK("ep_reduce_return_kernel");
+    return MOE_B200_OK;
+  }
+  if (!counts || !xp || !w_gate || !w_up || !w_down) return MOE_B200_ERR_INVALID_VALUE;
+  Layout L;
+  if ((rc = check_ws(&c1, n_rows, ws, ws_bytes, &L, down_splits))) return rc;
+  if (L.max_chunks > kChunkCap || c1.num_experts > 1024) return MOE_B200_ERR_UNSUPPORTED;
+  int32_t* hdr = reinterpret_cast<int32_t*>(ws);
+  int32_t* offsets = reinterpret_cast<int32_t*>(ws8(ws) + L.logits);  // scratch: E+1 ints
+  int32_t* prow = reinterpret_cast<int32_t*>(ws8(ws) + L.prow);
+  schedule_from_counts_kernel<<<1, 256, 0, s>>>(counts, c1.num_experts, chunk_rows_for(c1, n_rows), offsets,
+                                                reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab),
+                                                reinterpret_cast<int2*>(ws8(ws) + L.chunk_tab) + 2 * L.max_chunks,
+                                                hdr + 2, prow);
+  MOE_LAUNCH_CHECK("schedule_from_counts_kernel");
+  void* h = ws8(ws) + L.h;
+  float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);
+  if ((rc = launch_ffn(c1, n_rows, L, ws, xp, w_gate, w_up, w_down, h, ys, nullptr, nullptr,
+                       /*gu*/ true, /*dn*/ true, kFfnFused, s)))
+    return rc;
+  const int grid = std::max(1, std::min<int>(static_cast<int>((n_rows + 7) / 8), kNumSMs * 4));
+  ep_reduce_return_kernel<<<grid, 256, 0, s>>>(ys, L.splits, L.n_dp, L.T_pad, prow, P.ids[P.me],
+                                               static_cast<int>(n_rows), d, P, done_counter, epoch);
+  MOE_LAUNCH_CHECK("ep_reduce_return_kernel");
+  return MOE_B200_OK;
+}
+
 int moe_b200_gather_rows(int64_t n_rows, int64_t row_bytes, const void* src, const int32_t* idx,
                          void* dst, void* stream) {
   if (n_rows < 0 || row_bytes <= 0 || row_bytes % 16) return MOE_B200_ERR_INVALID_VALUE;

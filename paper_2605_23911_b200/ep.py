@@ -138,6 +138,31 @@ class CudaOps:
                                                 self._stream(self.device)), "expert_ffn")
         return out
 
+    def _ensure_ws(self, n, splits_max):
+        need = ctypes.c_size_t(0)
+        _lib.check(self.lib.moe_b200_expert_ffn_workspace_size(ctypes.byref(self.cfg1), n, splits_max,
+                                                               ctypes.byref(need)), "ws")
+        if need.value > self._ws_bytes:
+            self._ws_bytes = int(need.value * 1.25)
+            self._ws = torch.empty(self._ws_bytes, dtype=torch.uint8, device=self.device)
+            _lib.check(self.lib.moe_b200_workspace_init(ctypes.byref(self.cfg1), n, self._ptr(self._ws),
+                                                        self._ws_bytes, self._stream(self.device)), "ws_init")
+
+    def expert_ffn_return(self, counts, xp, global_tokens, peers, done, epoch):
+        """Local expert FFN over the received rows with the peer-memory return
+        fused into its K-split reduction (moe_b200_ep_p2p_ffn_return)."""
+        n = xp.shape[0]
+        splits = self._down_splits(global_tokens)
+        if n:
+            self._ensure_ws(n, self._down_splits(1))
+        c = counts.to(torch.int32).contiguous()
+        self._keep_ret = c
+        _lib.check(self.lib.moe_b200_ep_p2p_ffn_return(
+            ctypes.byref(self.cfg1), n, splits, self._ptr(c), self._ptr(xp), self._ptr(self.w.gate),
+            self._ptr(self.w.up), self._ptr(self.w.down), peers, self._ptr(done), epoch,
+            self._ptr(self._ws) if self._ws is not None else None, self._ws_bytes,
+            self._stream(self.device)), "ep_p2p_ffn_return")
+
     def combine(self, rows, inv, w, B):
         y = torch.empty((B, rows.shape[1]), dtype=torch.float32, device=self.device)
         _lib.check(self.lib.moe_b200_combine_rows(ctypes.byref(self.cfgk), B, self._ptr(rows), self._ptr(inv),
@@ -318,9 +343,9 @@ class PeerExchange:
                                                 ops._ptr(self.done[0:1]), e, s), "ep_p2p_dispatch")
         _lib.check(lib.moe_b200_ep_p2p_wait(peers, 1, e, s), "ep_p2p_wait")
         lc = torch.from_numpy(local_counts.astype(np.int32)).to(ep.device)
-        ye = ops.expert_ffn(lc, self.rows_local[:n_rows], global_tokens)
-        _lib.check(lib.moe_b200_ep_p2p_return(ctypes.byref(ops.cfgk), n_rows, ops._ptr(ye), peers,
-                                              ops._ptr(self.done[1:2]), e, s), "ep_p2p_return")
+        # local expert FFN; the return to the home ranks is fused into its
+        # K-split reduction (rows go straight into the home ranks' buffers)
+        ops.expert_ffn_return(lc, self.rows_local[:n_rows], global_tokens, peers, self.done[1:2], e)
         _lib.check(lib.moe_b200_ep_p2p_wait(peers, 2, e, s), "ep_p2p_wait")
         y = ops.combine(self.home_local[: B * k], self.inv_identity[: B * k], r["weights"], B)
         return y[:, :d]
