@@ -309,6 +309,17 @@ int moe_b200_ep_p2p_ffn_return(const moe_b200_config* cfg, int64_t num_rows, int
                                const void* w_down, const moe_b200_ep_peers* peers, int32_t* done_counter,
                                uint64_t epoch, void* ws, size_t ws_bytes, void* stream);
 
+/* 3'' The same with no host synchronisation: waits for flag set 1 itself,
+ *     takes the local per-expert counts from the all-gathered matrix on the
+ *     device, and lays the workspace out for up to max_rows received rows
+ *     (moe_b200_expert_ffn_workspace_size(cfg, max_rows, down_splits)).  With
+ *     moe_b200_ep_p2p_counts / _dispatch / _wait and moe_b200_combine_rows the
+ *     whole expert-parallel forward runs without a host synchronisation. */
+int moe_b200_ep_p2p_ffn_return_async(const moe_b200_config* cfg, int64_t max_rows, int down_splits,
+                                     const void* xp, const void* w_gate, const void* w_up, const void* w_down,
+                                     const moe_b200_ep_peers* peers, int32_t* done_counter, uint64_t epoch,
+                                     void* ws, size_t ws_bytes, void* stream);
+
 /* Copy the device status flags (MOE_B200_FLAG_*) to the host and clear them.
  * Synchronises `stream`. */
 int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws,

@@ -80,6 +80,8 @@ SIGNATURES = {
     "moe_b200_ep_p2p_wait": (_INT, [_PEERS, _INT, _U64, _P]),
     "moe_b200_ep_p2p_dispatch": (_INT, [_CFG, _I64, _P, _P, _P, _P, _PEERS, _P, _U64, _P]),
     "moe_b200_ep_p2p_return": (_INT, [_CFG, _I64, _P, _PEERS, _P, _U64, _P]),
+    "moe_b200_ep_p2p_ffn_return_async": (_INT, [_CFG, _I64, ctypes.c_int, _P, _P, _P, _P, _PEERS, _P, _U64, _P,
+                                                _SZ, _P]),
     "moe_b200_ep_p2p_ffn_return": (_INT, [_CFG, _I64, ctypes.c_int, _P, _P, _P, _P, _P, _PEERS, _P, _U64, _P,
                                           _SZ, _P]),
     "moe_b200_workspace_size": (_INT, [_CFG, _I64, ctypes.POINTER(_SZ)]),

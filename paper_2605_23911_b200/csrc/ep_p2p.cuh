@@ -171,9 +171,11 @@ __global__ void __launch_bounds__(256) ep_return_kernel(const float* __restrict_
 // tiled layout ys[split][d-pair][half][padded row][128] (prow: row -> padded row).
 __global__ void __launch_bounds__(256) ep_reduce_return_kernel(const float* __restrict__ ys, int splits, int n_dp,
                                                                int T_pad, const int32_t* __restrict__ prow,
-                                                               const int2* __restrict__ ids, int R, int d,
+                                                               const int2* __restrict__ ids, int R,
+                                                               const int32_t* __restrict__ R_dev, int d,
                                                                EpPeers P, int32_t* done_counter,
                                                                unsigned long long epoch) {
+  if (R_dev) R = *R_dev;  // received rows counted on the device (no host sync)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nwarps = gridDim.x * (blockDim.x / 32);
   const size_t half_stride = (size_t)T_pad * 128;
@@ -207,6 +209,20 @@ __global__ void __launch_bounds__(256) ep_reduce_return_kernel(const float* __re
       *done_counter = 0;
       for (int r = 0; r < P.n; ++r) st_release_sys_u64(P.flags[r] + 2 * P.n + P.me, epoch);
     }
+  }
+}
+
+// Local per-expert row counts from the all-gathered matrix, once the rows of
+// every source are in (flag set 1): counts_out[e] = sum_s counts[s][lo + e].
+__global__ void __launch_bounds__(256) ep_local_counts_kernel(EpPeers P, int E, int lo, int E_local,
+                                                              int32_t* __restrict__ counts_out,
+                                                              unsigned long long epoch) {
+  ep_wait_all(P.flags[P.me] + 1 * P.n, P.n, epoch);
+  const int32_t* cnt = P.counts[P.me];
+  for (int e = threadIdx.x; e < E_local; e += blockDim.x) {
+    int c = 0;
+    for (int s = 0; s < P.n; ++s) c += __ldcg(cnt + (size_t)s * E + lo + e);
+    counts_out[e] = c;
   }
 }
 

@@ -1216,7 +1216,8 @@ int moe_b200_ep_p2p_ffn_return(const moe_b200_config* cfg, int64_t n_rows, int d
   const int d = c1.hidden_dim;
   if (d % 4) return MOE_B200_ERR_UNSUPPORTED;
   if (n_rows == 0) {  // nothing received: still publish the (empty) return
-    ep_reduce_return_kernel<<<1, 256, 0, s>>>(nullptr, 1, 1, 1, nullptr, nullptr, 0, d, P, done_counter, epoch);
+    ep_reduce_return_kernel<<<1, 256, 0, s>>>(nullptr, 1, 1, 1, nullptr, nullptr, 0, nullptr, d, P, done_counter,
+                                              epoch);
     MOE_LAUNCH_CHECK("ep_reduce_return_kernel");
     return MOE_B200_OK;
   }
@@ -1239,7 +1240,53 @@ int moe_b200_ep_p2p_ffn_return(const moe_b200_config* cfg, int64_t n_rows, int d
     return rc;
   const int grid = std::max(1, std::min<int>(static_cast<int>((n_rows + 7) / 8), kNumSMs * 4));
   ep_reduce_return_kernel<<<grid, 256, 0, s>>>(ys, L.splits, L.n_dp, L.T_pad, prow, P.ids[P.me],
-                                               static_cast<int>(n_rows), d, P, done_counter, epoch);
+                                               static_cast<int>(n_rows), nullptr, d, P, done_counter, epoch);
+  MOE_LAUNCH_CHECK("ep_reduce_return_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_ep_p2p_ffn_return_async(const moe_b200_config* cfg, int64_t max_rows, int down_splits,
+                                     const void* xp, const void* w_gate, const void* w_up, const void* w_down,
+                                     const moe_b200_ep_peers* peers, int32_t* done_counter, uint64_t epoch,
+                                     void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  moe::EpPeers P{};
+  if ((rc = ep_peers_from(peers, &P))) return rc;
+  if (max_rows < 1 || down_splits < 0 || !done_counter || !xp || !w_gate || !w_up || !w_down)
+    return MOE_B200_ERR_INVALID_VALUE;
+  const int lo = P.expert_lo[P.me], E_local = P.expert_lo[P.me + 1] - lo, E = P.expert_lo[P.n];
+  if (E_local != cfg->num_experts) return MOE_B200_ERR_SHAPE_MISMATCH;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  moe_b200_config c1 = *cfg;
+  c1.top_k = 1;
+  const int d = c1.hidden_dim;
+  if (d % 4) return MOE_B200_ERR_UNSUPPORTED;
+  // the layout (and the FFN grid) for the worst case; the actual rows come
+  // from the device-side counts through the chunk table
+  Layout L;
+  if ((rc = check_ws(&c1, max_rows, ws, ws_bytes, &L, down_splits))) return rc;
+  if (L.max_chunks > kChunkCap || c1.num_experts > 1024) return MOE_B200_ERR_UNSUPPORTED;
+  int32_t* hdr = reinterpret_cast<int32_t*>(ws);
+  int32_t* counts = reinterpret_cast<int32_t*>(ws8(ws) + L.rt_misc);    // scratch: E_local ints
+  int32_t* offsets = reinterpret_cast<int32_t*>(ws8(ws) + L.logits);    // scratch: E_local + 1 ints
+  int32_t* prow = reinterpret_cast<int32_t*>(ws8(ws) + L.prow);
+  ep_local_counts_kernel<<<1, 256, 0, s>>>(P, E, lo, E_local, counts, epoch);
+  MOE_LAUNCH_CHECK("ep_local_counts_kernel");
+  schedule_from_counts_kernel<<<1, 256, 0, s>>>(counts, c1.num_experts, chunk_rows_for(c1, max_rows), offsets,
+                                                reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab),
+                                                reinterpret_cast<int2*>(ws8(ws) + L.chunk_tab) + 2 * L.max_chunks,
+                                                hdr + 2, prow);
+  MOE_LAUNCH_CHECK("schedule_from_counts_kernel");
+  void* h = ws8(ws) + L.h;
+  float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);
+  if ((rc = launch_ffn(c1, max_rows, L, ws, xp, w_gate, w_up, w_down, h, ys, nullptr, nullptr,
+                       /*gu*/ true, /*dn*/ true, kFfnFused, s)))
+    return rc;
+  const int grid = std::max(1, std::min<int>(static_cast<int>((max_rows + 7) / 8), kNumSMs * 4));
+  ep_reduce_return_kernel<<<grid, 256, 0, s>>>(ys, L.splits, L.n_dp, L.T_pad, prow, P.ids[P.me],
+                                               static_cast<int>(max_rows), offsets + E_local, d, P, done_counter,
+                                               epoch);
   MOE_LAUNCH_CHECK("ep_reduce_return_kernel");
   return MOE_B200_OK;
 }

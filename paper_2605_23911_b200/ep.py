@@ -254,9 +254,11 @@ class PeerExchange:
     buffers.  A forward then writes rows straight into the owners' buffers
     (dispatch fused with the local gather) and the expert outputs straight
     back into the home ranks' buffers, with device-side epoch flags instead
-    of library all-to-alls.  The one host synchronisation per forward reads
-    the all-gathered counts to size the local expert FFN, as in the NCCL
-    path.
+    of library all-to-alls.  Nothing synchronises with the host: the local
+    expert FFN is laid out for the worst case and takes its per-expert counts
+    from the all-gathered matrix on the device, so the forward is
+    asynchronous.  (The epoch is a launch argument, so a captured CUDA graph
+    would replay a stale epoch: not graph-replayable as is.)
     """
 
     def __init__(self, ep: "ExpertParallelMoE", max_tokens: int):
@@ -313,11 +315,17 @@ class PeerExchange:
         if n > 1:
             dist.barrier(group=ep.group)  # every rank mapped every buffer
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, global_tokens: int | None = None) -> torch.Tensor:
+        """Asynchronous (no host synchronisation).
+        ``global_tokens`` (default: world x local tokens) is the layer's total
+        batch; it fixes the down K-split count so every row matches the
+        single-GPU forward bit for bit."""
         ep, ops, lib = self.ep, self.ops, self.lib
         cfg = ep.config
         k, d = cfg.top_k, cfg.hidden_dim
         B = x.shape[0]
+        if global_tokens is None:
+            global_tokens = ep.world * B
         if B > self.max_tokens:
             raise ValueError(f"{B} tokens > max_tokens {self.max_tokens}")
         s = ops._stream(ep.device)
@@ -332,20 +340,19 @@ class PeerExchange:
         self._keep = (xb, r)  # alive while the launches run
         _lib.check(lib.moe_b200_ep_p2p_counts(ctypes.byref(ops.cfgk), B * k, ops._ptr(r["indices"]), peers, e, s),
                    "ep_p2p_counts")
-        _lib.check(lib.moe_b200_ep_p2p_wait(peers, 0, e, s), "ep_p2p_wait")
-        cnt = self.counts_local.cpu().numpy().astype(np.int64)  # the one host sync
-        lo, hi = ep.ranges[ep.rank]
-        local_counts = cnt[:, lo:hi].sum(axis=0)
-        n_rows = int(local_counts.sum())
-        global_tokens = int(cnt.sum()) // k
+        # dispatch waits for every source's counts (flag set 0) on the device
         _lib.check(lib.moe_b200_ep_p2p_dispatch(ctypes.byref(ops.cfgk), B, ops._ptr(xb), ops._ptr(r["indices"]),
                                                 ops._ptr(r["forward"]), ops._ptr(r["offsets"]), peers,
                                                 ops._ptr(self.done[0:1]), e, s), "ep_p2p_dispatch")
-        _lib.check(lib.moe_b200_ep_p2p_wait(peers, 1, e, s), "ep_p2p_wait")
-        lc = torch.from_numpy(local_counts.astype(np.int32)).to(ep.device)
-        # local expert FFN; the return to the home ranks is fused into its
-        # K-split reduction (rows go straight into the home ranks' buffers)
-        ops.expert_ffn_return(lc, self.rows_local[:n_rows], global_tokens, peers, self.done[1:2], e)
+        # local expert FFN over the received rows (flag set 1 awaited on the
+        # device, counts from the all-gathered matrix), the return to the home
+        # ranks fused into its K-split reduction
+        splits = ops._down_splits(global_tokens)
+        ops._ensure_ws(self.r_max, max(splits, ops._down_splits(1)))
+        _lib.check(lib.moe_b200_ep_p2p_ffn_return_async(
+            ctypes.byref(ops.cfg1), self.r_max, splits, ops._ptr(self.rows_local), ops._ptr(ops.w.gate),
+            ops._ptr(ops.w.up), ops._ptr(ops.w.down), peers, ops._ptr(self.done[1:2]), e, ops._ptr(ops._ws),
+            ops._ws_bytes, s), "ep_p2p_ffn_return_async")
         _lib.check(lib.moe_b200_ep_p2p_wait(peers, 2, e, s), "ep_p2p_wait")
         y = ops.combine(self.home_local[: B * k], self.inv_identity[: B * k], r["weights"], B)
         return y[:, :d]
