@@ -260,7 +260,8 @@ int moe_b200_combine_rows(const moe_b200_config* cfg, int64_t num_tokens, const 
  *   rows[r]    bf16 [R_max][d]       expert-major received rows
  *   ids[r]     int32x2 [R_max]       {source rank, expanded id} of each received row
  *   home[r]    fp32 [T_max][d]       returned expert outputs by expanded id
- * `epoch` grows by one per forward; flags are never reset. */
+ * `epoch` grows by one per forward (or pass 0 everywhere and give epoch_dev:
+ * device-side epochs); flags are never reset. */
 #define MOE_B200_EP_MAX_RANKS 16
 typedef struct {
   void* counts[MOE_B200_EP_MAX_RANKS];
@@ -270,6 +271,10 @@ typedef struct {
   void* home[MOE_B200_EP_MAX_RANKS];
   int expert_lo[MOE_B200_EP_MAX_RANKS + 1]; /* rank r owns experts [lo[r], lo[r+1]) */
   int n, me;
+  /* local device uint64[2] {counter, current}, zeroed once: with epoch = 0 in
+   * every call, moe_b200_ep_p2p_counts advances it on the device and the other
+   * steps read it, so a captured CUDA graph of the forward replays correctly */
+  void* epoch_dev;
 } moe_b200_ep_peers;
 
 /* cudaMalloc + IPC handle (64 bytes, opaque) of the allocation. */

@@ -59,6 +59,7 @@ class EpPeers(ctypes.Structure):
         ("expert_lo", ctypes.c_int32 * (EP_MAX_RANKS + 1)),
         ("n", ctypes.c_int32),
         ("me", ctypes.c_int32),
+        ("epoch_dev", ctypes.c_void_p),
     ]
 
 

@@ -34,7 +34,14 @@ struct EpPeers {
   float* home[kEpMaxRanks];                  // rank r: [T_max][d] returned outputs by expanded id
   int expert_lo[kEpMaxRanks + 1];            // rank r owns experts [lo[r], lo[r+1])
   int n, me;
+  unsigned long long* epoch_dev;             // local {counter, current}: device epochs (launch epoch 0)
 };
+
+// The epoch of this forward: the launch argument, or (0) the device-side one
+// that ep_counts_kernel advanced -- so a captured CUDA graph replays correctly.
+MOE_DEVICE unsigned long long ep_epoch(const EpPeers& P, unsigned long long epoch) {
+  return epoch ? epoch : *reinterpret_cast<volatile unsigned long long*>(P.epoch_dev + 1);
+}
 
 MOE_DEVICE void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -62,6 +69,16 @@ MOE_DEVICE int ep_owner(const EpPeers& P, int e) {
 __global__ void __launch_bounds__(256) ep_counts_kernel(const int32_t* __restrict__ topk_idx, int T, int E,
                                                         EpPeers P, unsigned long long epoch) {
   extern __shared__ int32_t hist[];
+  if (epoch == 0) {  // device epochs: this forward's = counter + 1 (the first kernel of the forward)
+    __shared__ unsigned long long s_ep;
+    if (threadIdx.x == 0) {
+      s_ep = P.epoch_dev[0] + 1;
+      P.epoch_dev[0] = s_ep;
+      P.epoch_dev[1] = s_ep;
+    }
+    __syncthreads();
+    epoch = s_ep;
+  }
   for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < T; i += blockDim.x) {
@@ -78,8 +95,8 @@ __global__ void __launch_bounds__(256) ep_counts_kernel(const int32_t* __restric
 }
 
 // wait until every source's flag of `set` reached `epoch` (one thread)
-__global__ void ep_wait_kernel(const unsigned long long* flags, int set, int n, unsigned long long epoch) {
-  ep_wait_all(flags + (size_t)set * n, n, epoch);
+__global__ void ep_wait_kernel(EpPeers P, int set, unsigned long long epoch) {
+  ep_wait_all(P.flags[P.me] + (size_t)set * P.n, P.n, ep_epoch(P, epoch));
 }
 
 // 2. dispatch: local permuted row p (expert-major, stable) -> destination.
@@ -93,6 +110,7 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(const __nv_bfloat16* _
   extern __shared__ int32_t ep_sm[];
   int32_t* dest0 = ep_sm;  // [E]: destination row of this source's first row of expert e
   const int32_t* cnt = P.counts[P.me];
+  epoch = ep_epoch(P, epoch);
   ep_wait_all(P.flags[P.me] + 0 * P.n, P.n, epoch);
   // dest0[e] = (rows of the owner's experts before e, all sources) + (rows of e
   //            from sources before me)
@@ -143,6 +161,7 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(const __nv_bfloat16* _
 __global__ void __launch_bounds__(256) ep_return_kernel(const float* __restrict__ out, const int2* __restrict__ ids,
                                                         int R, int d, EpPeers P, int32_t* done_counter,
                                                         unsigned long long epoch) {
+  epoch = ep_epoch(P, epoch);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nwarps = gridDim.x * (blockDim.x / 32);
   const int vpr = d / 4;
@@ -176,6 +195,7 @@ __global__ void __launch_bounds__(256) ep_reduce_return_kernel(const float* __re
                                                                EpPeers P, int32_t* done_counter,
                                                                unsigned long long epoch) {
   if (R_dev) R = *R_dev;  // received rows counted on the device (no host sync)
+  epoch = ep_epoch(P, epoch);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nwarps = gridDim.x * (blockDim.x / 32);
   const size_t half_stride = (size_t)T_pad * 128;
@@ -217,7 +237,7 @@ __global__ void __launch_bounds__(256) ep_reduce_return_kernel(const float* __re
 __global__ void __launch_bounds__(256) ep_local_counts_kernel(EpPeers P, int E, int lo, int E_local,
                                                               int32_t* __restrict__ counts_out,
                                                               unsigned long long epoch) {
-  ep_wait_all(P.flags[P.me] + 1 * P.n, P.n, epoch);
+  ep_wait_all(P.flags[P.me] + 1 * P.n, P.n, ep_epoch(P, epoch));
   const int32_t* cnt = P.counts[P.me];
   for (int e = threadIdx.x; e < E_local; e += blockDim.x) {
     int c = 0;

@@ -1345,6 +1345,7 @@ static int ep_peers_from(const moe_b200_ep_peers* in, moe::EpPeers* out) {
   for (int r = 0; r <= in->n; ++r) out->expert_lo[r] = in->expert_lo[r];
   out->n = in->n;
   out->me = in->me;
+  out->epoch_dev = static_cast<unsigned long long*>(in->epoch_dev);
   return MOE_B200_OK;
 }
 
@@ -1355,6 +1356,7 @@ int moe_b200_ep_p2p_counts(const moe_b200_config* cfg, int64_t num_rows, const i
   moe::EpPeers P{};
   if ((rc = ep_peers_from(peers, &P))) return rc;
   if (num_rows < 0 || (num_rows > 0 && !topk_idx)) return MOE_B200_ERR_INVALID_VALUE;
+  if (epoch == 0 && !P.epoch_dev) return MOE_B200_ERR_INVALID_VALUE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t smem = (size_t)cfg->num_experts * sizeof(int32_t);
   ep_counts_kernel<<<1, 256, smem, s>>>(topk_idx, static_cast<int>(num_rows), cfg->num_experts, P, epoch);
@@ -1367,7 +1369,8 @@ int moe_b200_ep_p2p_wait(const moe_b200_ep_peers* peers, int set, uint64_t epoch
   int rc;
   if ((rc = ep_peers_from(peers, &P))) return rc;
   if (set < 0 || set >= kEpFlagSets) return MOE_B200_ERR_INVALID_VALUE;
-  ep_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(P.flags[P.me], set, P.n, epoch);
+  if (epoch == 0 && !P.epoch_dev) return MOE_B200_ERR_INVALID_VALUE;
+  ep_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(P, set, epoch);
   MOE_LAUNCH_CHECK("ep_wait_kernel");
   return MOE_B200_OK;
 }

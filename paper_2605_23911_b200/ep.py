@@ -257,8 +257,8 @@ class PeerExchange:
     of library all-to-alls.  Nothing synchronises with the host: the local
     expert FFN is laid out for the worst case and takes its per-expert counts
     from the all-gathered matrix on the device, so the forward is
-    asynchronous.  (The epoch is a launch argument, so a captured CUDA graph
-    would replay a stale epoch: not graph-replayable as is.)
+    asynchronous, and with device-side epochs a captured CUDA graph of it
+    replays correctly (after one eager forward has sized the workspace).
     """
 
     def __init__(self, ep: "ExpertParallelMoE", max_tokens: int):
@@ -304,8 +304,11 @@ class PeerExchange:
             self.peers.expert_lo[r] = lo
         self.peers.expert_lo[n] = E
         self.peers.n, self.peers.me = n, me
-        self.epoch = 0
         dev = ep.device
+        # device-side epochs {counter, current}: every call passes epoch 0, the
+        # counts kernel advances it, so a captured CUDA graph replays correctly
+        self.epoch_dev = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.peers.epoch_dev = self.epoch_dev.data_ptr()
         self.done = torch.zeros(2, dtype=torch.int32, device=dev)  # dispatch / return CTA counters
         self.inv_identity = torch.arange(t_max, dtype=torch.int32, device=dev)
         # local views of the own buffers
@@ -330,8 +333,7 @@ class PeerExchange:
             raise ValueError(f"{B} tokens > max_tokens {self.max_tokens}")
         s = ops._stream(ep.device)
         peers = ctypes.byref(self.peers)
-        self.epoch += 1
-        e = self.epoch
+        e = 0  # device-side epoch
         r = ops.router.route(x)
         xb = x.to(torch.bfloat16)
         if xb.shape[1] != ops.w.hidden_pad:

@@ -601,10 +601,27 @@ def _p2p_worker(rank, world, port, case, q):
         outs = []
         for _ in range(2):
             outs.append(ep.forward(torch.from_numpy(tokens[b0:b1]).cuda()).cpu().numpy())
+        # the forward captured as a CUDA graph (device-side epochs), replayed on
+        # the same tokens and on negated ones (new routing)
+        xs = torch.from_numpy(tokens[b0:b1]).cuda()
+        ep.forward(xs)
         torch.cuda.synchronize()
         dist.barrier()
+        g_ = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_):
+            ys = ep.forward(xs)
+        dist.barrier()
+        g_.replay()
+        torch.cuda.synchronize()
+        graph_outs = [ys.cpu().numpy()]
+        xs.neg_()
+        dist.barrier()
+        g_.replay()
+        torch.cuda.synchronize()
+        graph_outs.append(ys.cpu().numpy())
+        dist.barrier()
         ep.p2p.close()
-        q.put((rank, b0, outs))
+        q.put((rank, b0, (outs, graph_outs)))
     except Exception as exc:  # surface the failure to the parent
         q.put((rank, -1, repr(exc)))
     finally:
@@ -614,7 +631,8 @@ def _p2p_worker(rank, world, port, case, q):
 def test_expert_parallel_p2p_two_processes_one_gpu(pkg):
     """Two ranks (processes) sharing the GPU through CUDA IPC: the peer-memory
     exchanges (device-side flags across processes) give every rank's token
-    shard exactly the single-GPU layer's bits."""
+    shard exactly the single-GPU layer's bits, eagerly and as a replayed CUDA
+    graph (device-side epochs) on new tokens."""
     import socket
     import torch.multiprocessing as mp
 
@@ -624,6 +642,7 @@ def test_expert_parallel_p2p_two_processes_one_gpu(pkg):
     tokens, wr, gate, up, down = O.make_instance(seed, e, k, d, f, b)
     layer = P.MoELayer(P.ModelConfig(e, k, d, f, P.Gating(g)), P.ExpertWeights(gate, up, down), wr, max_tokens=b)
     y_ref = _np(layer.forward(torch.from_numpy(tokens).cuda()))
+    y_ref_neg = _np(layer.forward(torch.from_numpy(-tokens).cuda()))
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
@@ -640,7 +659,10 @@ def test_expert_parallel_p2p_two_processes_one_gpu(pkg):
             p.join(timeout=60)
             if p.is_alive():
                 p.kill()
-    for rank, b0, outs in parts:
-        assert b0 >= 0, outs
+    for rank, b0, res in parts:
+        assert b0 >= 0, res
+        outs, graph_outs = res
         for y in outs:
             bits_equal(y, y_ref[b0:b0 + y.shape[0]])
+        bits_equal(graph_outs[0], y_ref[b0:b0 + graph_outs[0].shape[0]])
+        bits_equal(graph_outs[1], y_ref_neg[b0:b0 + graph_outs[1].shape[0]])
