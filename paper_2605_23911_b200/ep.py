@@ -19,11 +19,15 @@ output is computed by the same kernels with the same K order regardless of
 which other rows share its tile, and the home-rank combine runs the
 reference's ``out += w_j * g_j`` order (``pipeline.py:396-399``).
 
-Collectives go through ``torch.distributed`` (NCCL on GPUs).  The one host
-synchronisation per forward is the counts exchange that sizes the
-all-to-alls.  All row compute runs in libmoe_b200.so through ``CudaOps``; the
-host logic is written against a small ops interface so it can be exercised
-on CPU with gloo in the tests.
+Two transports.  ``transport="p2p"`` (``PeerExchange``): the exchanges run
+over peer memory in libmoe_b200.so (``csrc/ep_p2p.cuh``: rows written
+straight into the owners' buffers, outputs straight back, device-side epoch
+flags), with no host synchronisation; the forward is graph-capturable.
+``transport="collective"``: ``torch.distributed`` all-to-alls (NCCL on
+GPUs), whose one host synchronisation per forward is the counts exchange
+that sizes them.  All row compute runs in libmoe_b200.so through ``CudaOps``;
+the collective path's host logic is written against a small ops interface so
+it can be exercised on CPU with gloo in the tests.
 """
 
 from __future__ import annotations

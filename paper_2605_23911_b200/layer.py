@@ -2,7 +2,7 @@
 
 ``MoELayer`` owns the uploaded bf16 expert weights, the fp32 router weight,
 the routing buffers and the workspace, and runs the whole layer as ONE C-ABI
-call (five sm_100a launches, no host synchronisation, CUDA-graph
+call (four sm_100a launches, no host synchronisation, CUDA-graph
 capturable).  ``moe_forward`` / ``route`` mirror the reference functions
 (``moeperf/pipeline.py:572-615``, ``moeperf/router.py:116-133``) — same
 signature, same exception classes — and return numpy when given numpy.
