@@ -14,7 +14,7 @@ import threading
 from . import errors
 
 LIB_NAME = "libmoe_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("MOE_B200_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 OK = 0
 STATUS_TO_EXC = {

@@ -39,7 +39,10 @@ constexpr int kEpiWarps = 8;    // warps 4..11: two groups of 4 (one warp per TM
 constexpr int kEpiGroups = 2;   // 32-row chunks alternate between the groups
 constexpr int kBM = 128;        // weight rows (output features) per tile
 constexpr int kBK = 64;         // K per stage: one 128-byte swizzle row of bf16
-constexpr int kBoxRows = 32;    // token rows per TMA box
+#ifndef MOE_B200_BOX_ROWS
+#define MOE_B200_BOX_ROWS 32
+#endif
+constexpr int kBoxRows = MOE_B200_BOX_ROWS;  // token rows per TMA box
 constexpr int kSchedSlots = 4;  // tile-id ring between scheduler and consumers
 
 struct FfnParams {
