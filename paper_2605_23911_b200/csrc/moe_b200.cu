@@ -31,7 +31,17 @@ int cuda_fail(cudaError_t e, const char* what) {
   char buf[512];
   snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
   g_last_error = buf;
+  cudaGetLastError();  // reported here: do not leave a (non-sticky) error for the next launch check
   return MOE_B200_ERR_CUDA;
+}
+
+// Event record that also works inside stream capture: there it becomes an
+// external event-record node, so streams outside the graph can wait on it.
+cudaError_t record_event(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive)
+    return cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+  return cudaEventRecord(ev, s);
 }
 
 #define MOE_CUDA(call)                                \
@@ -810,7 +820,7 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
   } else if ((rc = launch_router_exact(*cfg, B, x, xb, w_router, L, ws, p, s))) {
     return rc;
   }
-  if (mid_event) MOE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(mid_event), s));
+  if (mid_event) MOE_CUDA(record_event(static_cast<cudaEvent_t>(mid_event), s));
   return launch_dispatch(*cfg, B, x, xb, topk_idx, counts, offsets, perm_fwd, perm_inv,
                          reinterpret_cast<int32_t*>(ws8(ws) + L.prow), reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab),
                          hdr + 2, xp, s);
@@ -904,7 +914,7 @@ static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, in
   if ((rc = check_ws(cfg, B, ws, ws_bytes, &L))) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto mark = [&](int i) -> int {
-    if (events && events[i]) MOE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s));
+    if (events && events[i]) MOE_CUDA(record_event(static_cast<cudaEvent_t>(events[i]), s));
     return MOE_B200_OK;
   };
   if ((rc = mark(0))) return rc;
@@ -1017,6 +1027,19 @@ int moe_b200_forward_timed(const moe_b200_config* cfg, int64_t B, const void* x,
 
 }  // extern "C"
 
+// Host-buffer I/O context.  The compute of a forward is captured once per
+// (staging slot, batch, buffer pointers) as a CUDA graph on a private stream
+// and replayed on the caller's stream: a graph launch instead of four kernel
+// launches with their descriptor / attribute set-up per call (host cost per
+// forward ~24 -> a few us).  MOE_B200_* tuning variables are read at capture.
+struct IoGraph {
+  int slot;
+  int64_t B;
+  const void* ptrs[12];
+  cudaGraphExec_t exec;
+};
+constexpr int kIoGraphs = 16;
+
 struct moe_b200_io {
   moe_b200_config cfg;
   int64_t max_tokens;
@@ -1024,9 +1047,11 @@ struct moe_b200_io {
   size_t x_bytes, y_bytes;
   void* x_dev[2];
   void* y_dev[2];
-  cudaStream_t s_in, s_out;
+  cudaStream_t s_in, s_out, s_cap;
   cudaEvent_t in_done[2], disp_done[2], comp_done[2], out_done[2];
   int64_t count;
+  std::vector<IoGraph> graphs;
+  int graphs_off;  // MOE_B200_IO_GRAPHS=0: eager launches
 };
 
 extern "C" {
@@ -1059,6 +1084,9 @@ int moe_b200_io_create(const moe_b200_config* cfg, int64_t max_tokens, int x_dty
   }
   if ((e = cudaStreamCreateWithFlags(&io->s_in, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "io stream");
   if ((e = cudaStreamCreateWithFlags(&io->s_out, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "io stream");
+  if ((e = cudaStreamCreateWithFlags(&io->s_cap, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "io stream");
+  const char* genv = getenv("MOE_B200_IO_GRAPHS");
+  io->graphs_off = genv && atoi(genv) == 0;
   *io_out = io;
   return MOE_B200_OK;
 }
@@ -1073,8 +1101,10 @@ int moe_b200_io_destroy(moe_b200_io* io) {
     for (cudaEvent_t ev : {io->in_done[i], io->disp_done[i], io->comp_done[i], io->out_done[i]})
       if (ev) cudaEventDestroy(ev);
   }
+  for (IoGraph& g : io->graphs) cudaGraphExecDestroy(g.exec);
   if (io->s_in) cudaStreamDestroy(io->s_in);
   if (io->s_out) cudaStreamDestroy(io->s_out);
+  if (io->s_cap) cudaStreamDestroy(io->s_cap);
   delete io;
   return MOE_B200_OK;
 }
@@ -1100,10 +1130,48 @@ int moe_b200_forward_host(moe_b200_io* io, int64_t B, const void* x_host, void* 
   if (reuse) MOE_CUDA(cudaStreamWaitEvent(s, io->out_done[slot], 0));
   // events[2] is recorded after the dispatch (the last reader of x)
   void* evs[5] = {nullptr, nullptr, io->disp_done[slot], nullptr, nullptr};
-  int rc = forward_impl(&io->cfg, B, io->x_dev[slot], io->x_dtype, w_router, w_gate, w_up, w_down,
-                        io->y_dev[slot], io->y_dtype, topk_idx, topk_w, counts, offsets, perm_fwd, perm_inv, ws,
-                        ws_bytes, stream, evs);
-  if (rc) return rc;
+  auto run = [&](cudaStream_t st) {
+    return forward_impl(&io->cfg, B, io->x_dev[slot], io->x_dtype, w_router, w_gate, w_up, w_down, io->y_dev[slot],
+                        io->y_dtype, topk_idx, topk_w, counts, offsets, perm_fwd, perm_inv, ws, ws_bytes, st, evs);
+  };
+  const void* key[12] = {w_router, w_gate, w_up, w_down, topk_idx, topk_w, counts, offsets, perm_fwd, perm_inv, ws,
+                         reinterpret_cast<const void*>(ws_bytes)};
+  cudaGraphExec_t exec = nullptr;
+  if (!io->graphs_off && B > 0) {
+    for (IoGraph& g : io->graphs)
+      if (g.slot == slot && g.B == B && memcmp(g.ptrs, key, sizeof(key)) == 0) exec = g.exec;
+    if (!exec) {
+      // capture this slot / batch once on the private stream (the kernels and
+      // the mid-forward event record become graph nodes)
+      cudaGraph_t graph = nullptr;
+      int rc = MOE_B200_OK;
+      if (cudaStreamBeginCapture(io->s_cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+        rc = run(io->s_cap);
+        const cudaError_t ce = cudaStreamEndCapture(io->s_cap, &graph);
+        if (rc == MOE_B200_OK && ce == cudaSuccess && graph &&
+            cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess)
+          exec = nullptr;
+        if (graph) cudaGraphDestroy(graph);
+        if (rc) return rc;  // a validation error is reported, not retried
+      }
+      cudaGetLastError();  // a failed capture leaves no sticky error: run eagerly below
+      if (exec) {
+        if ((int)io->graphs.size() >= kIoGraphs) {
+          cudaGraphExecDestroy(io->graphs.front().exec);
+          io->graphs.erase(io->graphs.begin());
+        }
+        IoGraph g{slot, B, {}, exec};
+        memcpy(g.ptrs, key, sizeof(key));
+        io->graphs.push_back(g);
+      }
+    }
+  }
+  if (exec) {
+    MOE_CUDA(cudaGraphLaunch(exec, s));
+  } else {
+    const int rc = run(s);
+    if (rc) return rc;
+  }
   MOE_CUDA(cudaEventRecord(io->comp_done[slot], s));
   // copy-out
   MOE_CUDA(cudaStreamWaitEvent(io->s_out, io->comp_done[slot], 0));

@@ -77,3 +77,22 @@ for _ in range(n):
 t1 = time.perf_counter()
 torch.cuda.synchronize()
 print(f"small: layer.forward {1e6 * (t1 - t0) / n:.1f} us host")
+
+# host cost per forward_host submission (pinned host buffers), graphs off / on
+for gflag in ("0", "1"):
+    os.environ["MOE_B200_IO_GRAPHS"] = gflag
+    xh = [x.cpu().pin_memory() for _ in range(2)]
+    yh = [torch.empty((B, d), dtype=torch.float32).pin_memory() for _ in range(2)]
+    pipe = layer.host_pipeline(x_dtype=torch.bfloat16, y_dtype=torch.float32)
+    for i in range(6):
+        pipe.submit(xh[i % 2], yh[i % 2])
+    pipe.sync()
+    n = 500
+    t0 = time.perf_counter()
+    for i in range(n):
+        pipe.submit(xh[i % 2], yh[i % 2])
+    t1 = time.perf_counter()
+    pipe.sync()
+    t2 = time.perf_counter()
+    print(f"small: forward_host graphs={gflag}: host {1e6 * (t1 - t0) / n:.1f} us per submit, wall {1e6 * (t2 - t0) / n:.1f} us per step")
+    pipe.close()
