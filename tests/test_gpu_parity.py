@@ -666,3 +666,24 @@ def test_expert_parallel_p2p_two_processes_one_gpu(pkg):
             bits_equal(y, y_ref[b0:b0 + y.shape[0]])
         bits_equal(graph_outs[0], y_ref[b0:b0 + graph_outs[0].shape[0]])
         bits_equal(graph_outs[1], y_ref_neg[b0:b0 + graph_outs[1].shape[0]])
+
+
+def test_varying_batch_sizes_reuse_one_layer(pkg):
+    """One layer (one workspace, self-resetting device counters) driven through
+    a sequence of different batch sizes — every regime of the router, the
+    down-split rule and the chunk widths — gives each batch exactly the bits
+    of a fresh layer sized for it, and its routing matches the oracle."""
+    P = pkg
+    e, k, d, f = 8, 2, 256, 512
+    bmax = 400
+    tokens, wr, gate, up, down = O.make_instance(81, e, k, d, f, bmax)
+    cfg = _cfg(P, e, k, d, f, "softmax")
+    layer = _layer(P, cfg, wr, gate, up, down, bmax)
+    for b in (1, 7, 400, 3, 300, 64, 400, 2, 129):
+        x = torch.from_numpy(tokens[:b]).cuda()
+        y = _np(layer.forward(x))
+        fresh = _layer(P, cfg, wr, gate, up, down, b)
+        bits_equal(y, _np(fresh.forward(x)))
+        idx_ref, w_ref = O.route(tokens[:b], wr, k, "softmax")
+        bits_equal(_np(layer.topk_idx[:b]).astype(np.int64), idx_ref)
+        bits_equal(_np(layer.topk_w[:b]), w_ref)
