@@ -464,21 +464,18 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
       float wsel = 0.0f;
       int isel = 0;
       for (int j = 0; j < p.k; ++j) {
-        uint64_t best = 0;
-        for (int e = lane; e < p.E; e += 32) {
+        // largest key (score bits desc, index asc) in two warp reductions: the
+        // max of score bits + 1 (0: no candidate), then the lowest index holding it
+        uint32_t kb = 0, kidx = 0xFFFFFFFFu;
+        for (int e = lane; e < p.E; e += 32) {  // ascending e: the first max is the lowest index
           float sc = static_cast<float>(row[e]);
           if (sc < 0.0f) continue;  // already selected (marked -1)
-          uint32_t bits = (sc == 0.0f) ? 0u : __float_as_uint(sc);
-          uint64_t key = (static_cast<uint64_t>(bits) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(e));
-          best = key > best ? key : best;
+          const uint32_t key = ((sc == 0.0f) ? 0u : __float_as_uint(sc)) + 1u;
+          if (key > kb) { kb = key; kidx = static_cast<uint32_t>(e); }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          uint64_t other = shfl_xor_u64(best, o);
-          best = other > best ? other : best;
-        }
-        int e_best = static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFu));
-        float s_best = __uint_as_float(static_cast<uint32_t>(best >> 32));
+        const uint32_t kmax = __reduce_max_sync(0xffffffffu, kb);
+        const int e_best = static_cast<int>(__reduce_min_sync(0xffffffffu, kb == kmax ? kidx : 0xFFFFFFFFu));
+        const float s_best = __uint_as_float(kmax - 1u);
         __syncwarp();
         if (lane == (e_best & 31)) row[e_best] = -1.0;
         __syncwarp();
