@@ -196,8 +196,11 @@ MOE_DEVICE TileInfo decode_tile(const FfnParams& p, int tile, int rank = 0) {
   return t;
 }
 
-// kPair: the kernel runs as clusters of two CTAs that process the two halves
-// of a pair tile (adjacent weight tiles of the same token chunk).  Each CTA
+// kPM: 0 single CTAs; 1 and 2 CTA pairs (clusters of two CTAs on one TPC)
+// that process the two halves of a pair tile (adjacent weight tiles of the
+// same token chunk).  Mode 2 is the default for 256-row token chunks.
+//
+// kPM == 1 (multicast pairs): each CTA
 // streams its own weights, but the shared token k-blocks are loaded ONCE per
 // pair: each CTA loads half the 32-row boxes with TMA multicast into both CTAs'
 // token slots, and each MMA releases a token slot in both CTAs (multicast
