@@ -412,7 +412,16 @@ RouterPlan plan_router(const moe_b200_config& c, int64_t B, int x_bf16) {
   const int64_t target = (kNumSMs * 4) / 5;
   const int64_t chains = B * (int64_t)E;
   if (chains >= 64LL * 1024 && r.expc % 2 == 0) {
-    r.te = 2; r.tt = 4; r.tokc = 32;
+    // 2 experts x 2 tokens per thread, 32-token blocks: 8 compute warps per SM
+    // (DeepSeek-512: 3565 vs 3583 us for 2x4, 3921 for 4x4)
+    r.te = 2; r.tt = 2; r.tokc = 32;
+    if (const char* env = getenv("MOE_B200_RX_TILE")) {  // tuning: "te,tt,tokc"
+      int te = 0, tt = 0, tokc = 0;
+      if (sscanf(env, "%d,%d,%d", &te, &tt, &tokc) == 3 && ((te == 2 && (tt == 2 || tt == 4)) || (te == 4 && tt == 4)) &&
+          tokc >= tt && tokc % tt == 0 && r.expc % te == 0) {
+        r.te = te; r.tt = tt; r.tokc = tokc;
+      }
+    }
   } else {
     r.te = 1; r.tt = 1;
     int g = 1;
@@ -444,6 +453,8 @@ int launch_router_t(const CUtensorMap& tmx, const RouterParams& p, const RouterP
 
 template <bool kBf16>
 int launch_router_x(const CUtensorMap& tmx, const RouterParams& p, const RouterPlan& plan, cudaStream_t s) {
+  if (plan.te == 4) return launch_router_t<kBf16, 4, 4, 64>(tmx, p, plan, s);
+  if (plan.te == 2 && plan.tt == 2) return launch_router_t<kBf16, 2, 2, 64>(tmx, p, plan, s);
   if (plan.te == 2) return launch_router_t<kBf16, 2, 4, 64>(tmx, p, plan, s);
   return launch_router_t<kBf16, 1, 1, 128>(tmx, p, plan, s);
 }

@@ -15,7 +15,8 @@ for a in sys.argv[2:]:
         tokens = int(a[2:])
         continue
     k_, vals = a.split("=")
-    variants = [dict(v, **{k_: x}) for v in variants for x in vals.split(",")]
+    sep = "|" if "|" in vals else ","  # '|' separates variants whose values contain commas
+    variants = [dict(v, **{k_: x}) for v in variants for x in vals.split(sep)]
 E, k, d, f, gating, B, _ = CONFIGS[name]
 B = tokens or B
 gen = torch.Generator(device="cuda").manual_seed(1234)

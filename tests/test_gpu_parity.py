@@ -687,3 +687,26 @@ def test_varying_batch_sizes_reuse_one_layer(pkg):
         idx_ref, w_ref = O.route(tokens[:b], wr, k, "softmax")
         bits_equal(_np(layer.topk_idx[:b]).astype(np.int64), idx_ref)
         bits_equal(_np(layer.topk_w[:b]), w_ref)
+
+
+@pytest.mark.parametrize("tile", ["", "2,4,32", "2,2,32", "4,4,32"])
+def test_throughput_router_tiles_bitexact(pkg, tile, monkeypatch):
+    """The throughput-regime exact router (>= 64K token x expert chains) with
+    each register tile: routing and permutation bit-exact against the oracle."""
+    P = pkg
+    if tile:
+        monkeypatch.setenv("MOE_B200_RX_TILE", tile)
+    e, k, d, f, b = 256, 8, 512, 64, 256  # 65536 chains
+    rng = np.random.default_rng(91)
+    tokens = rng.standard_normal((b, d)).astype(np.float32)
+    wr = (rng.standard_normal((d, e)) / np.sqrt(d)).astype(np.float32)
+    z = np.zeros((e * d, f), np.float32)
+    cfg = _cfg(P, e, k, d, f, "sigmoid_normalized")
+    layer = P.MoELayer(cfg, P.ExpertWeights(z, z, np.zeros((e * f, d), np.float32)), wr, max_tokens=b)
+    r = layer.route(torch.from_numpy(tokens).cuda(), logits=True)
+    idx_ref, w_ref = O.route(tokens, wr, k, "sigmoid_normalized")
+    bits_equal(_np(r["indices"]).astype(np.int64), idx_ref)
+    bits_equal(_np(r["weights"]), w_ref)
+    bits_equal(_np(r["logits"]), O.router_logits(tokens, wr))
+    fwd_ref, _ = O.build_permutation(idx_ref)
+    bits_equal(_np(r["forward"]).astype(np.int64), fwd_ref)
