@@ -137,6 +137,38 @@ def test_workspace_size_and_config_validation_without_gpu():
     assert lib.moe_b200_workspace_size(ctypes.byref(odd), 512, ctypes.byref(n)) == 9  # unsupported pitch
 
 
+def test_down_split_rule_and_workspace_monotonicity_without_gpu():
+    """The down K-split count (a function of config and batch only, so EP
+    ranks can reproduce the single-GPU bits): ~256 down tiles at small
+    batches, round(f/2d) at large ones; the workspace for max_tokens covers
+    every smaller batch's layout."""
+    from paper_2605_23911_b200 import _lib
+
+    lib = _lib.load()
+
+    def splits(e, k, d, f, b):
+        c = _lib.config_struct(e, k, d, f, 0)
+        s = ctypes.c_int(0)
+        assert lib.moe_b200_down_splits(ctypes.byref(c), b, ctypes.byref(s)) == 0
+        return s.value
+
+    mixtral = (8, 2, 4096, 14336)
+    assert [splits(*mixtral, b) for b in (1, 2, 4, 8, 32, 512)] == [8, 5, 3, 2, 2, 2]
+    assert splits(60, 4, 2048, 1408, 1) == 3 and splits(60, 4, 2048, 1408, 512) == 1
+    assert splits(256, 8, 7168, 2048, 512) == 1
+    prev = None
+    for b in range(1, 600):  # non-increasing in the batch
+        s = splits(*mixtral, b)
+        assert prev is None or s <= prev
+        prev = s
+    n_max, n_b = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    cfg = _lib.config_struct(*mixtral, 0)
+    assert lib.moe_b200_workspace_size(ctypes.byref(cfg), 512, ctypes.byref(n_max)) == 0
+    for b in (1, 2, 3, 5, 17, 300, 512):
+        assert lib.moe_b200_workspace_size(ctypes.byref(cfg), b, ctypes.byref(n_b)) == 0
+        assert n_b.value <= n_max.value
+
+
 def test_status_codes_map_to_reference_exceptions():
     from paper_2605_23911_b200 import _lib, errors
 
