@@ -628,8 +628,13 @@ def _p2p_worker(rank, world, port, case, q):
         dist.destroy_process_group()
 
 
-def test_expert_parallel_p2p_two_processes_one_gpu(pkg):
-    """Two ranks (processes) sharing the GPU through CUDA IPC: the peer-memory
+@pytest.mark.parametrize("world,case", [
+    (2, (13, 8, 2, 128, 256, 48, "softmax")),
+    # three ranks, uneven expert blocks (4 / 3 / 3 of 10), top-3 sigmoid
+    (3, (17, 10, 3, 128, 192, 45, "sigmoid_normalized")),
+])
+def test_expert_parallel_p2p_processes_one_gpu(pkg, world, case):
+    """Ranks (processes) sharing the GPU through CUDA IPC: the peer-memory
     exchanges (device-side flags across processes) give every rank's token
     shard exactly the single-GPU layer's bits, eagerly and as a replayed CUDA
     graph (device-side epochs) on new tokens."""
@@ -637,7 +642,6 @@ def test_expert_parallel_p2p_two_processes_one_gpu(pkg):
     import torch.multiprocessing as mp
 
     P = pkg
-    case = (13, 8, 2, 128, 256, 48, "softmax")
     seed, e, k, d, f, b, g = case
     tokens, wr, gate, up, down = O.make_instance(seed, e, k, d, f, b)
     layer = P.MoELayer(P.ModelConfig(e, k, d, f, P.Gating(g)), P.ExpertWeights(gate, up, down), wr, max_tokens=b)
@@ -648,7 +652,6 @@ def test_expert_parallel_p2p_two_processes_one_gpu(pkg):
         port = sk.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    world = 2
     procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, case, q)) for r in range(world)]
     for p in procs:
         p.start()
