@@ -325,10 +325,76 @@ int moe_b200_ep_p2p_ffn_return_async(const moe_b200_config* cfg, int64_t max_row
                                      const moe_b200_ep_peers* peers, int32_t* done_counter, uint64_t epoch,
                                      void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------ stage API -----------------------------------
+ * Device implementations of the reference's stage-level functions
+ * (moeperf/__init__.py:56-78) for callers that run the pipeline stage by
+ * stage.  The one-call forward above does not use them. */
+
+/* router.py:69-84 `gate_scores` on caller-given logits (B, E) fp32 -> scores
+ * (B, E) fp32, bit-exact (numpy pairwise fp64 softmax sum; numpy-SIMD-expf
+ * sigmoid).  A non-finite logit sets *flag (device uint32) to 1 and leaves its
+ * row unwritten (require_finite, router.py:80). */
+int moe_b200_gate_scores(int64_t num_tokens, int num_experts, int gating, const float* logits, float* scores,
+                         uint32_t* flag, void* stream);
+
+/* router.py:87-113 `topk_select`: k rounds of numpy argmax (first maximum,
+ * NaN first) with -1.0 masking; weights are the picked scores, renormalised
+ * by their fp32 pairwise sum in sigmoid mode (1/k when the sum is zero).
+ * idx (B, k) int32, w (B, k) fp32.  MOE_B200_ERR_INVALID_K unless 1 <= k <= E. */
+int moe_b200_topk_select(int64_t num_tokens, int num_experts, int k, int gating, const float* scores,
+                         int32_t* idx, float* w, void* stream);
+
+/* linalg.py:71-80 `sigmoid` (silu = 0) or linalg.py:83-86 `silu` (silu = 1),
+ * elementwise over n fp32 values, bit-exact with numpy's float32 path. */
+int moe_b200_sigmoid(int64_t n, const float* x, float* y, int silu, void* stream);
+
+/* linalg.py:45-68 `dense_matmul`: c (m, n) = a (m, K) @ b (K, n), fp32 in and
+ * out, exact fp64 products folded in ascending K (bit-exact). */
+int moe_b200_dense_matmul(int64_t m, int64_t K, int64_t n, const float* a, const float* b, float* c,
+                          void* stream);
+
+/* scheduler.py:78-103 `expert_histogram` + `expert_offsets` +
+ * `build_permutation` from given routing indices (B, k) int32 (no gather).
+ * Indices outside [0, E) set MOE_B200_FLAG_INDEX_OUT_OF_RANGE. */
+int moe_b200_schedule(const moe_b200_config* cfg, int64_t num_tokens, const int32_t* topk_idx, int32_t* counts,
+                      int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv, void* ws, size_t ws_bytes,
+                      void* stream);
+
+/* pipeline.py:165-183 `permute_tokens`, exact: dst[r] = src[perm_fwd[r] / k]
+ * for rows of row_bytes (a multiple of 16) bytes. */
+int moe_b200_permute_rows(int64_t n_rows, int64_t row_bytes, const void* src, const int32_t* perm_fwd, int k,
+                          void* dst, void* stream);
+
+/* fp32 -> bf16 (round to nearest even): the operand cast of the stage GEMMs. */
+int moe_b200_cast_bf16(int64_t n, const float* x, void* y, void* stream);
+
+/* pipeline.py:250-313 `fused_gate_up` over expert-grouped rows (counts[e]
+ * rows of expert e, ascending e; cfg->top_k ignored):
+ *   h (n_rows, f) bf16 = silu(xp Wg_e) * (xp Wu_e)   (tcgen05, fp32 accumulate)
+ * Workspace: moe_b200_expert_ffn_workspace_size(cfg, n_rows, 0). */
+int moe_b200_grouped_gate_up(const moe_b200_config* cfg, int64_t n_rows, const int32_t* counts, const void* xp,
+                             const void* w_gate, const void* w_up, void* h, void* ws, size_t ws_bytes, void* stream);
+
+/* pipeline.py:186-247 `grouped_gemm` over expert-grouped rows: out (n_rows, N)
+ * fp32 = a (n_rows, K) bf16 @ W_e, W the flat (E*K, N) bf16 stack; cfg gives
+ * E, hidden_dim = N and ffn_dim = K.  Workspace as moe_b200_grouped_gate_up. */
+int moe_b200_grouped_gemm(const moe_b200_config* cfg, int64_t n_rows, const int32_t* counts, const void* a,
+                          const void* w_stack, float* out, void* ws, size_t ws_bytes, void* stream);
+
+/* The activation pass of pipeline.py:316-370 `unfused_gate_up`:
+ * h[i] = bf16(silu(g[i]) * u[i]) with gu = [g (n) | u (n)] fp32, the fused
+ * epilogue's exact formula (so fused == unfused bit for bit). */
+int moe_b200_swiglu(int64_t n, const float* gu, void* h, void* stream);
+
 /* Copy the device status flags (MOE_B200_FLAG_*) to the host and clear them.
  * Synchronises `stream`. */
 int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws,
                         size_t ws_bytes, uint32_t* flags, void* stream);
+
+/* Re-read the MOE_B200_* tuning / test hooks from the environment.  They are
+ * read once (first use) and at every moe_b200_workspace_init, never on the
+ * forward path. */
+int moe_b200_tuning_reload(void);
 
 /* Human-readable status. */
 const char* moe_b200_strerror(int status);

@@ -291,6 +291,44 @@ def dense_moe_oracle(tokens, router_weight, gate, up, down, num_experts, k, gati
     return out
 
 
+def moe_rows(tokens, router_weight, expert, num_experts, k, gating, routing=None):
+    """Layer output for a subset of tokens, fetching only the experts they use.
+
+    Rows of the reference forward are independent (``SPEC.md:155-156``;
+    ``dense_moe_oracle`` is bitwise ``moe_forward``, ``pipeline.py:618-643``),
+    so y for a token subset is the dense per-token restatement over just those
+    tokens: route them (``router.py:116-133``), then for every selected expert
+    ``g = x Wg_e, u = x Wu_e, h = silu(g) * u, o = h Wd_e`` with the canonical
+    fp64 fold, combined ``out += w_j * o_j`` in ascending j from zero
+    (``pipeline.py:396-399``).  ``expert(e)`` returns ``(gate_e (d,f), up_e
+    (d,f), down_e (f,d))`` float32 — a full-size layer (DeepSeek-V3: 45 GB in
+    fp32) never has to be materialised on the host.  Tokens that share an
+    expert are folded together (same bits: the fold is per output element).
+    """
+    tokens = np.ascontiguousarray(np.asarray(tokens, dtype=F32))
+    b, d = tokens.shape
+    if routing is None:
+        idx, w = route(tokens, router_weight, k, gating)
+    else:
+        idx, w = routing
+    outs = {}
+    for e in np.unique(idx):
+        rows, slots = np.nonzero(idx == e)
+        ge, ue, de = expert(int(e))
+        a = tokens[rows]
+        g = dot_fp64_fold(a, ge)
+        u = dot_fp64_fold(a, ue)
+        h = (silu_f32(g) * u).astype(F32)
+        o = dot_fp64_fold(h, de)
+        for i, (r, j) in enumerate(zip(rows, slots)):
+            outs[(int(r), int(j))] = o[i]
+    y = np.zeros((b, d), dtype=F32)
+    for j in range(idx.shape[1]):
+        for r in range(b):
+            y[r] += w[r, j] * outs[(r, j)]
+    return dict(indices=idx, weights=w, y=y)
+
+
 def max_rel_error(y, y_ref) -> float:
     """``max|y−y_ref| / max(max|y_ref|, 1e-6)`` — the reference verify metric (``cli.py:733-737``)."""
     y = np.asarray(y, dtype=F64)

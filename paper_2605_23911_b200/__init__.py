@@ -8,10 +8,14 @@ types.  ``MoELayer`` is the resident-weights device layer used by the bench.
 """
 
 from .errors import (
+    AllZero,
+    DegenerateStage,
     DeviceError,
     IndexOutOfRange,
     InvalidBlockM,
     InvalidK,
+    InvalidSpec,
+    MissingPeakFlops,
     MoeperfError,
     NativeLibraryMissing,
     NonFiniteInput,
@@ -44,11 +48,22 @@ from .types import (
 __version__ = "0.1.0"
 
 
+_LAYER_NAMES = ("MoELayer", "HostPipeline", "DeviceExpertWeights", "upload_weights", "moe_forward", "route")
+# the reference's stage-level API (moeperf/__init__.py:56-78) on the device
+_STAGE_NAMES = ("gate_scores", "stable_softmax_row", "topk_select", "expert_histogram", "build_permutation",
+                "permute_tokens", "fused_gate_up", "unfused_gate_up", "grouped_gemm", "unpermute_combine",
+                "sigmoid", "silu", "dense_matmul", "dense_moe_oracle")
+
+
 def __getattr__(name):
     # Device-facing symbols import torch lazily so host-only users (trace,
     # types) do not pay for it.
-    if name in ("MoELayer", "HostPipeline", "DeviceExpertWeights", "upload_weights", "moe_forward", "route"):
+    if name in _LAYER_NAMES:
         from . import layer
 
         return getattr(layer, name)
+    if name in _STAGE_NAMES:
+        from . import stages
+
+        return getattr(stages, name)
     raise AttributeError(name)

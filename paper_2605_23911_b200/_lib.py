@@ -112,6 +112,17 @@ SIGNATURES = {
     "moe_b200_io_wait": (_INT, [_P, _P]),
     "moe_b200_launches_per_forward": (_INT, [_CFG, _I64]),
     "moe_b200_io_sync": (_INT, [_P]),
+    "moe_b200_tuning_reload": (_INT, []),
+    "moe_b200_gate_scores": (_INT, [_I64, _INT, _INT, _P, _P, _P, _P]),
+    "moe_b200_topk_select": (_INT, [_I64, _INT, _INT, _INT, _P, _P, _P, _P]),
+    "moe_b200_sigmoid": (_INT, [_I64, _P, _P, _INT, _P]),
+    "moe_b200_dense_matmul": (_INT, [_I64, _I64, _I64, _P, _P, _P, _P]),
+    "moe_b200_schedule": (_INT, [_CFG, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_permute_rows": (_INT, [_I64, _I64, _P, _P, _INT, _P, _P]),
+    "moe_b200_cast_bf16": (_INT, [_I64, _P, _P, _P]),
+    "moe_b200_grouped_gate_up": (_INT, [_CFG, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_grouped_gemm": (_INT, [_CFG, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "moe_b200_swiglu": (_INT, [_I64, _P, _P, _P]),
     "moe_b200_strerror": (ctypes.c_char_p, [_INT]),
     "moe_b200_last_error_detail": (ctypes.c_char_p, []),
     "moe_b200_version": (ctypes.c_char_p, []),
@@ -154,6 +165,12 @@ def check(status: int, what: str) -> None:
     detail = lib.moe_b200_last_error_detail().decode()
     exc = STATUS_TO_EXC.get(status, errors.DeviceError)
     raise exc(f"{what}: {msg}" + (f" ({detail})" if detail else ""))
+
+
+def reload_tuning() -> None:
+    """Re-read the MOE_B200_* tuning / test hooks (the library reads them once,
+    and at every workspace init, never on the forward path)."""
+    check(load().moe_b200_tuning_reload(), "tuning_reload")
 
 
 def config_struct(num_experts, top_k, hidden_dim, ffn_dim, gating_code) -> Config:

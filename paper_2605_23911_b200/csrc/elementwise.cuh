@@ -189,11 +189,14 @@ combine_token_kernel(const float* __restrict__ ys, int n_dp, int T_pad,
   // 16-byte columns of one token per thread, every partial load issued before
   // the first add (one L2 round trip after the row ids)
   const int t = blockIdx.x;
-  if (threadIdx.x < k) {  // row ids / weights: outputs of kernels before the FFN
-    s_row[threadIdx.x] = __ldg(prow + (size_t)t * k + threadIdx.x);
-    s_w[threadIdx.x] = __ldg(topk_w + (size_t)t * k + threadIdx.x);
+  // PDL: griddepcontrol.wait only orders this grid after its immediate
+  // predecessor (the FFN); the row ids / weights come from the router and the
+  // dispatch, two launches earlier, so they too are read after the wait.
+  pdl_wait();
+  if (threadIdx.x < k) {
+    s_row[threadIdx.x] = prow[(size_t)t * k + threadIdx.x];
+    s_w[threadIdx.x] = topk_w[(size_t)t * k + threadIdx.x];
   }
-  pdl_wait();  // partials of the FFN grid
   __syncthreads();
   const size_t half_stride = (size_t)T_pad * 128;
   constexpr int kSlots = kCombineMaxKS / kNV;

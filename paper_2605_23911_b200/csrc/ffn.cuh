@@ -677,7 +677,8 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             } else if (wq == 0 && nvalid_d > 0) {
               // lane c looks up row c's expanded slot; lane 0 issues all copies (scatter)
               const int rows = min(32, ch.z - c0);
-              const int xid = lane < rows ? __ldg(p.fwd + ch.y + c0 + lane) : 0;
+              // expanded slot of row c (fwd == null: the grouped-GEMM stage, rows stay in place)
+              const int xid = lane < rows ? (p.fwd ? __ldg(p.fwd + ch.y + c0 + lane) : ch.y + c0 + lane) : 0;
               if (p.scale_by_w && lane < rows) {
                 const float w = __ldg(p.topk_w + xid);
                 for (int qv = 0; qv < kBM; ++qv) sbuf[lane * kBM + qv] = __fmul_rn(sbuf[lane * kBM + qv], w);

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -20,6 +21,7 @@
 #include "router_seg.cuh"
 #include "dispatch.cuh"
 #include "ep_p2p.cuh"
+#include "stages.cuh"
 
 using namespace moe;
 
@@ -58,6 +60,65 @@ cudaError_t record_event(cudaEvent_t ev, cudaStream_t s) {
 
 constexpr size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Tuning / test hooks (MOE_B200_* environment variables).  Read once, off the
+// forward path: at the first use, at every moe_b200_workspace_init and by
+// moe_b200_tuning_reload (tests that flip a hook on an existing layer call it).
+// -1 / 0 mean "not set" (the built-in rule applies).
+struct Tuning {
+  int chunk_rows = 0;        // MOE_B200_CHUNK_ROWS (128 | 256)
+  int down_splits = 0;       // MOE_B200_DOWN_SPLITS
+  int seg_wide = -1;         // MOE_B200_SEG_WIDE (0: never 64-wide expert blocks)
+  long long seg_max_chains = 64LL * 1024;  // MOE_B200_SEG_MAX_CHAINS
+  int seg_len = 0;           // MOE_B200_SEG_LEN
+  int pdl = 0;               // MOE_B200_PDL
+  int rx_te = 0, rx_tt = 0, rx_tokc = 0;  // MOE_B200_RX_TILE "te,tt,tokc"
+  int ffn_pair = -1;         // MOE_B200_FFN_PAIR (0 | 1 | 2)
+  int ffn_variant = 2;       // MOE_B200_FFN_VARIANT
+  int force_exact = 0;       // MOE_B200_ROUTER_FORCE_EXACT
+  int io_graphs = 1;         // MOE_B200_IO_GRAPHS
+  int fused_combine = 1;     // MOE_B200_FUSED_COMBINE (0: separate combine launch)
+};
+Tuning g_tune;
+std::mutex g_tune_mu;
+std::atomic<bool> g_tune_loaded{false};
+
+void load_tuning_locked() {
+  Tuning t;
+  auto geti = [](const char* name, int def) {
+    const char* v = getenv(name);
+    return (v && *v) ? atoi(v) : def;
+  };
+  t.chunk_rows = geti("MOE_B200_CHUNK_ROWS", 0);
+  t.down_splits = geti("MOE_B200_DOWN_SPLITS", 0);
+  t.seg_wide = geti("MOE_B200_SEG_WIDE", -1);
+  if (const char* v = getenv("MOE_B200_SEG_MAX_CHAINS")) t.seg_max_chains = atoll(v);
+  t.seg_len = geti("MOE_B200_SEG_LEN", 0);
+  t.pdl = geti("MOE_B200_PDL", 0);
+  if (const char* v = getenv("MOE_B200_RX_TILE")) {
+    if (sscanf(v, "%d,%d,%d", &t.rx_te, &t.rx_tt, &t.rx_tokc) != 3) t.rx_te = t.rx_tt = t.rx_tokc = 0;
+  }
+  t.ffn_pair = geti("MOE_B200_FFN_PAIR", -1);
+  t.ffn_variant = geti("MOE_B200_FFN_VARIANT", 2);
+  t.force_exact = geti("MOE_B200_ROUTER_FORCE_EXACT", 0);
+  t.io_graphs = geti("MOE_B200_IO_GRAPHS", 1);
+  t.fused_combine = geti("MOE_B200_FUSED_COMBINE", 1);
+  g_tune = t;
+  g_tune_loaded = true;
+}
+
+const Tuning& tuning() {
+  if (!g_tune_loaded) {
+    std::lock_guard<std::mutex> lock(g_tune_mu);
+    if (!g_tune_loaded) load_tuning_locked();
+  }
+  return g_tune;
+}
+
+void reload_tuning() {
+  std::lock_guard<std::mutex> lock(g_tune_mu);
+  load_tuning_locked();
+}
+
 constexpr int kTbCap = 4096;      // max router token blocks per launch
 constexpr int kChunkCap = 8192;   // max expert row-chunks per launch
 constexpr int kBlkCap = 16384;    // max (token block x expert block) counters (segment router)
@@ -82,10 +143,8 @@ int chunk_rows_for(const moe_b200_config& c, int64_t B) {
   // Tokens per expert on average; big chunks keep one weight pass per expert
   // (Mixtral), small chunks for many-expert layers (DeepSeek / Qwen).
   const int64_t T = B * c.top_k;
-  if (const char* env = getenv("MOE_B200_CHUNK_ROWS")) {
-    const int v = atoi(env);
-    if (v == 128 || v == 256) return v;  // tuning hook (the FFN templates are BN 128 / 256)
-  }
+  const int v = tuning().chunk_rows;
+  if (v == 128 || v == 256) return v;  // tuning hook (the FFN templates are BN 128 / 256)
   return (T > 96LL * c.num_experts) ? 256 : 128;
 }
 
@@ -105,13 +164,13 @@ double expected_active_experts(const moe_b200_config& c, int64_t B) {
 // S=8/6/4 -> 161->131, 203->182, 248->229 us; B=16 keeps S=2; Qwen B=1/4:
 // S=4 -> 59->53, 82->76 us).  Partials are reduced deterministically in
 // combine.  MOE_B200_DOWN_SPLITS overrides (tuning).
-int down_split_count(const moe_b200_config& c, int64_t B, const char* env) {
+int down_split_count(const moe_b200_config& c, int64_t B, int force) {
   const int nkb = (c.ffn_dim + kBK - 1) / kBK;
   const int n_dp = (c.hidden_dim + 2 * kBM - 1) / (2 * kBM);
   int s = static_cast<int>((c.ffn_dim + c.hidden_dim) / (2 * c.hidden_dim));  // round(f / 2d)
   const int fill = static_cast<int>(std::lround(256.0 / (n_dp * expected_active_experts(c, B))));
   s = std::max(s, std::min(fill, nkb / 6));
-  if (env && atoi(env) > 0) s = atoi(env);  // 0: the rule above
+  if (force > 0) s = force;  // 0: the rule above
   s = std::max(1, std::min(s, 16));
   return std::min(s, nkb);
 }
@@ -120,7 +179,7 @@ int down_split_count(const moe_b200_config& c, int64_t B, const char* env) {
 // layer's count so their rows match the single-GPU forward bit for bit)
 void down_splits(const moe_b200_config& c, int64_t B, int* splits, int* kb_per_split, int s_force = 0) {
   const int nkb = (c.ffn_dim + kBK - 1) / kBK;
-  const int s = s_force > 0 ? std::min(std::min(s_force, 16), nkb) : down_split_count(c, B, getenv("MOE_B200_DOWN_SPLITS"));
+  const int s = s_force > 0 ? std::min(std::min(s_force, 16), nkb) : down_split_count(c, B, tuning().down_splits);
   int kps = (nkb + s - 1) / s;
   *kb_per_split = kps;
   *splits = (nkb + kps - 1) / kps;
@@ -137,8 +196,8 @@ int seg_expc(int E, int64_t B) {
   if (E <= 16) return 16;
   if (E <= 32) return 32;
   const int64_t n_tb = (B + kSegTT - 1) / kSegTT;
-  const char* env = getenv("MOE_B200_SEG_WIDE");  // 0: never 64-wide (A/B)
-  if (E <= 64 && n_tb * ((E + 31) / 32) > kNumSMs && !(env && atoi(env) == 0)) return 64;
+  // MOE_B200_SEG_WIDE=0: never 64-wide (A/B)
+  if (E <= 64 && n_tb * ((E + 31) / 32) > kNumSMs && tuning().seg_wide != 0) return 64;
   return 32;
 }
 
@@ -147,8 +206,7 @@ int seg_expc(int E, int64_t B) {
 // use the exact kernel (no magnitude DADD: half the fp64 work; measured
 // DeepSeek-V3 B=512: 257 us exact vs 430 us segment).
 int64_t seg_max_tokens(const moe_b200_config& c) {
-  int64_t chains = 64LL * 1024;
-  if (const char* env = getenv("MOE_B200_SEG_MAX_CHAINS")) chains = atoll(env);
+  const int64_t chains = tuning().seg_max_chains;
   return chains / std::max(1, c.num_experts);
 }
 
@@ -173,8 +231,7 @@ SegPlan plan_seg(const moe_b200_config& c, int64_t B) {
   int n_kb = base * 4 >= kNumSMs * 3 ? 1 : static_cast<int>(std::min<long>(max_kb, (kNumSMs * 3 / 2 + base - 1) / base));
   if (q.expc > 32) n_kb = 1;  // (64-wide blocks only when they fill the SMs; keeps n_kb <= d/256)
   q.seg_len = ((c.hidden_dim + (long)n_kb * S - 1) / ((long)n_kb * S) + 7) / 8 * 8;
-  if (const char* env = getenv("MOE_B200_SEG_LEN"))
-    if (q.expc <= 32) q.seg_len = std::max(8, atoi(env) / 8 * 8);
+  if (tuning().seg_len > 0 && q.expc <= 32) q.seg_len = std::max(8, tuning().seg_len / 8 * 8);
   q.kr = S * q.seg_len;
   q.n_kb = (c.hidden_dim + q.kr - 1) / q.kr;
   q.grid = q.n_tb * q.n_eb * q.n_kb;
@@ -383,8 +440,7 @@ cudaError_t launch_pdl_if(bool on, void (*kern)(KArgs...), dim3 grid, dim3 block
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
-  const char* env = getenv("MOE_B200_PDL");
-  return launch_pdl_if(env && atoi(env), kern, grid, block, smem, s, std::forward<Args>(args)...);
+  return launch_pdl_if(tuning().pdl != 0, kern, grid, block, smem, s, std::forward<Args>(args)...);
 }
 
 
@@ -415,9 +471,9 @@ RouterPlan plan_router(const moe_b200_config& c, int64_t B, int x_bf16) {
     // 2 experts x 4 tokens per thread, 32-token blocks (DeepSeek-512 A/B: 2x2
     // within +-0.5%, 4x4 +9%, 2x1 over 16-token blocks +4%)
     r.te = 2; r.tt = 4; r.tokc = 32;
-    if (const char* env = getenv("MOE_B200_RX_TILE")) {  // tuning: "te,tt,tokc"
-      int te = 0, tt = 0, tokc = 0;
-      if (sscanf(env, "%d,%d,%d", &te, &tt, &tokc) == 3 &&
+    {  // tuning: MOE_B200_RX_TILE="te,tt,tokc"
+      const int te = tuning().rx_te, tt = tuning().rx_tt, tokc = tuning().rx_tokc;
+      if (te > 0 &&
           ((te == 2 && (tt == 2 || tt == 4)) || (te == 4 && tt == 4)) &&
           tokc >= tt && tokc % tt == 0 && r.expc % te == 0 &&
           (r.expc / te) * (tokc / tt) + kRouterProducers <= 384) {  // router_kernel's launch bound
@@ -557,7 +613,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.ys = ys;
   p.topk_w = topk_w;
   p.fwd = fwd;
-  p.scale_by_w = fused ? 0 : 1;
+  p.scale_by_w = (!fused && topk_w) ? 1 : 0;
   p.gu_wait = (mode == kFfnFused && do_gu && do_dn) ? 1 : 0;
   p.gu_unfused = (mode == kFfnUnfusedGU) ? 1 : 0;
   p.gu32 = gu32;
@@ -574,12 +630,11 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   // multicast pair, mode 1, from the saved data movement; a tie uncapped).
   // MOE_B200_FFN_PAIR=0/1/2 forces a mode (all bit-identical).
   p.pair = (mode == kFfnFused && bn == 256) ? 2 : 0;
-  if (const char* env = getenv("MOE_B200_FFN_PAIR")) p.pair = mode == kFfnFused ? std::min(2, std::max(0, atoi(env))) : 0;
+  if (tuning().ffn_pair >= 0) p.pair = mode == kFfnFused ? std::min(2, tuning().ffn_pair) : 0;
   long max_tiles = (long)L.max_chunks * (p.n_mt_gu * (p.gu_unfused ? 2 : 1) + p.n_mt_dn * p.splits);
   int grid = static_cast<int>(std::max(1L, std::min<long>(kNumSMs, max_tiles)));
   if (p.pair) grid = std::max(2, grid & ~1);  // whole clusters
-  int variant = 2;
-  if (const char* env = getenv("MOE_B200_FFN_VARIANT")) variant = atoi(env);
+  const int variant = tuning().ffn_variant;
   return launch_ffn_kernel(bn, variant, m_wg, m_wu, m_xp, m_wd, m_h, p, grid, s);
 }
 
@@ -699,7 +754,12 @@ int launch_dispatch(const moe_b200_config& c, int64_t B, const void* x, int xb, 
 // ================================ C ABI =======================================
 extern "C" {
 
-const char* moe_b200_version(void) { return "moe_b200 0.1.0 (sm_100a)"; }
+const char* moe_b200_version(void) { return "moe_b200 0.2.0 (sm_100a)"; }
+
+int moe_b200_tuning_reload(void) {
+  reload_tuning();
+  return MOE_B200_OK;
+}
 
 // Debug hook (not part of the public header): record a per-tile timeline of
 // subsequent ffn launches into a device buffer of 4 u64 per tile, or NULL to stop.
@@ -740,11 +800,11 @@ int moe_b200_workspace_size(const moe_b200_config* cfg, int64_t max_tokens, size
   // the down-split count falls as B grows (down_split_count) while the padded
   // row space grows: size for the largest B of every split count <= max_tokens
   size_t total = layout_for(*cfg, max_tokens).total;
-  const char* env = getenv("MOE_B200_DOWN_SPLITS");
-  const int s_last = down_split_count(*cfg, max_tokens, env);
-  int s_prev = down_split_count(*cfg, 1, env);
+  const int force = tuning().down_splits;
+  const int s_last = down_split_count(*cfg, max_tokens, force);
+  int s_prev = down_split_count(*cfg, 1, force);
   for (int64_t b = 2; b <= max_tokens && s_prev > s_last; ++b) {
-    const int s_b = down_split_count(*cfg, b, env);
+    const int s_b = down_split_count(*cfg, b, force);
     if (s_b != s_prev) total = std::max(total, layout_for(*cfg, b - 1).total);
     s_prev = s_b;
   }
@@ -758,6 +818,7 @@ int moe_b200_workspace_init(const moe_b200_config* cfg, int64_t max_tokens, void
   if (rc) return rc;
   if (!ws || ws_bytes < kHeaderBytes) return MOE_B200_ERR_WORKSPACE;
   (void)max_tokens;
+  reload_tuning();  // the MOE_B200_* hooks are read here, not on the forward path
   MOE_CUDA(cudaMemsetAsync(ws, 0, kHeaderBytes, static_cast<cudaStream_t>(stream)));
   return MOE_B200_OK;
 }
@@ -802,7 +863,7 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
   p.chunk_rows = chunk_rows_for(*cfg, B);
   p.logits = logits;
   p.want_logits = logits != nullptr;
-  if (const char* env = getenv("MOE_B200_ROUTER_FORCE_EXACT")) p.force_exact = atoi(env);
+  p.force_exact = tuning().force_exact;
   p.lbuf = reinterpret_cast<float2*>(ws8(ws) + L.lbuf);
   p.topk_idx = topk_idx; p.topk_w = topk_w; p.counts = counts; p.offsets = offsets;
   p.fwd = perm_fwd; p.inv = perm_inv;
@@ -1098,8 +1159,7 @@ int moe_b200_io_create(const moe_b200_config* cfg, int64_t max_tokens, int x_dty
   if ((e = cudaStreamCreateWithFlags(&io->s_in, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "io stream");
   if ((e = cudaStreamCreateWithFlags(&io->s_out, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "io stream");
   if ((e = cudaStreamCreateWithFlags(&io->s_cap, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "io stream");
-  const char* genv = getenv("MOE_B200_IO_GRAPHS");
-  io->graphs_off = genv && atoi(genv) == 0;
+  io->graphs_off = tuning().io_graphs == 0;
   *io_out = io;
   return MOE_B200_OK;
 }
@@ -1491,6 +1551,165 @@ int moe_b200_ep_p2p_return(const moe_b200_config* cfg, int64_t num_rows, const f
       out_rows, P.ids[P.me], static_cast<int>(num_rows), cfg->hidden_dim, P, done_counter, epoch);
   MOE_LAUNCH_CHECK("ep_return_kernel");
   return MOE_B200_OK;
+}
+
+// ------------------------- reference stage API ----------------------------------
+// Device implementations of the stage functions the reference exports
+// (moeperf/__init__.py:56-78) for callers that run the pipeline stage by stage.
+
+static int stage_grid(long long n, int per_block) {
+  const long long b = (n + per_block - 1) / per_block;
+  return static_cast<int>(std::max<long long>(1, std::min<long long>(b, (long long)kNumSMs * 16)));
+}
+
+int moe_b200_gate_scores(int64_t B, int E, int gating, const float* logits, float* scores, uint32_t* flag,
+                         void* stream) {
+  if (B < 0 || E < 1 || E > kMaxExperts) return E > kMaxExperts ? MOE_B200_ERR_UNSUPPORTED : MOE_B200_ERR_INVALID_VALUE;
+  if (gating != MOE_B200_GATING_SOFTMAX && gating != MOE_B200_GATING_SIGMOID_NORMALIZED)
+    return MOE_B200_ERR_INVALID_VALUE;
+  if (B == 0) return MOE_B200_OK;
+  if (!logits || !scores || !flag) return MOE_B200_ERR_INVALID_VALUE;
+  const size_t smem = (size_t)kStageWarps * E * sizeof(double);
+  MOE_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(gate_scores_kernel), smem));
+  gate_scores_kernel<<<stage_grid(B, kStageWarps), kStageWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(
+      logits, scores, static_cast<int>(B), E, gating, flag);
+  MOE_LAUNCH_CHECK("gate_scores_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_topk_select(int64_t B, int E, int k, int gating, const float* scores, int32_t* idx, float* w,
+                         void* stream) {
+  if (B < 0 || E < 1) return MOE_B200_ERR_INVALID_VALUE;
+  if (k < 1 || k > E) return MOE_B200_ERR_INVALID_K;
+  if (E > kMaxExperts) return MOE_B200_ERR_UNSUPPORTED;
+  if (gating != MOE_B200_GATING_SOFTMAX && gating != MOE_B200_GATING_SIGMOID_NORMALIZED)
+    return MOE_B200_ERR_INVALID_VALUE;
+  if (B == 0) return MOE_B200_OK;
+  if (!scores || !idx || !w) return MOE_B200_ERR_INVALID_VALUE;
+  const size_t smem = (size_t)kStageWarps * (E + k) * sizeof(float);
+  MOE_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(topk_select_kernel), smem));
+  topk_select_kernel<<<stage_grid(B, kStageWarps), kStageWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(
+      scores, idx, w, static_cast<int>(B), E, k, gating);
+  MOE_LAUNCH_CHECK("topk_select_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_sigmoid(int64_t n, const float* x, float* y, int silu, void* stream) {
+  if (n < 0) return MOE_B200_ERR_INVALID_VALUE;
+  if (n == 0) return MOE_B200_OK;
+  if (!x || !y) return MOE_B200_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (silu) sigmoid_kernel<true><<<stage_grid(n, 256), 256, 0, s>>>(x, y, n);
+  else sigmoid_kernel<false><<<stage_grid(n, 256), 256, 0, s>>>(x, y, n);
+  MOE_LAUNCH_CHECK("sigmoid_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_dense_matmul(int64_t m, int64_t K, int64_t n, const float* a, const float* b, float* c, void* stream) {
+  if (m < 0 || K < 0 || n < 0 || m > INT32_MAX || K > INT32_MAX || n > INT32_MAX) return MOE_B200_ERR_INVALID_VALUE;
+  if (m == 0 || n == 0) return MOE_B200_OK;
+  if (!c || (K > 0 && (!a || !b))) return MOE_B200_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (K == 0) {
+    MOE_CUDA(cudaMemsetAsync(c, 0, (size_t)m * n * sizeof(float), s));
+    return MOE_B200_OK;
+  }
+  dense_matmul_kernel<<<stage_grid(m * n, 256), 256, 0, s>>>(a, b, c, static_cast<int>(m), static_cast<int>(K),
+                                                              static_cast<int>(n));
+  MOE_LAUNCH_CHECK("dense_matmul_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_permute_rows(int64_t n_rows, int64_t row_bytes, const void* src, const int32_t* perm_fwd, int k,
+                          void* dst, void* stream) {
+  if (n_rows < 0 || row_bytes <= 0 || row_bytes % 16 || k < 1) return MOE_B200_ERR_INVALID_VALUE;
+  if (n_rows == 0) return MOE_B200_OK;
+  if (!src || !perm_fwd || !dst) return MOE_B200_ERR_INVALID_VALUE;
+  permute_rows_kernel<<<stage_grid(n_rows * (row_bytes / 16), 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(src), perm_fwd, k, static_cast<uint8_t*>(dst), static_cast<int>(n_rows),
+      static_cast<int>(row_bytes));
+  MOE_LAUNCH_CHECK("permute_rows_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_cast_bf16(int64_t n, const float* x, void* y, void* stream) {
+  if (n < 0) return MOE_B200_ERR_INVALID_VALUE;
+  if (n == 0) return MOE_B200_OK;
+  if (!x || !y) return MOE_B200_ERR_INVALID_VALUE;
+  f32_to_bf16_kernel<<<stage_grid(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, static_cast<__nv_bfloat16*>(y), n);
+  MOE_LAUNCH_CHECK("f32_to_bf16_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_swiglu(int64_t n, const float* gu, void* h, void* stream) {
+  if (n < 0 || n % 4) return MOE_B200_ERR_INVALID_VALUE;
+  if (n == 0) return MOE_B200_OK;
+  if (!gu || !h) return MOE_B200_ERR_INVALID_VALUE;
+  swiglu_tiled_kernel<<<grid_for_rows(n / 4), kRowThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      gu, static_cast<__nv_bfloat16*>(h), static_cast<size_t>(n));
+  MOE_LAUNCH_CHECK("swiglu_kernel");
+  return MOE_B200_OK;
+}
+
+int moe_b200_schedule(const moe_b200_config* cfg, int64_t B, const int32_t* topk_idx, int32_t* counts,
+                      int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv, void* ws, size_t ws_bytes,
+                      void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (B < 0) return MOE_B200_ERR_SHAPE_MISMATCH;
+  Layout L;
+  if ((rc = check_ws(cfg, B, ws, ws_bytes, &L))) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* hdr = reinterpret_cast<int32_t*>(ws);
+  if (B == 0) {
+    MOE_CUDA(cudaMemsetAsync(counts, 0, cfg->num_experts * sizeof(int32_t), s));
+    MOE_CUDA(cudaMemsetAsync(offsets, 0, (cfg->num_experts + 1) * sizeof(int32_t), s));
+    return MOE_B200_OK;
+  }
+  if (!topk_idx || !counts || !offsets || !perm_fwd || !perm_inv) return MOE_B200_ERR_INVALID_VALUE;
+  return launch_dispatch(*cfg, B, nullptr, 0, topk_idx, counts, offsets, perm_fwd, perm_inv,
+                         reinterpret_cast<int32_t*>(ws8(ws) + L.prow), reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab),
+                         hdr + 2, nullptr, s, reinterpret_cast<uint32_t*>(hdr));
+}
+
+// expert-grouped rows (counts[e] rows for expert e, ascending e): the chunk
+// table from the counts, then one FFN launch in row-layout (staged) mode
+static int grouped_ffn(const moe_b200_config* cfg, int64_t n_rows, const int32_t* counts, const void* xp,
+                       const void* w_gate, const void* w_up, const void* w_down, void* h, float* out, void* ws,
+                       size_t ws_bytes, void* stream) {
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if (n_rows < 0) return MOE_B200_ERR_SHAPE_MISMATCH;
+  if (n_rows == 0) return MOE_B200_OK;
+  moe_b200_config c1 = *cfg;
+  c1.top_k = 1;
+  Layout L;
+  if ((rc = check_ws(&c1, n_rows, ws, ws_bytes, &L))) return rc;
+  if (L.max_chunks > kChunkCap || c1.num_experts > 1024) return MOE_B200_ERR_UNSUPPORTED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* hdr = reinterpret_cast<int32_t*>(ws);
+  schedule_from_counts_kernel<<<1, 256, 0, s>>>(counts, c1.num_experts, chunk_rows_for(c1, n_rows),
+                                                reinterpret_cast<int32_t*>(ws8(ws) + L.logits),
+                                                reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab),
+                                                reinterpret_cast<int2*>(ws8(ws) + L.chunk_tab) + 2 * L.max_chunks,
+                                                hdr + 2, reinterpret_cast<int32_t*>(ws8(ws) + L.prow));
+  MOE_LAUNCH_CHECK("schedule_from_counts_kernel");
+  const bool gu = w_down == nullptr;
+  return launch_ffn(c1, n_rows, L, ws, xp, w_gate, w_up, w_down, gu ? h : const_cast<void*>(xp), out, nullptr,
+                    nullptr, /*gu*/ gu, /*dn*/ !gu, kFfnStaged, s);
+}
+
+int moe_b200_grouped_gate_up(const moe_b200_config* cfg, int64_t n_rows, const int32_t* counts, const void* xp,
+                             const void* w_gate, const void* w_up, void* h, void* ws, size_t ws_bytes, void* stream) {
+  if (n_rows > 0 && (!counts || !xp || !w_gate || !w_up || !h)) return MOE_B200_ERR_INVALID_VALUE;
+  return grouped_ffn(cfg, n_rows, counts, xp, w_gate, w_up, nullptr, h, nullptr, ws, ws_bytes, stream);
+}
+
+int moe_b200_grouped_gemm(const moe_b200_config* cfg, int64_t n_rows, const int32_t* counts, const void* a,
+                          const void* w_stack, float* out, void* ws, size_t ws_bytes, void* stream) {
+  if (n_rows > 0 && (!counts || !a || !w_stack || !out)) return MOE_B200_ERR_INVALID_VALUE;
+  return grouped_ffn(cfg, n_rows, counts, a, nullptr, nullptr, w_stack, nullptr, out, ws, ws_bytes, stream);
 }
 
 int moe_b200_combine_rows(const moe_b200_config* cfg, int64_t B, const float* rows,

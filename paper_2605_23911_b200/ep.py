@@ -99,7 +99,10 @@ class CudaOps:
         return (r["indices"], r["weights"], r["counts"].clone(), r["forward"].clone(), r["inverse"].clone())
 
     def permute(self, x, fwd, k):
-        xb = x.to(torch.bfloat16).contiguous()
+        xb = x.to(torch.bfloat16)
+        if xb.shape[1] != self.w.hidden_pad:  # rows are gathered in 16-byte units at the padded width
+            xb = torch.nn.functional.pad(xb, (0, self.w.hidden_pad - xb.shape[1]))
+        xb = xb.contiguous()
         idx = (fwd // k).to(torch.int32).contiguous()
         return self.gather_rows(xb, idx)
 
@@ -201,9 +204,12 @@ class ExpertParallelMoE:
             return
         dist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits, group=self.group)
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, global_tokens: int | None = None) -> torch.Tensor:
+        """This rank's token shard -> its output rows.  ``global_tokens``: see
+        ``PeerExchange.forward`` (the collective transport learns it from the
+        counts exchange)."""
         if self.p2p is not None:
-            return self.p2p.forward(x)
+            return self.p2p.forward(x, global_tokens)
         cfg = self.config
         k, E, d = cfg.top_k, cfg.num_experts, cfg.hidden_dim
         B = x.shape[0]
@@ -275,8 +281,19 @@ class PeerExchange:
         d = ops.w.hidden_pad
         n_loc = ep.local_cfg.num_experts
         self.max_tokens = max_tokens
+        # peers size their writes by their OWN batches: agree on every rank's
+        # bound first, so the receive buffers cover the largest sender
+        if n > 1:
+            bounds = [None] * n
+            dist.all_gather_object(bounds, int(max_tokens), group=ep.group)
+        else:
+            bounds = [int(max_tokens)]
+        self.rank_max_tokens = [int(b) for b in bounds]
+        # the layer's batch when every rank runs its bound (the default
+        # global_tokens of forward: it fixes the down K-split count)
+        self.global_tokens = sum(self.rank_max_tokens)
         # worst case: every token of every rank sends min(k, E_local) rows here
-        self.r_max = max(1, n * max_tokens * min(k, n_loc))
+        self.r_max = max(1, sum(self.rank_max_tokens) * min(k, n_loc))
         t_max = max(1, max_tokens * k)
         sizes = {"counts": n * E * 4, "flags": 3 * n * 8, "rows": self.r_max * d * 2,
                  "ids": self.r_max * 8, "home": t_max * d * 4}
@@ -324,15 +341,18 @@ class PeerExchange:
 
     def forward(self, x: torch.Tensor, global_tokens: int | None = None) -> torch.Tensor:
         """Asynchronous (no host synchronisation).
-        ``global_tokens`` (default: world x local tokens) is the layer's total
-        batch; it fixes the down K-split count so every row matches the
-        single-GPU forward bit for bit."""
+        ``global_tokens`` is the layer's total batch over all ranks; it fixes
+        the down K-split count so every row matches the single-GPU forward bit
+        for bit.  Default: the sum of the ranks' ``max_tokens`` (all-gathered
+        at construction), i.e. every rank running a full batch; a rank whose
+        batch is partial passes the true total (there is no host
+        synchronisation here to learn it)."""
         ep, ops, lib = self.ep, self.ops, self.lib
         cfg = ep.config
         k, d = cfg.top_k, cfg.hidden_dim
         B = x.shape[0]
         if global_tokens is None:
-            global_tokens = ep.world * B
+            global_tokens = self.global_tokens if ep.world > 1 else B
         if B > self.max_tokens:
             raise ValueError(f"{B} tokens > max_tokens {self.max_tokens}")
         s = ops._stream(ep.device)

@@ -447,18 +447,50 @@ def _to_2d(a, name: str):
     return a
 
 
+def _array_fingerprint(a):
+    """Identity + content fingerprint of one weight stack.
+
+    The reference re-reads (and re-validates) the weight arrays on every call
+    (``pipeline.py:585-589``), so a cached device copy is reused only while
+    the arrays are unchanged: torch tensors by storage pointer and version
+    counter (bumped by every in-place op); numpy arrays by pointer, shape and
+    a checksum of their bytes (two wrap-around 64-bit reductions, read at
+    memory bandwidth — small next to the upload it saves).
+    """
+    if isinstance(a, torch.Tensor):
+        return ("t", a.data_ptr(), tuple(a.shape), str(a.dtype), a._version)
+    arr = np.asarray(a)
+    if not arr.flags.c_contiguous:
+        arr = np.ascontiguousarray(arr)
+    raw = arr.reshape(-1).view(np.uint8)
+    n8 = raw.size // 8 * 8
+    words = raw[:n8].view(np.uint64)
+    tail = bytes(raw[n8:])
+    s = int(np.add.reduce(words, dtype=np.uint64)) if words.size else 0
+    x = int(np.bitwise_xor.reduce(words)) if words.size else 0
+    return ("n", arr.__array_interface__["data"][0], arr.shape, arr.dtype.str, s, x, tail)
+
+
+def _weights_fingerprint(weights):
+    if isinstance(weights, DeviceExpertWeights):
+        return ("dev", id(weights))
+    return tuple(_array_fingerprint(getattr(weights, n)) for n in ("gate", "up", "down"))
+
+
 def _layer_for(weights, config: ModelConfig, router_weight, batch: int) -> MoELayer:
     key = id(weights)
+    fp = _weights_fingerprint(weights)
     entry = _LAYER_CACHE.get(key)
     if entry is not None:
-        ref, layer = entry
-        if ref() is weights and layer.config == config and layer.max_tokens >= batch:
+        ref, layer, fp0 = entry
+        if ref() is weights and layer.config == config and layer.max_tokens >= batch and fp0 == fp:
             layer.set_router_weight(router_weight)
             return layer
+        _LAYER_CACHE.pop(key, None)  # stale: the arrays changed (or the config / batch bound)
     layer = MoELayer(config, weights, router_weight, max_tokens=max(batch, 1))
     if len(_LAYER_CACHE) >= _LAYER_CACHE_MAX:
         _LAYER_CACHE.pop(next(iter(_LAYER_CACHE)))
-    _LAYER_CACHE[key] = (weakref.ref(weights), layer)
+    _LAYER_CACHE[key] = (weakref.ref(weights), layer, fp)
     return layer
 
 
@@ -492,8 +524,12 @@ def moe_forward(tokens, router_weight, weights, config: ModelConfig,
         y = torch.zeros((0, config.hidden_dim), dtype=torch.float32, device=layer.device)
         return _finish(y, like_numpy), trace_from_counts(config, 0, np.zeros(config.num_experts, np.int64), params)
     y = layer.forward(x, fused=params.fused)
-    counts = layer.counts.cpu().numpy().astype(np.int64)
+    # one host synchronisation: the histogram copy is queued, then the flag
+    # read waits for the stream (NonFiniteInput as the reference raises it)
+    counts_h = torch.empty(config.num_experts, dtype=torch.int32, pin_memory=True)
+    counts_h.copy_(layer.counts, non_blocking=True)
     layer.raise_if_nonfinite()
+    counts = counts_h.numpy().astype(np.int64)
     trace = trace_from_counts(config, B, counts, params)
     return _finish(y, like_numpy), trace
 

@@ -30,3 +30,13 @@ def pytest_configure(config):
 def golden():
     data = np.load(GOLDEN_PATH, allow_pickle=False)
     return {k: data[k] for k in data.files}
+
+
+@pytest.fixture(autouse=True)
+def _reload_tuning_after_test():
+    """The library reads the MOE_B200_* hooks once / at workspace init; after a
+    test that monkeypatched them (restored before this teardown runs), re-read."""
+    yield
+    mod = sys.modules.get("paper_2605_23911_b200._lib")
+    if mod is not None and getattr(mod, "_lib", None) is not None:
+        mod.reload_tuning()
