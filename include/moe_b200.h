@@ -391,6 +391,10 @@ int moe_b200_swiglu(int64_t n, const float* gu, void* h, void* stream);
 int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws,
                         size_t ws_bytes, uint32_t* flags, void* stream);
 
+/* Record `event` (a cudaEvent_t) on `stream`; inside a stream capture it
+ * becomes an external event-record node (a timing point of every replay). */
+int moe_b200_record_event(void* event, void* stream);
+
 /* Re-read the MOE_B200_* tuning / test hooks from the environment.  They are
  * read once (first use) and at every moe_b200_workspace_init, never on the
  * forward path. */

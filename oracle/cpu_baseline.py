@@ -41,6 +41,38 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
+def _rows_worker(args):
+    lo, hi = args
+    s = _STATE
+    t0 = time.perf_counter()
+    res = O.moe_rows(s["tokens"][lo:hi], s["wr"], s["expert"], s["E"], s["k"], s["gating"],
+                     routing=None if s["routing"] is None else (s["routing"][0][lo:hi], s["routing"][1][lo:hi]))
+    return lo, res["y"], res["indices"], time.perf_counter() - t0
+
+
+def run_rows_sharded(tokens, wr, expert, num_experts, k, gating, procs=None, routing=None):
+    """``O.moe_rows`` over ``tokens`` sharded across forked workers; ``expert(e)``
+    returns expert e's fp32 stacks (shared with the workers through fork).
+    Returns ``(y, indices, wall_seconds, procs)``."""
+    procs = procs or host_cores()
+    B = tokens.shape[0]
+    procs = max(1, min(procs, B))
+    _STATE.update(tokens=tokens, wr=wr, expert=expert, E=num_experts, k=k, gating=gating, routing=routing)
+    bounds = np.linspace(0, B, procs + 1).astype(int)
+    jobs = [(int(bounds[i]), int(bounds[i + 1])) for i in range(procs) if bounds[i + 1] > bounds[i]]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(len(jobs)) as pool:
+        pool.map(_noop, range(len(jobs)))
+        t0 = time.perf_counter()
+        parts = pool.map(_rows_worker, jobs, chunksize=1)
+        wall = time.perf_counter() - t0
+    parts.sort(key=lambda p: p[0])
+    y = np.concatenate([p[1] for p in parts])
+    idx = np.concatenate([p[2] for p in parts])
+    _STATE.clear()
+    return y, idx, wall, len(jobs)
+
+
 def run_sharded(tokens, wr, gate, up, down, num_experts, k, gating, procs=None):
     """Oracle forward over ``tokens`` sharded across ``procs`` forked workers.
 

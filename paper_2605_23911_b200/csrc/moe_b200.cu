@@ -756,6 +756,12 @@ extern "C" {
 
 const char* moe_b200_version(void) { return "moe_b200 0.2.0 (sm_100a)"; }
 
+int moe_b200_record_event(void* event, void* stream) {
+  if (!event) return MOE_B200_ERR_INVALID_VALUE;
+  MOE_CUDA(record_event(static_cast<cudaEvent_t>(event), static_cast<cudaStream_t>(stream)));
+  return MOE_B200_OK;
+}
+
 int moe_b200_tuning_reload(void) {
   reload_tuning();
   return MOE_B200_OK;

@@ -269,6 +269,30 @@ class MoELayer:
         return r
 
 
+    STAGE_NAMES = ("route", "permute", "ffn", "combine")
+
+    def forward_events(self, x: torch.Tensor, out: torch.Tensor, events) -> torch.Tensor:
+        """The one-call forward with five CUDA events recorded between its
+        launches: [route | permute | fused FFN | combine].  No host
+        synchronisation; inside a CUDA-graph capture the events become
+        external event-record nodes, so a captured sequence of forwards
+        times each stage of every replayed step on the device."""
+        x, xdt = self._prep_x(x)
+        B = x.shape[0]
+        ydt = _lib.DTYPE_BF16 if out.dtype == torch.bfloat16 else _lib.DTYPE_F32
+        for e in events:
+            if not e.cuda_event:
+                e.record()  # materialise the underlying cudaEvent_t (re-recorded by the library)
+        arr = (ctypes.c_void_p * 5)(*[e.cuda_event for e in events])
+        self._keep_events = arr
+        rc = self.lib.moe_b200_forward_timed(
+            ctypes.byref(self.cfg), B, _ptr(x), xdt, _ptr(self.router_weight),
+            _ptr(self.weights.gate), _ptr(self.weights.up), _ptr(self.weights.down),
+            _ptr(out), ydt, _ptr(self.topk_idx), _ptr(self.topk_w), _ptr(self.counts), _ptr(self.offsets),
+            _ptr(self.fwd), _ptr(self.inv), _ptr(self.ws), self.ws_bytes, _stream_ptr(self.device), arr)
+        _lib.check(rc, "moe_b200_forward_timed")
+        return out
+
     def timed_forward(self, x: torch.Tensor, iters: int = 10, flush: torch.Tensor | None = None) -> dict:
         """Per-stage device time (ms, mean over ``iters``) of the REAL one-call forward:
         CUDA events recorded by the library between [route | permute | fused FFN | combine]."""

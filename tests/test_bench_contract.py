@@ -40,3 +40,18 @@ def test_reference_arm_nonzero_rank_is_silent():
     r = _run({"RANK": "1", "WORLD_SIZE": "2"})
     assert r.returncode == 0, r.stderr[-2000:]
     assert not [l for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+def test_gpus_n_without_torchrun_spawns_ranks_and_prints_one_line():
+    """`python bench.py --gpus 2` (no torchrun, no WORLD_SIZE) re-launches itself
+    under torch.distributed.run: one JSON line from rank 0 with n_gpus 2."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                            "MASTER_PORT")}
+    args = [sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--config", "small", "--tokens", "8",
+            "--steps", "1", "--warmup", "3"]
+    r = subprocess.run(args, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"

@@ -285,7 +285,7 @@ def test_stage_errors_match_reference(P):
 
 def test_numerics_helpers_bitexact(P):
     rng = np.random.default_rng(7)
-    x = np.concatenate([rng.standard_normal(100000) * 30, [0.0, -0.0, 1e4, -1e4, 88.7, -103.9, -104.0]]).astype(
+    x = np.concatenate([rng.standard_normal(99995) * 30, [0.0, -0.0, 1e4, -1e4, 88.7, -103.9, -104.0]]).astype(
         np.float32).reshape(-1, 7)
     bits_equal(P.sigmoid(x), O.sigmoid_f32(x))
     bits_equal(P.silu(x), O.silu_f32(x))
