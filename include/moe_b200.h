@@ -128,8 +128,11 @@ int moe_b200_down_scatter(const moe_b200_config* cfg, int64_t num_tokens, const 
 int moe_b200_combine(const moe_b200_config* cfg, int64_t num_tokens, const float* ys, void* y,
                      int y_dtype, void* stream);
 
-/* Whole layer (pipeline.py:572-615 `moe_forward`): route, permute, gate+up,
- * down+scatter, combine — five launches, no host synchronisation.
+/* Whole layer (pipeline.py:572-615 `moe_forward`): route, dispatch (histogram,
+ * offsets, stable permutation, schedule, gather), and ONE persistent FFN
+ * launch whose down epilogue also applies the routing weights and the
+ * deterministic unpermute-combine -- three launches (four with the exact
+ * router's weight prep), no host synchronisation.
  * Intermediates live in `ws`; routing outputs are written to the caller's
  * buffers so the host can build the trace lazily from `counts`. */
 int moe_b200_forward(const moe_b200_config* cfg, int64_t num_tokens, const void* x, int x_dtype,
@@ -394,6 +397,11 @@ int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws
 /* Record `event` (a cudaEvent_t) on `stream`; inside a stream capture it
  * becomes an external event-record node (a timing point of every replay). */
 int moe_b200_record_event(void* event, void* stream);
+
+/* 1 when the forward fuses the weighted unpermute-combine into the FFN's
+ * down epilogue (the default; MOE_B200_FUSED_COMBINE=0 restores the separate
+ * combine launch -- bit-identical). */
+int moe_b200_combine_fused(void);
 
 /* Re-read the MOE_B200_* tuning / test hooks from the environment.  They are
  * read once (first use) and at every moe_b200_workspace_init, never on the

@@ -141,7 +141,9 @@ combine_tiled_kernel(const float* __restrict__ ys, int splits, int n_dp, int T_p
     for (int j = 0; j < k; ++j) {
       const int x = t * k + j;
       const float w = __ldg(topk_w + x);
-      const size_t row = (size_t)__ldg(prow + x);
+      const int prow_x = __ldg(prow + x);
+      if (prow_x < 0) continue;  // dropped slot (out-of-range routing override)
+      const size_t row = (size_t)prow_x;
       float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int s = 0; s < splits; ++s) {
         const float* src = ys + ((size_t)s * n_dp * 2 + blk) * half_stride + row * 128 + col;
@@ -214,6 +216,7 @@ combine_token_kernel(const float* __restrict__ ys, int n_dp, int T_pad,
     for (int i = 0; i < kSlots; ++i) {
       if (i < ks && v < d / 4) {
         const int j = i / kS, s = i % kS;
+        if (s_row[j] < 0) { a[c][i] = make_float4(0.f, 0.f, 0.f, 0.f); continue; }  // dropped slot
         const float* src = ys + ((size_t)s * n_dp * 2 + blk) * half_stride + (size_t)s_row[j] * 128 + col;
         a[c][i] = __ldg(reinterpret_cast<const float4*>(src));
       }
@@ -226,7 +229,7 @@ combine_token_kernel(const float* __restrict__ ys, int n_dp, int T_pad,
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int j = 0; j < kMaxK; ++j) {
-      if (j < k) {
+      if (j < k && s_row[j] >= 0) {
         float4 g = a[c][j * kS];
 #pragma unroll
         for (int s = 1; s < kS; ++s) {

@@ -135,7 +135,7 @@ constexpr int kHdrBlk = 16 + kTbCap + kChunkCap;
 constexpr size_t kHeaderBytes = align256((16 + kTbCap + kChunkCap + kBlkCap) * sizeof(int32_t));
 
 struct Layout {
-  size_t logits, lbuf, gpart, w64, chunk_tab, prow, xp, h, ys, rt_idx, rt_w, rt_misc, gu32, total;
+  size_t tok_cnt, logits, lbuf, gpart, w64, chunk_tab, prow, xp, h, ys, rt_idx, rt_w, rt_misc, gu32, total;
   int max_chunks, splits, kb_per_split, T_pad, n_ft, n_dp;
 };
 
@@ -255,6 +255,9 @@ Layout layout_for(const moe_b200_config& c, int64_t B, int s_force = 0) {
   const size_t h_tiled = (size_t)L.n_ft * L.T_pad * kBM * 2;
   const size_t ys_tiled = (size_t)L.splits * L.n_dp * 2 * L.T_pad * kBM * sizeof(float);
   size_t off = kHeaderBytes;
+  // fused-combine arrival counters (B x d/256), right after the header at the
+  // same offset for every B: zeroed once by workspace_init, self-resetting
+  L.tok_cnt = off;   off = align256(off + (size_t)B * L.n_dp * sizeof(int32_t));
   L.logits = off;    off = align256(off + (size_t)B * c.num_experts * sizeof(float));
   L.lbuf = off;      off = align256(off + (size_t)B * c.num_experts * sizeof(float2));
   {
@@ -579,7 +582,7 @@ enum FfnMode { kFfnFused = 0, kFfnStaged = 1, kFfnUnfusedGU = 2, kFfnTiledDown =
 int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, const void* xp,
                const void* w_gate, const void* w_up, const void* w_down, void* h, float* ys,
                const float* topk_w, const int32_t* fwd, bool do_gu, bool do_dn, int mode,
-               cudaStream_t s, float* gu32 = nullptr) {
+               cudaStream_t s, float* gu32 = nullptr, void* y = nullptr, int y_dtype = MOE_B200_DTYPE_F32) {
   const bool fused = (mode != kFfnStaged);  // tiled padded-row layouts
   const int E = c.num_experts, d = c.hidden_dim, f = c.ffn_dim;
   const int64_t T = B * c.top_k;
@@ -622,6 +625,14 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.gu_done = hdr + kHdrGuDone;
   p.tiled = fused ? 1 : 0;
   p.T_pad = L.T_pad;
+  if (y && mode == kFfnFused && do_gu && do_dn) {
+    // the weighted combine fused into the down epilogue (no combine launch)
+    p.y = y;
+    p.y_bf16 = y_dtype == MOE_B200_DTYPE_BF16;
+    p.k = c.top_k;
+    p.tok_cnt = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + L.tok_cnt);
+    p.prow = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(ws) + L.prow);
+  }
   p.trace = g_ffn_trace;
   const int bn = chunk_rows_for(c, B);
   // CTA pairs for large token chunks, where token re-reads are a real share of
@@ -726,8 +737,14 @@ int launch_combine(const moe_b200_config& c, int64_t B, const Layout& L, void* w
 
 int launch_dispatch(const moe_b200_config& c, int64_t B, const void* x, int xb, const int32_t* topk_idx,
                     int32_t* counts, int32_t* offsets, int32_t* fwd, int32_t* inv, int32_t* prow, int4* chunk_tab,
-                    int32_t* n_chunks, void* xp, cudaStream_t s, uint32_t* flags = nullptr) {
+                    int32_t* n_chunks, void* xp, cudaStream_t s, uint32_t* flags = nullptr,
+                    int32_t* tok_cnt = nullptr, int splits = 1, void* y = nullptr, int y_dtype = 0) {
   DispatchParams q{};
+  q.tok_cnt = tok_cnt;
+  q.n_dp = (c.hidden_dim + 2 * kBM - 1) / (2 * kBM);
+  q.splits = splits;
+  q.y = y;
+  q.y_bf16 = y_dtype == MOE_B200_DTYPE_BF16;
   q.trace = g_dispatch_trace;
   q.flags = flags;
   q.topk_idx = topk_idx;
@@ -761,6 +778,8 @@ int moe_b200_record_event(void* event, void* stream) {
   MOE_CUDA(record_event(static_cast<cudaEvent_t>(event), static_cast<cudaStream_t>(stream)));
   return MOE_B200_OK;
 }
+
+int moe_b200_combine_fused(void) { return tuning().fused_combine != 0; }
 
 int moe_b200_tuning_reload(void) {
   reload_tuning();
@@ -825,7 +844,10 @@ int moe_b200_workspace_init(const moe_b200_config* cfg, int64_t max_tokens, void
   if (!ws || ws_bytes < kHeaderBytes) return MOE_B200_ERR_WORKSPACE;
   (void)max_tokens;
   reload_tuning();  // the MOE_B200_* hooks are read here, not on the forward path
-  MOE_CUDA(cudaMemsetAsync(ws, 0, kHeaderBytes, static_cast<cudaStream_t>(stream)));
+  const size_t zero = kHeaderBytes + align256((size_t)std::max<int64_t>(max_tokens, 1) *
+                                               ((cfg->hidden_dim + 2 * kBM - 1) / (2 * kBM)) * sizeof(int32_t));
+  if (ws_bytes < zero) return MOE_B200_ERR_WORKSPACE;
+  MOE_CUDA(cudaMemsetAsync(ws, 0, zero, static_cast<cudaStream_t>(stream)));
   return MOE_B200_OK;
 }
 
@@ -1008,9 +1030,11 @@ static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, in
   if (B == 0) return events ? mark(1) : MOE_B200_OK;
   if ((rc = mark(2))) return rc;
   if (L.max_chunks > kChunkCap) return MOE_B200_ERR_UNSUPPORTED;
+  const bool fuse_comb = !unfused && tuning().fused_combine != 0;
+  if (y_dtype != MOE_B200_DTYPE_F32 && y_dtype != MOE_B200_DTYPE_BF16) return MOE_B200_ERR_INVALID_VALUE;
   if (!unfused) {
     if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
-                         /*gu*/ true, /*dn*/ true, kFfnFused, s)))
+                         /*gu*/ true, /*dn*/ true, kFfnFused, s, nullptr, fuse_comb ? y : nullptr, y_dtype)))
       return rc;
   } else {
     // ablation (pipeline.py:316-370): gate and up GEMMs as separate tiles
@@ -1029,7 +1053,7 @@ static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, in
       return rc;
   }
   if ((rc = mark(3))) return rc;
-  if ((rc = launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s))) return rc;
+  if (!fuse_comb && (rc = launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s))) return rc;
   return mark(4);
 }
 
@@ -1084,14 +1108,17 @@ int moe_b200_forward_routed(const moe_b200_config* cfg, int64_t B, const void* x
   void* xp = ws8(ws) + L.xp;
   void* h = ws8(ws) + L.h;
   float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);
+  const bool fuse_comb = tuning().fused_combine != 0;
   if ((rc = launch_dispatch(*cfg, B, x, x_dtype == MOE_B200_DTYPE_BF16, topk_idx, counts, offsets, perm_fwd, perm_inv,
                             reinterpret_cast<int32_t*>(ws8(ws) + L.prow), reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab),
-                            hdr + 2, xp, s, reinterpret_cast<uint32_t*>(hdr))))
+                            hdr + 2, xp, s, reinterpret_cast<uint32_t*>(hdr),
+                            fuse_comb ? reinterpret_cast<int32_t*>(ws8(ws) + L.tok_cnt) : nullptr, L.splits, y,
+                            y_dtype)))
     return rc;
   if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
-                       /*gu*/ true, /*dn*/ true, kFfnFused, s)))
+                       /*gu*/ true, /*dn*/ true, kFfnFused, s, nullptr, fuse_comb ? y : nullptr, y_dtype)))
     return rc;
-  return launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s);
+  return fuse_comb ? MOE_B200_OK : launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s);
 }
 
 int moe_b200_forward_timed(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
@@ -1276,7 +1303,8 @@ int moe_b200_io_wait(moe_b200_io* io, void* event) {
 int moe_b200_launches_per_forward(const moe_b200_config* cfg, int64_t B) {
   if (check_config(cfg)) return -1;
   if (B <= 0) return 0;
-  return B <= seg_max_tokens(*cfg) ? 4 : 5;  // segment router | weight prep + exact router
+  // segment router | weight prep + exact router; dispatch; FFN (+ combine when not fused)
+  return (B <= seg_max_tokens(*cfg) ? 1 : 2) + 2 + (tuning().fused_combine ? 0 : 1);
 }
 
 int moe_b200_io_sync(moe_b200_io* io) {

@@ -334,8 +334,14 @@ class MoELayer:
         t = self.timed_forward(x, iters=iters, flush=flush)
         B = x.shape[0]
         counts = self.counts.cpu().numpy().astype(np.int64)
-        groups = {"route": (STAGE_ROUTER,), "permute": (STAGE_PERMUTE,),
-                  "ffn": (STAGE_GATE_UP, STAGE_DOWN), "combine": (STAGE_UNPERMUTE,)}
+        if self.lib.moe_b200_combine_fused():
+            # the weighted combine runs in the FFN launch's down epilogue
+            groups = {"route": (STAGE_ROUTER,), "permute": (STAGE_PERMUTE,),
+                      "ffn": (STAGE_GATE_UP, STAGE_DOWN, STAGE_UNPERMUTE)}
+            t.pop("combine", None)
+        else:
+            groups = {"route": (STAGE_ROUTER,), "permute": (STAGE_PERMUTE,),
+                      "ffn": (STAGE_GATE_UP, STAGE_DOWN), "combine": (STAGE_UNPERMUTE,)}
         kernels = {"route": "router (+ weight prep)", "permute": "dispatch (schedule + gather)",
                    "ffn": "fused gate+up / down", "combine": "combine"}
         out = []
