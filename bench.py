@@ -322,7 +322,9 @@ def ours_arm(args, cfg_name):
     out = torch.empty((B, d), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
     lib = _lib.load()
-    stream = torch.cuda.current_stream(dev).cuda_stream
+
+    def mark(ev):  # an event on the CURRENT stream (inside a capture: an external event-record node)
+        _lib.check(lib.moe_b200_record_event(ev.cuda_event, torch.cuda.current_stream(dev).cuda_stream), "record")
 
     # routing-skew workload (BASELINE configs[4]): the reference harness's Zipf
     # table (skew.synthesize_routing, rank r -> expert r, weights 1/k) replaces
@@ -345,13 +347,13 @@ def ours_arm(args, cfg_name):
             if fused:
                 layer.forward_events(x, out, ev)
             else:
-                _lib.check(lib.moe_b200_record_event(ev[0].cuda_event, stream), "record")
+                mark(ev[0])
                 layer.forward(x, out, fused=False)
-                _lib.check(lib.moe_b200_record_event(ev[4].cuda_event, stream), "record")
+                mark(ev[4])
         else:
-            _lib.check(lib.moe_b200_record_event(ev[0].cuda_event, stream), "record")
+            mark(ev[0])
             layer.forward_routed(x, routed, out)
-            _lib.check(lib.moe_b200_record_event(ev[4].cuda_event, stream), "record")
+            mark(ev[4])
 
     warm_ev = _events(torch, 5)
     for _ in range(max(3, args.warmup)):

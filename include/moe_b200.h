@@ -398,10 +398,11 @@ int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws
  * becomes an external event-record node (a timing point of every replay). */
 int moe_b200_record_event(void* event, void* stream);
 
-/* 1 when the forward fuses the weighted unpermute-combine into the FFN's
- * down epilogue (the default; MOE_B200_FUSED_COMBINE=0 restores the separate
- * combine launch -- bit-identical). */
-int moe_b200_combine_fused(void);
+/* 1 when a forward of num_tokens tokens fuses the weighted unpermute-combine
+ * into the FFN's down epilogue (the default while num_tokens * ceil(d / 256)
+ * <= 65536; MOE_B200_FUSED_COMBINE=0 restores the separate combine launch --
+ * bit-identical). */
+int moe_b200_combine_fused(const moe_b200_config* cfg, int64_t num_tokens);
 
 /* Re-read the MOE_B200_* tuning / test hooks from the environment.  They are
  * read once (first use) and at every moe_b200_workspace_init, never on the

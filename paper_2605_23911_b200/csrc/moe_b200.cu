@@ -132,12 +132,24 @@ constexpr int kBlkCap = 16384;    // max (token block x expert block) counters (
 constexpr int kHdrTb = 16;
 constexpr int kHdrGuDone = 16 + kTbCap;
 constexpr int kHdrBlk = 16 + kTbCap + kChunkCap;
-constexpr size_t kHeaderBytes = align256((16 + kTbCap + kChunkCap + kBlkCap) * sizeof(int32_t));
+// fused-combine arrival counters, (token, 256-column block); the combine is
+// fused when B * ceil(d / 256) <= kTokCntCap (every BASELINE config), else it
+// runs as its own launch
+constexpr int kTokCntCap = 64 * 1024;
+constexpr int kHdrTok = 16 + kTbCap + kChunkCap + kBlkCap;
+constexpr size_t kHeaderBytes = align256((16 + kTbCap + kChunkCap + kBlkCap + kTokCntCap) * sizeof(int32_t));
 
 struct Layout {
-  size_t tok_cnt, logits, lbuf, gpart, w64, chunk_tab, prow, xp, h, ys, rt_idx, rt_w, rt_misc, gu32, total;
+  size_t logits, lbuf, gpart, w64, chunk_tab, prow, xp, h, ys, rt_idx, rt_w, rt_misc, gu32, total;
   int max_chunks, splits, kb_per_split, T_pad, n_ft, n_dp;
 };
+
+// the weighted combine runs in the FFN's down epilogue (ffn.cuh) unless
+// MOE_B200_FUSED_COMBINE=0 or the batch exceeds the arrival-counter capacity
+bool combine_fusable(const moe_b200_config& c, int64_t B) {
+  const int64_t n_dp = (c.hidden_dim + 2 * kBM - 1) / (2 * kBM);
+  return tuning().fused_combine != 0 && B * n_dp <= kTokCntCap;
+}
 
 int chunk_rows_for(const moe_b200_config& c, int64_t B) {
   // Tokens per expert on average; big chunks keep one weight pass per expert
@@ -255,9 +267,6 @@ Layout layout_for(const moe_b200_config& c, int64_t B, int s_force = 0) {
   const size_t h_tiled = (size_t)L.n_ft * L.T_pad * kBM * 2;
   const size_t ys_tiled = (size_t)L.splits * L.n_dp * 2 * L.T_pad * kBM * sizeof(float);
   size_t off = kHeaderBytes;
-  // fused-combine arrival counters (B x d/256), right after the header at the
-  // same offset for every B: zeroed once by workspace_init, self-resetting
-  L.tok_cnt = off;   off = align256(off + (size_t)B * L.n_dp * sizeof(int32_t));
   L.logits = off;    off = align256(off + (size_t)B * c.num_experts * sizeof(float));
   L.lbuf = off;      off = align256(off + (size_t)B * c.num_experts * sizeof(float2));
   {
@@ -630,7 +639,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
     p.y = y;
     p.y_bf16 = y_dtype == MOE_B200_DTYPE_BF16;
     p.k = c.top_k;
-    p.tok_cnt = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + L.tok_cnt);
+    p.tok_cnt = reinterpret_cast<int32_t*>(ws) + kHdrTok;
     p.prow = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(ws) + L.prow);
   }
   p.trace = g_ffn_trace;
@@ -779,7 +788,10 @@ int moe_b200_record_event(void* event, void* stream) {
   return MOE_B200_OK;
 }
 
-int moe_b200_combine_fused(void) { return tuning().fused_combine != 0; }
+int moe_b200_combine_fused(const moe_b200_config* cfg, int64_t num_tokens) {
+  if (check_config(cfg)) return 0;
+  return combine_fusable(*cfg, num_tokens) ? 1 : 0;
+}
 
 int moe_b200_tuning_reload(void) {
   reload_tuning();
@@ -844,10 +856,7 @@ int moe_b200_workspace_init(const moe_b200_config* cfg, int64_t max_tokens, void
   if (!ws || ws_bytes < kHeaderBytes) return MOE_B200_ERR_WORKSPACE;
   (void)max_tokens;
   reload_tuning();  // the MOE_B200_* hooks are read here, not on the forward path
-  const size_t zero = kHeaderBytes + align256((size_t)std::max<int64_t>(max_tokens, 1) *
-                                               ((cfg->hidden_dim + 2 * kBM - 1) / (2 * kBM)) * sizeof(int32_t));
-  if (ws_bytes < zero) return MOE_B200_ERR_WORKSPACE;
-  MOE_CUDA(cudaMemsetAsync(ws, 0, zero, static_cast<cudaStream_t>(stream)));
+  MOE_CUDA(cudaMemsetAsync(ws, 0, kHeaderBytes, static_cast<cudaStream_t>(stream)));
   return MOE_B200_OK;
 }
 
@@ -1030,7 +1039,7 @@ static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, in
   if (B == 0) return events ? mark(1) : MOE_B200_OK;
   if ((rc = mark(2))) return rc;
   if (L.max_chunks > kChunkCap) return MOE_B200_ERR_UNSUPPORTED;
-  const bool fuse_comb = !unfused && tuning().fused_combine != 0;
+  const bool fuse_comb = !unfused && combine_fusable(*cfg, B);
   if (y_dtype != MOE_B200_DTYPE_F32 && y_dtype != MOE_B200_DTYPE_BF16) return MOE_B200_ERR_INVALID_VALUE;
   if (!unfused) {
     if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
@@ -1108,11 +1117,11 @@ int moe_b200_forward_routed(const moe_b200_config* cfg, int64_t B, const void* x
   void* xp = ws8(ws) + L.xp;
   void* h = ws8(ws) + L.h;
   float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);
-  const bool fuse_comb = tuning().fused_combine != 0;
+  const bool fuse_comb = combine_fusable(*cfg, B);
   if ((rc = launch_dispatch(*cfg, B, x, x_dtype == MOE_B200_DTYPE_BF16, topk_idx, counts, offsets, perm_fwd, perm_inv,
                             reinterpret_cast<int32_t*>(ws8(ws) + L.prow), reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab),
                             hdr + 2, xp, s, reinterpret_cast<uint32_t*>(hdr),
-                            fuse_comb ? reinterpret_cast<int32_t*>(ws8(ws) + L.tok_cnt) : nullptr, L.splits, y,
+                            fuse_comb ? reinterpret_cast<int32_t*>(ws) + kHdrTok : nullptr, L.splits, y,
                             y_dtype)))
     return rc;
   if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
@@ -1304,7 +1313,7 @@ int moe_b200_launches_per_forward(const moe_b200_config* cfg, int64_t B) {
   if (check_config(cfg)) return -1;
   if (B <= 0) return 0;
   // segment router | weight prep + exact router; dispatch; FFN (+ combine when not fused)
-  return (B <= seg_max_tokens(*cfg) ? 1 : 2) + 2 + (tuning().fused_combine ? 0 : 1);
+  return (B <= seg_max_tokens(*cfg) ? 1 : 2) + 2 + (combine_fusable(*cfg, B) ? 0 : 1);
 }
 
 int moe_b200_io_sync(moe_b200_io* io) {

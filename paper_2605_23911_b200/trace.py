@@ -217,3 +217,64 @@ def stage_bytes(stage: str, config: ModelConfig, batch: int, counts, element_byt
     if stage == STAGE_UNPERMUTE:
         return (total * d + total + batch * d) * eb + total * INDEX_BYTES
     raise ValueError(stage)
+
+
+# ---------------------------------------------------------------------------
+# Activation-traffic comparison of the fused and unfused gate+up
+# (perfmodel.py:70-96 TrafficSource / TrafficReport, :122-180), plus the
+# device-MEASURED source: DRAM bytes of the two variants' launches from ncu.
+# ---------------------------------------------------------------------------
+
+TRAFFIC_CLOSED_FORM = "closed_form"
+TRAFFIC_TILE_TRACE = "tile_trace"
+TRAFFIC_MEASURED = "measured"
+
+
+@dataclass(frozen=True)
+class TrafficReport:
+    """Fused vs unfused gate+up activation traffic (``perfmodel.py:88-96``)."""
+
+    unfused_bytes: int
+    fused_bytes: int
+    savings_bytes: int
+    savings_ratio: float
+    source: str
+
+
+def _report(unfused: int, fused: int, source: str) -> TrafficReport:
+    savings = unfused - fused
+    return TrafficReport(unfused_bytes=int(unfused), fused_bytes=int(fused), savings_bytes=int(savings),
+                         savings_ratio=savings / unfused if unfused else 0.0, source=source)
+
+
+def activation_traffic_closed_form(expanded_tokens: int, ffn_dim: int, hidden_dim: int,
+                                   element_bytes: int = 2) -> TrafficReport:
+    """``perfmodel.py:122-145``: unfused moves ``s(4TF + 2Td)``, fused ``s(TF + Td)``."""
+    t, f, d, s = int(expanded_tokens), int(ffn_dim), int(hidden_dim), int(element_bytes)
+    if min(t, f, d, s) < 0 or f == 0 or d == 0 or s == 0:
+        raise ValueError("dimensions must be positive (tokens may be zero)")
+    return _report(s * (4 * t * f + 2 * t * d), s * (t * f + t * d), TRAFFIC_CLOSED_FORM)
+
+
+def traffic_from_traces(fused_trace: "PipelineTrace", unfused_trace: "PipelineTrace") -> TrafficReport:
+    """``perfmodel.py:148-180``: the same comparison from two stage traces."""
+    gf = fused_trace.stage(STAGE_GATE_UP)
+    gu = unfused_trace.stage(STAGE_GATE_UP)
+    if "intermediate" not in gf.writes or "gate_out" in gf.writes:
+        raise ShapeMismatch("first trace is not from a fused run")
+    if "gate_out" not in gu.writes:
+        raise ShapeMismatch("second trace is not from an unfused run")
+    fused = gf.reads["input"] + gf.writes["intermediate"]
+    unfused = gu.reads["input"] + gu.reads["buffer"] + gu.writes["gate_out"] + gu.writes["up_out"]
+    return _report(unfused, fused, TRAFFIC_TILE_TRACE)
+
+
+def traffic_from_measured(fused_dram_bytes: float, unfused_dram_bytes: float,
+                          weight_bytes: float = 0.0) -> TrafficReport:
+    """The comparison with MEASURED bytes: ``ncu`` dram__bytes_read + write of
+    the fused gate+up launch(es) and of the unfused ones (the two projection
+    launches plus the activation pass), minus the expert-weight stream both
+    variants read once (``weight_bytes``, the same in both), so the report
+    covers activation traffic only, as the closed form does."""
+    return _report(round(unfused_dram_bytes - weight_bytes), round(fused_dram_bytes - weight_bytes),
+                   TRAFFIC_MEASURED)

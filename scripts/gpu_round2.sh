@@ -1,0 +1,30 @@
+#!/bin/bash
+# Round-2 measurement session (1 GPU): every BASELINE config through bench.py
+# (value, e2e, roofline from in-graph events, parity gate, CPU baseline), the
+# skew sweep, the fusion ablation, the reference arm, the ncu launch list and
+# one `ncu --set full` capture of the FFN per config (DRAM traffic -> traffic.json),
+# the fused-vs-unfused DRAM bytes (measured TrafficReport).
+TAG=${1:-r02}
+mkdir -p gpurun_out
+B="timeout 900 python bench.py"
+$B --steps 50 --warmup 5 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+$B --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2>> gpurun_out/bench_$TAG.err
+for c in qwen60 deepseek small; do $B --config $c --steps 20 --warmup 3 >> gpurun_out/bench_configs_$TAG.json 2>> gpurun_out/bench_$TAG.err; done
+for t in 1 2 4 8 32 128; do $B --config mixtral --tokens $t --steps 20 --warmup 3 >> gpurun_out/bench_configs_$TAG.json 2>> gpurun_out/bench_$TAG.err; done
+for a in 0 0.5 0.8 1.2 1.6 2.0; do $B --config skew64 --zipf $a --steps 20 --warmup 3 >> gpurun_out/bench_skew_$TAG.json 2>> gpurun_out/bench_$TAG.err; done
+for c in mixtral qwen60 skew64; do $B --config $c --unfused --steps 20 --warmup 3 --no-cpu >> gpurun_out/bench_unfused_$TAG.json 2>> gpurun_out/bench_$TAG.err; done
+timeout 900 python bench.py --gpus 2 --steps 10 --warmup 3 > gpurun_out/bench_ep2_$TAG.json 2> gpurun_out/bench_ep2_$TAG.err
+N="timeout 600 ncu --clock-control none"
+$N --metrics gpu__time_duration.sum --csv --log-file gpurun_out/launches_$TAG.csv python scripts/run_layer.py mixtral 512 3 > /dev/null 2>&1
+$N --metrics gpu__time_duration.sum --csv --log-file gpurun_out/launches_qwen60_$TAG.csv python scripts/run_layer.py qwen60 512 3 > /dev/null 2>&1
+for c in mixtral qwen60 deepseek skew64; do
+  $N --set full --import-source on -k regex:ffn_kernel -s 1 -c 1 -o gpurun_out/prof_ffn_${c}_$TAG -f python scripts/run_layer.py $c 512 2 > /dev/null 2>&1
+done
+for k in router_seg dispatch; do
+  $N --set full --import-source on -k regex:$k -s 1 -c 1 -o gpurun_out/prof_${k}_$TAG -f python scripts/run_layer.py mixtral 512 2 > /dev/null 2>&1
+done
+# fusion ablation: DRAM bytes of every launch of one fused and one unfused forward
+for v in fused unfused; do
+  $N --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv --log-file gpurun_out/ablation_${v}_$TAG.csv python scripts/run_layer.py mixtral 512 2 $v > /dev/null 2>&1
+done
+echo done

@@ -1,5 +1,6 @@
 """Minimal driver for ncu captures: build a layer of a BASELINE config and run
-N forwards (no timing).  Usage: python scripts/run_layer.py [config] [tokens] [iters]"""
+N forwards (no timing).
+Usage: python scripts/run_layer.py [config] [tokens] [iters] [fused|unfused]"""
 
 import os
 import sys
@@ -22,7 +23,8 @@ gate = (torch.randn((E * d, f), generator=gen, device="cuda") / d ** 0.5).to(tor
 up = (torch.randn((E * d, f), generator=gen, device="cuda") / d ** 0.5).to(torch.bfloat16)
 down = (torch.randn((E * f, d), generator=gen, device="cuda") / f ** 0.5).to(torch.bfloat16)
 layer = P.MoELayer(P.ModelConfig(E, k, d, f, P.Gating(gating)), P.ExpertWeights(gate, up, down), wr, max_tokens=B)
+fused = (sys.argv[4] if len(sys.argv) > 4 else "fused") != "unfused"
 for _ in range(iters):
-    layer.forward(x)
+    layer.forward(x, fused=fused)
 torch.cuda.synchronize()
 print("counts", layer.counts.tolist())

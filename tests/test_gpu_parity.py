@@ -8,6 +8,8 @@ reference's fp32 result (metric of moeperf/cli.py:733-737).
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -530,7 +532,7 @@ def test_device_trace_records(pkg):
     recs = layer.device_trace(torch.from_numpy(tokens).cuda(), iters=3, peak_gbs=6500.0, peak_tflops=1650.0)
     assert [r["launch"] for r in recs][2] == "fused gate+up / down"
     assert all(r["time_us"] > 0 and r["bytes"] > 0 for r in recs)
-    fused_comb = bool(layer.lib.moe_b200_combine_fused())
+    fused_comb = bool(layer.lib.moe_b200_combine_fused(ctypes.byref(layer.cfg), b))
     # 3 GEMMs + SiLU*up (+ the weighted combine, fused into the same launch) (perfmodel.py:196-213)
     assert recs[2]["flops"] == 6 * b * k * d * f + 5 * b * k * f + (2 * b * k * d if fused_comb else 0)
     assert len(recs) == (3 if fused_comb else 4)
@@ -813,7 +815,7 @@ def test_fused_combine_bit_identical_to_combine_launch(pkg, shape, ydt, monkeypa
     out_dtype = torch.bfloat16 if ydt == "bf16" else torch.float32
     layer = _layer(P, _cfg(P, e, k, d, f, g), wr, gate, up, down, b, out_dtype=out_dtype)
     x = torch.from_numpy(tokens).cuda()
-    assert layer.lib.moe_b200_combine_fused() == 1
+    assert layer.lib.moe_b200_combine_fused(ctypes.byref(layer.cfg), b) == 1
     y_fused = [_np(layer.forward(x).float()) for _ in range(3)]
     monkeypatch.setenv("MOE_B200_FUSED_COMBINE", "0")
     _lib.reload_tuning()

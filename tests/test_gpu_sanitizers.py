@@ -1,0 +1,42 @@
+"""compute-sanitizer (memcheck, racecheck, synccheck, initcheck) over every
+kernel on small shapes: the mbarrier rings, the DSMEM hand-offs and
+cta_group::2 barriers of the FFN, the self-resetting counters and the fused
+combine's last-arriver protocol, the stage kernels, and the peer-memory EP
+flags (one rank).  Each run must report zero errors."""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+@pytest.mark.parametrize("target", ["layer", "pairs", "stages", "ep"])
+def test_compute_sanitizer_clean(tool, target, tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not found")
+    log = tmp_path / "san.log"
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "9", "--log-file", str(log), "--kernel-name",
+           "kns=3moe", sys.executable, os.path.join(ROOT, "scripts", "sanitize_target.py"), target]
+    if tool == "initcheck":
+        cmd[1:1] = ["--track-unused-memory", "no"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1500)
+    text = log.read_text() if log.exists() else ""
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"sanitizer_{tool}_{target}.log"), "w") as fh:
+        fh.write(text + "\n--- stdout ---\n" + r.stdout[-4000:] + "\n--- stderr ---\n" + r.stderr[-4000:])
+    assert "sanitize target done" in r.stdout, r.stderr[-3000:]
+    assert r.returncode == 0, text[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in text, text[-4000:]
