@@ -129,10 +129,11 @@ int moe_b200_combine(const moe_b200_config* cfg, int64_t num_tokens, const float
                      int y_dtype, void* stream);
 
 /* Whole layer (pipeline.py:572-615 `moe_forward`): route, dispatch (histogram,
- * offsets, stable permutation, schedule, gather), and ONE persistent FFN
- * launch whose down epilogue also applies the routing weights and the
- * deterministic unpermute-combine -- three launches (four with the exact
- * router's weight prep), no host synchronisation.
+ * offsets, stable permutation, schedule, gather), ONE persistent FFN launch
+ * (gate+up and down), and the deterministic weighted unpermute-combine,
+ * overlapped with the FFN's tail (moe_b200_combine_overlapped) -- four
+ * launches (five with the exact router's weight prep), no host
+ * synchronisation.
  * Intermediates live in `ws`; routing outputs are written to the caller's
  * buffers so the host can build the trace lazily from `counts`. */
 int moe_b200_forward(const moe_b200_config* cfg, int64_t num_tokens, const void* x, int x_dtype,
@@ -398,11 +399,14 @@ int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws
  * becomes an external event-record node (a timing point of every replay). */
 int moe_b200_record_event(void* event, void* stream);
 
-/* 1 when a forward of num_tokens tokens fuses the weighted unpermute-combine
- * into the FFN's down epilogue (the default while num_tokens * ceil(d / 256)
- * <= 65536; MOE_B200_FUSED_COMBINE=0 restores the separate combine launch --
- * bit-identical). */
-int moe_b200_combine_fused(const moe_b200_config* cfg, int64_t num_tokens);
+/* 1 when a forward of num_tokens tokens overlaps the weighted
+ * unpermute-combine with the FFN's tail: the FFN's down epilogue publishes
+ * per-(token, 256-column block) arrivals and the combine grid, launched behind
+ * it with programmatic dependent launch, combines each token as soon as its
+ * partial rows are in (default while num_tokens * ceil(d / 256) <= 65536 and
+ * the down K split is <= 4; MOE_B200_FUSED_COMBINE=0 runs the combine after
+ * the FFN -- bit-identical either way). */
+int moe_b200_combine_overlapped(const moe_b200_config* cfg, int64_t num_tokens);
 
 /* Re-read the MOE_B200_* tuning / test hooks from the environment.  They are
  * read once (first use) and at every moe_b200_workspace_init, never on the

@@ -248,8 +248,8 @@ def moe_forward(tokens, router_weight, gate, up, down, num_experts, k, gating,
 
     ``routing`` optionally overrides ``(indices, weights)`` (the paper's
     routing-override for the skew sweep); ``ffn`` optionally
-    replaces the gate_up/down pair with a faster exact implementation of the
-    same arithmetic (the C restatement in ``oracle/c``).
+    replaces the gate_up/down pair with another implementation of the same
+    arithmetic, ``ffn(permuted, offsets) -> (h, expert_out)``.
     """
     tokens = np.ascontiguousarray(np.asarray(tokens, dtype=F32))
     d = tokens.shape[1]

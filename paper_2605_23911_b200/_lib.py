@@ -114,7 +114,7 @@ SIGNATURES = {
     "moe_b200_io_sync": (_INT, [_P]),
     "moe_b200_tuning_reload": (_INT, []),
     "moe_b200_record_event": (_INT, [_P, _P]),
-    "moe_b200_combine_fused": (_INT, [_CFG, _I64]),
+    "moe_b200_combine_overlapped": (_INT, [_CFG, _I64]),
     "moe_b200_gate_scores": (_INT, [_I64, _INT, _INT, _P, _P, _P, _P]),
     "moe_b200_topk_select": (_INT, [_I64, _INT, _INT, _INT, _P, _P, _P, _P]),
     "moe_b200_sigmoid": (_INT, [_I64, _P, _P, _INT, _P]),

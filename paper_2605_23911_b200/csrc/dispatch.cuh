@@ -38,11 +38,10 @@ struct DispatchParams {
   int2* chunk_grp;          // {first chunk of the expert, chunks of the expert}
   int32_t* n_chunks;        // [1]
   uint32_t* flags;          // bit 4: an index outside [0, E) (row dropped)
-  // fused combine (ffn.cuh): a dropped row pre-arrives on its token's
-  // counters, and a token whose every slot is dropped gets y = 0 here
+  // overlapped combine (elementwise.cuh combine_flag_kernel): a dropped row
+  // pre-arrives on its token's counters with its S splits
   int32_t* tok_cnt;         // (B, n_dp) or null
-  int n_dp, splits, y_bf16;
-  void* y;
+  int n_dp, splits;
   unsigned long long* trace;  // debug: 16 u64 per CTA (globaltimer start, clock64 phase deltas)
 };
 
@@ -233,18 +232,9 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
       p.inv[i] = -1;
       p.prow[i] = -1;
       s_pos[lane] = -1;
-      if (p.tok_cnt) {
+      if (p.tok_cnt) {  // the overlapped combine counts this slot's S partials as arrived
         const int t = i / p.k;
-        for (int mt = 0; mt < p.n_dp; ++mt) {
-          int32_t* ctr = p.tok_cnt + (size_t)t * p.n_dp + mt;
-          if (atomicAdd(ctr, p.splits) == (p.k - 1) * p.splits) {  // every slot of t dropped
-            *ctr = 0;
-            for (int c = mt * 256; c < min(p.d, mt * 256 + 256); ++c) {
-              if (p.y_bf16) static_cast<__nv_bfloat16*>(p.y)[(size_t)t * p.d + c] = __float2bfloat16_rn(0.0f);
-              else static_cast<float*>(p.y)[(size_t)t * p.d + c] = 0.0f;
-            }
-          }
-        }
+        for (int mt = 0; mt < p.n_dp; ++mt) atomicAdd(p.tok_cnt + (size_t)t * p.n_dp + mt, p.splits);
       }
     }
   }

@@ -257,6 +257,98 @@ combine_token_kernel(const float* __restrict__ ys, int n_dp, int T_pad,
   }
 }
 
+// The combine overlapped with the FFN's tail: combine_token_kernel's
+// arithmetic (identical bits), but launched right behind the FFN with
+// programmatic dependent launch and WITHOUT griddepcontrol.wait -- its CTAs
+// start on SMs the persistent FFN grid releases and each spins (acquire) on
+// the arrival counters of its token's 256-column blocks (ffn.cuh
+// FfnParams::arrive) until all k * S partial rows are in, then combines and
+// resets the counters.  The FFN's last down tiles and this grid overlap, so
+// only the last tokens' combine is exposed after the FFN.
+template <bool kBf16Out, int kS, int kNV>
+__global__ void __launch_bounds__(kRowThreads)
+combine_flag_kernel(const float* __restrict__ ys, int n_dp, int T_pad, const int32_t* __restrict__ prow,
+                    const float* __restrict__ topk_w, void* __restrict__ y, int B, int k, int d,
+                    int32_t* __restrict__ arrive, int S) {
+  __shared__ int32_t s_row[kCombineMaxKS];
+  __shared__ float s_w[kCombineMaxKS];
+  const int t = blockIdx.x;
+  const int c_lo = blockIdx.y * kRowThreads * kNV * 4;                // first column of this CTA
+  const int mt_lo = c_lo / 256, mt_hi = min(n_dp, (c_lo + kRowThreads * kNV * 4 + 255) / 256);
+  const int target = k * S;
+  if (threadIdx.x < mt_hi - mt_lo) {
+    const int32_t* a = arrive + (size_t)t * n_dp + mt_lo + threadIdx.x;
+    int v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+      if (v >= target) break;
+      __nanosleep(128);
+    }
+  }
+  if (threadIdx.x < k) {
+    s_row[threadIdx.x] = __ldcg(prow + (size_t)t * k + threadIdx.x);
+    s_w[threadIdx.x] = __ldcg(topk_w + (size_t)t * k + threadIdx.x);
+  }
+  __syncthreads();
+  const size_t half_stride = (size_t)T_pad * 128;
+  constexpr int kSlots = kCombineMaxKS / kNV;
+  constexpr int kMaxK = kSlots / kS;
+  const int ks = k * kS;
+  const int v0 = blockIdx.y * kRowThreads * kNV + threadIdx.x;
+  float4 a[kNV][kSlots];
+#pragma unroll
+  for (int c = 0; c < kNV; ++c) {
+    const int v = v0 + c * kRowThreads;
+    const int feat = v * 4;
+    const size_t blk = (size_t)(feat >> 8) * 2 + ((feat >> 7) & 1);
+    const int col = feat & 127;
+#pragma unroll
+    for (int i = 0; i < kSlots; ++i) {
+      if (i < ks && v < d / 4) {
+        const int j = i / kS, s = i % kS;
+        if (s_row[j] < 0) { a[c][i] = make_float4(0.f, 0.f, 0.f, 0.f); continue; }
+        const float* src = ys + ((size_t)s * n_dp * 2 + blk) * half_stride + (size_t)s_row[j] * 128 + col;
+        a[c][i] = __ldcg(reinterpret_cast<const float4*>(src));
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kNV; ++c) {
+    const int v = v0 + c * kRowThreads;
+    if (v >= d / 4) continue;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+      if (j < k && s_row[j] >= 0) {
+        float4 g = a[c][j * kS];
+#pragma unroll
+        for (int s = 1; s < kS; ++s) {
+          const float4 b = a[c][j * kS + s];
+          g.x = __fadd_rn(g.x, b.x); g.y = __fadd_rn(g.y, b.y);
+          g.z = __fadd_rn(g.z, b.z); g.w = __fadd_rn(g.w, b.w);
+        }
+        const float w = s_w[j];
+        acc.x = __fadd_rn(acc.x, __fmul_rn(w, g.x));
+        acc.y = __fadd_rn(acc.y, __fmul_rn(w, g.y));
+        acc.z = __fadd_rn(acc.z, __fmul_rn(w, g.z));
+        acc.w = __fadd_rn(acc.w, __fmul_rn(w, g.w));
+      }
+    }
+    if (kBf16Out) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y);
+      __nv_bfloat162 p1 = __floats2bfloat162_rn(acc.z, acc.w);
+      uint2 o;
+      o.x = *reinterpret_cast<uint32_t*>(&p0);
+      o.y = *reinterpret_cast<uint32_t*>(&p1);
+      reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(y) + (size_t)t * d)[v] = o;
+    } else {
+      reinterpret_cast<float4*>(static_cast<float*>(y) + (size_t)t * d)[v] = acc;
+    }
+  }
+  __syncthreads();  // every partial of this CTA's blocks is read: reset their counters
+  if (threadIdx.x < mt_hi - mt_lo) arrive[(size_t)t * n_dp + mt_lo + threadIdx.x] = 0;
+}
+
 // Unfused ablation (pipeline.py:316-370 unfused_gate_up): the separate
 // activation pass h = bf16(silu(g) * u) over the tiled fp32 projections
 // [proj][f/128][T_pad][128] -> tiled bf16 h [f/128][T_pad][128], with the

@@ -70,54 +70,15 @@ struct FfnParams {
   int tiled;                 // 1: h / ys in the tiled padded-row layouts (fused forward)
   int T_pad;                 // padded-row capacity of the tiled layouts
   unsigned long long* trace; // optional (debug): 8 u64 per tile {sm, fetch, first load, epi done, epi start, mma start}
-  // Fused weighted combine (pipeline.py:373-399) in the down epilogue.  y !=
-  // null: every down tile's epilogue group, once its K-split partials are
-  // globally visible, arrives on tok_cnt[t][mt] for each of its rows; the
-  // k * splits-th arrival for (token t, 256-column block mt) sums that
-  // block's partials in split order and the slots in ascending j from +0
-  // (the reference's out += w_j * g_j) and writes y -- no combine launch.
-  void* y;                   // (B, d) fp32 or bf16 layer output
-  int y_bf16;
+  // Overlapped combine (elementwise.cuh combine_flag_kernel): arrive != null:
+  // once a down tile's K-split partial rows are globally visible, its
+  // epilogue adds 1 to arrive[t][mt] for every row (token t = expanded id / k,
+  // mt its 256-column block); the combine grid, launched behind this one with
+  // programmatic dependent launch, starts on the SMs this grid releases and
+  // combines each (token, block) as soon as its k * splits arrivals are in.
+  int32_t* arrive;           // (B, n_mt_dn) arrival counters, reset by the combine
   int k;                     // top-k: slot j of token t is expanded id t * k + j
-  int32_t* tok_cnt;          // (B, n_mt_dn) arrival counters, self-resetting
-  const int32_t* prow;       // (B * k) expanded id -> padded permuted row (-1: dropped slot)
 };
-
-// y[t, d0 + 4 * lane .. + 3] = sum_j fl(w[t, j] * (sum_s P_s[prow(t, j)])), ascending j
-// and s, fp32 from +0: the fused down epilogue's combine of one 128-column half
-// block of one token (one warp, one float4 per lane).
-MOE_DEVICE void combine_token_half(const FfnParams& p, int t, int blk, int col, int d0) {
-  const size_t half_stride = (size_t)p.T_pad * 128;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int j = 0; j < p.k; ++j) {
-    const int x = t * p.k + j;
-    const int row = p.prow[x];
-    if (row < 0) continue;  // dropped slot (out-of-range routing override)
-    const float w = p.topk_w[x];
-    const float* src = p.ys + (size_t)blk * half_stride + (size_t)row * 128 + col;
-    float4 g = __ldcg(reinterpret_cast<const float4*>(src));
-    for (int s = 1; s < p.splits; ++s) {
-      const float4 b = __ldcg(reinterpret_cast<const float4*>(src + (size_t)s * p.n_mt_dn * 2 * half_stride));
-      g.x = __fadd_rn(g.x, b.x); g.y = __fadd_rn(g.y, b.y);
-      g.z = __fadd_rn(g.z, b.z); g.w = __fadd_rn(g.w, b.w);
-    }
-    acc.x = __fadd_rn(acc.x, __fmul_rn(w, g.x));
-    acc.y = __fadd_rn(acc.y, __fmul_rn(w, g.y));
-    acc.z = __fadd_rn(acc.z, __fmul_rn(w, g.z));
-    acc.w = __fadd_rn(acc.w, __fmul_rn(w, g.w));
-  }
-  const size_t o = (size_t)t * p.d + d0 + col;
-  if (p.y_bf16) {
-    __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x, acc.y);
-    __nv_bfloat162 p1 = __floats2bfloat162_rn(acc.z, acc.w);
-    uint2 v;
-    v.x = *reinterpret_cast<uint32_t*>(&p0);
-    v.y = *reinterpret_cast<uint32_t*>(&p1);
-    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.y) + o) = v;
-  } else {
-    *reinterpret_cast<float4*>(static_cast<float*>(p.y) + o) = acc;
-  }
-}
 
 MOE_DEVICE unsigned long long globaltimer() {
   unsigned long long t;
@@ -336,7 +297,9 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
   auto sched_read = [&](int slot, uint32_t sphase, bool release_lane, bool warp_sync) -> int {
     if (kPair && rank == 1) mbar_wait_cluster(sched_full + slot, sphase);
     else mbar_wait(sched_full + slot, sphase);
-    const int t = sched_tile[slot];
+    // (the mbarrier pair orders the slot; the shared atomics also make that
+    // visible to compute-sanitizer racecheck, which does not model mbarriers)
+    const int t = atomicAdd(sched_tile + slot, 0);
     if (warp_sync) __syncwarp();
     if (release_lane) {
       if (kPair && rank == 1) mbar_arrive_cluster(r_sched_empty0 + slot * 8);
@@ -376,7 +339,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           }
           const int v = tile < total_tiles ? tile : -1;
           mbar_wait(sched_empty + slot, sphase ^ 1);
-          sched_tile[slot] = v;
+          atomicExch(sched_tile + slot, v);
           if constexpr (kPair) {  // hand the pair tile to rank 1 through DSMEM
             st_cluster_u32(r_sched_tile1 + slot * 4, static_cast<uint32_t>(v));
             mbar_arrive_cluster(r_sched_full1 + slot * 8);
@@ -694,6 +657,15 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       } else {
         // down tile: two 128-row halves; 32-row chunks alternate between the groups
         const int nq = (ch.z + 31) / 32;
+        // overlapped combine: tokens of this group's rows (lane: row q * 32 + lane
+        // of each of the group's chunks q), loaded now, used after the stores
+        constexpr int kRowsPerLane = kBN / 32 / kEpiGroups;
+        int arr_tok[kRowsPerLane];
+#pragma unroll
+        for (int i = 0; i < kRowsPerLane; ++i) {
+          const int c = (grp + kEpiGroups * i) * 32 + lane;
+          arr_tok[i] = (p.arrive && wq == 0 && c < ch.z) ? __ldg(p.fwd + ch.y + c) / p.k : -1;
+        }
         const int my_last = (nq - 1 - grp) >= 0 ? (nq - 1 - ((nq - 1 - grp) % kEpiGroups)) : -1;
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
@@ -742,35 +714,19 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         }
         if (my_last < 0) release_tmem();  // this group had no chunk: still release TMEM
         if (issuer) bulk_wait_all();
-        if (p.y && p.tiled) {
-          // ---- fused combine (off the TMEM critical path: the accumulator is released)
-          // this group's partial rows are complete: publish them to generic loads
-          if (issuer) fence_proxy_async_global();
-          int32_t* lcnt = reinterpret_cast<int32_t*>(stg_g);  // staging buffer: its bulk reads are done
-          int32_t* list = lcnt + 1;
-          if (wq == 0 && lane == 0) *lcnt = 0;
-          epi_bar_sync(grp);
-          __threadfence();
-          // one row per thread: chunk q = 2 wq + grp holds rows q*32 .. q*32+31
-          const int c = (2 * wq + grp) * 32 + lane;
-          if (c < ch.z) {
-            const int t = __ldg(p.fwd + ch.y + c) / p.k;
-            int32_t* ctr = p.tok_cnt + (size_t)t * p.n_mt_dn + ti.mt;
-            if (atomicAdd(ctr, 1) == p.k * p.splits - 1) {  // every slot x split of (t, mt) is written
-              *ctr = 0;                                    // self-reset for the next launch
-              list[atomicAdd(lcnt, 1)] = t;
-            }
+        if (p.arrive && p.tiled && wq == 0) {
+          // publish this group's partial rows to the overlapped combine: the
+          // issuer (lane 0) waited for its bulk writes above; proxy + gpu
+          // fences, then one relaxed arrival per row (the fence orders them)
+          if (lane == 0) {
+            fence_proxy_async_global();
+            __threadfence();
           }
-          epi_bar_sync(grp);
-          __threadfence();
-          const int n_last = *lcnt;
-          for (int it = wq; it < 2 * n_last; it += 4) {  // (token, half) items, one warp each
-            const int half = it & 1;
-            const int d0 = ti.mt * 2 * kBM + half * kBM;
-            if (d0 + lane * 4 < p.d)
-              combine_token_half(p, list[it >> 1], ti.mt * 2 + half, lane * 4, d0);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < kRowsPerLane; ++i) {
+            if (arr_tok[i] >= 0) atomicAdd(p.arrive + (size_t)arr_tok[i] * p.n_mt_dn + ti.mt, 1);
           }
-          epi_bar_sync(grp);  // the staging buffer is reused by the next tile
         }
       }
       if (p.trace && warp == 4 && lane == 0) p.trace[tile * 8 + 3] = globaltimer();

@@ -132,9 +132,9 @@ constexpr int kBlkCap = 16384;    // max (token block x expert block) counters (
 constexpr int kHdrTb = 16;
 constexpr int kHdrGuDone = 16 + kTbCap;
 constexpr int kHdrBlk = 16 + kTbCap + kChunkCap;
-// fused-combine arrival counters, (token, 256-column block); the combine is
-// fused when B * ceil(d / 256) <= kTokCntCap (every BASELINE config), else it
-// runs as its own launch
+// arrival counters of the combine overlapped with the FFN tail, (token,
+// 256-column block); overlapped while B * ceil(d / 256) <= kTokCntCap (every
+// BASELINE config), else the combine simply runs after the FFN
 constexpr int kTokCntCap = 64 * 1024;
 constexpr int kHdrTok = 16 + kTbCap + kChunkCap + kBlkCap;
 constexpr size_t kHeaderBytes = align256((16 + kTbCap + kChunkCap + kBlkCap + kTokCntCap) * sizeof(int32_t));
@@ -143,13 +143,6 @@ struct Layout {
   size_t logits, lbuf, gpart, w64, chunk_tab, prow, xp, h, ys, rt_idx, rt_w, rt_misc, gu32, total;
   int max_chunks, splits, kb_per_split, T_pad, n_ft, n_dp;
 };
-
-// the weighted combine runs in the FFN's down epilogue (ffn.cuh) unless
-// MOE_B200_FUSED_COMBINE=0 or the batch exceeds the arrival-counter capacity
-bool combine_fusable(const moe_b200_config& c, int64_t B) {
-  const int64_t n_dp = (c.hidden_dim + 2 * kBM - 1) / (2 * kBM);
-  return tuning().fused_combine != 0 && B * n_dp <= kTokCntCap;
-}
 
 int chunk_rows_for(const moe_b200_config& c, int64_t B) {
   // Tokens per expert on average; big chunks keep one weight pass per expert
@@ -195,6 +188,19 @@ void down_splits(const moe_b200_config& c, int64_t B, int* splits, int* kb_per_s
   int kps = (nkb + s - 1) / s;
   *kb_per_split = kps;
   *splits = (nkb + kps - 1) / kps;
+}
+
+// The combine runs overlapped with the FFN's tail (combine_flag_kernel behind
+// the FFN with programmatic dependent launch, driven by per-(token, block)
+// arrival counters) unless MOE_B200_FUSED_COMBINE=0, the batch exceeds the
+// counter capacity, or the K split is outside the combine kernels' register
+// budget (then the combine launches after the FFN as before; same bits).
+bool combine_overlapped(const moe_b200_config& c, int64_t B) {
+  const int64_t n_dp = (c.hidden_dim + 2 * kBM - 1) / (2 * kBM);
+  if (tuning().fused_combine == 0 || B < 1 || B * n_dp > kTokCntCap) return false;
+  int S = 0, kps = 0;
+  down_splits(c, B, &S, &kps);
+  return S <= 4 && c.top_k * S <= kCombineMaxKS;
 }
 
 // ---- segment (certified split-K) router plan --------------------------------
@@ -591,7 +597,7 @@ enum FfnMode { kFfnFused = 0, kFfnStaged = 1, kFfnUnfusedGU = 2, kFfnTiledDown =
 int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, const void* xp,
                const void* w_gate, const void* w_up, const void* w_down, void* h, float* ys,
                const float* topk_w, const int32_t* fwd, bool do_gu, bool do_dn, int mode,
-               cudaStream_t s, float* gu32 = nullptr, void* y = nullptr, int y_dtype = MOE_B200_DTYPE_F32) {
+               cudaStream_t s, float* gu32 = nullptr, int32_t* arrive = nullptr) {
   const bool fused = (mode != kFfnStaged);  // tiled padded-row layouts
   const int E = c.num_experts, d = c.hidden_dim, f = c.ffn_dim;
   const int64_t T = B * c.top_k;
@@ -634,13 +640,11 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.gu_done = hdr + kHdrGuDone;
   p.tiled = fused ? 1 : 0;
   p.T_pad = L.T_pad;
-  if (y && mode == kFfnFused && do_gu && do_dn) {
-    // the weighted combine fused into the down epilogue (no combine launch)
-    p.y = y;
-    p.y_bf16 = y_dtype == MOE_B200_DTYPE_BF16;
+  if (arrive && mode == kFfnFused && do_gu && do_dn) {
+    // the down epilogue publishes per-(token, block) arrivals for the combine
+    // grid that runs overlapped with this grid's tail
+    p.arrive = arrive;
     p.k = c.top_k;
-    p.tok_cnt = reinterpret_cast<int32_t*>(ws) + kHdrTok;
-    p.prow = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(ws) + L.prow);
   }
   p.trace = g_ffn_trace;
   const int bn = chunk_rows_for(c, B);
@@ -709,7 +713,7 @@ int launch_router_exact(const moe_b200_config& c, int64_t B, const void* x, int 
 
 
 int launch_combine(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, const float* topk_w, void* y,
-                   int y_dtype, cudaStream_t s) {
+                   int y_dtype, cudaStream_t s, int32_t* arrive = nullptr) {
   if (y_dtype != MOE_B200_DTYPE_F32 && y_dtype != MOE_B200_DTYPE_BF16) return MOE_B200_ERR_INVALID_VALUE;
   const int d = c.hidden_dim, k = c.top_k;
   const float* ys = reinterpret_cast<const float*>(ws8(ws) + L.ys);
@@ -717,7 +721,27 @@ int launch_combine(const moe_b200_config& c, int64_t B, const Layout& L, void* w
   const bool bf = y_dtype == MOE_B200_DTYPE_BF16;
   const int S = L.splits;
   cudaError_t e;
-  if (S <= 4 && k * S <= kCombineMaxKS) {
+  if (arrive) {
+    // overlapped with the FFN's tail: programmatic dependent launch, the
+    // CTAs wait on the FFN's per-(token, block) arrival counters
+    using K = void (*)(const float*, int, int, const int32_t*, const float*, void*, int, int, int, int32_t*, int);
+    const bool wide = k * S <= kCombineMaxKS / 4;
+    K kern;
+#define MOE_COMBINE_PICK(SS)                                                                   \
+  kern = wide ? (bf ? combine_flag_kernel<true, SS, 4> : combine_flag_kernel<false, SS, 4>) \
+              : (bf ? combine_flag_kernel<true, SS, 1> : combine_flag_kernel<false, SS, 1>)
+    switch (S) {
+      case 1: MOE_COMBINE_PICK(1); break;
+      case 2: MOE_COMBINE_PICK(2); break;
+      case 3: MOE_COMBINE_PICK(3); break;
+      default: MOE_COMBINE_PICK(4); break;
+    }
+#undef MOE_COMBINE_PICK
+    const int nv = wide ? 4 : 1;
+    const unsigned col_blocks = (unsigned)((d / 4 + kRowThreads * nv - 1) / (kRowThreads * nv));
+    e = launch_pdl_if(true, kern, dim3((unsigned)B, col_blocks), dim3(kRowThreads), 0, s, ys, L.n_dp, L.T_pad, prow,
+                      topk_w, y, (int)B, k, d, arrive, S);
+  } else if (S <= 4 && k * S <= kCombineMaxKS) {
     using K = void (*)(const float*, int, int, const int32_t*, const float*, void*, int, int, int);
     const bool wide = k * S <= kCombineMaxKS / 4;  // 4 columns per thread
     K kern;
@@ -747,13 +771,11 @@ int launch_combine(const moe_b200_config& c, int64_t B, const Layout& L, void* w
 int launch_dispatch(const moe_b200_config& c, int64_t B, const void* x, int xb, const int32_t* topk_idx,
                     int32_t* counts, int32_t* offsets, int32_t* fwd, int32_t* inv, int32_t* prow, int4* chunk_tab,
                     int32_t* n_chunks, void* xp, cudaStream_t s, uint32_t* flags = nullptr,
-                    int32_t* tok_cnt = nullptr, int splits = 1, void* y = nullptr, int y_dtype = 0) {
+                    int32_t* tok_cnt = nullptr, int splits = 1) {
   DispatchParams q{};
   q.tok_cnt = tok_cnt;
   q.n_dp = (c.hidden_dim + 2 * kBM - 1) / (2 * kBM);
   q.splits = splits;
-  q.y = y;
-  q.y_bf16 = y_dtype == MOE_B200_DTYPE_BF16;
   q.trace = g_dispatch_trace;
   q.flags = flags;
   q.topk_idx = topk_idx;
@@ -788,9 +810,9 @@ int moe_b200_record_event(void* event, void* stream) {
   return MOE_B200_OK;
 }
 
-int moe_b200_combine_fused(const moe_b200_config* cfg, int64_t num_tokens) {
+int moe_b200_combine_overlapped(const moe_b200_config* cfg, int64_t num_tokens) {
   if (check_config(cfg)) return 0;
-  return combine_fusable(*cfg, num_tokens) ? 1 : 0;
+  return combine_overlapped(*cfg, num_tokens) ? 1 : 0;
 }
 
 int moe_b200_tuning_reload(void) {
@@ -1039,11 +1061,12 @@ static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, in
   if (B == 0) return events ? mark(1) : MOE_B200_OK;
   if ((rc = mark(2))) return rc;
   if (L.max_chunks > kChunkCap) return MOE_B200_ERR_UNSUPPORTED;
-  const bool fuse_comb = !unfused && combine_fusable(*cfg, B);
+  const bool overlap = !unfused && combine_overlapped(*cfg, B);
+  int32_t* arrive = overlap ? reinterpret_cast<int32_t*>(ws) + kHdrTok : nullptr;
   if (y_dtype != MOE_B200_DTYPE_F32 && y_dtype != MOE_B200_DTYPE_BF16) return MOE_B200_ERR_INVALID_VALUE;
   if (!unfused) {
     if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
-                         /*gu*/ true, /*dn*/ true, kFfnFused, s, nullptr, fuse_comb ? y : nullptr, y_dtype)))
+                         /*gu*/ true, /*dn*/ true, kFfnFused, s, nullptr, arrive)))
       return rc;
   } else {
     // ablation (pipeline.py:316-370): gate and up GEMMs as separate tiles
@@ -1061,8 +1084,15 @@ static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, in
                          /*gu*/ false, /*dn*/ true, kFfnTiledDown, s)))
       return rc;
   }
-  if ((rc = mark(3))) return rc;
-  if (!fuse_comb && (rc = launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s))) return rc;
+  if (overlap) {
+    // no event between the FFN and the overlapped combine (it would serialise
+    // them): the "ffn" interval covers both, the "combine" one is empty
+    if ((rc = launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s, arrive))) return rc;
+    if ((rc = mark(3))) return rc;
+  } else {
+    if ((rc = mark(3))) return rc;
+    if ((rc = launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s))) return rc;
+  }
   return mark(4);
 }
 
@@ -1117,17 +1147,17 @@ int moe_b200_forward_routed(const moe_b200_config* cfg, int64_t B, const void* x
   void* xp = ws8(ws) + L.xp;
   void* h = ws8(ws) + L.h;
   float* ys = reinterpret_cast<float*>(ws8(ws) + L.ys);
-  const bool fuse_comb = combine_fusable(*cfg, B);
+  const bool overlap = combine_overlapped(*cfg, B);
+  int32_t* arrive = overlap ? reinterpret_cast<int32_t*>(ws) + kHdrTok : nullptr;
   if ((rc = launch_dispatch(*cfg, B, x, x_dtype == MOE_B200_DTYPE_BF16, topk_idx, counts, offsets, perm_fwd, perm_inv,
                             reinterpret_cast<int32_t*>(ws8(ws) + L.prow), reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab),
                             hdr + 2, xp, s, reinterpret_cast<uint32_t*>(hdr),
-                            fuse_comb ? reinterpret_cast<int32_t*>(ws) + kHdrTok : nullptr, L.splits, y,
-                            y_dtype)))
+                            arrive, L.splits)))
     return rc;
   if ((rc = launch_ffn(*cfg, B, L, ws, xp, w_gate, w_up, w_down, h, ys, topk_w, perm_fwd,
-                       /*gu*/ true, /*dn*/ true, kFfnFused, s, nullptr, fuse_comb ? y : nullptr, y_dtype)))
+                       /*gu*/ true, /*dn*/ true, kFfnFused, s, nullptr, arrive)))
     return rc;
-  return fuse_comb ? MOE_B200_OK : launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s);
+  return launch_combine(*cfg, B, L, ws, topk_w, y, y_dtype, s, arrive);
 }
 
 int moe_b200_forward_timed(const moe_b200_config* cfg, int64_t B, const void* x, int x_dtype,
@@ -1313,7 +1343,7 @@ int moe_b200_launches_per_forward(const moe_b200_config* cfg, int64_t B) {
   if (check_config(cfg)) return -1;
   if (B <= 0) return 0;
   // segment router | weight prep + exact router; dispatch; FFN (+ combine when not fused)
-  return (B <= seg_max_tokens(*cfg) ? 1 : 2) + 2 + (combine_fusable(*cfg, B) ? 0 : 1);
+  return (B <= seg_max_tokens(*cfg) ? 1 : 2) + 3;  // (+ router weight prep) router, dispatch, FFN, combine
 }
 
 int moe_b200_io_sync(moe_b200_io* io) {

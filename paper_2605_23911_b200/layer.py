@@ -334,7 +334,7 @@ class MoELayer:
         t = self.timed_forward(x, iters=iters, flush=flush)
         B = x.shape[0]
         counts = self.counts.cpu().numpy().astype(np.int64)
-        if self.lib.moe_b200_combine_fused(ctypes.byref(self.cfg), B):
+        if self.lib.moe_b200_combine_overlapped(ctypes.byref(self.cfg), B):
             # the weighted combine runs in the FFN launch's down epilogue
             groups = {"route": (STAGE_ROUTER,), "permute": (STAGE_PERMUTE,),
                       "ffn": (STAGE_GATE_UP, STAGE_DOWN, STAGE_UNPERMUTE)}

@@ -532,8 +532,8 @@ def test_device_trace_records(pkg):
     recs = layer.device_trace(torch.from_numpy(tokens).cuda(), iters=3, peak_gbs=6500.0, peak_tflops=1650.0)
     assert [r["launch"] for r in recs][2] == "fused gate+up / down"
     assert all(r["time_us"] > 0 and r["bytes"] > 0 for r in recs)
-    fused_comb = bool(layer.lib.moe_b200_combine_fused(ctypes.byref(layer.cfg), b))
-    # 3 GEMMs + SiLU*up (+ the weighted combine, fused into the same launch) (perfmodel.py:196-213)
+    fused_comb = bool(layer.lib.moe_b200_combine_overlapped(ctypes.byref(layer.cfg), b))
+    # 3 GEMMs + SiLU*up (+ the weighted combine, overlapped with the FFN's tail) (perfmodel.py:196-213)
     assert recs[2]["flops"] == 6 * b * k * d * f + 5 * b * k * f + (2 * b * k * d if fused_comb else 0)
     assert len(recs) == (3 if fused_comb else 4)
 
@@ -792,22 +792,25 @@ def test_throughput_router_tiles_bitexact(pkg, tile, monkeypatch):
 
 
 # ---------------------------------------------------------------------------
-# the weighted unpermute-combine fused into the FFN's down epilogue
+# the weighted unpermute-combine overlapped with the FFN's tail (arrival
+# counters published by the down epilogue, combine grid behind the FFN with
+# programmatic dependent launch)
 # ---------------------------------------------------------------------------
 
 @pytest.mark.parametrize("shape", [
     (8, 2, 512, 1024, 512, "softmax"),             # 256-row chunks, cta_group::2 pairs, S = 1
-    (8, 2, 1024, 2048, 4, "softmax"),              # tiny batch: K split S > 1
+    (8, 2, 1024, 2048, 4, "softmax"),              # tiny batch: K split S = 5 (> 4: combine after the FFN)
+    (8, 2, 1024, 2048, 16, "softmax"),             # S = 2..4, overlapped
     (16, 4, 384, 512, 100, "sigmoid_normalized"),  # d = 384: a half-empty last 256-column block
     (256, 8, 264, 256, 64, "sigmoid_normalized"),  # d = 264: a 8-column tail; k = 8
     (60, 4, 256, 176, 96, "softmax"),
 ])
 @pytest.mark.parametrize("ydt", ["f32", "bf16"])
-def test_fused_combine_bit_identical_to_combine_launch(pkg, shape, ydt, monkeypatch):
-    """The combine in the down epilogue (per-(token, 256-column block)
-    last-arriver, split order then slot order from +0) gives exactly the bits
-    of the separate combine launch (MOE_B200_FUSED_COMBINE=0), repeatedly
-    (self-resetting counters), and matches the oracle."""
+def test_overlapped_combine_bit_identical_to_combine_launch(pkg, shape, ydt, monkeypatch):
+    """The combine overlapped with the FFN tail (per-(token, 256-column block)
+    arrival counters, split order then slot order from +0) gives exactly the
+    bits of the combine launched after the FFN (MOE_B200_FUSED_COMBINE=0),
+    repeatedly (self-resetting counters), and matches the oracle."""
     P = pkg
     from paper_2605_23911_b200 import _lib
     e, k, d, f, b, g = shape
@@ -815,18 +818,21 @@ def test_fused_combine_bit_identical_to_combine_launch(pkg, shape, ydt, monkeypa
     out_dtype = torch.bfloat16 if ydt == "bf16" else torch.float32
     layer = _layer(P, _cfg(P, e, k, d, f, g), wr, gate, up, down, b, out_dtype=out_dtype)
     x = torch.from_numpy(tokens).cuda()
-    assert layer.lib.moe_b200_combine_fused(ctypes.byref(layer.cfg), b) == 1
-    y_fused = [_np(layer.forward(x).float()) for _ in range(3)]
+    s = ctypes.c_int(0)
+    layer.lib.moe_b200_down_splits(ctypes.byref(layer.cfg), b, ctypes.byref(s))
+    assert layer.lib.moe_b200_combine_overlapped(ctypes.byref(layer.cfg), b) == int(s.value <= 4)
+    y_ov = [_np(layer.forward(x).float()) for _ in range(3)]
     monkeypatch.setenv("MOE_B200_FUSED_COMBINE", "0")
     _lib.reload_tuning()
+    assert layer.lib.moe_b200_combine_overlapped(ctypes.byref(layer.cfg), b) == 0
     y_sep = _np(layer.forward(x).float())
     monkeypatch.delenv("MOE_B200_FUSED_COMBINE")
     _lib.reload_tuning()
-    for y in y_fused:
+    for y in y_ov:
         bits_equal(y, y_sep)
     if b * d * f <= 6e7:
         ref = O.moe_forward(tokens, wr, gate, up, down, e, k, g)["y"]
-        assert O.max_rel_error(y_fused[0], ref) <= TOL
+        assert O.max_rel_error(y_ov[0], ref) <= TOL
     # a smaller batch through the same workspace afterwards
     bits_equal(_np(layer.forward(x[: max(1, b // 3)]).float()), _fresh_y(P, e, k, d, f, g, wr, gate, up, down,
                                                                           tokens[: max(1, b // 3)], out_dtype))
@@ -837,10 +843,10 @@ def _fresh_y(P, e, k, d, f, g, wr, gate, up, down, tokens, out_dtype):
     return _np(layer.forward(torch.from_numpy(tokens).cuda()).float())
 
 
-def test_fused_combine_routed_with_dropped_slots(pkg, monkeypatch):
+def test_overlapped_combine_routed_with_dropped_slots(pkg, monkeypatch):
     """Routing override with out-of-range indices: the dropped slots are left
     out of their tokens' sums (a token with every slot dropped gets y = 0),
-    identically with the fused and the separate combine, and flagged."""
+    identically with the overlapped and the trailing combine, and flagged."""
     P = pkg
     from paper_2605_23911_b200 import _lib
     e, k, d, f, b = 8, 2, 512, 512, 40

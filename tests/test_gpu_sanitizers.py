@@ -30,8 +30,6 @@ def test_compute_sanitizer_clean(tool, target, tmp_path):
     log = tmp_path / "san.log"
     cmd = [SAN, "--tool", tool, "--error-exitcode", "9", "--log-file", str(log), "--kernel-name",
            "kns=3moe", sys.executable, os.path.join(ROOT, "scripts", "sanitize_target.py"), target]
-    if tool == "initcheck":
-        cmd[1:1] = ["--track-unused-memory", "no"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1500)
     text = log.read_text() if log.exists() else ""
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
