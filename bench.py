@@ -37,6 +37,7 @@ per step, same metric/config; under torchrun only rank 0 runs it.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import socket
@@ -285,7 +286,8 @@ def ours_arm(args, cfg_name):
 
     import paper_2605_23911_b200 as P
     from paper_2605_23911_b200 import _lib
-    from paper_2605_23911_b200.trace import DEVICE_STAGES, STAGE_DOWN, STAGE_GATE_UP, stage_bytes, stage_flops
+    from paper_2605_23911_b200.trace import (DEVICE_STAGES, STAGE_DOWN, STAGE_GATE_UP, STAGE_UNPERMUTE, stage_bytes,
+                                             stage_flops)
 
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
@@ -371,18 +373,40 @@ def ours_arm(args, cfg_name):
                f"no flush: inputs larger than L2 (streamed expert weights {streamed / 1e9:.2f} GB/step >= 16x the "
                f"126 MB L2)")
 
-    # K forwards captured as one CUDA graph; every step records its stage
-    # events as external event-record nodes (timed in the replay regime)
+    # Two CUDA graphs of K captured forwards each.  `timed`: the forwards as
+    # they run in production (plus, when L2 is flushed between steps, one
+    # event pair per step to exclude the flush); `staged`: every forward also
+    # records its stage events as external event-record nodes -- the stage
+    # times (and the dominant kernel's roofline) in the same back-to-back
+    # regime.  value comes from `timed`; `stage_sum_ms` from `staged` shows the
+    # cost of the extra event nodes.
     K = args.steps
     evs = [_events(torch, 5) for _ in range(K)]
+    tev = [_events(torch, 2) for _ in range(K)]
     torch.cuda.synchronize(dev)
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
+
+    def plain(i):
+        if flush_between:
+            flush.zero_()
+            mark(tev[i][0])
+        if routed is None:
+            layer.forward(x, out, fused=fused)
+        else:
+            layer.forward_routed(x, routed, out)
+        if flush_between:
+            mark(tev[i][1])
+
+    g_timed, g_staged = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_timed):
+        for i in range(K):
+            plain(i)
+    with torch.cuda.graph(g_staged):
         for i in range(K):
             if flush_between:
                 flush.zero_()
             step(evs[i])
-    graph.replay()
+    g_timed.replay()
+    g_staged.replay()
     torch.cuda.synchronize(dev)
 
     sampler = ClockSampler(local % ndev)
@@ -390,24 +414,26 @@ def ours_arm(args, cfg_name):
     # keep the GPU busy ~1 s so the clock samples see the timed region's state
     t_end = time.time() + 1.0
     while time.time() < t_end:
-        graph.replay()
+        g_timed.replay()
         torch.cuda.synchronize(dev)
     t0, t1 = _events(torch, 2)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     t0.record()
-    graph.replay()
+    g_timed.replay()
     t1.record()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    g_staged.replay()  # the stage breakdown, right after (same regime)
+    torch.cuda.synchronize(dev)
     clocks = sampler.stop()
     step_ms = [evs[i][0].elapsed_time(evs[i][4]) for i in range(K)]
     if flush_between:
-        total_ms = sum(step_ms)
+        total_ms = sum(tev[i][0].elapsed_time(tev[i][1]) for i in range(K))
         timing_desc = ("one CUDA-graph replay of K captured one-call C-ABI forwards (each preceded by an L2 "
-                       "flush); device time summed over the steps' own events (flushes excluded)")
+                       "flush); device time summed over each step's event pair (flushes excluded)")
     else:
         total_ms = t0.elapsed_time(t1)
         timing_desc = "CUDA events around one CUDA-graph replay of K back-to-back captured one-call C-ABI forwards"
@@ -441,9 +467,18 @@ def ours_arm(args, cfg_name):
                  + stage_bytes(STAGE_DOWN, cfg, B, counts, element_bytes=2))
     tot_b = sum(stage_bytes(s, cfg, B, counts, element_bytes=2) for s in DEVICE_STAGES)
     tot_f = sum(stage_flops(s, cfg, B) for s in DEVICE_STAGES)
-    if "ffn" in stages:
+    overlapped = bool(lib.moe_b200_combine_overlapped(ctypes.byref(layer.cfg), B))
+    if "ffn" in stages and overlapped:
+        # the "ffn" interval spans the FFN and the combine overlapped with its tail
+        kern_ms = stages["ffn"]
+        kern_bytes = ffn_bytes + stage_bytes(STAGE_UNPERMUTE, cfg, B, counts, element_bytes=2)
+        kern_name = ("ffn_kernel (fused gate+up SiLU*up and K-split down, one persistent launch) + the "
+                     "weighted combine overlapped with its tail (combine_flag_kernel)")
+        bytes_model = ("perfmodel.stage_bytes(GateUp)+stage_bytes(Down)+stage_bytes(Unpermute), element_bytes=2, "
+                       "actual histogram")
+    elif "ffn" in stages:
         kern_ms, kern_bytes = stages["ffn"], ffn_bytes
-        kern_name = "ffn_kernel (fused gate+up SiLU*up, K-split down and weighted combine: one persistent launch)"
+        kern_name = "ffn_kernel (fused gate+up SiLU*up and K-split down, one persistent launch)"
         bytes_model = "perfmodel.stage_bytes(GateUp)+stage_bytes(Down), element_bytes=2, actual histogram"
     else:
         kern_ms, kern_bytes = stages["step"], tot_b

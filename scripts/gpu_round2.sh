@@ -27,4 +27,8 @@ done
 for v in fused unfused; do
   $N --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv --log-file gpurun_out/ablation_${v}_$TAG.csv python scripts/run_layer.py mixtral 512 2 $v > /dev/null 2>&1
 done
+
+# per-tile FFN timelines and the segment router's per-CTA phase timeline
+for c in mixtral qwen60 deepseek; do timeout 300 python scripts/ffn_timeline.py $c ${c}_$TAG > /dev/null 2>&1; done
+for c in mixtral qwen60; do timeout 300 python scripts/router_seg_timeline.py $c >> gpurun_out/router_timeline_$TAG.log 2>&1; done
 echo done
