@@ -352,6 +352,12 @@ int moe_b200_topk_select(int64_t num_tokens, int num_experts, int k, int gating,
  * elementwise over n fp32 values, bit-exact with numpy's float32 path. */
 int moe_b200_sigmoid(int64_t n, const float* x, float* y, int silu, void* stream);
 
+/* numpy's float64 exp as the softmax computes it (router.py:65, :82:
+ * np.exp on float64; on AVX-512 hosts numpy dispatches to SVML's
+ * __svml_exp8_ha, which this reproduces bit for bit for |x| < 707.7; beyond,
+ * x < 0 gives +0 -- see router.cuh np_exp64).  Elementwise over n doubles. */
+int moe_b200_np_exp64(int64_t n, const double* x, double* y, void* stream);
+
 /* linalg.py:45-68 `dense_matmul`: c (m, n) = a (m, K) @ b (K, n), fp32 in and
  * out, exact fp64 products folded in ascending K (bit-exact). */
 int moe_b200_dense_matmul(int64_t m, int64_t K, int64_t n, const float* a, const float* b, float* c,

@@ -119,6 +119,7 @@ SIGNATURES = {
     "moe_b200_topk_select": (_INT, [_I64, _INT, _INT, _INT, _P, _P, _P, _P]),
     "moe_b200_sigmoid": (_INT, [_I64, _P, _P, _INT, _P]),
     "moe_b200_dense_matmul": (_INT, [_I64, _I64, _I64, _P, _P, _P, _P]),
+    "moe_b200_np_exp64": (_INT, [_I64, _P, _P, _P]),
     "moe_b200_schedule": (_INT, [_CFG, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "moe_b200_permute_rows": (_INT, [_I64, _I64, _P, _P, _INT, _P, _P]),
     "moe_b200_cast_bf16": (_INT, [_I64, _P, _P, _P]),

@@ -1678,6 +1678,15 @@ int moe_b200_sigmoid(int64_t n, const float* x, float* y, int silu, void* stream
   return MOE_B200_OK;
 }
 
+int moe_b200_np_exp64(int64_t n, const double* x, double* y, void* stream) {
+  if (n < 0) return MOE_B200_ERR_INVALID_VALUE;
+  if (n == 0) return MOE_B200_OK;
+  if (!x || !y) return MOE_B200_ERR_INVALID_VALUE;
+  np_exp64_kernel<<<stage_grid(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(x, y, n);
+  MOE_LAUNCH_CHECK("np_exp64_kernel");
+  return MOE_B200_OK;
+}
+
 int moe_b200_dense_matmul(int64_t m, int64_t K, int64_t n, const float* a, const float* b, float* c, void* stream) {
   if (m < 0 || K < 0 || n < 0 || m > INT32_MAX || K > INT32_MAX || n > INT32_MAX) return MOE_B200_ERR_INVALID_VALUE;
   if (m == 0 || n == 0) return MOE_B200_OK;

@@ -149,6 +149,57 @@ MOE_DEVICE float np_expf(float x) {
   return __double2float_rn(static_cast<double>(p) * __longlong_as_double(qe));
 }
 
+// numpy's float64 exp on x86-64 with AVX-512 (SIMD dispatch to Intel SVML's
+// __svml_exp8_ha, vendored in numpy), reconstructed from its machine code and
+// constant tables and checked bit-exact against np.exp on every float32 input
+// in (-707.70, 0] (tests/test_gpu_stage_api.py, on the box's own numpy).
+// Tang-style: n = RZ(x / ln2 * 16) with a shifter, j = n mod 16, r = x - n ln2/16
+// (two-part ln2), degree-6 polynomial, 2^(j/16) as top + tail, scalef by
+// floor(n / 16).  The softmax (router.py:78-83) only ever feeds it
+// s = fp32(l - max) <= 0; for s <= -707.70 (SVML's separate rare path) it
+// returns +0: such terms (< 2^-1000) never change the pairwise sum (which
+// holds exp(0) = 1) nor their own fp32 score (0) -- the softmax's bits are
+// those of numpy either way.
+__device__ __constant__ uint64_t kNpExpTop[16] = {
+    0x3ff0000000000000ull, 0x3ff0b5586cf9890full, 0x3ff172b83c7d517bull, 0x3ff2387a6e756238ull,
+    0x3ff306fe0a31b715ull, 0x3ff3dea64c123422ull, 0x3ff4bfdad5362a27ull, 0x3ff5ab07dd485429ull,
+    0x3ff6a09e667f3bcdull, 0x3ff7a11473eb0187ull, 0x3ff8ace5422aa0dbull, 0x3ff9c49182a3f090ull,
+    0x3ffae89f995ad3adull, 0x3ffc199bdd85529cull, 0x3ffd5818dcfba487ull, 0x3ffea4afa2a490daull};
+__device__ __constant__ uint64_t kNpExpTail[16] = {
+    0x0000000000000000ull, 0x3c979aa65d837b6dull, 0xbc801b15eaa59348ull, 0x3c968efde3a8a894ull,
+    0x3c834d754db0abb6ull, 0x3c859f48a72a4c6dull, 0x3c7690cebb7aafb0ull, 0x3c9063e1e21c5409ull,
+    0xbc93b3efbf5e2228ull, 0xbc7b32dcb94da51dull, 0x3c8db72fc1f0eab4ull, 0x3c71affc2b91ce27ull,
+    0x3c8c1a7792cb3387ull, 0x3c736eae30af0cb3ull, 0x3c74a385a63d07a7ull, 0xbc8ff7128fd391f0ull};
+
+MOE_DEVICE double np_exp64(double x) {
+  if (!(fabs(x) < 707.7032713517042)) return x < 0.0 ? 0.0 : exp(x);  // (softmax: x <= 0 always)
+  const double inv_ln2 = __longlong_as_double(0x3ff71547652b82feLL);
+  const double shifter = __longlong_as_double(0x42f8000000003ff0LL);
+  const double ln2_hi = __longlong_as_double(0x3fe62e42fefa39efLL);
+  const double ln2_lo = __longlong_as_double(0x3c7abc9e3b39803fLL);
+  const double c6 = __longlong_as_double(0x3f57411836940c04LL), c5 = __longlong_as_double(0x3f81101cbbc265c0LL);
+  const double c4 = __longlong_as_double(0x3fa55557242d68feLL), c3 = __longlong_as_double(0x3fc5555553939732LL);
+  const double c2 = __longlong_as_double(0x3fe000000000d008LL), c1 = __longlong_as_double(0x3fefffffffffff70LL);
+  const double t = __fma_rz(x, inv_ln2, shifter);
+  const double n = __dsub_rn(t, shifter);
+  const int j = static_cast<int>(__double_as_longlong(t) & 15);
+  double r = __fma_rn(-n, ln2_hi, x);
+  r = __fma_rn(-ln2_lo, n, r);
+  r = __longlong_as_double(__double_as_longlong(r) & 0xbfffffffffffffffLL);
+  const double r2 = __dmul_rn(r, r);
+  double a = __fma_rn(c6, r, c5);
+  const double b = __fma_rn(c4, r, c3);
+  const double c = __fma_rn(c2, r, c1);
+  a = __fma_rn(r2, a, b);
+  a = __fma_rn(r2, a, c);
+  const double top = __longlong_as_double(static_cast<long long>(kNpExpTop[j]));
+  const double p = __fma_rn(a, r, __longlong_as_double(static_cast<long long>(kNpExpTail[j])));
+  const double res = __fma_rn(top, p, top);
+  // scalef(res, floor(n)): exact -- res * 2^m stays normal for |x| < 707.7
+  const int m = static_cast<int>(floor(n));
+  return __dmul_rn(res, __longlong_as_double(static_cast<long long>(m + 1023) << 52));
+}
+
 MOE_DEVICE float np_sigmoid(float x) {
   float t = np_expf(-fabsf(x));
   float den = __fadd_rn(1.0f, t);
@@ -446,7 +497,7 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
       for (int e = lane; e < p.E; e += 32) p.logits[(size_t)t * p.E + e] = lo[e];
     // ---- scores (lo is a representative: every candidate gives the same bits)
     if (p.gating == 0) {
-      for (int e = lane; e < p.E; e += 32) row[e] = exp(static_cast<double>(__fsub_rn(lo[e], m)));
+      for (int e = lane; e < p.E; e += 32) row[e] = np_exp64(static_cast<double>(__fsub_rn(lo[e], m)));
       __syncwarp();
       double S = 0.0;
       if (lane == 0) S = pairwise_sum<double>(row, p.E);

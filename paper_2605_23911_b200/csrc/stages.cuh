@@ -42,7 +42,7 @@ gate_scores_kernel(const float* __restrict__ logits, float* __restrict__ scores,
     if (gating == 0) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      for (int e = lane; e < E; e += 32) row[e] = exp(static_cast<double>(__fsub_rn(l[e], m)));
+      for (int e = lane; e < E; e += 32) row[e] = np_exp64(static_cast<double>(__fsub_rn(l[e], m)));
       __syncwarp();
       double S = 0.0;
       if (lane == 0) S = pairwise_sum<double>(row, E);
@@ -110,6 +110,14 @@ topk_select_kernel(const float* __restrict__ scores, int32_t* __restrict__ idx, 
     }
     __syncwarp();
   }
+}
+
+// numpy's float64 exp (np_exp64) over n values: the exhaustive check of the
+// port the softmax uses (tests/test_gpu_stage_api.py).
+__global__ void __launch_bounds__(256)
+np_exp64_kernel(const double* __restrict__ x, double* __restrict__ y, long long n) {
+  for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
+    y[i] = np_exp64(x[i]);
 }
 
 // linalg.py:71-86, elementwise, bit-exact with numpy's float32 arithmetic.

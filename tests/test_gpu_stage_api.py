@@ -321,6 +321,35 @@ def test_sigmoid_port_exhaustive(P):
                                      f"want {ref[bad[0]]!r}")
 
 
+def test_softmax_exp_port_exhaustive(P):
+    """The softmax's float64 exp (router.cuh np_exp64, the port of numpy's
+    SVML exp) against THIS box's np.exp on every float32 input the softmax
+    can feed it (s = fp32(l - max) in (-707.70, 0]; 1.13e9 values), bit for
+    bit.  (numpy picks its exp kernel per CPU at run time: the check runs
+    where the parity is claimed.)"""
+    from paper_2605_23911_b200 import _lib
+    lib = _lib.load()
+    hi = int(np.array([-707.70327], np.float32).view(np.uint32)[0])
+    chunk = 1 << 26
+    dev = torch.device("cuda")
+    total = 0
+    for c0 in range(0x80000000, hi + 1, chunk):
+        c1 = min(hi + 1, c0 + chunk)
+        x = np.arange(c0, c1, dtype=np.uint64).astype(np.uint32).view(np.float32).astype(np.float64)
+        x = x[np.abs(x) < 707.7032713517042]
+        xt = torch.from_numpy(x).to(dev)
+        yt = torch.empty_like(xt)
+        _lib.check(lib.moe_b200_np_exp64(x.size, xt.data_ptr(), yt.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                   "np_exp64")
+        y = yt.cpu().numpy()
+        ref = np.exp(x)
+        if not np.array_equal(y.view(np.uint64), ref.view(np.uint64)):
+            bad = np.nonzero(y.view(np.uint64) != ref.view(np.uint64))[0]
+            raise AssertionError(f"{bad.size} mismatches, first x={x[bad[0]]!r}: {y[bad[0]]!r} vs {ref[bad[0]]!r}")
+        total += x.size
+    assert total > 1_100_000_000
+
+
 # ---------------------------------------------------------------------------
 # the reference's edge cases through the FUSED router kernels (identity W_r)
 # ---------------------------------------------------------------------------
