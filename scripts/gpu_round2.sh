@@ -17,11 +17,16 @@ timeout 900 python bench.py --gpus 2 --steps 10 --warmup 3 > gpurun_out/bench_ep
 N="timeout 600 ncu --clock-control none"
 $N --metrics gpu__time_duration.sum --csv --log-file gpurun_out/launches_$TAG.csv python scripts/run_layer.py mixtral 512 3 > /dev/null 2>&1
 $N --metrics gpu__time_duration.sum --csv --log-file gpurun_out/launches_qwen60_$TAG.csv python scripts/run_layer.py qwen60 512 3 > /dev/null 2>&1
+# ncu --set full captures go to /tmp (each ~8 MB; gpurun brings back <= 64 MiB):
+# their raw metric pages come back as csv, and the Mixtral FFN report itself
 for c in mixtral qwen60 deepseek skew64; do
-  $N --set full --import-source on -k regex:ffn_kernel -s 1 -c 1 -o gpurun_out/prof_ffn_${c}_$TAG -f python scripts/run_layer.py $c 512 2 > /dev/null 2>&1
+  $N --set full --import-source on -k regex:ffn_kernel -s 1 -c 1 -o /tmp/prof_ffn_${c}_$TAG -f python scripts/run_layer.py $c 512 2 > /dev/null 2>&1
+  ncu -i /tmp/prof_ffn_${c}_$TAG.ncu-rep --page raw --csv > gpurun_out/prof_ffn_${c}_${TAG}_raw.csv 2>/dev/null
 done
-for k in router_seg dispatch; do
-  $N --set full --import-source on -k regex:$k -s 1 -c 1 -o gpurun_out/prof_${k}_$TAG -f python scripts/run_layer.py mixtral 512 2 > /dev/null 2>&1
+cp /tmp/prof_ffn_mixtral_$TAG.ncu-rep gpurun_out/ 2>/dev/null
+for k in router_seg dispatch combine_flag; do
+  $N --set full --import-source on -k regex:$k -s 1 -c 1 -o /tmp/prof_${k}_$TAG -f python scripts/run_layer.py mixtral 512 2 > /dev/null 2>&1
+  ncu -i /tmp/prof_${k}_$TAG.ncu-rep --page raw --csv > gpurun_out/prof_${k}_${TAG}_raw.csv 2>/dev/null
 done
 # fusion ablation: DRAM bytes of every launch of one fused and one unfused forward
 for v in fused unfused; do

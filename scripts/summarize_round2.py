@@ -123,12 +123,14 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__cycles_elapsed.avg.per_second", "launch__grid_size", "launch__registers_per_thread"]
 tfile = os.path.join(P, "traffic.json")
 traffic = json.load(open(tfile)) if os.path.exists(tfile) else {}
-for kern, cfg in [("ffn", c) for c in ("mixtral", "qwen60", "deepseek", "skew64")] + [("router_seg", None),
-                                                                                      ("dispatch", None)]:
-    rep = os.path.join(G, f"prof_{kern}_{cfg}_{tag}.ncu-rep" if cfg else f"prof_{kern}_{tag}.ncu-rep")
-    if not os.path.exists(rep):
+for kern, cfg in [("ffn", c) for c in ("mixtral", "qwen60", "deepseek", "skew64")] + [
+        ("router_seg", None), ("dispatch", None), ("combine_flag", None)]:
+    raw = os.path.join(G, f"prof_{kern}_{cfg}_{tag}_raw.csv" if cfg else f"prof_{kern}_{tag}_raw.csv")
+    if not os.path.exists(raw):
         continue
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    txt = open(raw).read()
+    with open(os.path.join(P, os.path.basename(raw)), "w") as fh:
+        fh.write(txt)
     rr = list(csv.reader(io.StringIO(txt)))
     if len(rr) < 3:
         continue
