@@ -489,7 +489,11 @@ def ours_arm(args, cfg_name):
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(f"{cfg_name}_{B}_ffn")
+            tj = json.load(open(tfile))
+            traffic = tj.get(f"{cfg_name}_{B}_ffn")
+            if traffic is not None and "ffn" in stages and overlapped:
+                comb = tj.get(f"{cfg_name}_{B}_combine")
+                traffic = traffic + comb if comb is not None else None
         except Exception:
             traffic = None
 

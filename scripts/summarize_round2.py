@@ -142,13 +142,13 @@ for kern, cfg in [("ffn", c) for c in ("mixtral", "qwen60", "deepseek", "skew64"
         for m in METRICS:
             if m in d:
                 out.append(f"  {m:70s} {d[m]:>16s} {units[h.index(m)]}")
-        if kern == "ffn":
+        if kern in ("ffn", "combine_flag"):
             try:
                 rd = float(d["dram__bytes_read.sum"].replace(",", "")) * SCALE.get(
                     units[h.index("dram__bytes_read.sum")], 1)
                 wrb = float(d["dram__bytes_write.sum"].replace(",", "")) * SCALE.get(
                     units[h.index("dram__bytes_write.sum")], 1)
-                traffic[f"{cfg}_512_ffn"] = rd + wrb
+                traffic[f"{cfg}_512_ffn" if kern == "ffn" else "mixtral_512_combine"] = rd + wrb
             except Exception:
                 pass
 json.dump(traffic, open(tfile, "w"), indent=1)
