@@ -77,6 +77,7 @@ struct Tuning {
   int force_exact = 0;       // MOE_B200_ROUTER_FORCE_EXACT
   int io_graphs = 1;         // MOE_B200_IO_GRAPHS
   int fused_combine = 1;     // MOE_B200_FUSED_COMBINE (0: separate combine launch)
+  int carveout = -1;         // MOE_B200_CARVEOUT: shared-memory carveout (%) of the small kernels
 };
 Tuning g_tune;
 std::mutex g_tune_mu;
@@ -102,6 +103,7 @@ void load_tuning_locked() {
   t.force_exact = geti("MOE_B200_ROUTER_FORCE_EXACT", 0);
   t.io_graphs = geti("MOE_B200_IO_GRAPHS", 1);
   t.fused_combine = geti("MOE_B200_FUSED_COMBINE", 1);
+  t.carveout = geti("MOE_B200_CARVEOUT", -1);
   g_tune = t;
   g_tune_loaded = true;
 }
@@ -432,6 +434,23 @@ cudaError_t ensure_dyn_smem(const void* kern, size_t bytes) {
   return e;
 }
 
+// Preferred shared-memory carveout of the small kernels (router, dispatch,
+// combine): the persistent FFN runs at the maximum carveout, so kernels that
+// ask for a different L1 / shared split make the SMs reconfigure at every
+// boundary.  MOE_B200_CARVEOUT (percent) sets it; once per (kernel, value).
+void apply_carveout(const void* kern) {
+  const int v = tuning().carveout;
+  if (v < 0) return;
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& d : done)
+    if (d.first == kern && d.second == v) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+  cudaGetLastError();
+  done.push_back({kern, v});
+}
+
 // ------------------------------- launches --------------------------------------
 // Launch with programmatic stream serialization (PDL) when MOE_B200_PDL=1:
 // the kernel may start while its predecessor finishes and calls pdl_wait()
@@ -739,6 +758,7 @@ int launch_combine(const moe_b200_config& c, int64_t B, const Layout& L, void* w
 #undef MOE_COMBINE_PICK
     const int nv = wide ? 4 : 1;
     const unsigned col_blocks = (unsigned)((d / 4 + kRowThreads * nv - 1) / (kRowThreads * nv));
+    apply_carveout(reinterpret_cast<const void*>(kern));
     e = launch_pdl_if(true, kern, dim3((unsigned)B, col_blocks), dim3(kRowThreads), 0, s, ys, L.n_dp, L.T_pad, prow,
                       topk_w, y, (int)B, k, d, arrive, S);
   } else if (S <= 4 && k * S <= kCombineMaxKS) {
@@ -791,6 +811,7 @@ int launch_dispatch(const moe_b200_config& c, int64_t B, const void* x, int xb, 
   auto kern = xb ? (smem_idx ? dispatch_kernel<true, true> : dispatch_kernel<true, false>)
                  : (smem_idx ? dispatch_kernel<false, true> : dispatch_kernel<false, false>);
   if (smem > 48 * 1024) MOE_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem));
+  apply_carveout(reinterpret_cast<const void*>(kern));
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kDispThreads), smem, s, q);
   if (e != cudaSuccess) return cuda_fail(e, "dispatch launch");
   return MOE_B200_OK;
@@ -948,6 +969,7 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
     void (*kern)(RouterParams) = xb ? (wvec ? router_seg_kernel<true, true> : router_seg_kernel<true, false>)
                                     : (wvec ? router_seg_kernel<false, true> : router_seg_kernel<false, false>);
     MOE_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(kern), q.smem));
+    apply_carveout(reinterpret_cast<const void*>(kern));
     kern<<<grid, kSegThreads, q.smem, s>>>(p);
     MOE_LAUNCH_CHECK("router_seg_kernel");
   } else if ((rc = launch_router_exact(*cfg, B, x, xb, w_router, L, ws, p, s))) {

@@ -123,6 +123,53 @@ MOE_DEVICE T pairwise_sum(const T* a, int n) {
   return ret;
 }
 
+// Warp-cooperative form of the same sum (identical bits, every add in the same
+// order): for a block of n <= 128 values, lanes 0..7 run the eight strided
+// accumulators r[j] = a[j] + a[j+8] + ... in parallel, the fixed
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree runs on shuffles, and the tail is
+// added in order; n <= 256 splits once at numpy's n2 (the halves on lanes
+// 0..7 and 8..15).  All lanes return the sum.  Larger n: one lane, serially.
+template <typename T>
+MOE_DEVICE T pairwise_block_warp(const T* a, int n, int lane, int base) {
+  // lanes base..base+7 hold the strided accumulators of a[0 .. n)
+  const int j = lane - base;
+  T r = T(0);
+  if (n >= 8 && j >= 0 && j < 8) {
+    r = a[j];
+    for (int i = 8 + j; i < n - (n % 8); i += 8) r = r + a[i];
+  }
+  // tree over lanes base..base+7 (other lanes compute garbage, unused)
+  const T r1 = __shfl_down_sync(0xffffffffu, r, 1);
+  const T p01 = r + r1;                          // valid at even j: r_j + r_{j+1}
+  const T q = __shfl_down_sync(0xffffffffu, p01, 2);
+  const T p0123 = p01 + q;                       // valid at j % 4 == 0
+  const T h = __shfl_down_sync(0xffffffffu, p0123, 4);
+  T res = p0123 + h;                             // valid at j == 0
+  res = __shfl_sync(0xffffffffu, res, base);
+  if (n < 8) {
+    res = T(0);
+    for (int i = 0; i < n; ++i) res = res + a[i];
+    return res;
+  }
+  for (int i = n - (n % 8); i < n; ++i) res = res + a[i];
+  return res;
+}
+
+template <typename T>
+MOE_DEVICE T pairwise_sum_warp(const T* a, int n, int lane) {
+  if (n <= 128) return pairwise_block_warp(a, n, lane, 0);
+  if (n <= 256) {
+    int n2 = n / 2;
+    n2 -= n2 % 8;  // both halves <= 128 for n <= 256
+    const T left = pairwise_block_warp(a, n2, lane, 0);
+    const T right = pairwise_block_warp(a + n2, n - n2, lane, 8);
+    return left + right;
+  }
+  T s = T(0);
+  if (lane == 0) s = pairwise_sum(a, n);
+  return __shfl_sync(0xffffffffu, s, 0);
+}
+
 // ---------------------------------------------------------------------------
 // numpy float32 exp (AVX512F/AVX2 SIMD kernel), reconstructed per SURVEY
 // Appendix A step 3 and checked against np.exp (tests).  Every operation is
@@ -499,9 +546,7 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
     if (p.gating == 0) {
       for (int e = lane; e < p.E; e += 32) row[e] = np_exp64(static_cast<double>(__fsub_rn(lo[e], m)));
       __syncwarp();
-      double S = 0.0;
-      if (lane == 0) S = pairwise_sum<double>(row, p.E);
-      S = __shfl_sync(0xffffffffu, S, 0);
+      const double S = pairwise_sum_warp<double>(row, p.E, lane);
       __syncwarp();
       for (int e = lane; e < p.E; e += 32) {
         float sc = __double2float_rn(__ddiv_rn(row[e], S));

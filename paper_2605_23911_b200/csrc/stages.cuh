@@ -44,9 +44,7 @@ gate_scores_kernel(const float* __restrict__ logits, float* __restrict__ scores,
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
       for (int e = lane; e < E; e += 32) row[e] = np_exp64(static_cast<double>(__fsub_rn(l[e], m)));
       __syncwarp();
-      double S = 0.0;
-      if (lane == 0) S = pairwise_sum<double>(row, E);
-      S = __shfl_sync(0xffffffffu, S, 0);
+      const double S = pairwise_sum_warp<double>(row, E, lane);
       for (int e = lane; e < E; e += 32) out[e] = __double2float_rn(__ddiv_rn(row[e], S));
       __syncwarp();
     } else {
