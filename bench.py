@@ -162,7 +162,7 @@ def reference_arm(args, cfg_name):
     B = args.tokens or B0
     import torch
 
-    from oracle.cpu_baseline import host_cores, run_rows_sharded
+    from oracle.cpu_baseline import host_cores, import_reference, run_reference_sharded, run_rows_sharded
 
     torch.set_num_threads(host_cores())
     gen = torch.Generator().manual_seed(1234)
@@ -182,12 +182,25 @@ def reference_arm(args, cfg_name):
     procs = host_cores()
     t_token = k * 3 * d * f / 1.4e8  # ~1.4e8 fp64 fold products / s / core
     n_tok = min(B, cpu_sample_tokens(procs, args.steps + args.warmup, t_token))
+    ref_mod = import_reference() if full else None
+    if ref_mod is not None:
+        # the reference's own moe_forward (pipeline.py:572), unmodified
+        run = lambda xs: run_reference_sharded(xs, wr, stacks[0], stacks[1], dn, E, k, gating, procs)  # noqa: E731
+        kind = "reference"
+        what = (f"the reference package's own moeperf.moe_forward (pipeline.py:572; installed unmodified in "
+                f"baseline/_ref) on {{n}} of {B} tokens per step, token-sharded over {{p}} forked workers")
+    else:
+        run = lambda xs: run_rows_sharded(xs, wr, expert, E, k, gating, procs)  # noqa: E731
+        kind = "port"
+        what = (f"{{n}} of {B} tokens per step, token-sharded over {{p}} forked numpy workers running "
+                f"oracle/moe_oracle.py moe_rows (the dense per-token restatement of moeperf moe_forward, "
+                f"bitwise equal to it)")
     for _ in range(args.warmup):
-        run_rows_sharded(x[:n_tok], wr, expert, E, k, gating, procs)
+        run(x[:n_tok])
     walls = []
     for i in range(args.steps):
         lo = (i * n_tok) % max(1, B - n_tok + 1)
-        _, _, wall, used = run_rows_sharded(x[lo:lo + n_tok], wr, expert, E, k, gating, procs)
+        _, _, wall, used = run(x[lo:lo + n_tok])
         walls.append(wall)
     total = sum(walls)
     value = n_tok * len(walls) / total
@@ -199,10 +212,8 @@ def reference_arm(args, cfg_name):
         "data": f"synthetic (torch CPU Philox N(0,1) tokens, {wdesc})",
         "config": {"workload": f"{label}, {B} tokens", "tokens": B, "model_shape": [E, k, d, f], "gating": gating,
                    "sample_tokens_per_step": n_tok},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": f"{n_tok} of {B} tokens per step, token-sharded over {procs} forked numpy "
-                                   f"workers running oracle/moe_oracle.py moe_rows (the dense per-token "
-                                   f"restatement of moeperf moe_forward, bitwise equal to it)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": kind,
+                         "sample": what.format(n=n_tok, p=used)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -215,10 +226,22 @@ def cpu_leg(x, wr, gate, up, down, E, k, d, f, gating, B, gpu_idx, routing=None)
     The experts those tokens use (known from the GPU routing) are copied to
     the host as fp32 once, outside the timing; returns (cpu_baseline, y, idx,
     rows)."""
-    from oracle.cpu_baseline import host_cores, run_rows_sharded
+    from oracle.cpu_baseline import host_cores, import_reference, run_reference_sharded, run_rows_sharded
 
     procs = host_cores()
     want = min(B, procs * 2)
+    if routing is None and E * _expert_bytes(d, f) <= CPU_EXPERT_BUDGET and import_reference() is not None:
+        # the reference's own moe_forward (pipeline.py:572) on the first tokens, full fp32 weights
+        n_tok = want
+        xs = x[:n_tok].float().cpu().numpy()
+        host = [t.float().cpu().numpy() for t in (wr, gate, up, down)]
+        y, idx, wall, nproc = run_reference_sharded(xs, *host, E, k, gating, procs)
+        del host
+        cb = {"value": n_tok / wall, "unit": UNIT, "cores": nproc, "kind": "reference",
+              "sample": f"{n_tok} of the {B} tokens through the reference package's own moeperf.moe_forward "
+                        f"(pipeline.py:572, installed unmodified in baseline/_ref), token-sharded over {nproc} "
+                        f"forked workers, {wall:.1f} s"}
+        return cb, y, idx, n_tok
     n_tok, used = 0, set()
     for t in range(want):
         nxt = used | set(int(e) for e in gpu_idx[t])

@@ -73,6 +73,68 @@ def run_rows_sharded(tokens, wr, expert, num_experts, k, gating, procs=None, rou
     return y, idx, wall, len(jobs)
 
 
+REF_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+
+
+def import_reference():
+    """The UNMODIFIED reference package (``moeperf``, installed into
+    ``baseline/_ref`` from /root/reference with pip --target), or None."""
+    import sys
+    try:
+        import moeperf  # noqa: F401
+    except ImportError:
+        if os.path.isdir(REF_PATH) and REF_PATH not in sys.path:
+            sys.path.append(REF_PATH)
+        try:
+            import moeperf  # noqa: F401
+        except ImportError:
+            return None
+    import moeperf
+    return moeperf
+
+
+def _ref_worker(args):
+    lo, hi = args
+    s = _STATE
+    m = s["moeperf"]
+    t0 = time.perf_counter()
+    y, _ = m.moe_forward(s["tokens"][lo:hi], s["wr"], s["weights"], s["config"], m.PipelineParams())
+    t_fwd = time.perf_counter() - t0
+    r = m.route(s["tokens"][lo:hi], s["wr"], s["config"])  # (indices for the parity check; not timed)
+    return lo, y, r.indices, t_fwd
+
+
+def run_reference_sharded(tokens, wr, gate, up, down, num_experts, k, gating, procs=None):
+    """The reference's own ``moe_forward`` (``pipeline.py:572``) over
+    ``tokens``, token-sharded across forked workers (rows are independent:
+    the sharded output is bitwise the unsharded one).  Returns ``(y, indices,
+    seconds, procs)`` -- seconds = the slowest worker's moe_forward time (the
+    workers run concurrently; the indices for the parity check come from a
+    separate, untimed ``route`` call) -- or None when the reference is not
+    installed."""
+    m = import_reference()
+    if m is None:
+        return None
+    procs = procs or host_cores()
+    B, d = tokens.shape
+    procs = max(1, min(procs, B))
+    f = gate.shape[1]
+    config = m.ModelConfig(num_experts, k, d, f, m.Gating(gating))
+    weights = m.ExpertWeights(gate=gate, up=up, down=down)
+    _STATE.update(tokens=tokens, wr=wr, weights=weights, config=config, moeperf=m)
+    bounds = np.linspace(0, B, procs + 1).astype(int)
+    jobs = [(int(bounds[i]), int(bounds[i + 1])) for i in range(procs) if bounds[i + 1] > bounds[i]]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(len(jobs)) as pool:
+        pool.map(_noop, range(len(jobs)))
+        parts = pool.map(_ref_worker, jobs, chunksize=1)
+    parts.sort(key=lambda p: p[0])
+    y = np.concatenate([p[1] for p in parts])
+    idx = np.concatenate([p[2] for p in parts])
+    _STATE.clear()
+    return y, idx, max(p[3] for p in parts), len(jobs)
+
+
 def run_sharded(tokens, wr, gate, up, down, num_experts, k, gating, procs=None):
     """Oracle forward over ``tokens`` sharded across ``procs`` forked workers.
 
