@@ -38,6 +38,7 @@ constexpr int kFfnThreads = 384;
 constexpr int kEpiWarps = 8;    // warps 4..11: two groups of 4 (one warp per TMEM lane quadrant)
 constexpr int kEpiGroups = 2;   // 32-row chunks alternate between the groups
 constexpr int kBM = 128;        // weight rows (output features) per tile
+constexpr uint32_t kAcc2 = 256; // TMEM column offset of a tile's second accumulator (up / down half 1)
 constexpr int kBK = 64;         // K per stage: one 128-byte swizzle row of bf16
 #ifndef MOE_B200_BOX_ROWS
 #define MOE_B200_BOX_ROWS 32
@@ -76,6 +77,7 @@ struct FfnParams {
   // mt its 256-column block); the combine grid, launched behind this one with
   // programmatic dependent launch, starts on the SMs this grid releases and
   // combines each (token, block) as soon as its k * splits arrivals are in.
+  int tmem_db;               // 1: chunks of <= 128 rows alternate two TMEM accumulator slots
   int32_t* arrive;           // (B, n_mt_dn) arrival counters, reset by the combine
   int k;                     // top-k: slot j of token t is expanded id t * k + j
 };
@@ -115,7 +117,11 @@ struct FfnCfg {
   static constexpr int kBStages = k2 ? 4 : kBN == 256 ? (kV == 3 ? 2 : 3) : (kV == 3 ? 2 : 4);
   static constexpr int kRingBytes = kAStages * kABytes + kBStages * kBBytes;
   static constexpr int kDataBytes = kRingBytes + kStgBufs * kStgBytes;
-  static constexpr uint32_t kTmemCols = 2 * kBN <= 256 ? 256 : 512;
+  // 512 columns: two accumulators (gate / up, or the two down halves) at
+  // +0 and +kAcc2, each holding up to 256 token columns -- or, for token
+  // chunks of <= 128 rows, TWO such pairs (slots at +0 and +128): the next
+  // tile's MMAs run into the other slot while this tile's epilogue drains
+  static constexpr uint32_t kTmemCols = 512;
   static constexpr int kSmemBytes = kDataBytes + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(kSmemBytes <= 232448, "shared memory");
 };
@@ -240,9 +246,9 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
   uint64_t* a_empty = a_full + C::kAStages;
   uint64_t* b_full = a_empty + C::kAStages;
   uint64_t* b_empty = b_full + C::kBStages;
-  uint64_t* tmem_full = b_empty + C::kBStages;
-  uint64_t* tmem_empty = tmem_full + 1;
-  uint64_t* sched_full = tmem_empty + 1;
+  uint64_t* tmem_full = b_empty + C::kBStages;  // [2]: per accumulator slot
+  uint64_t* tmem_empty = tmem_full + 2;         // [2]
+  uint64_t* sched_full = tmem_empty + 2;
   uint64_t* sched_empty = sched_full + kSchedSlots;
   int32_t* sched_tile = reinterpret_cast<int32_t*>(sched_empty + kSchedSlots);
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(sched_tile + kSchedSlots);
@@ -266,8 +272,10 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       mbar_init(b_full + s, k2 ? 2 : 1);
       mbar_init(b_empty + s, kPM == 1 ? 2 : 1);  // pair: both CTAs' MMAs release the shared slot
     }
-    mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, (k2 ? 2 : 1) * kEpiWarps);  // one arrival per epilogue warp (k2: of both CTAs)
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(tmem_full + s, 1);
+      mbar_init(tmem_empty + s, (k2 ? 2 : 1) * kEpiWarps);  // one arrival per epilogue warp (k2: of both CTAs)
+    }
     for (int s = 0; s < kSchedSlots; ++s) {
       mbar_init(sched_full + s, 1);
       // MMA lane + one lane per epilogue warp (pair: of both CTAs, plus rank 1's producer)
@@ -439,7 +447,8 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
     // ============================== MMA issuer ==============================
     int as = 0, bs = 0;
     uint32_t aph = 0, bph = 0;
-    uint32_t acc_phase = 0;
+    uint32_t eph = 0;          // TMEM-empty phases of the two accumulator slots (bits 0, 1)
+    int next_acc = 0;          // accumulator slot of the next narrow tile
     int slot = 0;
     uint32_t sphase = 0;
     while (true) {
@@ -458,7 +467,19 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         kb0 = ti.split * p.kb_per_split;
         kb1 = min(nkb_dn, kb0 + p.kb_per_split);
       }
-      mbar_wait(tmem_empty, acc_phase ^ 1);
+      // narrow tile (<= 128 token columns): one accumulator slot, alternating;
+      // wide: both slots (its accumulators span 256 columns each)
+      const bool narrow = p.tmem_db && n_mma <= 128;
+      const int acc_slot = next_acc;
+      if (narrow) {
+        next_acc ^= 1;
+        mbar_wait(tmem_empty + acc_slot, ((eph >> acc_slot) & 1u) ^ 1u);
+      } else {
+        mbar_wait(tmem_empty, (eph & 1u) ^ 1u);
+        mbar_wait(tmem_empty + 1, ((eph >> 1) & 1u) ^ 1u);
+      }
+      const uint32_t acc_lo = tmem_base + (narrow ? acc_slot * 128u : 0u);
+      uint64_t* full_bar = tmem_full + (narrow ? acc_slot : 0);
       tc_fence_after();
       if (p.trace && lane == 0) p.trace[tile * 8 + 5] = globaltimer();
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -469,7 +490,10 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             tc_fence_after();
             if (elect_one()) {
               mma_commit_mc(b_empty + bs, 3);
-              if (kb == kb1 - 1) mma_commit(tmem_full);
+              if (kb == kb1 - 1) {
+                mma_commit(full_bar);
+                if (!narrow) mma_commit(tmem_full + 1);
+              }
             }
             __syncwarp();
             if (++bs == C::kBStages) { bs = 0; bph ^= 1; }
@@ -498,32 +522,38 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
             const uint64_t bdesc = make_smem_desc_sw128(sb + kk * 32, 16, 1024);
             const uint64_t adesc0 = make_smem_desc_sw128(sa0 + kk * 2048, C::kABytes / 2, 1024);
             const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
-            if constexpr (k2) mma_bf16_2sm(tmem_base, adesc0, bdesc, idesc, acc);
-            else mma_bf16(tmem_base, adesc0, bdesc, idesc, acc);
+            if constexpr (k2) mma_bf16_2sm(acc_lo, adesc0, bdesc, idesc, acc);
+            else mma_bf16(acc_lo, adesc0, bdesc, idesc, acc);
             if (!single) {
               const uint32_t sa1 = smem_u32(a_ring + as1 * C::kABytes);
               const uint64_t adesc1 = make_smem_desc_sw128(sa1 + kk * 2048, C::kABytes / 2, 1024);
-              if constexpr (k2) mma_bf16_2sm(tmem_base + kBN, adesc1, bdesc, idesc, acc);
-              else mma_bf16(tmem_base + kBN, adesc1, bdesc, idesc, acc);
+              if constexpr (k2) mma_bf16_2sm(acc_lo + kAcc2, adesc1, bdesc, idesc, acc);
+              else mma_bf16(acc_lo + kAcc2, adesc1, bdesc, idesc, acc);
             }
           }
           if constexpr (k2) {  // release both CTAs' slots; both epilogues start
             mma_commit2_mc(a_empty + as0, 3);
             if (!single) mma_commit2_mc(a_empty + as1, 3);
             mma_commit2_mc(b_empty + bs, 3);
-            if (kb == kb1 - 1) mma_commit2_mc(tmem_full, 3);
+            if (kb == kb1 - 1) {
+              mma_commit2_mc(full_bar, 3);
+              if (!narrow) mma_commit2_mc(tmem_full + 1, 3);
+            }
           } else {
             mma_commit(a_empty + as0);
             if (!single) mma_commit(a_empty + as1);
             if constexpr (kPair) mma_commit_mc(b_empty + bs, 3);  // the slot is shared by the pair
             else mma_commit(b_empty + bs);
-            if (kb == kb1 - 1) mma_commit(tmem_full);
+            if (kb == kb1 - 1) {
+              mma_commit(full_bar);
+              if (!narrow) mma_commit(tmem_full + 1);
+            }
           }
         }
         __syncwarp();
         if (++bs == C::kBStages) { bs = 0; bph ^= 1; }
       }
-      acc_phase ^= 1;
+      eph ^= narrow ? (1u << acc_slot) : 3u;
     }
   } else if (warp >= 4) {
     // =============================== epilogue ===============================
@@ -532,16 +562,22 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
     const bool issuer = (wq == 0 && lane == 0);  // one bulk-copy issuer per group
     uint8_t* stg_g = stg + grp * C::kStgBytes;
+    // accumulator slots: the same narrow / wide sequence as the MMA issuer
+    uint32_t fph = 0;  // TMEM-full phases of the two slots (bits 0, 1)
+    int next_acc = 0;
+    bool narrow = true;
+    int acc_slot = 0;
     // release the accumulator: one arrival per warp (k2: on rank 0's barrier)
     auto release_tmem = [&]() {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (k2) mbar_arrive_cluster(lead_tmem_empty);
-        else mbar_arrive(tmem_empty);
+        for (int s = narrow ? acc_slot : 0; s < (narrow ? acc_slot + 1 : 2); ++s) {
+          if constexpr (k2) mbar_arrive_cluster(lead_tmem_empty + s * 8);
+          else mbar_arrive(tmem_empty + s);
+        }
       }
     };
-    uint32_t acc_phase = 0;
     int slot = 0;
     uint32_t sphase = 0;
     while (true) {
@@ -550,11 +586,21 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
       if (tile < 0) break;
       const TileInfo ti = decode_tile(p, tile, rank);
       const int4 ch = __ldg(p.chunk_tab + ti.chunk);
-      mbar_wait(tmem_full, acc_phase);
+      narrow = p.tmem_db && max(16, (ch.z + 15) & ~15) <= 128;
+      acc_slot = next_acc;
+      if (narrow) {
+        next_acc ^= 1;
+        mbar_wait(tmem_full + acc_slot, (fph >> acc_slot) & 1u);
+        fph ^= 1u << acc_slot;
+      } else {
+        mbar_wait(tmem_full, fph & 1u);
+        mbar_wait(tmem_full + 1, (fph >> 1) & 1u);
+        fph ^= 3u;
+      }
+      const uint32_t acc_lo = tmem_base + (narrow ? acc_slot * 128u : 0u);
       tc_fence_after();
       if (ti.dummy) {  // pair mode, missing second tile: nothing to write
         release_tmem();
-        acc_phase ^= 1;
         continue;
       }
       if (p.trace && warp == 4 && lane == 0) p.trace[tile * 8 + 4] = globaltimer();
@@ -569,7 +615,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         for (int q = grp; q < nq; q += kEpiGroups) {
           const int c0 = q * 32;
           uint32_t a[32];
-          tmem_ld_32x32b_x32(tmem_base + lane_base + c0, a);
+          tmem_ld_32x32b_x32(acc_lo + lane_base + c0, a);
           tmem_wait_ld();
           if (q == my_last) release_tmem();
           float* sbuf = reinterpret_cast<float*>(stg_g);
@@ -602,8 +648,8 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           const int q = qq * kEpiGroups + grp;
           if (q * 32 < ch.z) {
             uint32_t g[32], u[32];
-            tmem_ld_32x32b_x32(tmem_base + lane_base + q * 32, g);
-            tmem_ld_32x32b_x32(tmem_base + lane_base + kBN + q * 32, u);
+            tmem_ld_32x32b_x32(acc_lo + lane_base + q * 32, g);
+            tmem_ld_32x32b_x32(acc_lo + lane_base + kAcc2 + q * 32, u);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -674,7 +720,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           for (int q = grp; q < nq; q += kEpiGroups) {
             const int c0 = q * 32;
             uint32_t a[32];
-            tmem_ld_32x32b_x32(tmem_base + lane_base + half * kBN + c0, a);
+            tmem_ld_32x32b_x32(acc_lo + lane_base + half * kAcc2 + c0, a);
             tmem_wait_ld();
             if (half == 1 && q == my_last) release_tmem();
             float* sbuf = reinterpret_cast<float*>(stg_g);
@@ -730,7 +776,6 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
         }
       }
       if (p.trace && warp == 4 && lane == 0) p.trace[tile * 8 + 3] = globaltimer();
-      acc_phase ^= 1;
     }
   }
 

@@ -78,6 +78,8 @@ struct Tuning {
   int io_graphs = 1;         // MOE_B200_IO_GRAPHS
   int fused_combine = 1;     // MOE_B200_FUSED_COMBINE (0: separate combine launch)
   int carveout = -1;         // MOE_B200_CARVEOUT: shared-memory carveout (%) of the small kernels
+  int tmem_db = 1;           // MOE_B200_TMEM_DB: double-buffered TMEM accumulators for <= 128-row chunks
+  int seg_w64 = 0;           // MOE_B200_SEG_W64: segment router reads W pre-widened to fp64
 };
 Tuning g_tune;
 std::mutex g_tune_mu;
@@ -104,6 +106,8 @@ void load_tuning_locked() {
   t.io_graphs = geti("MOE_B200_IO_GRAPHS", 1);
   t.fused_combine = geti("MOE_B200_FUSED_COMBINE", 1);
   t.carveout = geti("MOE_B200_CARVEOUT", -1);
+  t.tmem_db = geti("MOE_B200_TMEM_DB", 1);
+  t.seg_w64 = geti("MOE_B200_SEG_W64", 0);
   g_tune = t;
   g_tune_loaded = true;
 }
@@ -659,6 +663,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.gu_done = hdr + kHdrGuDone;
   p.tiled = fused ? 1 : 0;
   p.T_pad = L.T_pad;
+  p.tmem_db = tuning().tmem_db != 0;
   if (arrive && mode == kFfnFused && do_gu && do_dn) {
     // the down epilogue publishes per-(token, block) arrivals for the combine
     // grid that runs overlapped with this grid's tail
@@ -968,6 +973,17 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
     const bool wvec = (cfg->num_experts % 4) == 0;
     void (*kern)(RouterParams) = xb ? (wvec ? router_seg_kernel<true, true> : router_seg_kernel<true, false>)
                                     : (wvec ? router_seg_kernel<false, true> : router_seg_kernel<false, false>);
+    if (tuning().seg_w64) {
+      // W widened to fp64 once per call (the hot loop then converts only x)
+      double* w64 = reinterpret_cast<double*>(ws8(ws) + L.w64);
+      const long n = (long)cfg->hidden_dim * cfg->num_experts;
+      widen_f64_kernel<<<static_cast<int>(std::min<long>((n + 255) / 256, (long)kNumSMs * 8)), 256, 0, s>>>(
+          w_router, w64, n);
+      MOE_LAUNCH_CHECK("widen_f64_kernel");
+      p.wlin64 = w64;
+      kern = xb ? (wvec ? router_seg_kernel<true, true, true> : router_seg_kernel<true, false, true>)
+                : (wvec ? router_seg_kernel<false, true, true> : router_seg_kernel<false, false, true>);
+    }
     MOE_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(kern), q.smem));
     apply_carveout(reinterpret_cast<const void*>(kern));
     kern<<<grid, kSegThreads, q.smem, s>>>(p);

@@ -36,6 +36,7 @@ struct RouterParams {
   const void* x;        // (B, d) fp32 or bf16
   const float* wr;      // (d, E) fp32
   const double* w64;    // prepared W64[eb][d_pad][expc] (router_prep_kernel)
+  const double* wlin64; // segment kernel, W widened to fp64 in its (d, E) layout (widen_f64_kernel)
   int x_bf16;
   int B, d, E, k, gating;
   int tokc, expc;       // CTA tile: tokc tokens x expc experts
@@ -283,6 +284,14 @@ constexpr int kRouterMaxStages = 12;
 // expert blocks, so a chunk of an expert block is ONE contiguous bulk copy.
 // Non-finite entries set flag bit 2 (NonFiniteInput on router_weight).
 // ---------------------------------------------------------------------------
+// W (d, E) fp32 -> fp64, same layout: the segment router's operand, so its
+// hot loop converts only the token values (F2F.F64.F32 runs at a quarter of
+// the DFMA rate).
+__global__ void __launch_bounds__(256) widen_f64_kernel(const float* __restrict__ w, double* __restrict__ o, long n) {
+  for (long i = (long)blockIdx.x * 256 + threadIdx.x; i < n; i += (long)gridDim.x * 256)
+    o[i] = static_cast<double>(w[i]);
+}
+
 __global__ void router_prep_kernel(const float* __restrict__ wr, double* __restrict__ w64, int d, int E,
                                    int expc, int d_pad, int n_eblocks, uint32_t* flags) {
   const long total = (long)n_eblocks * d_pad * expc;

@@ -39,6 +39,8 @@
 // (dispatch.cuh).  All counters self-reset.
 #pragma once
 
+#include <type_traits>
+
 #include "router.cuh"
 
 namespace moe {
@@ -78,7 +80,7 @@ MOE_DEVICE void seg_finalize(const RouterParams& p, int t, int e, double s, doub
   p.lbuf[(size_t)t * p.E + e] = r;
 }
 
-template <bool kXBf16, bool kWVec>
+template <bool kXBf16, bool kWVec, bool kW64 = false>
 __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const RouterParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TT = kSegTT, TE = kSegTE;
@@ -118,7 +120,8 @@ __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const Router
 #pragma unroll
   for (int j = 0; j < TE; ++j) ex_ok[j] = (ebase + j) < p.E;
 
-  auto load_blk = [&](int k, float (&xb)[TT][8], float (&wb)[8][TE]) {
+  using WT = typename std::conditional<kW64, double, float>::type;
+  auto load_blk = [&](int k, float (&xb)[TT][8], WT (&wb)[8][TE]) {
 #pragma unroll
     for (int i = 0; i < TT; ++i) {
       if (tok_ok[i]) {
@@ -130,23 +133,38 @@ __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const Router
     }
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
+      if constexpr (kW64) {
+        const double* wrow = p.wlin64 + (size_t)(k + r) * p.E + ebase;
+        if (kWVec) {  // E % 4 == 0: two 16-byte loads
+          double2 a = make_double2(0.0, 0.0), b = make_double2(0.0, 0.0);
+          if (ex_ok[0]) { a = __ldg(reinterpret_cast<const double2*>(wrow)); b = __ldg(reinterpret_cast<const double2*>(wrow) + 1); }
+          wb[r][0] = a.x; wb[r][1] = a.y; wb[r][2] = b.x; wb[r][3] = b.y;
+        } else {
+#pragma unroll
+          for (int j = 0; j < TE; ++j) wb[r][j] = ex_ok[j] ? __ldg(wrow + j) : 0.0;
+        }
+        continue;
+      }
       const float* wrow = p.wr + (size_t)(k + r) * p.E + ebase;
       if (kWVec) {
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (ex_ok[0]) v = __ldg(reinterpret_cast<const float4*>(wrow));
-        wb[r][0] = v.x; wb[r][1] = v.y; wb[r][2] = v.z; wb[r][3] = v.w;
+        wb[r][0] = static_cast<WT>(v.x); wb[r][1] = static_cast<WT>(v.y);
+        wb[r][2] = static_cast<WT>(v.z); wb[r][3] = static_cast<WT>(v.w);
       } else {
 #pragma unroll
-        for (int j = 0; j < TE; ++j) wb[r][j] = ex_ok[j] ? __ldg(wrow + j) : 0.0f;
+        for (int j = 0; j < TE; ++j) wb[r][j] = ex_ok[j] ? static_cast<WT>(__ldg(wrow + j)) : WT(0);
       }
     }
   };
 
   if (kbeg < kend) {
-    float xc[TT][8], wc[8][TE];
+    float xc[TT][8];
+    WT wc[8][TE];
     load_blk(kbeg, xc, wc);
     for (int k = kbeg; k < kend; k += 8) {
-      float xn[TT][8], wn[8][TE];
+      float xn[TT][8];
+      WT wn[8][TE];
       if (k + 8 < kend) load_blk(k + 8, xn, wn);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {

@@ -875,3 +875,29 @@ def test_overlapped_combine_routed_with_dropped_slots(pkg, monkeypatch):
     # token 3 = its one valid slot
     ref3 = O.moe_forward(tokens[3:4], wr, gate, up, down, e, 1, "softmax", routing=(idx[3:4, :1], w[3:4, :1]))["y"]
     assert O.max_rel_error(y_fused[3:4], ref3) <= TOL
+
+
+@pytest.mark.parametrize("shape", [
+    (8, 2, 512, 1024, 512, "softmax"),           # 256-row chunk cap: experts of <= 128 and > 128 rows mixed
+    (60, 4, 256, 176, 96, "softmax"),            # 128-row chunks, every tile narrow
+    (8, 2, 1024, 2048, 16, "sigmoid_normalized"),  # small batch, K split > 1
+])
+def test_tmem_double_buffer_bit_identical(pkg, shape, monkeypatch):
+    """Chunks of <= 128 rows alternate two TMEM accumulator slots (the next
+    tile's MMAs run while this tile's epilogue drains): identical bits to the
+    single-slot kernel (MOE_B200_TMEM_DB=0), in every CTA-pair mode."""
+    P = pkg
+    from paper_2605_23911_b200 import _lib
+    e, k, d, f, b, g = shape
+    tokens, wr, gate, up, down = O.make_instance(93, e, k, d, f, b)
+    layer = _layer(P, _cfg(P, e, k, d, f, g), wr, gate, up, down, b)
+    x = torch.from_numpy(tokens).cuda()
+    ys = {}
+    for db in ("1", "0"):
+        for pair in ("0", "1", "2"):
+            monkeypatch.setenv("MOE_B200_TMEM_DB", db)
+            monkeypatch.setenv("MOE_B200_FFN_PAIR", pair)
+            _lib.reload_tuning()
+            ys[db + pair] = _np(layer.forward(x))
+    for key, y in ys.items():
+        bits_equal(y, ys["00"])
