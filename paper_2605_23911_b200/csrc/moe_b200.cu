@@ -80,6 +80,7 @@ struct Tuning {
   int carveout = -1;         // MOE_B200_CARVEOUT: shared-memory carveout (%) of the small kernels
   int tmem_db = 1;           // MOE_B200_TMEM_DB: double-buffered TMEM accumulators for <= 128-row chunks
   int seg_w64 = 0;           // MOE_B200_SEG_W64: segment router reads W pre-widened to fp64
+  int rx_quarter = 1;        // MOE_B200_RX_QUARTER: 4 x 2 quarter-warp tiles in the exact router (0: 2 x 4)
 };
 Tuning g_tune;
 std::mutex g_tune_mu;
@@ -108,6 +109,7 @@ void load_tuning_locked() {
   t.carveout = geti("MOE_B200_CARVEOUT", -1);
   t.tmem_db = geti("MOE_B200_TMEM_DB", 1);
   t.seg_w64 = geti("MOE_B200_SEG_W64", 0);
+  t.rx_quarter = geti("MOE_B200_RX_QUARTER", 1);
   g_tune = t;
   g_tune_loaded = true;
 }
@@ -509,13 +511,17 @@ RouterPlan plan_router(const moe_b200_config& c, int64_t B, int x_bf16) {
   const int64_t target = (kNumSMs * 4) / 5;
   const int64_t chains = B * (int64_t)E;
   if (chains >= 64LL * 1024 && r.expc % 2 == 0) {
-    // 2 experts x 4 tokens per thread, 32-token blocks (DeepSeek-512 A/B: 2x2
-    // within +-0.5%, 4x4 +9%, 2x1 over 16-token blocks +4%)
+    // 32 x 32 blocks: 4 experts x 2 tokens per thread in the quarter-warp
+    // layout (router_kernel kQ) when the expert block is 32 wide; else 2 x 4
+    // strided tiles (DeepSeek-512 A/B of the strided tiles: 2x2 within
+    // +-0.5%, 4x4 +9%, 2x1 over 16-token blocks +4%)
     r.te = 2; r.tt = 4; r.tokc = 32;
+    if (r.expc == 32 && tuning().rx_quarter != 0) r.te = 4, r.tt = 2;
     {  // tuning: MOE_B200_RX_TILE="te,tt,tokc"
       const int te = tuning().rx_te, tt = tuning().rx_tt, tokc = tuning().rx_tokc;
       if (te > 0 &&
-          ((te == 2 && (tt == 2 || tt == 4)) || (te == 4 && tt == 4)) &&
+          ((te == 2 && (tt == 2 || tt == 4)) || (te == 4 && tt == 4) ||
+           (te == 4 && tt == 2 && tokc == 32 && r.expc == 32)) &&
           tokc >= tt && tokc % tt == 0 && r.expc % te == 0 &&
           (r.expc / te) * (tokc / tt) + kRouterProducers <= 384) {  // router_kernel's launch bound
         r.te = te; r.tt = tt; r.tokc = tokc;
@@ -552,6 +558,7 @@ int launch_router_t(const CUtensorMap& tmx, const RouterParams& p, const RouterP
 
 template <bool kBf16>
 int launch_router_x(const CUtensorMap& tmx, const RouterParams& p, const RouterPlan& plan, cudaStream_t s) {
+  if (plan.te == 4 && plan.tt == 2) return launch_router_t<kBf16, 4, 2, 64>(tmx, p, plan, s);
   if (plan.te == 4) return launch_router_t<kBf16, 4, 4, 64>(tmx, p, plan, s);
   if (plan.te == 2 && plan.tt == 2) return launch_router_t<kBf16, 2, 2, 64>(tmx, p, plan, s);
   if (plan.te == 2) return launch_router_t<kBf16, 2, 4, 64>(tmx, p, plan, s);

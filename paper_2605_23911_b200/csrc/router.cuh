@@ -325,7 +325,12 @@ MOE_DEVICE void bulk_load_smem(void* dst, const void* src, uint32_t bytes, uint6
 // ---------------------------------------------------------------------------
 struct RouterSmem {
   static __host__ __device__ size_t w_bytes(int expc, int kc) { return (size_t)kc * expc * 8; }
-  static __host__ __device__ size_t x_bytes(int tokc, int kc) { return ((size_t)tokc * (kc + 1) * 8 + 127) / 128 * 128; }
+  // fp64 x chunk: token-major rows of kc + 1 (padded), or k-major rows of
+  // tokc + 2 (the 4 x 2 quarter-warp tile layout); sized for either
+  static __host__ __device__ size_t x_bytes(int tokc, int kc) {
+    const size_t a = (size_t)tokc * (kc + 1), b = (size_t)kc * (tokc + 2);
+    return ((a > b ? a : b) * 8 + 127) / 128 * 128;
+  }
   static __host__ __device__ size_t raw_bytes(int tokc, int xb, int kc) { return ((size_t)tokc * kc * xb + 127) / 128 * 128; }
   static __host__ __device__ size_t stage_bytes(int tokc, int expc, int xb, int kc) {
     return w_bytes(expc, kc) + x_bytes(tokc, kc) + raw_bytes(tokc, xb, kc);
@@ -462,6 +467,11 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
   float* lo = reinterpret_cast<float*>(base + (size_t)p.E * 8);
   float* hi = lo + p.E;
   double* win = reinterpret_cast<double*>(base + (size_t)p.E * 16);  // exact-chain window
+  // debug timeline (segment kernel): phase-2 sub-steps of the CTA's first token
+  // as clock64 deltas from phase-2 entry in slots 8, 9, 13, 14
+  unsigned long long* tr2 = (p.trace && p.seg_len && tid == 0) ? p.trace + (size_t)blockIdx.x * 16 : nullptr;
+  const long long c2 = clock64();
+  auto stamp2 = [&](int i) { if (tr2 && tr2[i] == 0) tr2[i] = clock64() - c2; };
   for (int t = t_begin + warp; t < t_end; t += nwarps) {
     const float2* lb = p.lbuf + (size_t)t * p.E;
     for (int e = lane; e < p.E; e += 32) {
@@ -470,6 +480,7 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
       hi[e] = v.y;
     }
     __syncwarp();
+    stamp2(8);
     // ---- certification; `round` 0: unknown (+ everything if want_logits),
     //      1: whatever the outputs still depend on
     float m = 0.0f;
@@ -549,6 +560,7 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
       }
       (void)any;
     }
+    stamp2(9);
     if (p.want_logits)
       for (int e = lane; e < p.E; e += 32) p.logits[(size_t)t * p.E + e] = lo[e];
     // ---- scores (lo is a representative: every candidate gives the same bits)
@@ -565,6 +577,7 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
       for (int e = lane; e < p.E; e += 32) row[e] = static_cast<double>(np_sigmoid(lo[e]));
     }
     __syncwarp();
+    stamp2(13);
       // top-k over keys (score bits desc, index asc); scores are >= +0.
       float wsel = 0.0f;
       int isel = 0;
@@ -593,6 +606,7 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
         }
       }
       __syncwarp();
+      stamp2(14);
       if (p.gating == 1) {
         // renormalise over the selected k with numpy's fp32 pairwise sum
         float* wrow = reinterpret_cast<float*>(row);
@@ -652,6 +666,9 @@ router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
   const int nch = (p.d + kKC - 1) / kKC;
   const int d_pad = (p.d + kRouterKC - 1) / kRouterKC * kRouterKC;
   const int ntok = min(p.tokc, p.B - t0);  // valid token rows of this block
+  // 4 x 2 quarter-warp tiles (32 x 32 CTA block, 4 compute warps; host-checked)
+  constexpr bool kQ = (kTE == 4 && kTT == 2);
+  constexpr int kQTok = 32, kQExp = 32;
   if (p.trace && threadIdx.x == 0) p.trace[4096 * 4 + 2048 * 4 + blockIdx.x] = globaltimer_ns();
   pdl_launch_dependents();
   if (tid == 0) {
@@ -704,13 +721,68 @@ router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
           else v = reinterpret_cast<const float*>(raw)[i];
           if (!isfinite(v)) nonfinite_x = true;
         }
-        dx[row * (kKC + 1) + kk] = static_cast<double>(v);
+        if constexpr (kQ) dx[kk * (kQTok + 2) + row] = static_cast<double>(v);  // k-major (see compute)
+        else dx[row * (kKC + 1) + kk] = static_cast<double>(v);
       }
       mbar_arrive(full + s);
       // refill: chunk c+S-1 goes into the stage of chunk c-1 once compute released it
       if (ptid == 0 && c + p.stages - 1 < nch) issue(c + p.stages - 1);
     }
     if (nonfinite_x) atomicOr(p.flags, 1u);
+  } else if constexpr (kQ) {
+    // ===================== compute chains, quarter-warp tiles ================
+    // 32 tokens x 32 experts per CTA, 4 warps of 16 x 16 chains; lane = 8
+    // token pairs (lane % 8) x 4 expert quads (lane / 8), 4 x 2 chains each.
+    // Shared-memory operand cost per step (LDS.128, measured on B200,
+    // scripts/probes/lds_probe.cu): x pair distinct within each quarter-warp
+    // 4 cycles, W quads uniform within each quarter-warp 2 + 2 cycles -- 8
+    // cycles per 8 DFMA per warp (the 2 x 2 / 2 x 4 strided tiles: 9-10
+    // cycles per 4-8 DFMA).  x is k-major fp64 in the stage (kQTok + 2 row
+    // stride: 16-byte aligned pairs, 2-way store conflicts for the producers).
+    const int cw = tid / 32, lane = tid & 31;
+    const int tok0 = 16 * (cw >> 1) + 2 * (lane & 7);
+    const int ex0 = 16 * (cw & 1) + 4 * (lane >> 3);
+    double acc[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { acc[i][0] = -0.0; acc[i][1] = -0.0; }
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % p.stages;
+      const uint32_t ph = (c / p.stages) & 1;
+      mbar_wait(full + s, ph);
+      const uint8_t* st = smem + s * sbytes;
+      const double* dw = reinterpret_cast<const double*>(st) + ex0;
+      const double* dx = reinterpret_cast<const double*>(st + wbytes) + tok0;
+      const int kvalid = min(kKC, p.d - c * kKC);
+      auto step = [&](int kk) {
+        const double2 xv = *reinterpret_cast<const double2*>(dx + kk * (kQTok + 2));
+        const double2 wa = *reinterpret_cast<const double2*>(dw + kk * kQExp);
+        const double2 wb = *reinterpret_cast<const double2*>(dw + kk * kQExp + 2);
+        acc[0][0] = __fma_rn(xv.x, wa.x, acc[0][0]); acc[0][1] = __fma_rn(xv.y, wa.x, acc[0][1]);
+        acc[1][0] = __fma_rn(xv.x, wa.y, acc[1][0]); acc[1][1] = __fma_rn(xv.y, wa.y, acc[1][1]);
+        acc[2][0] = __fma_rn(xv.x, wb.x, acc[2][0]); acc[2][1] = __fma_rn(xv.y, wb.x, acc[2][1]);
+        acc[3][0] = __fma_rn(xv.x, wb.y, acc[3][0]); acc[3][1] = __fma_rn(xv.y, wb.y, acc[3][1]);
+      };
+      if (kvalid == kKC) {
+#pragma unroll 16
+        for (int kk = 0; kk < kKC; ++kk) step(kk);
+      } else {
+        for (int kk = 0; kk < kvalid; ++kk) step(kk);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = e0 + ex0 + i;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int t = t0 + tok0 + j;
+        if (t < p.B && e < p.E) {
+          const float l = __double2float_rn(acc[i][j]);
+          p.lbuf[(size_t)t * p.E + e] = make_float2(l, l);  // exact: a zero-width interval
+        }
+      }
+    }
   } else {
     // ============================ compute chains ===========================
     // Experts e0 + eg + i*n_eg, tokens t0 + tg + j*n_tg: the warp's W loads are

@@ -41,4 +41,8 @@ for i in range(1, 10):
     v = t[:, i][t[:, i] > 0]
     if len(v):
         print(f"  {names[i]:10s} n={len(v):5d} cycles min/med/max {v.min()}/{int(np.median(v))}/{v.max()}")
+for i, nm in ((8, "p2 lbuf"), (9, "p2 certified"), (13, "p2 scores"), (14, "p2 topk")):
+    v = t[:, i][t[:, i] > 0]
+    if len(v):
+        print(f"  {nm:12s} n={len(v):5d} cycles from phase-2 entry min/med/max {v.min()}/{int(np.median(v))}/{v.max()}")
 print(f"  exact chains: certify-round {int(t[:, 11].sum())}, max-uncertain {int(t[:, 12].sum())}; logits {B*E}")

@@ -768,14 +768,18 @@ def test_varying_batch_sizes_reuse_one_layer(pkg):
         bits_equal(_np(layer.topk_w[:b]), w_ref)
 
 
-@pytest.mark.parametrize("tile", ["", "2,4,32", "2,2,32", "4,4,32"])
-def test_throughput_router_tiles_bitexact(pkg, tile, monkeypatch):
+@pytest.mark.parametrize("tile", ["", "2,4,32", "2,2,32", "4,4,32", "4,2,32"])
+@pytest.mark.parametrize("shape", [(256, 512), (259, 520)])
+def test_throughput_router_tiles_bitexact(pkg, tile, shape, monkeypatch):
     """The throughput-regime exact router (>= 64K token x expert chains) with
-    each register tile: routing and permutation bit-exact against the oracle."""
+    each register tile (default: the 4 x 2 quarter-warp layout), also over a
+    ragged last token block and a partial last k-chunk: routing and
+    permutation bit-exact against the oracle."""
     P = pkg
     if tile:
         monkeypatch.setenv("MOE_B200_RX_TILE", tile)
-    e, k, d, f, b = 256, 8, 512, 64, 256  # 65536 chains
+    b, d = shape
+    e, k, f = 256, 8, 64  # >= 65536 chains
     rng = np.random.default_rng(91)
     tokens = rng.standard_normal((b, d)).astype(np.float32)
     wr = (rng.standard_normal((d, e)) / np.sqrt(d)).astype(np.float32)
