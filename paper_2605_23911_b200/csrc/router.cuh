@@ -248,6 +248,41 @@ MOE_DEVICE double np_exp64(double x) {
   return __dmul_rn(res, __longlong_as_double(static_cast<long long>(m + 1023) << 52));
 }
 
+// np_exp64 for a whole warp (every lane calls it, uniform control flow): the
+// 2^(j/16) table entries come from lanes j of (top_i, tail_i) by shuffles
+// instead of divergent constant-cache reads (16 distinct addresses serialise).
+// Same operations, same bits as np_exp64.
+MOE_DEVICE double np_exp64_warp(double x, double top_i, double tail_i) {
+  const bool big = !(fabs(x) < 707.7032713517042);
+  const double xs = big ? 0.0 : x;
+  const double inv_ln2 = __longlong_as_double(0x3ff71547652b82feLL);
+  const double shifter = __longlong_as_double(0x42f8000000003ff0LL);
+  const double ln2_hi = __longlong_as_double(0x3fe62e42fefa39efLL);
+  const double ln2_lo = __longlong_as_double(0x3c7abc9e3b39803fLL);
+  const double c6 = __longlong_as_double(0x3f57411836940c04LL), c5 = __longlong_as_double(0x3f81101cbbc265c0LL);
+  const double c4 = __longlong_as_double(0x3fa55557242d68feLL), c3 = __longlong_as_double(0x3fc5555553939732LL);
+  const double c2 = __longlong_as_double(0x3fe000000000d008LL), c1 = __longlong_as_double(0x3fefffffffffff70LL);
+  const double t = __fma_rz(xs, inv_ln2, shifter);
+  const double n = __dsub_rn(t, shifter);
+  const int j = static_cast<int>(__double_as_longlong(t) & 15);
+  const double top = __shfl_sync(0xffffffffu, top_i, j);
+  const double tail = __shfl_sync(0xffffffffu, tail_i, j);
+  double r = __fma_rn(-n, ln2_hi, xs);
+  r = __fma_rn(-ln2_lo, n, r);
+  r = __longlong_as_double(__double_as_longlong(r) & 0xbfffffffffffffffLL);
+  const double r2 = __dmul_rn(r, r);
+  double a = __fma_rn(c6, r, c5);
+  const double b = __fma_rn(c4, r, c3);
+  const double c = __fma_rn(c2, r, c1);
+  a = __fma_rn(r2, a, b);
+  a = __fma_rn(r2, a, c);
+  const double pp = __fma_rn(a, r, tail);
+  const double res = __fma_rn(top, pp, top);
+  const int m = static_cast<int>(floor(n));
+  if (big) return x < 0.0 ? 0.0 : exp(x);
+  return __dmul_rn(res, __longlong_as_double(static_cast<long long>(m + 1023) << 52));
+}
+
 MOE_DEVICE float np_sigmoid(float x) {
   float t = np_expf(-fabsf(x));
   float den = __fadd_rn(1.0f, t);
@@ -392,7 +427,7 @@ MOE_DEVICE bool cta_arrive_last(int32_t* counter, int n) {
 // W_r[:, e] (4 windows in flight, hiding L2 latency), every lane runs the same
 // dependent fold on shuffled operands (identical result in all lanes).
 template <bool kXBf16>
-MOE_DEVICE float exact_chain_logit_warp(const RouterParams& p, int t, int e, int lane, double* win) {
+__device__ __noinline__ float exact_chain_logit_warp(const RouterParams& p, int t, int e, int lane, double* win) {
   // fma(x, w, a) == fl(x*w + a) because x*w is exact in fp64: the lanes form
   // the products of a 128-step window (4 each, operands loaded one window
   // ahead), the window goes through shared memory, and every lane folds it
@@ -445,6 +480,103 @@ MOE_DEVICE float exact_chain_logit_warp(const RouterParams& p, int t, int e, int
 
 MOE_DEVICE bool same_bits(float a, float b) { return __float_as_uint(a) == __float_as_uint(b); }
 
+// warp max of floats (no NaN among the inputs: the logits are finite here)
+MOE_DEVICE float warp_max_f32(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+constexpr int kTopkRegs = 8;  // phase-2 top-k keeps E <= 256 scores in registers
+
+// Certification of one token's logit intervals (phase 2's slow path, taken
+// only when some interval is unknown or has nonzero width): resolves, with
+// the exact sequential chain, every logit the outputs depend on and returns
+// the (certain) row max for the softmax.  Out of line: the common path stays
+// a short straight run of code (the router executes it once per CTA, from a
+// cold instruction cache).
+template <bool kXBf16>
+__device__ __noinline__ float certify_token(const RouterParams& p, int t, float* lo, float* hi, double* win, int lane) {
+  float m = 0.0f;
+  for (int round = 0; round < 2; ++round) {
+    bool any = false;
+    for (int e0 = 0; e0 < p.E; e0 += 32) {
+      const int e = e0 + lane;
+      bool nd = false;
+      if (e < p.E) {
+        const float a = lo[e], b = hi[e];
+        const bool unsure = !same_bits(a, b);
+        if (round == 0) {
+          nd = isnan(a) || (p.want_logits && unsure);
+        } else if (unsure) {
+          if (p.gating == 0) {
+            nd = !same_bits(__fsub_rn(a, m), __fsub_rn(b, m));
+          } else {
+            const float sa = np_sigmoid(a);
+            float c = a;
+            int steps = 0;
+            while (!nd && !same_bits(c, b)) {
+              c = nextafterf(c, b);
+              nd = (++steps > 8) || !same_bits(np_sigmoid(c), sa);
+            }
+          }
+        }
+      }
+      // resolve the flagged logits of this 32-wide slice one at a time, warp-wide
+      uint32_t todo = __ballot_sync(0xffffffffu, nd);
+      while (todo) {
+        const int j = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const float v = exact_chain_logit_warp<kXBf16>(p, t, e0 + j, lane, win);
+        if (lane == j) {
+          lo[e] = v;
+          hi[e] = v;
+        }
+        if (p.trace && p.seg_len && lane == 0) atomicAdd(p.trace + (size_t)blockIdx.x * 16 + 11, 1ull);
+      }
+      any |= nd;
+    }
+    __syncwarp();
+    if (round == 0 && p.gating == 0) {
+      // the row max must be certain; otherwise resolve every unsure logit
+      float mlo = -__int_as_float(0x7f800000), mhi = mlo;
+      for (int e = lane; e < p.E; e += 32) {
+        mlo = fmaxf(mlo, lo[e]);
+        mhi = fmaxf(mhi, hi[e]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mlo = fmaxf(mlo, __shfl_xor_sync(0xffffffffu, mlo, o));
+        mhi = fmaxf(mhi, __shfl_xor_sync(0xffffffffu, mhi, o));
+      }
+      if (mlo != mhi) {
+        for (int e0 = 0; e0 < p.E; e0 += 32) {
+          const int e = e0 + lane;
+          uint32_t todo = __ballot_sync(0xffffffffu, e < p.E && !same_bits(lo[e], hi[e]));
+          while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const float v = exact_chain_logit_warp<kXBf16>(p, t, e0 + j, lane, win);
+            if (lane == j) {
+              lo[e] = v;
+              hi[e] = v;
+            }
+            if (p.trace && p.seg_len && lane == 0) atomicAdd(p.trace + (size_t)blockIdx.x * 16 + 12, 1ull);
+          }
+        }
+        __syncwarp();
+        mlo = -__int_as_float(0x7f800000);
+        for (int e = lane; e < p.E; e += 32) mlo = fmaxf(mlo, lo[e]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mlo = fmaxf(mlo, __shfl_xor_sync(0xffffffffu, mlo, o));
+      }
+      m = mlo;
+    }
+    (void)any;
+  }
+  return m;
+}
+
 // ---------------------------------------------------------------------------
 // Phase 2 (one warp per token): scores + top-k + sigmoid renormalisation from
 // the certified logit intervals.  A logit interval [lo, hi] holds every fp32
@@ -471,7 +603,7 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
   // as clock64 deltas from phase-2 entry in slots 8, 9, 13, 14
   unsigned long long* tr2 = (p.trace && p.seg_len && tid == 0) ? p.trace + (size_t)blockIdx.x * 16 : nullptr;
   const long long c2 = clock64();
-  auto stamp2 = [&](int i) { if (tr2 && tr2[i] == 0) tr2[i] = clock64() - c2; };
+  auto stamp2 = [&](int i) { if (tr2) tr2[i] = clock64() - c2; };
   for (int t = t_begin + warp; t < t_end; t += nwarps) {
     const float2* lb = p.lbuf + (size_t)t * p.E;
     for (int e = lane; e < p.E; e += 32) {
@@ -482,93 +614,35 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
     __syncwarp();
     stamp2(8);
     // ---- certification; `round` 0: unknown (+ everything if want_logits),
-    //      1: whatever the outputs still depend on
+    //      1: whatever the outputs still depend on.  Fast path: every interval
+    //      has zero width (the common case) -- nothing to resolve, m = max.
+    bool unsure_any = false;
+    for (int e = lane; e < p.E; e += 32) unsure_any |= isnan(lo[e]) || !same_bits(lo[e], hi[e]);
+    unsure_any = __any_sync(0xffffffffu, unsure_any);
     float m = 0.0f;
-    for (int round = 0; round < 2; ++round) {
-      bool any = false;
-      for (int e0 = 0; e0 < p.E; e0 += 32) {
-        const int e = e0 + lane;
-        bool nd = false;
-        if (e < p.E) {
-          const float a = lo[e], b = hi[e];
-          const bool unsure = !same_bits(a, b);
-          if (round == 0) {
-            nd = isnan(a) || (p.want_logits && unsure);
-          } else if (unsure) {
-            if (p.gating == 0) {
-              nd = !same_bits(__fsub_rn(a, m), __fsub_rn(b, m));
-            } else {
-              const float sa = np_sigmoid(a);
-              float c = a;
-              int steps = 0;
-              while (!nd && !same_bits(c, b)) {
-                c = nextafterf(c, b);
-                nd = (++steps > 8) || !same_bits(np_sigmoid(c), sa);
-              }
-            }
-          }
-        }
-        // resolve the flagged logits of this 32-wide slice one at a time, warp-wide
-        uint32_t todo = __ballot_sync(0xffffffffu, nd);
-        while (todo) {
-          const int j = __ffs(todo) - 1;
-          todo &= todo - 1;
-          const float v = exact_chain_logit_warp<kXBf16>(p, t, e0 + j, lane, win);
-          if (lane == j) {
-            lo[e] = v;
-            hi[e] = v;
-          }
-          if (p.trace && p.seg_len && lane == 0) atomicAdd(p.trace + (size_t)blockIdx.x * 16 + 11, 1ull);
-        }
-        any |= nd;
-      }
-      __syncwarp();
-      if (round == 0 && p.gating == 0) {
-        // the row max must be certain; otherwise resolve every unsure logit
-        float mlo = -__int_as_float(0x7f800000), mhi = mlo;
-        for (int e = lane; e < p.E; e += 32) {
-          mlo = fmaxf(mlo, lo[e]);
-          mhi = fmaxf(mhi, hi[e]);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          mlo = fmaxf(mlo, __shfl_xor_sync(0xffffffffu, mlo, o));
-          mhi = fmaxf(mhi, __shfl_xor_sync(0xffffffffu, mhi, o));
-        }
-        if (mlo != mhi) {
-          for (int e0 = 0; e0 < p.E; e0 += 32) {
-            const int e = e0 + lane;
-            uint32_t todo = __ballot_sync(0xffffffffu, e < p.E && !same_bits(lo[e], hi[e]));
-            while (todo) {
-              const int j = __ffs(todo) - 1;
-              todo &= todo - 1;
-              const float v = exact_chain_logit_warp<kXBf16>(p, t, e0 + j, lane, win);
-              if (lane == j) {
-                lo[e] = v;
-                hi[e] = v;
-              }
-              if (p.trace && p.seg_len && lane == 0) atomicAdd(p.trace + (size_t)blockIdx.x * 16 + 12, 1ull);
-            }
-          }
-          __syncwarp();
-          mlo = -__int_as_float(0x7f800000);
-          for (int e = lane; e < p.E; e += 32) mlo = fmaxf(mlo, lo[e]);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) mlo = fmaxf(mlo, __shfl_xor_sync(0xffffffffu, mlo, o));
-        }
-        m = mlo;
-      }
-      (void)any;
+    if (!unsure_any && p.gating == 0) {
+      float mx = -__int_as_float(0x7f800000);
+      for (int e = lane; e < p.E; e += 32) mx = fmaxf(mx, lo[e]);
+      m = warp_max_f32(mx);
     }
+    if (unsure_any) m = certify_token<kXBf16>(p, t, lo, hi, win, lane);
     stamp2(9);
     if (p.want_logits)
       for (int e = lane; e < p.E; e += 32) p.logits[(size_t)t * p.E + e] = lo[e];
     // ---- scores (lo is a representative: every candidate gives the same bits)
     if (p.gating == 0) {
-      for (int e = lane; e < p.E; e += 32) row[e] = np_exp64(static_cast<double>(__fsub_rn(lo[e], m)));
+      const double top_i = __longlong_as_double(static_cast<long long>(kNpExpTop[lane & 15]));
+      const double tail_i = __longlong_as_double(static_cast<long long>(kNpExpTail[lane & 15]));
+      for (int e0 = 0; e0 < p.E; e0 += 32) {
+        const int e = e0 + lane;
+        const double v = np_exp64_warp(e < p.E ? static_cast<double>(__fsub_rn(lo[e], m)) : 0.0, top_i, tail_i);
+        if (e < p.E) row[e] = v;
+      }
       __syncwarp();
+      stamp2(15);
       const double S = pairwise_sum_warp<double>(row, p.E, lane);
       __syncwarp();
+      stamp2(1);
       for (int e = lane; e < p.E; e += 32) {
         float sc = __double2float_rn(__ddiv_rn(row[e], S));
         row[e] = static_cast<double>(sc);
@@ -581,7 +655,42 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
       // top-k over keys (score bits desc, index asc); scores are >= +0.
       float wsel = 0.0f;
       int isel = 0;
-      for (int j = 0; j < p.k; ++j) {
+      if (p.E <= 32 * kTopkRegs) {
+        // the lane's scores e = lane + 32 i in registers (ascending i: the
+        // first max within the lane is its lowest index); k rounds of two
+        // warp reductions, the winner's owner marks it selected
+        float sc[kTopkRegs];
+#pragma unroll
+        for (int i = 0; i < kTopkRegs; ++i) {
+          const int e = lane + 32 * i;
+          sc[i] = e < p.E ? static_cast<float>(row[e]) : -1.0f;
+        }
+        for (int j = 0; j < p.k; ++j) {
+          uint32_t kb = 0, kidx = 0xFFFFFFFFu;
+#pragma unroll
+          for (int i = 0; i < kTopkRegs; ++i) {
+            const float v = sc[i];
+            if (!(v < 0.0f)) {
+              const uint32_t key = ((v == 0.0f) ? 0u : __float_as_uint(v)) + 1u;
+              if (key > kb) { kb = key; kidx = static_cast<uint32_t>(lane + 32 * i); }
+            }
+          }
+          const uint32_t kmax = __reduce_max_sync(0xffffffffu, kb);
+          const int e_best = static_cast<int>(__reduce_min_sync(0xffffffffu, kb == kmax ? kidx : 0xFFFFFFFFu));
+          const float s_best = __uint_as_float(kmax - 1u);
+          if (lane == (e_best & 31)) {
+#pragma unroll
+            for (int i = 0; i < kTopkRegs; ++i)
+              if (i == (e_best >> 5)) sc[i] = -1.0f;
+          }
+          if (lane == j) { wsel = s_best; isel = e_best; }
+          if (j >= 32 && lane == 0) {  // k > 32: write directly (rare)
+            p.topk_idx[(size_t)t * p.k + j] = e_best;
+            p.topk_w[(size_t)t * p.k + j] = s_best;
+          }
+        }
+      }
+      for (int j = 0; j < (p.E <= 32 * kTopkRegs ? 0 : p.k); ++j) {
         // largest key (score bits desc, index asc) in two warp reductions: the
         // max of score bits + 1 (0: no candidate), then the lowest index holding it
         uint32_t kb = 0, kidx = 0xFFFFFFFFu;
@@ -634,6 +743,7 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
         p.topk_w[(size_t)t * p.k + lane] = wsel;
       }
       __syncwarp();
+      tr2 = nullptr;  // (debug timeline: the first token only)
     }
 }
 

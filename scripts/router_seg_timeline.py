@@ -37,11 +37,11 @@ print(f"{name} B={B}: route us median {np.median(ts):.1f} min {min(ts):.1f}; CTA
 g0 = (t[:, 0] - t[:, 0].min()) / 1e3
 print(f"  CTA start spread us: med {np.median(g0):.1f} max {g0.max():.1f}")
 names = ["", "phase1", "part-store", "cta-reduce", "arrive1", "finalize", "arrive2", "phase2", "arrive3", "phase3"]
-for i in range(1, 10):
+for i in range(2, 8):
     v = t[:, i][t[:, i] > 0]
     if len(v):
         print(f"  {names[i]:10s} n={len(v):5d} cycles min/med/max {v.min()}/{int(np.median(v))}/{v.max()}")
-for i, nm in ((8, "p2 lbuf"), (9, "p2 certified"), (13, "p2 scores"), (14, "p2 topk")):
+for i, nm in ((8, "p2 lbuf"), (9, "p2 certified"), (15, "p2 exp"), (1, "p2 sum"), (13, "p2 scores"), (14, "p2 topk")):
     v = t[:, i][t[:, i] > 0]
     if len(v):
         print(f"  {nm:12s} n={len(v):5d} cycles from phase-2 entry min/med/max {v.min()}/{int(np.median(v))}/{v.max()}")
