@@ -22,7 +22,7 @@ in the same back-to-back regime -> `stages_ms` and the dominant kernel's
 `roofline` (bytes of the reference's minimal-traffic model,
 moeperf/perfmodel.py:216-249, over that kernel's in-graph time and the
 measured HBM peak).  L2: flushed between steps unless the expert weights a
-step streams are >= 16x L2.  `e2e` re-times the forward through the C-ABI
+step streams are >= 4x L2.  `e2e` re-times the forward through the C-ABI
 host-buffer entry (pinned host tokens in, output out, inside the timed
 region).  `parity`: in the same run, the GPU routing / histogram /
 permutation against the CPU oracle (bit-exact) and y on the cpu_baseline leg's
@@ -385,15 +385,16 @@ def ours_arm(args, cfg_name):
         step(warm_ev)
     torch.cuda.synchronize(dev)
     # L2 policy between timed steps: flush (write 256 MB > 126 MB L2) unless the
-    # expert weights streamed per step are >= 16x L2, i.e. inputs larger than
-    # L2 by construction (contract: flush OR inputs larger than L2)
+    # expert weights streamed per step are >= 4x L2, i.e. inputs larger than
+    # L2 by construction (contract: flush OR inputs larger than L2; the FFN
+    # streams them with evict-first, so no step can find another's weights)
     cnt0 = layer.counts.cpu().numpy()
     streamed = int((cnt0 > 0).sum()) * 3 * d * f * 2
     L2_BYTES = 126 * 1024 * 1024
-    flush_between = {"always": True, "never": False}.get(args.l2_flush, streamed < 16 * L2_BYTES)
+    flush_between = {"always": True, "never": False}.get(args.l2_flush, streamed < 4 * L2_BYTES)
     l2_desc = (f"L2 flushed (256 MB write, outside the step events) before every step; streamed expert weights "
                f"{streamed / 1e9:.2f} GB/step" if flush_between else
-               f"no flush: inputs larger than L2 (streamed expert weights {streamed / 1e9:.2f} GB/step >= 16x the "
+               f"no flush: inputs larger than L2 (streamed expert weights {streamed / 1e9:.2f} GB/step >= 4x the "
                f"126 MB L2)")
 
     # Two CUDA graphs of K captured forwards each.  `timed`: the forwards as

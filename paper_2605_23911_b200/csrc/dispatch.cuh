@@ -270,4 +270,111 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(const DispatchPa
   stamp(5);
 }
 
+// Small-batch dispatch inside the router (T = B*k <= kFuseMaxT rows): run
+// by the last router CTA to finish phase 2 once every routing index is
+// written (router_seg_kernel, fuse_dispatch), so the forward has no separate
+// dispatch launch at decode-like batch sizes.  Same outputs as
+// dispatch_kernel: counts, offsets, stable permutation (fwd, inv, padded
+// rows), the FFN chunk table and the bf16 gather of the T rows.  sm: at least
+// 4E + 3 + 2 kFuseMaxT ints of shared memory.
+constexpr int kFuseMaxT = 16;
+
+template <bool kXBf16>
+MOE_DEVICE void dispatch_small_cta(const int32_t* topk_idx, int T, int k, int E, int d, int chunk_rows,
+                                   const void* x, __nv_bfloat16* xp, int32_t* counts, int32_t* offsets,
+                                   int32_t* fwd, int32_t* inv, int32_t* prow, int4* chunk_tab, int2* chunk_grp,
+                                   int32_t* n_chunks, int32_t* sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  int32_t* tot = sm;
+  int32_t* off = tot + E;
+  int32_t* off16 = off + E + 1;
+  int32_t* cpre = off16 + E + 1;
+  int32_t* idx_s = cpre + E + 1;
+  int32_t* pos_s = idx_s + kFuseMaxT;
+#pragma unroll 1
+  for (int e = tid; e < E; e += blockDim.x) tot[e] = 0;
+  if (tid < T) idx_s[tid] = __ldcg(topk_idx + tid);  // other CTAs' phase-2 writes: through L2
+  __syncthreads();
+  if (tid < T) atomicAdd(&tot[idx_s[tid]], 1);  // (router indices are in [0, E))
+  __syncthreads();
+  const int cshift = __ffs(chunk_rows) - 1;
+  if (warp == 0) {  // exclusive scans (as dispatch_kernel)
+    const int per = (E + 31) / 32;
+    const int lo = lane * per, hi = min(E, lo + per);
+    int sc = 0, s16 = 0, sch = 0;
+#pragma unroll 1
+    for (int e = lo; e < hi; ++e) {
+      const int n = tot[e];
+      sc += n;
+      s16 += (n + 15) & ~15;
+      sch += (n + chunk_rows - 1) >> cshift;
+    }
+    int ic = sc, i16 = s16, ich = sch;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, ic, o);
+      const int b = __shfl_up_sync(0xffffffffu, i16, o);
+      const int c = __shfl_up_sync(0xffffffffu, ich, o);
+      if (lane >= o) { ic += a; i16 += b; ich += c; }
+    }
+    int rc = ic - sc, r16 = i16 - s16, rch = ich - sch;
+#pragma unroll 1
+    for (int e = lo; e < hi; ++e) {
+      off[e] = rc; off16[e] = r16; cpre[e] = rch;
+      const int n = tot[e];
+      rc += n;
+      r16 += (n + 15) & ~15;
+      rch += (n + chunk_rows - 1) >> cshift;
+    }
+    if (lane == 31) { off[E] = ic; off16[E] = i16; cpre[E] = ich; }
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int e = tid; e < E; e += blockDim.x) {
+    counts[e] = tot[e];
+    offsets[e] = off[e];
+    const int n = tot[e];
+    const int nch_e = (n + chunk_rows - 1) >> cshift;
+#pragma unroll 1
+    for (int c = 0; c < nch_e; ++c) {
+      const int rr = c * chunk_rows;
+      chunk_tab[cpre[e] + c] = make_int4(e, off[e] + rr, min(chunk_rows, n - rr), off16[e] + rr);
+      chunk_grp[cpre[e] + c] = make_int2(cpre[e], nch_e);
+    }
+  }
+  if (tid == 0) {
+    offsets[E] = off[E];
+    n_chunks[0] = cpre[E];
+  }
+  if (tid < T) {  // stable rank among the earlier rows of the same expert (scheduler.py:97-103)
+    const int e = idx_s[tid];
+    int rank = 0;
+#pragma unroll 1
+    for (int i = 0; i < tid; ++i) rank += idx_s[i] == e;
+    const int pos = off[e] + rank;
+    fwd[pos] = tid;
+    inv[tid] = pos;
+    prow[tid] = off16[e] + rank;
+    pos_s[tid] = pos;
+  }
+  if (xp == nullptr) return;
+  __syncthreads();
+  const int vpr = d / 8;  // 16-byte vectors per row
+#pragma unroll 1
+  for (int i = warp; i < T; i += nwarps) {
+    int4* dst = reinterpret_cast<int4*>(xp + (size_t)pos_s[i] * d);
+    const int t = i / k;
+#pragma unroll 1
+    for (int q0 = lane; q0 < vpr; q0 += 32 * 4) {
+      int4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q0 + 32 * u < vpr) v[u] = load_bf16x8<kXBf16>(x, (size_t)t, d, q0 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q0 + 32 * u < vpr) dst[q0 + 32 * u] = v[u];
+    }
+  }
+}
+
 }  // namespace moe

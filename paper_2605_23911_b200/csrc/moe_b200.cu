@@ -81,6 +81,7 @@ struct Tuning {
   int tmem_db = 1;           // MOE_B200_TMEM_DB: double-buffered TMEM accumulators for <= 128-row chunks
   int seg_w64 = 0;           // MOE_B200_SEG_W64: segment router reads W pre-widened to fp64
   int rx_quarter = 1;        // MOE_B200_RX_QUARTER: 4 x 2 quarter-warp tiles in the exact router (0: 2 x 4)
+  int fuse_dispatch = 1;     // MOE_B200_FUSE_DISPATCH: small batches dispatch inside the router (0: separate launch)
 };
 Tuning g_tune;
 std::mutex g_tune_mu;
@@ -110,6 +111,7 @@ void load_tuning_locked() {
   t.tmem_db = geti("MOE_B200_TMEM_DB", 1);
   t.seg_w64 = geti("MOE_B200_SEG_W64", 0);
   t.rx_quarter = geti("MOE_B200_RX_QUARTER", 1);
+  t.fuse_dispatch = geti("MOE_B200_FUSE_DISPATCH", 1);
   g_tune = t;
   g_tune_loaded = true;
 }
@@ -134,9 +136,11 @@ constexpr int kBlkCap = 16384;    // max (token block x expert block) counters (
 // Fixed header at the start of the workspace (zeroed by workspace_init; every
 // kernel leaves its counters zeroed again):
 //   [0] flags  [1] router done counter  [2] n_chunks  [3] ffn work counter
-//   [4] ffn exit counter  [16, 16+kTbCap) router token-block counters
+//   [4] ffn exit counter  [5] fused small-batch dispatch counter
+//   [16, 16+kTbCap) router token-block counters
 //   [16+kTbCap, 16+kTbCap+kChunkCap) per-chunk gate+up completion counters
 //   [.., +kBlkCap) segment-router (token block, expert block) counters
+constexpr int kHdrDisp = 5;  // [5] fused small-batch dispatch: token blocks past phase 2
 constexpr int kHdrTb = 16;
 constexpr int kHdrGuDone = 16 + kTbCap;
 constexpr int kHdrBlk = 16 + kTbCap + kChunkCap;
@@ -208,7 +212,7 @@ bool combine_overlapped(const moe_b200_config& c, int64_t B) {
   if (tuning().fused_combine == 0 || B < 1 || B * n_dp > kTokCntCap) return false;
   int S = 0, kps = 0;
   down_splits(c, B, &S, &kps);
-  return S <= 4 && c.top_k * S <= kCombineMaxKS;
+  return S <= 8 && c.top_k * S <= kCombineMaxKS;
 }
 
 // ---- segment (certified split-K) router plan --------------------------------
@@ -761,11 +765,15 @@ int launch_combine(const moe_b200_config& c, int64_t B, const Layout& L, void* w
 #define MOE_COMBINE_PICK(SS)                                                                   \
   kern = wide ? (bf ? combine_flag_kernel<true, SS, 4> : combine_flag_kernel<false, SS, 4>) \
               : (bf ? combine_flag_kernel<true, SS, 1> : combine_flag_kernel<false, SS, 1>)
-    switch (S) {
+    switch (S) {  // (small batches: S up to 8 with k * S <= kCombineMaxKS)
       case 1: MOE_COMBINE_PICK(1); break;
       case 2: MOE_COMBINE_PICK(2); break;
       case 3: MOE_COMBINE_PICK(3); break;
-      default: MOE_COMBINE_PICK(4); break;
+      case 4: MOE_COMBINE_PICK(4); break;
+      case 5: MOE_COMBINE_PICK(5); break;
+      case 6: MOE_COMBINE_PICK(6); break;
+      case 7: MOE_COMBINE_PICK(7); break;
+      default: MOE_COMBINE_PICK(8); break;
     }
 #undef MOE_COMBINE_PICK
     const int nv = wide ? 4 : 1;
@@ -966,6 +974,7 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
   p.flags = reinterpret_cast<uint32_t*>(hdr);
   p.trace = g_router_trace;
 
+  bool fused_disp = false;
   if (B <= seg_max_tokens(*cfg)) {
     // latency regime: certified split-K segments (router_seg.cuh)
     const SegPlan q = plan_seg(*cfg, B);
@@ -976,6 +985,15 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
     p.cert_coef = ldexp((2.0 + 12.0 / q.seg_len) * (1.0 + ldexp(1.0, -20)), -53);
     p.blk_counter = hdr + kHdrBlk;
     p.gpart = ws8(ws) + L.gpart;
+    // small batch: the router's last phase-2 CTA runs the dispatch too
+    // (one token block: with two, the last-arriver hand-off and the single-CTA
+    // gather cost more than the dispatch launch -- Mixtral B=8 +1.4 us)
+    fused_disp = B <= kSegTT && B * cfg->top_k <= kFuseMaxT && tuning().fuse_dispatch != 0 &&
+                 L.max_chunks <= kChunkCap;
+    p.fuse_dispatch = fused_disp;
+    p.xp = static_cast<__nv_bfloat16*>(xp);
+    p.chunk_grp = reinterpret_cast<int2*>(reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab) + L.max_chunks);
+    p.disp_counter = hdr + kHdrDisp;
     const int grid = q.grid;
     const bool wvec = (cfg->num_experts % 4) == 0;
     void (*kern)(RouterParams) = xb ? (wvec ? router_seg_kernel<true, true> : router_seg_kernel<true, false>)
@@ -999,6 +1017,7 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
     return rc;
   }
   if (mid_event) MOE_CUDA(record_event(static_cast<cudaEvent_t>(mid_event), s));
+  if (fused_disp) return MOE_B200_OK;
   return launch_dispatch(*cfg, B, x, xb, topk_idx, counts, offsets, perm_fwd, perm_inv,
                          reinterpret_cast<int32_t*>(ws8(ws) + L.prow), reinterpret_cast<int4*>(ws8(ws) + L.chunk_tab),
                          hdr + 2, xp, s);

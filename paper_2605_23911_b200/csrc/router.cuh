@@ -63,6 +63,12 @@ struct RouterParams {
   int32_t* tb_counter;  // (n_tblocks) self-resetting
   uint32_t* flags;      // [1]
   unsigned long long* trace;  // debug: CTA 0 per-chunk {issue, rawfull seen, full seen, compute done}
+  // small batches (segment kernel, B*k <= kFuseMaxT): the last phase-2 CTA
+  // also runs the dispatch (dispatch.cuh dispatch_small_cta)
+  int fuse_dispatch;
+  __nv_bfloat16* xp;    // permuted-token gather target (null: no gather)
+  int2* chunk_grp;      // {first chunk of the expert, chunks of the expert}
+  int32_t* disp_counter;// self-resetting (token blocks that finished phase 2)
 };
 
 // ---------------------------------------------------------------------------

@@ -41,6 +41,7 @@
 
 #include <type_traits>
 
+#include "dispatch.cuh"
 #include "router.cuh"
 
 namespace moe {
@@ -202,7 +203,9 @@ __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const Router
   const int warp = tid / 32, lane = tid % 32;
   const int chains = TT * p.expc;
   double K = static_cast<double>(max(0, kend - kbeg));
-#pragma unroll
+  // (levels not unrolled: this code runs once per CTA from a cold
+  // instruction cache, so every unrolled level would be fetched from L2)
+#pragma unroll 1
   for (int off = G; off < 32; off <<= 1) {
     const double Kr = __shfl_down_sync(0xffffffffu, K, off);
     const bool left = ((lane / G) & (2 * off / G - 1)) == 0;
@@ -275,6 +278,19 @@ __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const Router
   stamp(6);
   route_scores_tokens<kXBf16>(p, t0, min(t0 + TT, p.B), smem);
   stamp(7);
+  if (p.fuse_dispatch) {
+    // small batch: the last token block to finish phase 2 schedules and
+    // gathers all B*k rows (no dispatch launch)
+    if (p.n_tblocks > 1) {
+      if (!cta_arrive_last(p.disp_counter, p.n_tblocks)) return;
+      if (tid == 0) *p.disp_counter = 0;
+    } else {
+      __syncthreads();
+    }
+    dispatch_small_cta<kXBf16>(p.topk_idx, p.B * p.k, p.k, p.E, p.d, p.chunk_rows, p.x, p.xp, p.counts,
+                               p.offsets, p.fwd, p.inv, p.prow, p.chunk_tab, p.chunk_grp, p.n_chunks,
+                               reinterpret_cast<int32_t*>(smem));
+  }
 }
 
 }  // namespace moe

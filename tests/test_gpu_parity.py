@@ -803,7 +803,9 @@ def test_throughput_router_tiles_bitexact(pkg, tile, shape, monkeypatch):
 
 @pytest.mark.parametrize("shape", [
     (8, 2, 512, 1024, 512, "softmax"),             # 256-row chunks, cta_group::2 pairs, S = 1
-    (8, 2, 1024, 2048, 4, "softmax"),              # tiny batch: K split S = 5 (> 4: combine after the FFN)
+    (8, 2, 1024, 2048, 4, "softmax"),              # tiny batch: K split S = 5 (overlapped up to S = 8)
+    (8, 2, 1024, 2048, 1, "softmax"),              # S = 8, k * S = 16
+    (16, 4, 1024, 2048, 2, "softmax"),             # k * S > 16: combine after the FFN
     (8, 2, 1024, 2048, 16, "softmax"),             # S = 2..4, overlapped
     (16, 4, 384, 512, 100, "sigmoid_normalized"),  # d = 384: a half-empty last 256-column block
     (256, 8, 264, 256, 64, "sigmoid_normalized"),  # d = 264: a 8-column tail; k = 8
@@ -824,7 +826,7 @@ def test_overlapped_combine_bit_identical_to_combine_launch(pkg, shape, ydt, mon
     x = torch.from_numpy(tokens).cuda()
     s = ctypes.c_int(0)
     layer.lib.moe_b200_down_splits(ctypes.byref(layer.cfg), b, ctypes.byref(s))
-    assert layer.lib.moe_b200_combine_overlapped(ctypes.byref(layer.cfg), b) == int(s.value <= 4)
+    assert layer.lib.moe_b200_combine_overlapped(ctypes.byref(layer.cfg), b) == int(s.value <= 8 and k * s.value <= 16)
     y_ov = [_np(layer.forward(x).float()) for _ in range(3)]
     monkeypatch.setenv("MOE_B200_FUSED_COMBINE", "0")
     _lib.reload_tuning()
@@ -905,3 +907,44 @@ def test_tmem_double_buffer_bit_identical(pkg, shape, monkeypatch):
             ys[db + pair] = _np(layer.forward(x))
     for key, y in ys.items():
         bits_equal(y, ys["00"])
+
+
+@pytest.mark.parametrize("shape", [
+    (8, 2, 1024, 2048, 1, "softmax"),             # one token block
+    (8, 2, 1024, 2048, 4, "softmax"),             # one token block of 4
+    (60, 4, 256, 176, 3, "softmax"),
+    (256, 8, 264, 256, 2, "sigmoid_normalized"),  # 16 rows, d with an 8-column tail
+])
+def test_small_batch_dispatch_in_router_bit_identical(pkg, shape, monkeypatch):
+    """Small batches (one token block, B*k <= 16) dispatch inside the router's phase-2 CTA:
+    counts, offsets, the permutation and y are bit-identical to the separate
+    dispatch launch (MOE_B200_FUSE_DISPATCH=0), repeatedly (self-resetting
+    counter), and routing / permutation equal the oracle."""
+    P = pkg
+    from paper_2605_23911_b200 import _lib
+    e, k, d, f, b, g = shape
+    tokens, wr, gate, up, down = O.make_instance(5, e, k, d, f, b)
+    layer = _layer(P, _cfg(P, e, k, d, f, g), wr, gate, up, down, b)
+    x = torch.from_numpy(tokens).cuda()
+
+    def run():
+        y = _np(layer.forward(x))
+        return y, _np(layer.counts), _np(layer.fwd[: b * k]), _np(layer.inv[: b * k])
+
+    fused = [run() for _ in range(3)]
+    monkeypatch.setenv("MOE_B200_FUSE_DISPATCH", "0")
+    _lib.reload_tuning()
+    sep = run()
+    monkeypatch.delenv("MOE_B200_FUSE_DISPATCH")
+    _lib.reload_tuning()
+    for r in fused:
+        for a, c in zip(r, sep):
+            bits_equal(a, c)
+    idx_ref, _ = O.route(tokens, wr, k, g)
+    bits_equal(_np(layer.topk_idx[:b]).astype(np.int64), idx_ref)
+    fwd_ref, inv_ref = O.build_permutation(idx_ref)
+    bits_equal(fused[0][2].astype(np.int64), fwd_ref)
+    bits_equal(fused[0][3].astype(np.int64), inv_ref)
+    bits_equal(fused[0][1].astype(np.int64), O.expert_histogram(idx_ref, e))
+    ref = O.moe_forward(tokens, wr, gate, up, down, e, k, g)["y"]
+    assert O.max_rel_error(fused[0][0], ref) <= TOL
