@@ -495,6 +495,123 @@ MOE_DEVICE float warp_max_f32(float v) {
 
 constexpr int kTopkRegs = 8;  // phase-2 top-k keeps E <= 256 scores in registers
 
+// Scores (softmax: numpy float64 exp of the fp32-shifted logits, pairwise
+// sum, divide; sigmoid: numpy float32 logistic) and top-k of one token from
+// the logits lo[] (shared memory, one warp): lane j < min(k, 32) returns
+// selection j in (isel, wsel); for k > 32 the selections past 31 are written
+// to the outputs of token t directly (t < 0: not supported, callers check).
+// Used by phase 2 and by the certification's candidate enumeration.
+MOE_DEVICE void eval_route_outputs(const RouterParams& p, int t, const float* lo, float m, double* row, int lane,
+                                   int& isel_out, float& wsel_out) {
+  // ---- scores (lo is a representative: every candidate gives the same bits)
+  if (p.gating == 0) {
+    const double top_i = __longlong_as_double(static_cast<long long>(kNpExpTop[lane & 15]));
+    const double tail_i = __longlong_as_double(static_cast<long long>(kNpExpTail[lane & 15]));
+    for (int e0 = 0; e0 < p.E; e0 += 32) {
+      const int e = e0 + lane;
+      const double v = np_exp64_warp(e < p.E ? static_cast<double>(__fsub_rn(lo[e], m)) : 0.0, top_i, tail_i);
+      if (e < p.E) row[e] = v;
+    }
+    __syncwarp();
+    const double S = pairwise_sum_warp<double>(row, p.E, lane);
+    __syncwarp();
+    for (int e = lane; e < p.E; e += 32) {
+      float sc = __double2float_rn(__ddiv_rn(row[e], S));
+      row[e] = static_cast<double>(sc);
+    }
+  } else {
+    for (int e = lane; e < p.E; e += 32) row[e] = static_cast<double>(np_sigmoid(lo[e]));
+  }
+  __syncwarp();
+    // top-k over keys (score bits desc, index asc); scores are >= +0.
+    float wsel = 0.0f;
+    int isel = 0;
+    if (p.E <= 32 * kTopkRegs) {
+      // the lane's scores e = lane + 32 i in registers (ascending i: the
+      // first max within the lane is its lowest index); k rounds of two
+      // warp reductions, the winner's owner marks it selected
+      float sc[kTopkRegs];
+#pragma unroll
+      for (int i = 0; i < kTopkRegs; ++i) {
+        const int e = lane + 32 * i;
+        sc[i] = e < p.E ? static_cast<float>(row[e]) : -1.0f;
+      }
+      for (int j = 0; j < p.k; ++j) {
+        uint32_t kb = 0, kidx = 0xFFFFFFFFu;
+#pragma unroll
+        for (int i = 0; i < kTopkRegs; ++i) {
+          const float v = sc[i];
+          if (!(v < 0.0f)) {
+            const uint32_t key = ((v == 0.0f) ? 0u : __float_as_uint(v)) + 1u;
+            if (key > kb) { kb = key; kidx = static_cast<uint32_t>(lane + 32 * i); }
+          }
+        }
+        const uint32_t kmax = __reduce_max_sync(0xffffffffu, kb);
+        const int e_best = static_cast<int>(__reduce_min_sync(0xffffffffu, kb == kmax ? kidx : 0xFFFFFFFFu));
+        const float s_best = __uint_as_float(kmax - 1u);
+        if (lane == (e_best & 31)) {
+#pragma unroll
+          for (int i = 0; i < kTopkRegs; ++i)
+            if (i == (e_best >> 5)) sc[i] = -1.0f;
+        }
+        if (lane == j) { wsel = s_best; isel = e_best; }
+        if (j >= 32 && lane == 0) {  // k > 32: write directly (rare)
+          p.topk_idx[(size_t)t * p.k + j] = e_best;
+          p.topk_w[(size_t)t * p.k + j] = s_best;
+        }
+      }
+    }
+    for (int j = 0; j < (p.E <= 32 * kTopkRegs ? 0 : p.k); ++j) {
+      // largest key (score bits desc, index asc) in two warp reductions: the
+      // max of score bits + 1 (0: no candidate), then the lowest index holding it
+      uint32_t kb = 0, kidx = 0xFFFFFFFFu;
+      for (int e = lane; e < p.E; e += 32) {  // ascending e: the first max is the lowest index
+        float sc = static_cast<float>(row[e]);
+        if (sc < 0.0f) continue;  // already selected (marked -1)
+        const uint32_t key = ((sc == 0.0f) ? 0u : __float_as_uint(sc)) + 1u;
+        if (key > kb) { kb = key; kidx = static_cast<uint32_t>(e); }
+      }
+      const uint32_t kmax = __reduce_max_sync(0xffffffffu, kb);
+      const int e_best = static_cast<int>(__reduce_min_sync(0xffffffffu, kb == kmax ? kidx : 0xFFFFFFFFu));
+      const float s_best = __uint_as_float(kmax - 1u);
+      __syncwarp();
+      if (lane == (e_best & 31)) row[e_best] = -1.0;
+      __syncwarp();
+      if (lane == j) { wsel = s_best; isel = e_best; }
+      if (j >= 32) {  // k > 32: write directly (rare)
+        if (lane == 0) {
+          p.topk_idx[(size_t)t * p.k + j] = e_best;
+          p.topk_w[(size_t)t * p.k + j] = s_best;
+        }
+      }
+    }
+    __syncwarp();
+    if (p.gating == 1) {
+      // renormalise over the selected k with numpy's fp32 pairwise sum
+      float* wrow = reinterpret_cast<float*>(row);
+      if (lane < p.k && lane < 32) wrow[lane] = wsel;
+      __syncwarp();
+      if (p.k > 32 && lane == 0) {
+        for (int j = 32; j < p.k; ++j) wrow[j] = p.topk_w[(size_t)t * p.k + j];
+      }
+      __syncwarp();
+      float S = 0.0f;
+      if (lane == 0) S = pairwise_sum<float>(wrow, p.k);
+      S = __shfl_sync(0xffffffffu, S, 0);
+      const float uni = __double2float_rn(1.0 / static_cast<double>(p.k));
+      if (lane < p.k) wsel = (S == 0.0f) ? uni : __fdiv_rn(wsel, S);
+      if (p.k > 32 && lane == 0) {
+        for (int j = 32; j < p.k; ++j) {
+          float v = wrow[j];
+          p.topk_w[(size_t)t * p.k + j] = (S == 0.0f) ? uni : __fdiv_rn(v, S);
+        }
+      }
+      __syncwarp();
+    }
+  isel_out = isel;
+  wsel_out = wsel;
+}
+
 // Certification of one token's logit intervals (phase 2's slow path, taken
 // only when some interval is unknown or has nonzero width): resolves, with
 // the exact sequential chain, every logit the outputs depend on and returns
@@ -502,10 +619,61 @@ constexpr int kTopkRegs = 8;  // phase-2 top-k keeps E <= 256 scores in register
 // a short straight run of code (the router executes it once per CTA, from a
 // cold instruction cache).
 template <bool kXBf16>
-__device__ __noinline__ float certify_token(const RouterParams& p, int t, float* lo, float* hi, double* win, int lane) {
+__device__ __noinline__ float certify_token(const RouterParams& p, int t, float* lo, float* hi, double* win,
+                                            double* row, int lane) {
   float m = 0.0f;
   for (int round = 0; round < 2; ++round) {
     bool any = false;
+    if (round == 1 && p.gating == 0 && !p.want_logits && p.k <= 32) {
+      // Enumeration certificate (softmax): when at most two logits still have
+      // an uncertain shifted value fp32(l - m), each with exactly two fp32
+      // candidates {lo, hi = nextafter(lo)}, evaluate the token's outputs
+      // (top-k indices and weight bits) for every combination of candidates.
+      // If they all agree, the outputs do not depend on which value the
+      // reference fold rounds to: no exact recompute is needed (the exact
+      // chain costs d x 8 cycles of latency).
+      int nf = 0, fe[2] = {0, 0};
+      bool ok = true;
+      for (int e0 = 0; e0 < p.E && ok; e0 += 32) {
+        const int e = e0 + lane;
+        bool f = false, two = true;
+        if (e < p.E) {
+          const float a = lo[e], b = hi[e];
+          f = !same_bits(a, b) && !same_bits(__fsub_rn(a, m), __fsub_rn(b, m));
+          two = !f || same_bits(nextafterf(a, __int_as_float(0x7f800000)), b);
+        }
+        uint32_t bal = __ballot_sync(0xffffffffu, f);
+        ok = __all_sync(0xffffffffu, two) && ok;
+        while (bal && ok) {
+          if (nf == 2) { ok = false; break; }
+          fe[nf++] = e0 + __ffs(bal) - 1;
+          bal &= bal - 1;
+        }
+      }
+      if (ok && nf > 0) {
+        float orig[2] = {lo[fe[0]], lo[fe[1]]};
+        int i0 = 0, i1 = 0;
+        float w0 = 0.0f, w1 = 0.0f;
+        eval_route_outputs(p, t, lo, m, row, lane, i0, w0);
+        bool same = true;
+        for (int c = 1; c < (1 << nf) && same; ++c) {
+          __syncwarp();
+          if (lane == 0)
+            for (int q = 0; q < nf; ++q) lo[fe[q]] = ((c >> q) & 1) ? hi[fe[q]] : orig[q];
+          __syncwarp();
+          eval_route_outputs(p, t, lo, m, row, lane, i1, w1);
+          same = __all_sync(0xffffffffu, lane >= p.k || (i1 == i0 && same_bits(w1, w0)));
+        }
+        __syncwarp();
+        if (lane == 0)
+          for (int q = 0; q < nf; ++q) {
+            lo[fe[q]] = orig[q];
+            if (same) hi[fe[q]] = orig[q];  // certified: lo is a valid representative
+          }
+        __syncwarp();
+        if (same && p.trace && p.seg_len && lane == 0) atomicAdd(p.trace + (size_t)blockIdx.x * 16 + 12, 1ull << 32);
+      }
+    }
     for (int e0 = 0; e0 < p.E; e0 += 32) {
       const int e = e0 + lane;
       bool nd = false;
@@ -631,119 +799,14 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
       for (int e = lane; e < p.E; e += 32) mx = fmaxf(mx, lo[e]);
       m = warp_max_f32(mx);
     }
-    if (unsure_any) m = certify_token<kXBf16>(p, t, lo, hi, win, lane);
+    if (unsure_any) m = certify_token<kXBf16>(p, t, lo, hi, win, row, lane);
     stamp2(9);
     if (p.want_logits)
       for (int e = lane; e < p.E; e += 32) p.logits[(size_t)t * p.E + e] = lo[e];
-    // ---- scores (lo is a representative: every candidate gives the same bits)
-    if (p.gating == 0) {
-      const double top_i = __longlong_as_double(static_cast<long long>(kNpExpTop[lane & 15]));
-      const double tail_i = __longlong_as_double(static_cast<long long>(kNpExpTail[lane & 15]));
-      for (int e0 = 0; e0 < p.E; e0 += 32) {
-        const int e = e0 + lane;
-        const double v = np_exp64_warp(e < p.E ? static_cast<double>(__fsub_rn(lo[e], m)) : 0.0, top_i, tail_i);
-        if (e < p.E) row[e] = v;
-      }
-      __syncwarp();
-      stamp2(15);
-      const double S = pairwise_sum_warp<double>(row, p.E, lane);
-      __syncwarp();
-      stamp2(1);
-      for (int e = lane; e < p.E; e += 32) {
-        float sc = __double2float_rn(__ddiv_rn(row[e], S));
-        row[e] = static_cast<double>(sc);
-      }
-    } else {
-      for (int e = lane; e < p.E; e += 32) row[e] = static_cast<double>(np_sigmoid(lo[e]));
-    }
-    __syncwarp();
-    stamp2(13);
-      // top-k over keys (score bits desc, index asc); scores are >= +0.
-      float wsel = 0.0f;
-      int isel = 0;
-      if (p.E <= 32 * kTopkRegs) {
-        // the lane's scores e = lane + 32 i in registers (ascending i: the
-        // first max within the lane is its lowest index); k rounds of two
-        // warp reductions, the winner's owner marks it selected
-        float sc[kTopkRegs];
-#pragma unroll
-        for (int i = 0; i < kTopkRegs; ++i) {
-          const int e = lane + 32 * i;
-          sc[i] = e < p.E ? static_cast<float>(row[e]) : -1.0f;
-        }
-        for (int j = 0; j < p.k; ++j) {
-          uint32_t kb = 0, kidx = 0xFFFFFFFFu;
-#pragma unroll
-          for (int i = 0; i < kTopkRegs; ++i) {
-            const float v = sc[i];
-            if (!(v < 0.0f)) {
-              const uint32_t key = ((v == 0.0f) ? 0u : __float_as_uint(v)) + 1u;
-              if (key > kb) { kb = key; kidx = static_cast<uint32_t>(lane + 32 * i); }
-            }
-          }
-          const uint32_t kmax = __reduce_max_sync(0xffffffffu, kb);
-          const int e_best = static_cast<int>(__reduce_min_sync(0xffffffffu, kb == kmax ? kidx : 0xFFFFFFFFu));
-          const float s_best = __uint_as_float(kmax - 1u);
-          if (lane == (e_best & 31)) {
-#pragma unroll
-            for (int i = 0; i < kTopkRegs; ++i)
-              if (i == (e_best >> 5)) sc[i] = -1.0f;
-          }
-          if (lane == j) { wsel = s_best; isel = e_best; }
-          if (j >= 32 && lane == 0) {  // k > 32: write directly (rare)
-            p.topk_idx[(size_t)t * p.k + j] = e_best;
-            p.topk_w[(size_t)t * p.k + j] = s_best;
-          }
-        }
-      }
-      for (int j = 0; j < (p.E <= 32 * kTopkRegs ? 0 : p.k); ++j) {
-        // largest key (score bits desc, index asc) in two warp reductions: the
-        // max of score bits + 1 (0: no candidate), then the lowest index holding it
-        uint32_t kb = 0, kidx = 0xFFFFFFFFu;
-        for (int e = lane; e < p.E; e += 32) {  // ascending e: the first max is the lowest index
-          float sc = static_cast<float>(row[e]);
-          if (sc < 0.0f) continue;  // already selected (marked -1)
-          const uint32_t key = ((sc == 0.0f) ? 0u : __float_as_uint(sc)) + 1u;
-          if (key > kb) { kb = key; kidx = static_cast<uint32_t>(e); }
-        }
-        const uint32_t kmax = __reduce_max_sync(0xffffffffu, kb);
-        const int e_best = static_cast<int>(__reduce_min_sync(0xffffffffu, kb == kmax ? kidx : 0xFFFFFFFFu));
-        const float s_best = __uint_as_float(kmax - 1u);
-        __syncwarp();
-        if (lane == (e_best & 31)) row[e_best] = -1.0;
-        __syncwarp();
-        if (lane == j) { wsel = s_best; isel = e_best; }
-        if (j >= 32) {  // k > 32: write directly (rare)
-          if (lane == 0) {
-            p.topk_idx[(size_t)t * p.k + j] = e_best;
-            p.topk_w[(size_t)t * p.k + j] = s_best;
-          }
-        }
-      }
-      __syncwarp();
-      stamp2(14);
-      if (p.gating == 1) {
-        // renormalise over the selected k with numpy's fp32 pairwise sum
-        float* wrow = reinterpret_cast<float*>(row);
-        if (lane < p.k && lane < 32) wrow[lane] = wsel;
-        __syncwarp();
-        if (p.k > 32 && lane == 0) {
-          for (int j = 32; j < p.k; ++j) wrow[j] = p.topk_w[(size_t)t * p.k + j];
-        }
-        __syncwarp();
-        float S = 0.0f;
-        if (lane == 0) S = pairwise_sum<float>(wrow, p.k);
-        S = __shfl_sync(0xffffffffu, S, 0);
-        const float uni = __double2float_rn(1.0 / static_cast<double>(p.k));
-        if (lane < p.k) wsel = (S == 0.0f) ? uni : __fdiv_rn(wsel, S);
-        if (p.k > 32 && lane == 0) {
-          for (int j = 32; j < p.k; ++j) {
-            float v = wrow[j];
-            p.topk_w[(size_t)t * p.k + j] = (S == 0.0f) ? uni : __fdiv_rn(v, S);
-          }
-        }
-        __syncwarp();
-      }
+    int isel = 0;
+    float wsel = 0.0f;
+    eval_route_outputs(p, t, lo, m, row, lane, isel, wsel);
+    stamp2(14);
       if (lane < p.k) {
         p.topk_idx[(size_t)t * p.k + lane] = isel;
         p.topk_w[(size_t)t * p.k + lane] = wsel;

@@ -45,4 +45,5 @@ for i, nm in ((8, "p2 lbuf"), (9, "p2 certified"), (15, "p2 exp"), (1, "p2 sum")
     v = t[:, i][t[:, i] > 0]
     if len(v):
         print(f"  {nm:12s} n={len(v):5d} cycles from phase-2 entry min/med/max {v.min()}/{int(np.median(v))}/{v.max()}")
-print(f"  exact chains: certify-round {int(t[:, 11].sum())}, max-uncertain {int(t[:, 12].sum())}; logits {B*E}")
+print(f"  exact chains: certify-round {int(t[:, 11].sum())}, max-uncertain {int((t[:, 12] & 0xFFFFFFFF).sum())}; "
+      f"enumeration-certified tokens {int((t[:, 12] >> 32).sum())}; logits {B*E}")

@@ -475,3 +475,46 @@ def test_certificate_recompute_fires_near_midpoints(P, gating):
     lg = O.router_logits(x, wr)
     assert (lg != a[None, :]).any() and (lg == a[None, :]).any()
     assert recomputed > 0, "the certificate never sent a logit to the exact chain"
+
+
+def test_certificate_enumeration_avoids_recompute(P):
+    """Softmax routing with ONE logit (a non-selected expert, far below the
+    row max) whose exact fold sits one fp64 ulp from an fp32 rounding
+    midpoint: its certified interval holds two fp32 candidates, and phase 2
+    evaluates the token's outputs for both instead of running the exact chain.
+    Routing stays bit-exact, the enumeration fires and no logit is recomputed."""
+    from paper_2605_23911_b200 import _lib
+    lib = _lib.load()
+    E, k, d, B = 8, 2, 64, 64
+    rng = np.random.default_rng(11)
+    a = np.array([2.0, 1.75, 0.5, -0.25, 1.0, -1.0, 0.125, -20.3], np.float32)
+    wr = np.zeros((d, E), np.float32)
+    wr[0] = a
+    wr[1, 7] = np.float32(np.spacing(np.float32(20.3)) / 2) * -1.0   # half an fp32 ulp (toward -inf)
+    wr[2, 7] = np.float32(2.0 ** -48)                                 # one fp64 ulp at |l| ~ 20
+    wr[3:] = (rng.standard_normal((d - 3, E)) * 1e-30).astype(np.float32)
+    x = np.zeros((B, d), np.float32)
+    x[:, 0] = 1.0
+    x[:, 1] = 1.0
+    x[:, 2] = rng.choice([-1.0, 1.0], B).astype(np.float32)
+    cfg = P.ModelConfig(E, k, d, 8, P.Gating("softmax"))
+    z = np.zeros((E * d, 8), np.float32)
+    layer = P.MoELayer(cfg, P.ExpertWeights(z, z, np.zeros((E * 8, d), np.float32)), wr, max_tokens=B)
+    trace = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
+    lib.moe_b200_debug_set_router_trace.argtypes = [ctypes.c_void_p]
+    lib.moe_b200_debug_set_router_trace(ctypes.c_void_p(trace.data_ptr()))
+    try:
+        r = layer.route(torch.from_numpy(x).cuda())
+        torch.cuda.synchronize()
+    finally:
+        lib.moe_b200_debug_set_router_trace(ctypes.c_void_p(0))
+    t = trace.view(-1, 16).cpu().numpy()
+    enumerated = int((t[:, 12] >> 32).sum())
+    recomputed = int(t[:, 11].sum() + (t[:, 12] & 0xFFFFFFFF).sum())
+    idx_ref, w_ref = O.route(x, wr, k, "softmax")
+    bits_equal(r["indices"].cpu().numpy().astype(np.int64), idx_ref)
+    bits_equal(r["weights"].cpu().numpy(), w_ref)
+    lg = O.router_logits(x, wr)
+    assert len(np.unique(lg[:, 7])) == 2, "the construction should put expert 7 on both sides of the midpoint"
+    assert enumerated > 0, "the enumeration certificate never fired"
+    assert recomputed == 0, f"{recomputed} logits went to the exact chain"
