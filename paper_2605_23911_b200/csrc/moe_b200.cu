@@ -19,6 +19,7 @@
 #include "ffn.cuh"
 #include "router.cuh"
 #include "router_seg.cuh"
+#include "router_screen.cuh"
 #include "dispatch.cuh"
 #include "ep_p2p.cuh"
 #include "stages.cuh"
@@ -82,6 +83,7 @@ struct Tuning {
   int seg_w64 = 0;           // MOE_B200_SEG_W64: segment router reads W pre-widened to fp64
   int rx_quarter = 1;        // MOE_B200_RX_QUARTER: 4 x 2 quarter-warp tiles in the exact router (0: 2 x 4)
   int fuse_dispatch = 1;     // MOE_B200_FUSE_DISPATCH: small batches dispatch inside the router (0: separate launch)
+  int screen = -1;           // MOE_B200_SCREEN: sigmoid router via the INT8 screen (-1 auto, 0 off, 1 always)
 };
 Tuning g_tune;
 std::mutex g_tune_mu;
@@ -112,6 +114,7 @@ void load_tuning_locked() {
   t.seg_w64 = geti("MOE_B200_SEG_W64", 0);
   t.rx_quarter = geti("MOE_B200_RX_QUARTER", 1);
   t.fuse_dispatch = geti("MOE_B200_FUSE_DISPATCH", 1);
+  t.screen = geti("MOE_B200_SCREEN", -1);
   g_tune = t;
   g_tune_loaded = true;
 }
@@ -149,10 +152,15 @@ constexpr int kHdrBlk = 16 + kTbCap + kChunkCap;
 // BASELINE config), else the combine simply runs after the FFN
 constexpr int kTokCntCap = 64 * 1024;
 constexpr int kHdrTok = 16 + kTbCap + kChunkCap + kBlkCap;
-constexpr size_t kHeaderBytes = align256((16 + kTbCap + kChunkCap + kBlkCap + kTokCntCap) * sizeof(int32_t));
+// per-expert statistics of the screening router (router_screen.cuh; max |w|,
+// max quantisation error, sum |G2| as u32, sum |Q| as u64), self-resetting
+constexpr int kHdrScr = 16 + kTbCap + kChunkCap + kBlkCap + kTokCntCap;
+static_assert(kHdrScr % 2 == 0, "u64 alignment of the screen statistics");
+constexpr size_t kHeaderBytes = align256((kHdrScr + 5 * kMaxExperts) * sizeof(int32_t));
 
 struct Layout {
   size_t logits, lbuf, gpart, w64, chunk_tab, prow, xp, h, ys, rt_idx, rt_w, rt_misc, gu32, total;
+  size_t s_xq, s_wq, s_xst, s_xqs, s_part, s_cand, s_ncand, s_elist, s_rpart;  // screening router (0: unused)
   int max_chunks, splits, kb_per_split, T_pad, n_ft, n_dp;
 };
 
@@ -271,6 +279,76 @@ SegPlan plan_seg(const moe_b200_config& c, int64_t B) {
   return q;
 }
 
+// ---- screening router plan (router_screen.cuh) --------------------------------
+// Sigmoid gating in the exact router's regime (B x E above the segment
+// router's chain budget): INT8 screen + candidate refinement.
+// MOE_B200_SCREEN=0 keeps the exact router, =1 uses the screen for every
+// sigmoid batch (tests / A/B).
+bool screen_applies(const moe_b200_config& c, int64_t B) {
+  const int v = tuning().screen;
+  if (v == 0 || c.gating != MOE_B200_GATING_SIGMOID_NORMALIZED || c.top_k > kScrMaxCand || B < 1) return false;
+  // the refinement keeps the segment's W rows and every token row in shared memory
+  if ((size_t)2 * c.num_experts * 12 + (size_t)B * 12 > (size_t)220 * 1024) return false;
+  if (v == 1) return true;
+  return B > seg_max_tokens(c);
+}
+
+struct ScreenPlan {
+  int B_pad, E_pad, d_pad, n_tt, n_eb, nkb, n_ks, kbps, n_rs, rs_len, rs_first;
+  size_t ref_smem, sel_smem, ph2_smem;
+};
+
+int screen_splits(int nkb, long tiles, int* kbps) {
+  const int want = static_cast<int>(std::max(1L, std::min<long>(nkb, kNumSMs / std::max(1L, tiles))));
+  *kbps = (nkb + want - 1) / want;
+  return (nkb + *kbps - 1) / *kbps;
+}
+
+ScreenPlan plan_screen(const moe_b200_config& c, int64_t B) {
+  ScreenPlan q{};
+  const int E = c.num_experts, d = c.hidden_dim;
+  q.B_pad = static_cast<int>((B + kScrM - 1) / kScrM * kScrM);
+  q.E_pad = (E + kScrN - 1) / kScrN * kScrN;
+  q.d_pad = (d + kScrKB - 1) / kScrKB * kScrKB;
+  q.n_tt = q.B_pad / kScrM;
+  q.n_eb = q.E_pad / kScrN;
+  q.nkb = q.d_pad / kScrKB;
+  q.n_ks = screen_splits(q.nkb, (long)q.n_tt * q.n_eb, &q.kbps);
+  // refine: ~128 segments of the d axis (one per CTA), the W rows of a
+  // segment in shared memory (<= 200 KB); segment 0 takes the remainder
+  // x rows of the segment staged per token group (odd row stride)
+  // (even lengths: the token rows are staged as 4-byte words, bf16 pairs;
+  // the W rows are widened to fp64; W rows + all B token rows of the segment
+  // + the unit offsets fit in shared memory)
+  auto smem_for = [&](int l) {
+    const size_t x = std::max((size_t)B * (size_t)(l | 1) * 4, (size_t)l * E * 4);  // (W staging reuses the x area)
+    return (size_t)l * E * 8 + x + (size_t)(E + 1) * 4;
+  };
+  int len = std::max(8, (d + kNumSMs - 5) / (kNumSMs - 4));  // one wave of segments
+  len = (len + 1) & ~1;
+  while (len > 2 && smem_for(len) > (size_t)220 * 1024) len -= 2;
+  q.rs_len = len;
+  q.n_rs = (d + len - 1) / len;
+  q.rs_first = d - (q.n_rs - 1) * len;
+  q.ref_smem = smem_for(len);
+  q.sel_smem = (size_t)2 * E * sizeof(float);
+  q.ph2_smem = (size_t)kScrPh2Tok * (E * 16 + kChainWin * 8) + kScrPh2Tok * 32 * sizeof(float);
+  return q;
+}
+
+// rows of the screen's split-K partial slab for any batch <= B (the split
+// count falls as the token tiles grow, not monotonically in B)
+size_t screen_part_rows(const moe_b200_config& c, int64_t B) {
+  const ScreenPlan q = plan_screen(c, B);
+  size_t rows = 0;
+  for (int tt = 1; tt <= q.n_tt; ++tt) {
+    int kbps = 0;
+    const int ks = screen_splits(q.nkb, (long)tt * q.n_eb, &kbps);
+    rows = std::max(rows, (size_t)ks * tt * kScrM);
+  }
+  return rows;
+}
+
 Layout layout_for(const moe_b200_config& c, int64_t B, int s_force = 0) {
   Layout L{};
   const int64_t T = B * c.top_k;
@@ -315,6 +393,18 @@ Layout layout_for(const moe_b200_config& c, int64_t B, int s_force = 0) {
   L.rt_misc = off;   off = align256(off + (size_t)(2 * c.num_experts + 1 + 2 * T) * sizeof(int32_t));
   // unfused ablation: tiled fp32 gate and up projections [2][f/128][T_pad][128]
   L.gu32 = off;      off = align256(off + (size_t)2 * L.n_ft * L.T_pad * kBM * sizeof(float));
+  if (screen_applies(c, B)) {
+    const ScreenPlan q = plan_screen(c, B);
+    L.s_xq = off;     off = align256(off + (size_t)kScrPlanes * q.B_pad * q.d_pad);
+    L.s_wq = off;     off = align256(off + (size_t)kScrPlanes * q.E_pad * q.d_pad);
+    L.s_xst = off;    off = align256(off + (size_t)B * sizeof(int4));
+    L.s_xqs = off;    off = align256(off + (size_t)B * sizeof(long long));
+    L.s_part = off;   off = align256(off + screen_part_rows(c, B) * q.E_pad * sizeof(long long));
+    L.s_cand = off;   off = align256(off + (size_t)B * kScrMaxCand * sizeof(int32_t));
+    L.s_ncand = off;  off = align256(off + (size_t)B * sizeof(int32_t));
+    L.s_elist = off;  off = align256(off + (size_t)c.num_experts * B * sizeof(int32_t));
+    L.s_rpart = off;  off = align256(off + (size_t)q.n_rs * B * kScrMaxCand * sizeof(double2));
+  }
   L.total = off;
   return L;
 }
@@ -897,6 +987,7 @@ int moe_b200_workspace_size(const moe_b200_config* cfg, int64_t max_tokens, size
   int rc = check_config(cfg);
   if (rc) return rc;
   if (max_tokens < 0 || !bytes) return MOE_B200_ERR_INVALID_VALUE;
+  reload_tuning();  // (the hooks shape the layout: size and init read the same values)
   // the down-split count falls as B grows (down_split_count) while the padded
   // row space grows: size for the largest B of every split count <= max_tokens
   size_t total = layout_for(*cfg, max_tokens).total;
@@ -931,6 +1022,77 @@ int moe_b200_read_flags(const moe_b200_config* cfg, int64_t max_tokens, void* ws
   MOE_CUDA(cudaMemcpyAsync(flags, ws, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   MOE_CUDA(cudaMemsetAsync(ws, 0, sizeof(uint32_t), s));
   MOE_CUDA(cudaStreamSynchronize(s));
+  return MOE_B200_OK;
+}
+
+// Screening router (router_screen.cuh): W max -> digit planes -> INT8 screen
+// GEMM -> intervals + candidates -> candidate refinement -> merge + phase 2.
+int launch_router_screen(const moe_b200_config& c, int64_t B, const void* x, int xb, const float* w_router,
+                         const Layout& L, void* ws, RouterParams& p, cudaStream_t s) {
+  const ScreenPlan q = plan_screen(c, B);
+  int32_t* hdr = reinterpret_cast<int32_t*>(ws);
+  ScreenParams sp{};
+  sp.x = x; sp.wr = w_router;
+  sp.B = static_cast<int>(B); sp.d = c.hidden_dim; sp.E = c.num_experts; sp.k = c.top_k;
+  sp.B_pad = q.B_pad; sp.E_pad = q.E_pad; sp.d_pad = q.d_pad;
+  sp.n_ks = q.n_ks; sp.kb_per_split = q.kbps;
+  sp.xq = reinterpret_cast<int8_t*>(ws8(ws) + L.s_xq);
+  sp.wq = reinterpret_cast<int8_t*>(ws8(ws) + L.s_wq);
+  sp.xst = reinterpret_cast<int4*>(ws8(ws) + L.s_xst);
+  sp.xqs = reinterpret_cast<long long*>(ws8(ws) + L.s_xqs);
+  uint32_t* st = reinterpret_cast<uint32_t*>(hdr + kHdrScr);
+  sp.wmax = st; sp.ecount = reinterpret_cast<int32_t*>(st + kMaxExperts); sp.wg2 = st + 2 * kMaxExperts;
+  sp.wrs = reinterpret_cast<unsigned long long*>(st + 3 * kMaxExperts);
+  sp.spart = reinterpret_cast<long long*>(ws8(ws) + L.s_part);
+  sp.cand = reinterpret_cast<int32_t*>(ws8(ws) + L.s_cand);
+  sp.ncand = reinterpret_cast<int32_t*>(ws8(ws) + L.s_ncand);
+  sp.elist = reinterpret_cast<int32_t*>(ws8(ws) + L.s_elist);
+  sp.rpart = reinterpret_cast<double2*>(ws8(ws) + L.s_rpart);
+  sp.n_rs = q.n_rs; sp.rs_len = q.rs_len; sp.rs_first = q.rs_first;
+  sp.lbuf = p.lbuf;
+  sp.flags = p.flags;
+  // TMA maps over the stacked digit planes (rows: plane-major)
+  CUtensorMap tmx, tmw;
+  {
+    int rc = get_encoder();
+    if (rc) return rc;
+    auto enc = [&](CUtensorMap* m, void* base, int rows) -> bool {
+      cuuint64_t dims[2] = {(cuuint64_t)q.d_pad, (cuuint64_t)rows};
+      cuuint64_t strides[1] = {(cuuint64_t)q.d_pad};
+      cuuint32_t box[2] = {(cuuint32_t)kScrKB, (cuuint32_t)kScrM};
+      cuuint32_t estr[2] = {1, 1};
+      return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    if (!enc(&tmx, sp.xq, kScrPlanes * q.B_pad) || !enc(&tmw, sp.wq, kScrPlanes * q.E_pad)) {
+      g_last_error = "cuTensorMapEncodeTiled(screen digits) failed";
+      return MOE_B200_ERR_CUDA;
+    }
+  }
+  screen_wmax_kernel<<<dim3((c.hidden_dim + 63) / 64, (c.num_experts + 31) / 32), 256, 0, s>>>(sp);
+  MOE_LAUNCH_CHECK("screen_wmax_kernel");
+  const int n_wtiles = (q.d_pad / kScrKB) * (q.E_pad / 32);
+  if (xb) screen_digits_kernel<true><<<static_cast<unsigned>(B + n_wtiles), 256, 0, s>>>(sp);
+  else screen_digits_kernel<false><<<static_cast<unsigned>(B + n_wtiles), 256, 0, s>>>(sp);
+  MOE_LAUNCH_CHECK("screen_digits_kernel");
+  MOE_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(screen_gemm_kernel), kScrGemmSmem));
+  screen_gemm_kernel<<<q.n_tt * q.n_eb * q.n_ks, kScrThreads, kScrGemmSmem, s>>>(tmx, tmw, sp);
+  MOE_LAUNCH_CHECK("screen_gemm_kernel");
+  MOE_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(screen_select_kernel), q.sel_smem));
+  screen_select_kernel<<<static_cast<unsigned>(B), kScrSelThreads, q.sel_smem, s>>>(sp);
+  MOE_LAUNCH_CHECK("screen_select_kernel");
+  auto ref = xb ? screen_refine_kernel<true> : screen_refine_kernel<false>;
+  MOE_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(ref), q.ref_smem));
+  ref<<<q.n_rs, kScrRefThreads, q.ref_smem, s>>>(sp);
+  MOE_LAUNCH_CHECK("screen_refine_kernel");
+  p.screen = 1;
+  p.seg_len = 0;
+  const double coef = ldexp((2.0 + 12.0 / q.rs_len) * (1.0 + ldexp(1.0, -20)), -53);
+  auto ph2 = xb ? screen_phase2_kernel<true> : screen_phase2_kernel<false>;
+  MOE_CUDA(ensure_dyn_smem(reinterpret_cast<const void*>(ph2), q.ph2_smem));
+  ph2<<<static_cast<unsigned>((B + kScrPh2Tok - 1) / kScrPh2Tok), kScrPh2Threads, q.ph2_smem, s>>>(sp, p, coef);
+  MOE_LAUNCH_CHECK("screen_phase2_kernel");
   return MOE_B200_OK;
 }
 
@@ -975,7 +1137,8 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
   p.trace = g_router_trace;
 
   bool fused_disp = false;
-  if (B <= seg_max_tokens(*cfg)) {
+  const bool use_screen = screen_applies(*cfg, B) && !p.want_logits && !p.force_exact;
+  if (B <= seg_max_tokens(*cfg) && !use_screen) {
     // latency regime: certified split-K segments (router_seg.cuh)
     const SegPlan q = plan_seg(*cfg, B);
     if (q.n_tb > kTbCap || (long)q.n_tb * q.n_eb > kBlkCap) return MOE_B200_ERR_UNSUPPORTED;
@@ -1013,6 +1176,8 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
     apply_carveout(reinterpret_cast<const void*>(kern));
     kern<<<grid, kSegThreads, q.smem, s>>>(p);
     MOE_LAUNCH_CHECK("router_seg_kernel");
+  } else if (use_screen) {
+    if ((rc = launch_router_screen(*cfg, B, x, xb, w_router, L, ws, p, s))) return rc;
   } else if ((rc = launch_router_exact(*cfg, B, x, xb, w_router, L, ws, p, s))) {
     return rc;
   }

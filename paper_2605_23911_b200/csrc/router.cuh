@@ -24,6 +24,8 @@
 // counters self-reset.
 #pragma once
 
+#include <cfloat>
+
 #include "common.cuh"
 
 namespace moe {
@@ -69,6 +71,9 @@ struct RouterParams {
   __nv_bfloat16* xp;    // permuted-token gather target (null: no gather)
   int2* chunk_grp;      // {first chunk of the expert, chunks of the expert}
   int32_t* disp_counter;// self-resetting (token blocks that finished phase 2)
+  // screen mode (router_screen.cuh): lbuf holds screen intervals (refined for
+  // the candidates); phase 2 first excludes the experts that cannot reach the top-k
+  int screen;
 };
 
 // ---------------------------------------------------------------------------
@@ -493,6 +498,39 @@ MOE_DEVICE float warp_max_f32(float v) {
   return v;
 }
 
+// Screen mode (router_screen.cuh, sigmoid gating): score bounds of a logit
+// interval.  np_sigmoid is accurate to a few ulps but not monotone at the
+// ulp level: the bounds carry a 2^-20 relative (and 2^-126 absolute) margin.
+// logit >= l, upper bound for a logit <= l
+MOE_DEVICE float scr_score_lo(float l) {
+  if (isnan(l)) return 0.0f;
+  return __fmul_rd(np_sigmoid(l), 1.0f - 0x1p-20f);
+}
+MOE_DEVICE float scr_score_hi(float l) {
+  if (isnan(l)) return 2.0f;
+  return __fmaf_ru(np_sigmoid(l), 1.0f + 0x1p-20f, 0x1p-126f);
+}
+
+// k-th largest of v[0..n) (a warp; destroys v): k rounds of warp max, each
+// removing one instance
+MOE_DEVICE float scr_kth_largest(float* v, int n, int k, int lane) {
+  float m = 0.0f;
+  for (int j = 0; j < k; ++j) {
+    float bm = -1.0f;
+    int bi = 0x7fffffff;
+    for (int e = lane; e < n; e += 32)
+      if (v[e] > bm) { bm = v[e]; bi = e; }
+    m = bm;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const int owner = __reduce_min_sync(0xffffffffu, bm == m ? bi : 0x7fffffff);
+    __syncwarp();
+    if (lane == (owner & 31) && owner < n) v[owner] = -1.0f;
+    __syncwarp();
+  }
+  return m;
+}
+
 constexpr int kTopkRegs = 8;  // phase-2 top-k keeps E <= 256 scores in registers
 
 // Scores (softmax: numpy float64 exp of the fp32-shifted logits, pairwise
@@ -689,6 +727,8 @@ __device__ __noinline__ float certify_token(const RouterParams& p, int t, float*
             const float sa = np_sigmoid(a);
             float c = a;
             int steps = 0;
+            // every logit >= 18 scores exactly 1.0f (expf(-18) < 2^-25: 1 + t rounds to 1)
+            if (a >= 18.0f) c = b;
             while (!nd && !same_bits(c, b)) {
               c = nextafterf(c, b);
               nd = (++steps > 8) || !same_bits(np_sigmoid(c), sa);
@@ -764,10 +804,13 @@ __device__ __noinline__ float certify_token(const RouterParams& p, int t, float*
 // is recomputed with the exact sequential chain.  want_logits resolves all.
 // ---------------------------------------------------------------------------
 template <bool kXBf16>
-MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_end, uint8_t* smem) {
+MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_end, uint8_t* smem,
+                                    int warp_override = -1) {
   const int tid = threadIdx.x;
-  const int nwarps = blockDim.x / 32;
-  const int warp = tid / 32, lane = tid % 32;
+  // warp_override >= 0: only the calling warp, on token t_begin, with its
+  // scratch at smem (the screening router's per-token fallback)
+  const int nwarps = warp_override >= 0 ? 1 : blockDim.x / 32;
+  const int warp = warp_override >= 0 ? 0 : tid / 32, lane = tid % 32;
   uint8_t* base = smem + (size_t)warp * (p.E * 16 + kChainWin * 8);
   double* row = reinterpret_cast<double*>(base);
   float* lo = reinterpret_cast<float*>(base + (size_t)p.E * 8);
@@ -786,6 +829,19 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
       hi[e] = v.y;
     }
     __syncwarp();
+    if (p.screen) {
+      // exclusion: an expert whose upper score bound is below the k-th largest
+      // lower bound has k experts strictly above it and is never selected;
+      // its logit becomes a certain -FLT_MAX (score 0 < S_k)
+      float* sl = reinterpret_cast<float*>(row);
+      for (int e = lane; e < p.E; e += 32) sl[e] = scr_score_lo(lo[e]);
+      __syncwarp();
+      const float Sk = scr_kth_largest(sl, p.E, p.k, lane);
+      if (Sk >= 0x1p-100f)
+        for (int e = lane; e < p.E; e += 32)
+          if (scr_score_hi(hi[e]) < Sk) { lo[e] = -FLT_MAX; hi[e] = -FLT_MAX; }
+      __syncwarp();
+    }
     stamp2(8);
     // ---- certification; `round` 0: unknown (+ everything if want_logits),
     //      1: whatever the outputs still depend on.  Fast path: every interval
@@ -823,7 +879,7 @@ MOE_DEVICE void route_scores_tokens(const RouterParams& p, int t_begin, int t_en
 // warps release stages through empty[s] (one arrival per warp).
 template <bool kXBf16, int kTE, int kTT, int kKC>
 __global__ void __launch_bounds__(384)
-router_kernel(const __grid_constant__ CUtensorMap tm_x, const RouterParams p) {
+router_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ RouterParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x;
   const int nthreads = blockDim.x;

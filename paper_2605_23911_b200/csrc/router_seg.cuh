@@ -13,12 +13,15 @@
 // with C_s the prefix of the segment totals; the segment sums themselves err
 // by at most u * m_s.  Hence with
 //   A = sum_s (L_s |C_s| + m_s),   s^ = sum_s c_s
-// the reference value lies in [s^ - D, s^ + D] for D = u A (2 + 12/L)(1 + 2^-20):
+// the reference value lies in [s^ - D, s^ + D] for D = u A (2 + 12/L)(1 + 2^-20) + 8u|s^|:
 //   u A        bounds the reference fold's own rounding (|a_i| <= |C_s| + |b_j|),
 //   u sum m_s  (<= u A) the segment folds' rounding,
 //   u sum |C_node| over the merge tree (<= 5 warp-tree levels plus the
 //              sequential cross-warp / cross-k-block prefixes, each level
-//              <= 2A/L) the merges' rounding,
+//              <= 2A/L) the merges' rounding of the interior prefixes, and
+//   8u|s^|     the rightmost nodes' (<= 7 merges -- 5 tree levels, the last
+//              warp, the last k-block -- end at the total, which is not a
+//              segment boundary, so A/L does not bound it),
 // and (1 + 2^-20) covers the O(d u) second-order terms and the rounding of A
 // itself (tests/test_certificate.py restates this arithmetic in numpy and
 // checks it on random and adversarial inputs).  The fp32 rounding of every point of that interval
@@ -75,14 +78,16 @@ MOE_DEVICE void seg_finalize(const RouterParams& p, int t, int e, double s, doub
   if (!(A > 0.0) || !isfinite(s) || p.force_exact) {
     r = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));  // unknown: recompute exactly
   } else {
-    const double D = __dmul_ru(A, p.cert_coef);
+    // + 8 u |s|: the merges' roundings of the running total itself (the
+    // rightmost node of each merge level sums up to the whole chain)
+    const double D = __dadd_ru(__dmul_ru(A, p.cert_coef), __dmul_ru(fabs(s), 0x1p-50));
     r = make_float2(__double2float_rn(__dsub_rd(s, D)), __double2float_rn(__dadd_ru(s, D)));
   }
   p.lbuf[(size_t)t * p.E + e] = r;
 }
 
 template <bool kXBf16, bool kWVec, bool kW64 = false>
-__global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const RouterParams p) {
+__global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const __grid_constant__ RouterParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TT = kSegTT, TE = kSegTE;
   const int tid = threadIdx.x;

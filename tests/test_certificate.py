@@ -8,7 +8,7 @@ m_s = sum |partial|, and merges adjacent ranges with
     C = C_l + C_r,  A = A_l + A_r + K_r |C_l|,  K = K_l + K_r
 in the kernel's order: a binary shuffle tree over the 32/G segments of a warp,
 then sequentially over the 8 warps, then sequentially over the k-blocks.  It
-claims the sequential value lies in [s - D, s + D], D = u A (2 + 12/L)(1 + 2^-20).
+claims the sequential value lies in [s - D, s + D], D = u A (2 + 12/L)(1 + 2^-20) + 8u|s|.
 This test restates that arithmetic in numpy (same fp64 operations, same
 merge order) and checks the claim on random and adversarial inputs.
 """
@@ -57,7 +57,7 @@ def certificate(p: np.ndarray, seg_len: int, G: int = 2, threads: int = 256):
             blk = _merge(blk, wv)
         total = blk if total is None else _merge(total, blk)  # sequential over k-blocks
     s_hat, A, _ = total
-    D = A * (2.0 + 12.0 / seg_len) * (1.0 + 2.0 ** -20) * U
+    D = A * (2.0 + 12.0 / seg_len) * (1.0 + 2.0 ** -20) * U + abs(s_hat) * 2.0 ** -50
     return s_hat, A, D
 
 
