@@ -609,14 +609,6 @@ __global__ void __launch_bounds__(kScrRefThreads) screen_refine_kernel(const Scr
     out = ((size_t)j * p.B + t) * kScrMaxCand + id % kScrMaxCand;
     return true;
   };
-  auto xval = [&](int xo, int kk) -> double {
-    if constexpr (kXBf16) {
-      const uint32_t w = xs[xo + (kk >> 1)];
-      return static_cast<double>(__uint_as_float((kk & 1) ? (w & 0xFFFF0000u) : (w << 16)));
-    } else {
-      return static_cast<double>(__uint_as_float(xs[xo + kk]));
-    }
-  };
   // two chains per lane (independent folds); a warp's 32 consecutive list
   // entries span 1-3 experts, so each W read is a broadcast of few words
   const int stride = 2 * 32 * nw;
@@ -626,11 +618,30 @@ __global__ void __launch_bounds__(kScrRefThreads) screen_refine_kernel(const Scr
     const bool va = chain(q0 + lane, ea, xa, oa);
     const bool vb = chain(q0 + 32 + lane, eb, xbo, ob);
     double acc_a = -0.0, mag_a = 0.0, acc_b = -0.0, mag_b = 0.0;
+    // two k steps per iteration (len is even): one word holds both bf16 x values
+    const double* wa = ws + ea;
+    const double* wb = ws + eb;
+    const uint32_t* pa = xs + xa;
+    const uint32_t* pb = xs + xbo;
 #pragma unroll 2
-    for (int kk = 0; kk < len; ++kk) {
-      const double* wrow = ws + (size_t)kk * p.E;
-      acc_a = __fma_rn(xval(xa, kk), wrow[ea], acc_a);
-      acc_b = __fma_rn(xval(xbo, kk), wrow[eb], acc_b);
+    for (int kk = 0; kk < len; kk += 2) {
+      float xa0, xa1, xb0, xb1;
+      if constexpr (kXBf16) {
+        const uint32_t ua = pa[kk >> 1], ub = pb[kk >> 1];
+        xa0 = __uint_as_float(ua << 16); xa1 = __uint_as_float(ua & 0xFFFF0000u);
+        xb0 = __uint_as_float(ub << 16); xb1 = __uint_as_float(ub & 0xFFFF0000u);
+      } else {
+        xa0 = __uint_as_float(pa[kk]); xa1 = __uint_as_float(pa[kk + 1]);
+        xb0 = __uint_as_float(pb[kk]); xb1 = __uint_as_float(pb[kk + 1]);
+      }
+      const double w_a0 = wa[(size_t)kk * p.E], w_a1 = wa[(size_t)(kk + 1) * p.E];
+      const double w_b0 = wb[(size_t)kk * p.E], w_b1 = wb[(size_t)(kk + 1) * p.E];
+      acc_a = __fma_rn(static_cast<double>(xa0), w_a0, acc_a);
+      acc_b = __fma_rn(static_cast<double>(xb0), w_b0, acc_b);
+      mag_a = __dadd_rn(mag_a, fabs(acc_a));
+      mag_b = __dadd_rn(mag_b, fabs(acc_b));
+      acc_a = __fma_rn(static_cast<double>(xa1), w_a1, acc_a);
+      acc_b = __fma_rn(static_cast<double>(xb1), w_b1, acc_b);
       mag_a = __dadd_rn(mag_a, fabs(acc_a));
       mag_b = __dadd_rn(mag_b, fabs(acc_b));
     }
