@@ -17,6 +17,13 @@ timeout 900 python bench.py --gpus 2 --steps 10 --warmup 3 > gpurun_out/bench_ep
 N="timeout 600 ncu --clock-control none"
 $N --metrics gpu__time_duration.sum --csv --log-file gpurun_out/launches_$TAG.csv python scripts/run_layer.py mixtral 512 3 > /dev/null 2>&1
 $N --metrics gpu__time_duration.sum --csv --log-file gpurun_out/launches_qwen60_$TAG.csv python scripts/run_layer.py qwen60 512 3 > /dev/null 2>&1
+$N --metrics gpu__time_duration.sum --csv --log-file gpurun_out/launches_deepseek_$TAG.csv python scripts/run_layer.py deepseek 512 3 > /dev/null 2>&1
+$N --metrics gpu__time_duration.sum --csv --log-file gpurun_out/launches_mixtral1_$TAG.csv python scripts/run_layer.py mixtral 1 3 > /dev/null 2>&1
+# the sigmoid router's INT8 screen path (DeepSeek-V3): every kernel of one route, and an A/B line with the exact router
+$N --set full --import-source on -k regex:screen -s 6 -c 6 -o /tmp/prof_screen_deepseek_$TAG -f python scripts/run_layer.py deepseek 512 2 > /dev/null 2>&1
+ncu -i /tmp/prof_screen_deepseek_$TAG.ncu-rep --page raw --csv > gpurun_out/prof_screen_deepseek_${TAG}_raw.csv 2>/dev/null
+MOE_B200_SCREEN=0 $B --config deepseek --steps 20 --warmup 3 --no-cpu > gpurun_out/bench_exact_router_$TAG.json 2>> gpurun_out/bench_$TAG.err
+timeout 300 python scripts/screen_debug.py deepseek 512 > gpurun_out/screen_debug_$TAG.log 2>&1
 # ncu --set full captures go to /tmp (each ~8 MB; gpurun brings back <= 64 MiB):
 # their raw metric pages come back as csv, and the Mixtral FFN report itself
 for c in mixtral qwen60 deepseek skew64; do

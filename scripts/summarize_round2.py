@@ -67,7 +67,8 @@ out.append("| workload | us/step | tok/s | e2e tok/s | roofline frac | stages ms
 out.append("|---|---|---|---|---|---|---|---|")
 rows = []
 for name in (f"bench_{tag}.json", f"bench_configs_{tag}.json", f"bench_skew_{tag}.json",
-             f"bench_unfused_{tag}.json", f"bench_ep2_{tag}.json", f"bench_ref_{tag}.json"):
+             f"bench_unfused_{tag}.json", f"bench_exact_router_{tag}.json", f"bench_ep2_{tag}.json",
+             f"bench_ref_{tag}.json"):
     for d in jl(name):
         rows.append((name, d))
         if d.get("impl") != "reference":
@@ -99,14 +100,15 @@ def ncu_launches(path):
     return [launches[i] for i in sorted(launches)]
 
 
-for cfg_name, fn in (("mixtral 512", f"launches_{tag}.csv"), ("qwen60 512", f"launches_qwen60_{tag}.csv")):
+FIRST = ("router_seg", "router_prep", "screen_wmax")  # the first launch of a forward
+for cfg_name, fn in (("mixtral 512", f"launches_{tag}.csv"), ("qwen60 512", f"launches_qwen60_{tag}.csv"),
+                     ("deepseek 512", f"launches_deepseek_{tag}.csv"), ("mixtral 1", f"launches_mixtral1_{tag}.csv")):
     section(f"launch list (ncu gpu__time_duration, cold, serialised) -- {cfg_name}, last forward")
     ls = [x for x in ncu_launches(os.path.join(G, fn)) if "moe::" in x["name"]]
     if not ls:
         continue
-    n_per = 3 if not any("combine" in x["name"] for x in ls[-4:]) else 4
-    n_per = 4 if any("router_prep" in x["name"] for x in ls[-4:]) else n_per
-    last = ls[-n_per:]
+    starts = [i for i, x in enumerate(ls) if any(f in x["name"] for f in FIRST)]
+    last = ls[starts[-1]:] if starts else ls[-4:]
     tot = sum(x["gpu__time_duration.sum"] for x in last)
     for x in last:
         t = x["gpu__time_duration.sum"]
@@ -124,7 +126,7 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
 tfile = os.path.join(P, "traffic.json")
 traffic = json.load(open(tfile)) if os.path.exists(tfile) else {}
 for kern, cfg in [("ffn", c) for c in ("mixtral", "qwen60", "deepseek", "skew64")] + [
-        ("router_seg", None), ("dispatch", None), ("combine_flag", None)]:
+        ("router_seg", None), ("dispatch", None), ("combine_flag", None), ("screen", "deepseek")]:
     raw = os.path.join(G, f"prof_{kern}_{cfg}_{tag}_raw.csv" if cfg else f"prof_{kern}_{tag}_raw.csv")
     if not os.path.exists(raw):
         continue
@@ -190,6 +192,13 @@ json.dump(rep, open(os.path.join(P, f"fusion_ablation_{tag}.json"), "w"), indent
 out.append("```")
 out.append(json.dumps(rep, indent=1)[:4000])
 out.append("```")
+
+dbg = os.path.join(G, f"screen_debug_{tag}.log")
+if os.path.exists(dbg):
+    section("screening router (DeepSeek-V3, 512 tokens): phase-2 path counters")
+    out.append("```")
+    out.extend(open(dbg).read().strip().splitlines())
+    out.append("```")
 
 open(os.path.join(P, f"summary_{tag}.md"), "w").write("\n".join(out) + "\n")
 print("\n".join(out))
