@@ -132,8 +132,8 @@ int moe_b200_combine(const moe_b200_config* cfg, int64_t num_tokens, const float
  * offsets, stable permutation, schedule, gather), ONE persistent FFN launch
  * (gate+up and down), and the deterministic weighted unpermute-combine,
  * overlapped with the FFN's tail (moe_b200_combine_overlapped) -- four
- * launches (five with the exact router's weight prep), no host
- * synchronisation.
+ * launches (five with the exact router's weight prep; nine when a sigmoid
+ * router above 64K logits runs the INT8 screen), no host synchronisation.
  * Intermediates live in `ws`; routing outputs are written to the caller's
  * buffers so the host can build the trace lazily from `counts`. */
 int moe_b200_forward(const moe_b200_config* cfg, int64_t num_tokens, const void* x, int x_dtype,
