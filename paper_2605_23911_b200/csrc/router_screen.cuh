@@ -675,6 +675,10 @@ __global__ void __launch_bounds__(kScrPh2Threads) screen_phase2_kernel(const __g
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   const int t0 = blockIdx.x * kScrPh2Tok, t1 = min(sp.B, t0 + kScrPh2Tok);
+  // debug timeline (p.trace): per CTA {globaltimer at entry, clock64 deltas}
+  unsigned long long* tr = (p.trace && threadIdx.x == 0) ? p.trace + 64 + (size_t)blockIdx.x * 8 : nullptr;
+  const long long c_start = clock64();
+  if (tr) { tr[0] = globaltimer_ns(); }
   if (blockIdx.x == 0)
     for (int e = threadIdx.x; e < sp.E; e += blockDim.x) sp.ecount[e] = 0;
   const int J = (sp.n_rs + 31) / 32;
@@ -751,7 +755,9 @@ __global__ void __launch_bounds__(kScrPh2Threads) screen_phase2_kernel(const __g
       sp.lbuf[(size_t)t * sp.E + e] = r;
     }
   }
+  if (tr) tr[1] = clock64() - c_start;
   __syncthreads();
+  if (tr) tr[2] = clock64() - c_start;
   // ---- selection, one warp per token
   const int t = t0 + warp;
   if (warp >= kScrPh2Tok || t >= t1) return;
@@ -831,6 +837,7 @@ __global__ void __launch_bounds__(kScrPh2Threads) screen_phase2_kernel(const __g
     p.topk_idx[(size_t)t * p.k + lane] = isel;
     p.topk_w[(size_t)t * p.k + lane] = (S == 0.0f) ? uni : __fdiv_rn(wsel, S);
   }
+  if (tr) { tr[3] = clock64() - c_start; tr[4] = globaltimer_ns(); }
 }
 
 }  // namespace moe

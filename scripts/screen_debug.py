@@ -30,6 +30,14 @@ layer.route(x)
 torch.cuda.synchronize()
 lib.moe_b200_debug_set_router_trace(None)
 c = buf[:8].cpu().numpy()
+tl = buf[64:64 + 8 * 1024].view(-1, 8).cpu().numpy()
+tl = tl[tl[:, 0] > 0]
+if len(tl):
+    g0 = (tl[:, 0] - tl[:, 0].min()) / 1e3
+    g1 = (tl[:, 4] - tl[:, 0].min()) / 1e3
+    print(f"  phase-2 CTAs {len(tl)}: start spread us {g0.max():.1f}, end us med {np.median(g1):.1f} max {g1.max():.1f}")
+    for i, nm in ((1, "merged"), (2, "synced"), (3, "selected")):
+        print(f"    {nm:9s} cycles med {np.median(tl[:, i]):.0f} max {tl[:, i].max():.0f}")
 print(f"{name} B={B}: route us median {np.median(ts):.1f} min {min(ts):.1f}")
 print("  chains: inconclusive", c[0], "empty-intersection", c[1], "width>0", c[2])
 print("  tokens: general(no cand)", c[3], "general(Sk tiny)", c[4], "general(unsure)", c[5], "lean", c[6])
