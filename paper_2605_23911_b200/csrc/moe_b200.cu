@@ -1571,8 +1571,14 @@ int moe_b200_io_wait(moe_b200_io* io, void* event) {
 int moe_b200_launches_per_forward(const moe_b200_config* cfg, int64_t B) {
   if (check_config(cfg)) return -1;
   if (B <= 0) return 0;
-  // segment router | weight prep + exact router; dispatch; FFN (+ combine when not fused)
-  return (B <= seg_max_tokens(*cfg) ? 1 : 2) + 3;  // (+ router weight prep) router, dispatch, FFN, combine
+  // the forward's router path (route_impl): INT8 screen (6 launches), segment
+  // router (1; the small-batch dispatch runs inside it), or weight prep + exact
+  // router (2); then dispatch, FFN and the combine
+  const bool screen = screen_applies(*cfg, B) && !tuning().force_exact;
+  const bool seg = !screen && B <= seg_max_tokens(*cfg);
+  const bool fused_disp = seg && B <= kSegTT && B * cfg->top_k <= kFuseMaxT && tuning().fuse_dispatch != 0 &&
+                          layout_for(*cfg, B).max_chunks <= kChunkCap;
+  return (screen ? 6 : seg ? 1 : 2) + (fused_disp ? 0 : 1) + 2;
 }
 
 int moe_b200_io_sync(moe_b200_io* io) {
