@@ -36,7 +36,8 @@ def main(which):
     if which == "layer":
         layer_case(8, 2, 256, 512, 64, "softmax", routed=True, unfused=True)      # segment router, 128-row chunks
         layer_case(16, 4, 128, 256, 48, "sigmoid_normalized", y_bf16=True)
-        layer_case(256, 8, 64, 64, 300, "sigmoid_normalized")                     # exact router (> 64K chains)
+        layer_case(256, 8, 64, 64, 300, "sigmoid_normalized")                     # INT8 screen router (> 64K chains)
+        layer_case(256, 8, 64, 64, 300, "softmax")                                # exact router (> 64K chains)
     elif which == "pairs":
         layer_case(4, 2, 256, 384, 512, "softmax")                                # 256-row chunks: cta_group::2 pairs
     elif which == "stages":

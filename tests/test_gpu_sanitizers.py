@@ -1,5 +1,6 @@
 """compute-sanitizer (memcheck, racecheck, synccheck) over every
-kernel on small shapes: the mbarrier rings, the DSMEM hand-offs and
+kernel on small shapes (the segment, exact and INT8-screen routers included):
+the mbarrier rings, the DSMEM hand-offs and
 cta_group::2 barriers of the FFN, the self-resetting counters and the fused
 combine's last-arriver protocol, the stage kernels, and the peer-memory EP
 flags (one rank).  Each run must report zero errors.  (initcheck is not in
