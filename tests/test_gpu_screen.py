@@ -135,3 +135,39 @@ def test_screen_router_matches_exact_router_on_layer(P, monkeypatch):
     assert torch.equal(outs[0][2].view(torch.int32), outs[1][2].view(torch.int32))
     assert torch.equal(outs[0][0].view(torch.int32), outs[1][0].view(torch.int32))
     del rng
+
+
+def test_screen_router_max_experts_and_k(P, monkeypatch):
+    """E = 1024 (the library maximum: 8 expert tiles) and k = 32 (the
+    candidate-list capacity; any tie or near-tie spills into the exact
+    fallback), 150 tokens: the default regime (B x E > 64K chains)."""
+    rng = np.random.default_rng(21)
+    b, d, e, k = 150, 384, 1024, 32
+    x = rng.standard_normal((b, d)).astype(np.float32)
+    wr = (rng.standard_normal((d, e)) / np.sqrt(d)).astype(np.float32)
+    r = _route(P, x, wr, k, monkeypatch, screen="-1")
+    idx_ref, w_ref = O.route(x, wr, k, "sigmoid_normalized")
+    bits_equal(r["indices"].astype(np.int64), idx_ref)
+    bits_equal(r["weights"], w_ref)
+
+
+def test_screen_router_inside_expert_parallel_layer(P, monkeypatch):
+    """Expert parallelism (peer-memory transport, one rank) routes through the
+    screen: bitwise equal to the single-GPU layer."""
+    from paper_2605_23911_b200.ep import ExpertParallelMoE
+
+    monkeypatch.setenv("MOE_B200_SCREEN", "1")
+    e, k, d, f, b = 64, 6, 512, 256, 96
+    tokens, wr, gate, up, down = O.make_instance(31, e, k, d, f, b)
+    cfg = P.ModelConfig(e, k, d, f, P.Gating("sigmoid_normalized"))
+    w = P.ExpertWeights(gate, up, down)
+    layer = P.MoELayer(cfg, w, wr, max_tokens=b)
+    x = torch.from_numpy(tokens).cuda()
+    y_ref = layer.forward(x).cpu().numpy()
+    idx_ref, _ = O.route(tokens, wr, k, "sigmoid_normalized")
+    bits_equal(layer.topk_idx[:b].cpu().numpy().astype(np.int64), idx_ref)
+    ep = ExpertParallelMoE(cfg, wr, w, max_tokens=b, transport="p2p")
+    for _ in range(2):
+        bits_equal(ep.forward(x).cpu().numpy(), y_ref)
+    ep.p2p.close()
+
