@@ -84,6 +84,7 @@ struct Tuning {
   int rx_quarter = 1;        // MOE_B200_RX_QUARTER: 4 x 2 quarter-warp tiles in the exact router (0: 2 x 4)
   int fuse_dispatch = 1;     // MOE_B200_FUSE_DISPATCH: small batches dispatch inside the router (0: separate launch)
   int screen = -1;           // MOE_B200_SCREEN: sigmoid router via the INT8 screen (-1 auto, 0 off, 1 always)
+  int seg_tt1 = 1;           // MOE_B200_SEG_TT1: single-token batches use 1-token segment tiles (0: 4-token tiles)
 };
 Tuning g_tune;
 std::mutex g_tune_mu;
@@ -115,6 +116,7 @@ void load_tuning_locked() {
   t.rx_quarter = geti("MOE_B200_RX_QUARTER", 1);
   t.fuse_dispatch = geti("MOE_B200_FUSE_DISPATCH", 1);
   t.screen = geti("MOE_B200_SCREEN", -1);
+  t.seg_tt1 = geti("MOE_B200_SEG_TT1", 1);
   g_tune = t;
   g_tune_loaded = true;
 }
@@ -249,7 +251,7 @@ int64_t seg_max_tokens(const moe_b200_config& c) {
 }
 
 struct SegPlan {
-  int expc, n_eb, n_tb, n_kb, seg_len, kr, grid;
+  int tt, expc, n_eb, n_tb, n_kb, seg_len, kr, grid;
   size_t smem;
 };
 
@@ -257,7 +259,8 @@ SegPlan plan_seg(const moe_b200_config& c, int64_t B) {
   SegPlan q{};
   q.expc = seg_expc(c.num_experts, B);
   q.n_eb = (c.num_experts + q.expc - 1) / q.expc;
-  q.n_tb = static_cast<int>((B + kSegTT - 1) / kSegTT);
+  q.tt = (B == 1 && tuning().seg_tt1 != 0 && !tuning().seg_w64) ? 1 : kSegTT;  // tokens per CTA
+  q.n_tb = static_cast<int>((B + q.tt - 1) / q.tt);
   const int G = q.expc / kSegTE;
   const int S = kSegThreads / G;
   // k-blocks: one when the (token, expert) blocks alone fill >= 3/4 of the
@@ -273,7 +276,7 @@ SegPlan plan_seg(const moe_b200_config& c, int64_t B) {
   q.kr = S * q.seg_len;
   q.n_kb = (c.hidden_dim + q.kr - 1) / q.kr;
   q.grid = q.n_tb * q.n_eb * q.n_kb;
-  const size_t part = (size_t)(kSegThreads / 32) * kSegTT * q.expc * 16 + 64;  // warp partials
+  const size_t part = (size_t)(kSegThreads / 32) * q.tt * q.expc * 16 + 64;  // warp partials
   const size_t ph2 = (size_t)(kSegThreads / 32) * (c.num_experts * 16 + kChainWin * 8);
   q.smem = std::max(part, ph2);
   return q;
@@ -1142,7 +1145,7 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
     // latency regime: certified split-K segments (router_seg.cuh)
     const SegPlan q = plan_seg(*cfg, B);
     if (q.n_tb > kTbCap || (long)q.n_tb * q.n_eb > kBlkCap) return MOE_B200_ERR_UNSUPPORTED;
-    p.tokc = kSegTT; p.expc = q.expc;
+    p.tokc = q.tt; p.expc = q.expc;
     p.n_eblocks = q.n_eb; p.n_tblocks = q.n_tb;
     p.kr = q.kr; p.seg_len = q.seg_len; p.n_kb = q.n_kb;
     p.cert_coef = ldexp((2.0 + 12.0 / q.seg_len) * (1.0 + ldexp(1.0, -20)), -53);
@@ -1161,6 +1164,9 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
     const bool wvec = (cfg->num_experts % 4) == 0;
     void (*kern)(RouterParams) = xb ? (wvec ? router_seg_kernel<true, true> : router_seg_kernel<true, false>)
                                     : (wvec ? router_seg_kernel<false, true> : router_seg_kernel<false, false>);
+    if (q.tt == 1)
+      kern = xb ? (wvec ? router_seg_kernel<true, true, false, 1> : router_seg_kernel<true, false, false, 1>)
+                : (wvec ? router_seg_kernel<false, true, false, 1> : router_seg_kernel<false, false, false, 1>);
     if (tuning().seg_w64) {
       // W widened to fp64 once per call (the hot loop then converts only x)
       double* w64 = reinterpret_cast<double*>(ws8(ws) + L.w64);

@@ -86,10 +86,12 @@ MOE_DEVICE void seg_finalize(const RouterParams& p, int t, int e, double s, doub
   p.lbuf[(size_t)t * p.E + e] = r;
 }
 
-template <bool kXBf16, bool kWVec, bool kW64 = false>
+// kTT: tokens per CTA / thread tile (4; a single-token batch uses 1, so no
+// thread folds padding rows and the CTA reduction moves a quarter of the data)
+template <bool kXBf16, bool kWVec, bool kW64 = false, int kTT = kSegTT>
 __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const __grid_constant__ RouterParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int TT = kSegTT, TE = kSegTE;
+  constexpr int TT = kTT, TE = kSegTE;
   const int tid = threadIdx.x;
   const int kb = blockIdx.x % p.n_kb;
   const int rest = blockIdx.x / p.n_kb;

@@ -62,6 +62,8 @@ ROUTER_MODES = {
     # INT8 screen + candidate refinement for every sigmoid batch (logits are
     # not requested: the screen only certifies what the outputs depend on)
     "screen": {"MOE_B200_SCREEN": "1"},
+    # single-token batches on the 4-token segment tiles
+    "seg_tt4": {"MOE_B200_SEG_TT1": "0"},
 }
 
 
