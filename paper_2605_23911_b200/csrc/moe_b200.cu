@@ -84,7 +84,7 @@ struct Tuning {
   int rx_quarter = 1;        // MOE_B200_RX_QUARTER: 4 x 2 quarter-warp tiles in the exact router (0: 2 x 4)
   int fuse_dispatch = 1;     // MOE_B200_FUSE_DISPATCH: small batches dispatch inside the router (0: separate launch)
   int screen = -1;           // MOE_B200_SCREEN: sigmoid router via the INT8 screen (-1 auto, 0 off, 1 always)
-  int seg_tt1 = 1;           // MOE_B200_SEG_TT1: single-token batches use 1-token segment tiles (0: 4-token tiles)
+  int seg_tt1 = 1;           // MOE_B200_SEG_TT1: 1- and 2-token batches use 1- / 2-token segment tiles (0: 4-token tiles)
 };
 Tuning g_tune;
 std::mutex g_tune_mu;
@@ -259,7 +259,7 @@ SegPlan plan_seg(const moe_b200_config& c, int64_t B) {
   SegPlan q{};
   q.expc = seg_expc(c.num_experts, B);
   q.n_eb = (c.num_experts + q.expc - 1) / q.expc;
-  q.tt = (B == 1 && tuning().seg_tt1 != 0 && !tuning().seg_w64) ? 1 : kSegTT;  // tokens per CTA
+  q.tt = (B <= 2 && tuning().seg_tt1 != 0 && !tuning().seg_w64) ? static_cast<int>(B) : kSegTT;  // tokens per CTA
   q.n_tb = static_cast<int>((B + q.tt - 1) / q.tt);
   const int G = q.expc / kSegTE;
   const int S = kSegThreads / G;
@@ -1167,6 +1167,9 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
     if (q.tt == 1)
       kern = xb ? (wvec ? router_seg_kernel<true, true, false, 1> : router_seg_kernel<true, false, false, 1>)
                 : (wvec ? router_seg_kernel<false, true, false, 1> : router_seg_kernel<false, false, false, 1>);
+    else if (q.tt == 2)
+      kern = xb ? (wvec ? router_seg_kernel<true, true, false, 2> : router_seg_kernel<true, false, false, 2>)
+                : (wvec ? router_seg_kernel<false, true, false, 2> : router_seg_kernel<false, false, false, 2>);
     if (tuning().seg_w64) {
       // W widened to fp64 once per call (the hot loop then converts only x)
       double* w64 = reinterpret_cast<double*>(ws8(ws) + L.w64);

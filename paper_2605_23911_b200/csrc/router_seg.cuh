@@ -86,8 +86,8 @@ MOE_DEVICE void seg_finalize(const RouterParams& p, int t, int e, double s, doub
   p.lbuf[(size_t)t * p.E + e] = r;
 }
 
-// kTT: tokens per CTA / thread tile (4; a single-token batch uses 1, so no
-// thread folds padding rows and the CTA reduction moves a quarter of the data)
+// kTT: tokens per CTA / thread tile (4; 1- and 2-token batches use 1 / 2, so
+// no thread folds padding rows and the CTA reduction moves less data)
 template <bool kXBf16, bool kWVec, bool kW64 = false, int kTT = kSegTT>
 __global__ void __launch_bounds__(kSegThreads, 1) router_seg_kernel(const __grid_constant__ RouterParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
