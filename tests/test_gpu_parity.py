@@ -662,6 +662,31 @@ def test_expert_parallel_p2p_single_rank_matches_layer_bitwise(pkg):
     ep.p2p.close()
 
 
+@pytest.mark.parametrize("case", [
+    (9, 16, 4, 256, 512, 64, "sigmoid_normalized"),
+    (12, 8, 2, 264, 200, 37, "softmax"),   # d with an 8-column tail (padded rows in CudaOps.permute)
+])
+def test_expert_parallel_collective_transport_on_gpu(pkg, case):
+    """The collective transport's device path (CudaOps: route, permute,
+    source-major -> expert-major gathers, the local expert FFN with the global
+    batch's K split, the home combine) on one rank -- the all-to-alls reduce to
+    copies -- reproduces the fused single-GPU forward bit for bit."""
+    P = pkg
+    from paper_2605_23911_b200.ep import ExpertParallelMoE
+
+    seed, e, k, d, f, b, g = case
+    tokens, wr, gate, up, down = O.make_instance(seed, e, k, d, f, b)
+    cfg = _cfg(P, e, k, d, f, g)
+    w = P.ExpertWeights(gate, up, down)
+    layer = P.MoELayer(cfg, w, wr, max_tokens=b)
+    x = torch.from_numpy(tokens).cuda()
+    y_ref = _np(layer.forward(x))
+    ep = ExpertParallelMoE(cfg, wr, w, max_tokens=b, transport="collective")
+    for _ in range(2):
+        bits_equal(_np(ep.forward(x)), y_ref)
+    bits_equal(_np(ep.forward(x[:11])), _np(layer.forward(x[:11])))
+
+
 def _p2p_worker(rank, world, port, case, q):
     import os
     import torch.distributed as dist
