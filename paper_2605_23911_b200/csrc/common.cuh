@@ -123,6 +123,25 @@ MOE_DEVICE void tma_load_2d_hint(const CUtensorMap* map, uint64_t* bar, void* ds
       : "memory");
 }
 
+// 3-D tile loads (the weight maps viewed as [column block][row][64 columns]):
+// one instruction fills a whole 16 KB weight slot (two 64-column halves).
+MOE_DEVICE void tma_load_3d_hint(const CUtensorMap* map, uint64_t* bar, void* dst, int32_t c0, int32_t c1,
+                                 int32_t c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+MOE_DEVICE void tma_load_3d_2sm(const CUtensorMap* map, uint32_t bar_cluster, void* dst, int32_t c0, int32_t c1,
+                                int32_t c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+
 // Prefetch a 2-D tile into L2 (no shared memory, no completion tracking).
 MOE_DEVICE void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(

@@ -80,6 +80,7 @@ struct FfnParams {
   int tmem_db;               // 1: chunks of <= 128 rows alternate two TMEM accumulator slots
   int32_t* arrive;           // (B, n_mt_dn) arrival counters, reset by the combine
   int k;                     // top-k: slot j of token t is expanded id t * k + j
+  int w3d;                   // 1: tm_wg / tm_wu / tm_wd are 3-D [64-col block][row][64 col] views (one load per slot)
 };
 
 MOE_DEVICE unsigned long long globaltimer() {
@@ -377,12 +378,20 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           if constexpr (k2) {
             const uint32_t bar = lead_a_full + as * 8;
             mbar_arrive_expect_tx_cluster(bar, C::kABytes);
-            tma_load_2d_2sm(m, bar, sa, col, krow, pol_w);
-            tma_load_2d_2sm(m, bar, sa + C::kABytes / 2, col + 64, krow, pol_w);
+            if (p.w3d) {
+              tma_load_3d_2sm(m, bar, sa, 0, krow, col / 64, pol_w);
+            } else {
+              tma_load_2d_2sm(m, bar, sa, col, krow, pol_w);
+              tma_load_2d_2sm(m, bar, sa + C::kABytes / 2, col + 64, krow, pol_w);
+            }
           } else {
             mbar_arrive_expect_tx(a_full + as, C::kABytes);
-            tma_load_2d_hint(m, a_full + as, sa, col, krow, pol_w);
-            tma_load_2d_hint(m, a_full + as, sa + C::kABytes / 2, col + 64, krow, pol_w);
+            if (p.w3d) {
+              tma_load_3d_hint(m, a_full + as, sa, 0, krow, col / 64, pol_w);
+            } else {
+              tma_load_2d_hint(m, a_full + as, sa, col, krow, pol_w);
+              tma_load_2d_hint(m, a_full + as, sa + C::kABytes / 2, col + 64, krow, pol_w);
+            }
           }
           if (++as == C::kAStages) { as = 0; aph ^= 1; }
         };

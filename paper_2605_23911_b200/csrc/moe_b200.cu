@@ -84,6 +84,7 @@ struct Tuning {
   int rx_quarter = 1;        // MOE_B200_RX_QUARTER: 4 x 2 quarter-warp tiles in the exact router (0: 2 x 4)
   int fuse_dispatch = 1;     // MOE_B200_FUSE_DISPATCH: small batches dispatch inside the router (0: separate launch)
   int screen = -1;           // MOE_B200_SCREEN: sigmoid router via the INT8 screen (-1 auto, 0 off, 1 always)
+  int w3d = 1;               // MOE_B200_W3D: one 3-D TMA load per 16 KB weight slot (0: two 2-D loads)
   int seg_tt1 = 1;           // MOE_B200_SEG_TT1: 1- and 2-token batches use 1- / 2-token segment tiles (0: 4-token tiles)
 };
 Tuning g_tune;
@@ -116,6 +117,7 @@ void load_tuning_locked() {
   t.rx_quarter = geti("MOE_B200_RX_QUARTER", 1);
   t.fuse_dispatch = geti("MOE_B200_FUSE_DISPATCH", 1);
   t.screen = geti("MOE_B200_SCREEN", -1);
+  t.w3d = geti("MOE_B200_W3D", 1);
   t.seg_tt1 = geti("MOE_B200_SEG_TT1", 1);
   g_tune = t;
   g_tune_loaded = true;
@@ -516,6 +518,27 @@ int encode_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t co
   return MOE_B200_OK;
 }
 
+// A weight matrix (rows x cols bf16, cols % 64 == 0) as a 3-D tensor
+// [cols / 64][rows][64]: box {64, box_rows, 2} loads two adjacent 64-column
+// halves -- one 16 KB weight slot -- in one TMA instruction, in the same
+// shared-memory layout as two 2-D boxes.
+int encode_map_w3d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  int rc = get_encoder();
+  if (rc) return rc;
+  cuuint64_t dims[3] = {64, rows, cols / 64};
+  cuuint64_t strides[2] = {cols * 2, 128};
+  cuuint32_t box[3] = {64, box_rows, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    g_last_error = "cuTensorMapEncodeTiled(3-D weights) failed";
+    return MOE_B200_ERR_CUDA;
+  }
+  return MOE_B200_OK;
+}
+
 // Largest dynamic shared memory already granted per (kernel, device):
 // cudaFuncSetAttribute is a driver call, so it runs only when a launch needs more.
 cudaError_t ensure_dyn_smem(const void* kern, size_t bytes) {
@@ -731,12 +754,15 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   CUtensorMap m_wg, m_wu, m_xp, m_wd, m_h;
   int rc;
   const void* any_w = do_gu ? w_gate : w_down;
-  if ((rc = make_map_bf16(&m_wg, do_gu ? w_gate : any_w, do_gu ? (uint64_t)E * d : (uint64_t)E * f,
-                          do_gu ? f : d, 64, 64))) return rc;
-  if ((rc = make_map_bf16(&m_wu, do_gu ? w_up : any_w, do_gu ? (uint64_t)E * d : (uint64_t)E * f,
-                          do_gu ? f : d, 64, 64))) return rc;
-  if ((rc = make_map_bf16(&m_wd, do_dn ? w_down : any_w, do_dn ? (uint64_t)E * f : (uint64_t)E * d,
-                          do_dn ? d : f, 64, 64))) return rc;
+  // 3-D weight views (one TMA per 16 KB weight slot) when every weight's
+  // column count is a multiple of 64 (else the 2-D maps zero-fill the tail)
+  const bool w3d = tuning().w3d != 0 && f % 64 == 0 && d % 64 == 0;
+  auto wmap = [&](CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+    return w3d ? encode_map_w3d(m, base, rows, cols, 64) : make_map_bf16(m, base, rows, cols, 64, 64);
+  };
+  if ((rc = wmap(&m_wg, do_gu ? w_gate : any_w, do_gu ? (uint64_t)E * d : (uint64_t)E * f, do_gu ? f : d))) return rc;
+  if ((rc = wmap(&m_wu, do_gu ? w_up : any_w, do_gu ? (uint64_t)E * d : (uint64_t)E * f, do_gu ? f : d))) return rc;
+  if ((rc = wmap(&m_wd, do_dn ? w_down : any_w, do_dn ? (uint64_t)E * f : (uint64_t)E * d, do_dn ? d : f))) return rc;
   if ((rc = make_map_bf16(&m_xp, do_gu ? xp : h, T, do_gu ? d : f, 64, kBoxRows))) return rc;
   if (fused) {
     // tiled h: [n_ft * T_pad rows][128 cols]
@@ -768,6 +794,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.tiled = fused ? 1 : 0;
   p.T_pad = L.T_pad;
   p.tmem_db = tuning().tmem_db != 0;
+  p.w3d = w3d ? 1 : 0;
   if (arrive && mode == kFfnFused && do_gu && do_dn) {
     // the down epilogue publishes per-(token, block) arrivals for the combine
     // grid that runs overlapped with this grid's tail
