@@ -47,6 +47,10 @@ constexpr int kBoxRows = MOE_B200_BOX_ROWS;  // token rows per TMA box
 constexpr int kSchedSlots = 4;  // tile-id ring between scheduler and consumers
 
 struct FfnParams {
+  // down weights as a 3-D view with a 4-block box: a down tile's two adjacent
+  // 128-row hidden tiles (two ring slots, 512 contiguous bytes per row) in one
+  // TMA request when the slots are adjacent in the ring (w3d only)
+  alignas(64) CUtensorMap tm_wd4;
   const int4* chunk_tab;     // {expert, row0, nrows, padded row0} per token chunk
   const int2* chunk_grp;     // {first chunk, chunks} of the chunk's expert
   const int32_t* n_chunks;   // device count of chunks
@@ -81,6 +85,7 @@ struct FfnParams {
   int32_t* arrive;           // (B, n_mt_dn) arrival counters, reset by the combine
   int k;                     // top-k: slot j of token t is expanded id t * k + j
   int w3d;                   // 1: tm_wg / tm_wu / tm_wd are 3-D [64-col block][row][64 col] views (one load per slot)
+  int wd4;                   // 1: tm_wd4 is valid (down tiles load both hidden halves in one request)
 };
 
 MOE_DEVICE unsigned long long globaltimer() {
@@ -233,7 +238,7 @@ template <int kBN, int kV, int kPM = 0>
 __global__ void __launch_bounds__(kFfnThreads, 1)
 ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CUtensorMap tm_wu,
            const __grid_constant__ CUtensorMap tm_xp, const __grid_constant__ CUtensorMap tm_wd,
-           const __grid_constant__ CUtensorMap tm_h, const FfnParams p) {
+           const __grid_constant__ CUtensorMap tm_h, const __grid_constant__ FfnParams p) {
   constexpr bool kPair = kPM != 0;
   constexpr bool k2 = kPM == 2;
   using C = FfnCfg<kBN, kV, k2>;
@@ -263,6 +268,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
     tma_prefetch_desc(&tm_xp);
     tma_prefetch_desc(&tm_wd);
     tma_prefetch_desc(&tm_h);
+    if (p.wd4) tma_prefetch_desc(&p.tm_wd4);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::kAStages; ++s) {
@@ -395,6 +401,33 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           }
           if (++as == C::kAStages) { as = 0; aph ^= 1; }
         };
+        // a down tile's two hidden halves: one 32 KB request into two adjacent
+        // ring slots (the first slot's full barrier carries the bytes; the MMA
+        // waits it before the second, which gets a plain arrival)
+        auto load_a_pair = [&](int col, int krow) {
+          // (single-CTA tiles only: with cta_group::2 pairs the 32 KB requests measured
+          // far slower, Mixtral-512 553 -> 740 us)
+          if (!p.wd4 || k2 || as + 1 >= C::kAStages) {
+            load_a(&tm_wd, col, krow);
+            load_a(&tm_wd, col + kBM, krow);
+            return;
+          }
+          mbar_wait(a_empty + as, aph ^ 1);
+          mbar_wait(a_empty + as + 1, aph ^ 1);
+          uint8_t* sa = a_ring + as * C::kABytes;
+          if constexpr (k2) {
+            const uint32_t bar = lead_a_full + as * 8;
+            mbar_arrive_expect_tx_cluster(bar, 2 * C::kABytes);
+            tma_load_3d_2sm(&p.tm_wd4, bar, sa, 0, krow, col / 64, pol_w);
+            mbar_arrive_cluster(lead_a_full + (as + 1) * 8);
+          } else {
+            mbar_arrive_expect_tx(a_full + as, 2 * C::kABytes);
+            tma_load_3d_hint(&p.tm_wd4, a_full + as, sa, 0, krow, col / 64, pol_w);
+            mbar_arrive(a_full + as + 1);
+          }
+          as += 2;
+          if (as == C::kAStages) { as = 0; aph ^= 1; }
+        };
         int kb0, kb1;
         if (ti.is_gu) {
           kb0 = 0; kb1 = nkb_gu;
@@ -422,8 +455,7 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
           } else {
             // a down tile is a PAIR of 128-row hidden tiles sharing the token slot
             const int krow = ch.x * p.f + kb * kBK;
-            load_a(&tm_wd, a_col, krow);
-            load_a(&tm_wd, a_col + kBM, krow);
+            load_a_pair(a_col, krow);
           }
           mbar_wait(b_empty + bs, bph ^ 1);
           uint8_t* sb = b_ring + bs * C::kBBytes;

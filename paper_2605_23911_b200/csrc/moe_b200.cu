@@ -84,7 +84,7 @@ struct Tuning {
   int rx_quarter = 1;        // MOE_B200_RX_QUARTER: 4 x 2 quarter-warp tiles in the exact router (0: 2 x 4)
   int fuse_dispatch = 1;     // MOE_B200_FUSE_DISPATCH: small batches dispatch inside the router (0: separate launch)
   int screen = -1;           // MOE_B200_SCREEN: sigmoid router via the INT8 screen (-1 auto, 0 off, 1 always)
-  int w3d = 1;               // MOE_B200_W3D: one 3-D TMA load per 16 KB weight slot (0: two 2-D loads)
+  int w3d = 2;               // MOE_B200_W3D: 3-D TMA weight loads, 1 = one per 16 KB slot, 2 = + a down tile's two slots in one (single-CTA tiles); 0: 2-D
   int seg_tt1 = 1;           // MOE_B200_SEG_TT1: 1- and 2-token batches use 1- / 2-token segment tiles (0: 4-token tiles)
 };
 Tuning g_tune;
@@ -117,7 +117,7 @@ void load_tuning_locked() {
   t.rx_quarter = geti("MOE_B200_RX_QUARTER", 1);
   t.fuse_dispatch = geti("MOE_B200_FUSE_DISPATCH", 1);
   t.screen = geti("MOE_B200_SCREEN", -1);
-  t.w3d = geti("MOE_B200_W3D", 1);
+  t.w3d = geti("MOE_B200_W3D", 2);
   t.seg_tt1 = geti("MOE_B200_SEG_TT1", 1);
   g_tune = t;
   g_tune_loaded = true;
@@ -522,12 +522,13 @@ int encode_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t co
 // [cols / 64][rows][64]: box {64, box_rows, 2} loads two adjacent 64-column
 // halves -- one 16 KB weight slot -- in one TMA instruction, in the same
 // shared-memory layout as two 2-D boxes.
-int encode_map_w3d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+int encode_map_w3d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                   uint32_t box_blocks = 2) {
   int rc = get_encoder();
   if (rc) return rc;
   cuuint64_t dims[3] = {64, rows, cols / 64};
   cuuint64_t strides[2] = {cols * 2, 128};
-  cuuint32_t box[3] = {64, box_rows, 2};
+  cuuint32_t box[3] = {64, box_rows, box_blocks};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -795,6 +796,10 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.T_pad = L.T_pad;
   p.tmem_db = tuning().tmem_db != 0;
   p.w3d = w3d ? 1 : 0;
+  if (w3d && do_dn && tuning().w3d > 1) {  // down tiles' two slots in one request (not for CTA pairs)
+    if ((rc = encode_map_w3d(&p.tm_wd4, w_down, (uint64_t)E * f, d, 64, 4))) return rc;
+    p.wd4 = 1;
+  }
   if (arrive && mode == kFfnFused && do_gu && do_dn) {
     // the down epilogue publishes per-(token, block) arrivals for the combine
     // grid that runs overlapped with this grid's tail
