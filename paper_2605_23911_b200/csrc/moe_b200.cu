@@ -464,8 +464,10 @@ struct MapKey {
   const void* base;
   uint64_t rows, cols;
   uint32_t box_cols, box_rows;
+  uint32_t blocks;  // 0: 2-D map; > 0: 3-D weight view with this many 64-column blocks per box
   bool operator==(const MapKey& o) const {
-    return base == o.base && rows == o.rows && cols == o.cols && box_cols == o.box_cols && box_rows == o.box_rows;
+    return base == o.base && rows == o.rows && cols == o.cols && box_cols == o.box_cols &&
+           box_rows == o.box_rows && blocks == o.blocks;
   }
 };
 constexpr int kMapCache = 64;
@@ -483,7 +485,7 @@ int encode_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t co
 // Row-major bf16 matrix (rows x cols), box (box_cols x box_rows), 128B swizzle.
 int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
                   uint32_t box_cols, uint32_t box_rows) {
-  const MapKey k{base, rows, cols, box_cols, box_rows};
+  const MapKey k{base, rows, cols, box_cols, box_rows, 0};
   std::lock_guard<std::mutex> lock(g_maps.mu);
   for (int i = 0; i < g_maps.n; ++i)
     if (g_maps.key[i] == k) {
@@ -537,6 +539,24 @@ int encode_map_w3d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t col
     g_last_error = "cuTensorMapEncodeTiled(3-D weights) failed";
     return MOE_B200_ERR_CUDA;
   }
+  return MOE_B200_OK;
+}
+
+// encode_map_w3d through the map cache (every launch_ffn call asks for them)
+int make_map_w3d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                 uint32_t box_blocks) {
+  const MapKey k{base, rows, cols, 64, box_rows, box_blocks};
+  std::lock_guard<std::mutex> lock(g_maps.mu);
+  for (int i = 0; i < g_maps.n; ++i)
+    if (g_maps.key[i] == k) {
+      *m = g_maps.map[i];
+      return MOE_B200_OK;
+    }
+  const int rc = encode_map_w3d(m, base, rows, cols, box_rows, box_blocks);
+  if (rc) return rc;
+  const int slot = g_maps.n < kMapCache ? g_maps.n++ : (g_maps.next++ % kMapCache);
+  g_maps.key[slot] = k;
+  g_maps.map[slot] = *m;
   return MOE_B200_OK;
 }
 
@@ -759,7 +779,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   // column count is a multiple of 64 (else the 2-D maps zero-fill the tail)
   const bool w3d = tuning().w3d != 0 && f % 64 == 0 && d % 64 == 0;
   auto wmap = [&](CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
-    return w3d ? encode_map_w3d(m, base, rows, cols, 64) : make_map_bf16(m, base, rows, cols, 64, 64);
+    return w3d ? make_map_w3d(m, base, rows, cols, 64, 2) : make_map_bf16(m, base, rows, cols, 64, 64);
   };
   if ((rc = wmap(&m_wg, do_gu ? w_gate : any_w, do_gu ? (uint64_t)E * d : (uint64_t)E * f, do_gu ? f : d))) return rc;
   if ((rc = wmap(&m_wu, do_gu ? w_up : any_w, do_gu ? (uint64_t)E * d : (uint64_t)E * f, do_gu ? f : d))) return rc;
@@ -797,7 +817,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
   p.tmem_db = tuning().tmem_db != 0;
   p.w3d = w3d ? 1 : 0;
   if (w3d && do_dn && tuning().w3d > 1) {  // down tiles' two slots in one request (not for CTA pairs)
-    if ((rc = encode_map_w3d(&p.tm_wd4, w_down, (uint64_t)E * f, d, 64, 4))) return rc;
+    if ((rc = make_map_w3d(&p.tm_wd4, w_down, (uint64_t)E * f, d, 64, 4))) return rc;
     p.wd4 = 1;
   }
   if (arrive && mode == kFfnFused && do_gu && do_dn) {
