@@ -14,6 +14,8 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "elementwise.cuh"
 #include "ffn.cuh"
@@ -27,6 +29,16 @@
 using namespace moe;
 
 namespace {
+
+// NVTX ranges per stage (host-side launch regions; nsys / ncu correlate them
+// with the kernels launched inside).  Header-only NVTX3: without an attached
+// tool a push / pop is a null-pointer check.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 thread_local std::string g_last_error;
 
@@ -769,6 +781,7 @@ int launch_ffn(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, c
                const void* w_gate, const void* w_up, const void* w_down, void* h, float* ys,
                const float* topk_w, const int32_t* fwd, bool do_gu, bool do_dn, int mode,
                cudaStream_t s, float* gu32 = nullptr, int32_t* arrive = nullptr) {
+  NvtxRange nvtx("moe_b200.ffn");
   const bool fused = (mode != kFfnStaged);  // tiled padded-row layouts
   const int E = c.num_experts, d = c.hidden_dim, f = c.ffn_dim;
   const int64_t T = B * c.top_k;
@@ -894,6 +907,7 @@ int launch_router_exact(const moe_b200_config& c, int64_t B, const void* x, int 
 
 int launch_combine(const moe_b200_config& c, int64_t B, const Layout& L, void* ws, const float* topk_w, void* y,
                    int y_dtype, cudaStream_t s, int32_t* arrive = nullptr) {
+  NvtxRange nvtx("moe_b200.combine");
   if (y_dtype != MOE_B200_DTYPE_F32 && y_dtype != MOE_B200_DTYPE_BF16) return MOE_B200_ERR_INVALID_VALUE;
   const int d = c.hidden_dim, k = c.top_k;
   const float* ys = reinterpret_cast<const float*>(ws8(ws) + L.ys);
@@ -957,6 +971,7 @@ int launch_dispatch(const moe_b200_config& c, int64_t B, const void* x, int xb, 
                     int32_t* counts, int32_t* offsets, int32_t* fwd, int32_t* inv, int32_t* prow, int4* chunk_tab,
                     int32_t* n_chunks, void* xp, cudaStream_t s, uint32_t* flags = nullptr,
                     int32_t* tok_cnt = nullptr, int splits = 1) {
+  NvtxRange nvtx("moe_b200.dispatch");
   DispatchParams q{};
   q.tok_cnt = tok_cnt;
   q.n_dp = (c.hidden_dim + 2 * kBM - 1) / (2 * kBM);
@@ -1156,6 +1171,7 @@ static int route_impl(const moe_b200_config* cfg, int64_t B, const void* x, int 
                       const float* w_router, int32_t* topk_idx, float* topk_w, int32_t* counts,
                       int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv, float* logits,
                       void* ws, size_t ws_bytes, void* stream, void* xp, void* mid_event = nullptr) {
+  NvtxRange nvtx("moe_b200.route");
   int rc = check_config(cfg);
   if (rc) return rc;
   if (B < 0) return MOE_B200_ERR_SHAPE_MISMATCH;
@@ -1331,6 +1347,7 @@ static int forward_impl(const moe_b200_config* cfg, int64_t B, const void* x, in
                      const void* w_down, void* y, int y_dtype, int32_t* topk_idx, float* topk_w,
                      int32_t* counts, int32_t* offsets, int32_t* perm_fwd, int32_t* perm_inv,
                      void* ws, size_t ws_bytes, void* stream, void** events, bool unfused = false) {
+  NvtxRange nvtx("moe_b200.forward");
   int rc = check_config(cfg);
   if (rc) return rc;
   Layout L;
