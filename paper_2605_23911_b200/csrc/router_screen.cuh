@@ -21,10 +21,11 @@
 //     two adjacent classes -- and class 4 (D2 G2, weight 1) is dropped into the
 //     error bound.  K is split across CTAs; the int32 partials are combined as
 //     exact int64.  The interval adds (all rounded up): the quantisation error
-//     err_x sum|w| + err_w sum|x^|, the dropped class 64 min(sum|D2|, sum|G2|),
-//     and the reference fold's own rounding d u sum|x||w| (every term measured
-//     per row / column in the prep kernels).  Its fp32 rounding [lo, hi]
-//     contains the reference logit.
+//     err_x sum|w| + err_w sum|x^| (err = half a unit, 2^(u-1)), the dropped
+//     class 64 min(sum|D2|, sum|G2|), and the reference fold's own rounding
+//     d u sum|x||w| (the sums per row / column from the prep kernels;
+//     tests/test_screen_bound.py restates the bound in exact rationals).  Its
+//     fp32 rounding [lo, hi] contains the reference logit.
 //  2. select: per token the k-th largest lower score bound S_k; experts whose
 //     upper score bound is below S_k can never be selected (their score is
 //     strictly below k others').  The rest (~k per token) are candidates.
