@@ -665,9 +665,32 @@ def ep_arm(args, cfg, label, B, world, rank, dev, shared_gpu):
     gate = (torch.randn((El * d, f), generator=gen_r, device=dev) / d ** 0.5).to(torch.bfloat16)
     up = (torch.randn((El * d, f), generator=gen_r, device=dev) / d ** 0.5).to(torch.bfloat16)
     down = (torch.randn((El * f, d), generator=gen_r, device=dev) / f ** 0.5).to(torch.bfloat16)
-    layer = ExpertParallelMoE(cfg, wr, P.ExpertWeights(gate, up, down), max_tokens=Bl, device=dev,
-                              transport=args.ep_transport)
     cpu = torch.device("cpu")
+    # The peer-memory transport maps the other ranks' buffers with CUDA IPC; if
+    # that (or the first forward) fails on any rank -- e.g. no peer access
+    # between the devices -- every rank falls back to the NCCL all-to-alls.
+    transport, fallback = args.ep_transport, None
+    layer = None
+    try:
+        layer = ExpertParallelMoE(cfg, wr, P.ExpertWeights(gate, up, down), max_tokens=Bl, device=dev,
+                                  transport=transport)
+        layer.forward(x, global_tokens=B)
+        torch.cuda.synchronize(dev)
+        ok = 1
+    except Exception as exc:  # noqa: BLE001 -- any failure: agree on the fallback below
+        ok, fallback = 0, f"{type(exc).__name__}: {str(exc)[:200]}"
+    flag = torch.tensor([ok], dtype=torch.int32, device=cpu if shared_gpu else dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) == 0 and transport == "p2p":
+        if layer is not None and layer.p2p is not None:
+            layer.p2p.close()
+        transport = "collective"
+        fallback = fallback or "a peer rank failed to set up the peer-memory transport"
+        layer = ExpertParallelMoE(cfg, wr, P.ExpertWeights(gate, up, down), max_tokens=Bl, device=dev,
+                                  transport=transport)
+    elif int(flag.item()) == 0:
+        raise RuntimeError(f"expert-parallel setup failed: {fallback}")
+    args.ep_transport = transport
 
     def allreduce_max(vals):
         t = torch.tensor(vals, dtype=torch.float64, device=cpu if shared_gpu else dev)
@@ -747,7 +770,10 @@ def ep_arm(args, cfg, label, B, world, rank, dev, shared_gpu):
                                          if args.ep_transport == "p2p" else "NCCL all-to-all") + ")"
                                       + (" -- ranks SHARE GPUs: functional run, not a scaling measurement"
                                          if shared_gpu else ""),
-                       "timing": "CUDA events over K graph replays of the whole EP forward, max over ranks"},
+                       "timing": ("CUDA events over K graph replays of the whole EP forward, max over ranks"
+                                  if graphed else "CUDA events over K eager EP forwards, max over ranks"),
+                       "ep_transport": args.ep_transport,
+                       "ep_transport_fallback": fallback},
             "e2e": {"value": B / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": B * d * 2,
                     "d2h_bytes_per_step": B * d * 4,
                     "path": "per rank: pinned-host token shard copied into the graph's input, EP forward replay, "
