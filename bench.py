@@ -728,12 +728,13 @@ def ep_arm(args, cfg, label, B, world, rank, dev, shared_gpu):
     # The peer-memory transport maps the other ranks' buffers with CUDA IPC; if
     # that (or the first forward) fails on any rank -- e.g. no peer access
     # between the devices -- every rank falls back to the NCCL all-to-alls.
+    # (the ranks agree on success after construction, before any forward: a
+    # peer-memory forward on the healthy ranks would wait on a failed peer)
     transport, fallback = args.ep_transport, None
     layer = None
     try:
         layer = ExpertParallelMoE(cfg, wr, P.ExpertWeights(gate, up, down), max_tokens=Bl, device=dev,
                                   transport=transport)
-        layer.forward(x, global_tokens=B)
         torch.cuda.synchronize(dev)
         ok = 1
     except Exception as exc:  # noqa: BLE001 -- any failure: agree on the fallback below
