@@ -26,11 +26,15 @@ from .trace import (
     DEVICE_STAGES,
     PipelineTrace,
     StageRecord,
+    TrafficReport,
+    activation_traffic_closed_form,
     build_block_schedule,
     expert_offsets,
     stage_bytes,
     stage_flops,
     trace_from_counts,
+    traffic_from_measured,
+    traffic_from_traces,
 )
 from .types import (
     MODEL_PRESETS,
