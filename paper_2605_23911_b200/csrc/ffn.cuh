@@ -323,10 +323,13 @@ ffn_kernel(const __grid_constant__ CUtensorMap tm_wg, const __grid_constant__ CU
     return t;
   };
   const uint32_t tmem_base = *tmem_base_smem;
-  // prologue done: let the combine grid queue up, then wait for the dispatch
-  // (chunk table, permuted tokens) to be complete and visible
-  pdl_launch_dependents();
+  // prologue done: wait for the dispatch (chunk table, permuted tokens) to be
+  // complete and visible, THEN let the combine grid queue up: the overlapped
+  // combine reads prow / topk_w (dispatch and router outputs) without a
+  // griddepcontrol.wait of its own, so with MOE_B200_PDL=1 it must not launch
+  // before every FFN CTA has seen the dispatch complete
   pdl_wait();
+  pdl_launch_dependents();
 
   const int nch = __ldg(p.n_chunks);
   const int mt_gu_q = kPair ? (p.n_mt_gu + 1) / 2 : p.n_mt_gu;  // queue entries per chunk

@@ -615,8 +615,11 @@ void apply_carveout(const void* kern) {
 // the kernel may start while its predecessor finishes and calls pdl_wait()
 // before reading the predecessor's outputs (common.cuh).  Off by default: it
 // measured no gain on the graph-replayed forward (A/B 510 vs 508 us, Mixtral;
-// on the FFN -> combine edge alone 601 vs 600 us Mixtral, 209 vs 209 us Qwen)
-// and one test sequence (Mixtral then Qwen layers) stalled with it on.
+// on the FFN -> combine edge alone 601 vs 600 us Mixtral, 209 vs 209 us Qwen;
+// round 2, all edges: Mixtral-512 562 vs 575, Qwen 200.9 vs 200.7, DeepSeek
+// 3394 vs 3392, skew64 574.5 vs 580.9 us).  (Its one failure -- the overlapped
+// combine launched before the dispatch finished, ffn.cuh -- is fixed; the GPU
+// suites pass with it on.)
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl_if(bool on, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                           Args&&... args) {
